@@ -1,0 +1,190 @@
+// Greedy root-node aggregation on the GPU (aggregation.hpp:29-98), bit-exact.
+//
+// Pass 1 of the reference visits nodes in ascending order and makes node i a
+// root when neither i nor any strong neighbour has been claimed.  With
+// N[x] = row x of the normalised S (which always holds its diagonal), node i is
+// a root iff no lower-index root r has N[r] ∩ N[i] ≠ ∅: pass 1 is the
+// lexicographically-first maximal independent set of the conflict graph
+// pattern(S S^T).  It is computed by a sync-free wavefront: one thread per
+// node, blocks draw tickets in launch order, a node waits only on lower-index
+// conflict neighbours (so the nodes it waits on belong to blocks that already
+// hold a ticket -- no deadlock) and decides OUT as soon as one of them is a
+// root.  Claims, pass 2 (strongest edge, ties to the lowest aggregate id,
+// aggregation.hpp:55-76) and the singleton ids (78-82) are then parallel maps
+// and scans.
+#include <cuda/atomic>
+
+#include "ops.cuh"
+
+namespace amgcu {
+
+namespace {
+
+constexpr int kUndecided = 0, kRoot = 1, kOut = 2;
+constexpr int kMisThreads = 128;
+
+__global__ void k_unit_diag_check(int32_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                  const double* __restrict__ va, int32_t* __restrict__ bad) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int32_t lo = rp[i], hi = rp[i + 1];
+    while (lo < hi) {
+        const int32_t mid = (lo + hi) >> 1;
+        if (ci[mid] < i) lo = mid + 1;
+        else hi = mid;
+    }
+    const double d = (lo < rp[i + 1] && ci[lo] == i) ? va[lo] : 0.0;
+    if (d != 1.0) atomicExch(bad, 1);
+}
+
+__global__ void __launch_bounds__(kMisThreads)
+    k_lfmis(int32_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci, const int32_t* __restrict__ trp,
+            const int32_t* __restrict__ tci, int32_t* __restrict__ state, unsigned int* __restrict__ ticket) {
+    __shared__ unsigned int blk;
+    if (threadIdx.x == 0) blk = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const int32_t i = static_cast<int32_t>(blk) * kMisThreads + threadIdx.x;
+    if (i >= n) return;
+    // The decision is published inside the loop: a lane that exits a spin loop
+    // before storing could wait at the warp's reconvergence point while its
+    // neighbours spin on the value it has not yet written.
+    cuda::atomic_ref<int32_t, cuda::thread_scope_device> me(state[i]);
+    while (true) {
+        bool pending = false, hit_root = false;
+        for (int32_t p = rp[i]; p < rp[i + 1] && !hit_root; ++p) {
+            const int32_t x = ci[p];
+            for (int32_t q = trp[x]; q < trp[x + 1]; ++q) {
+                const int32_t r = tci[q];
+                if (r >= i) break;  // rows of S^T are ascending
+                cuda::atomic_ref<int32_t, cuda::thread_scope_device> st(state[r]);
+                const int32_t v = st.load(cuda::memory_order_relaxed);
+                if (v == kRoot) {
+                    hit_root = true;
+                    break;
+                }
+                if (v == kUndecided) pending = true;
+            }
+        }
+        if (hit_root || !pending) {
+            me.store(hit_root ? kOut : kRoot, cuda::memory_order_relaxed);
+            break;
+        }
+        __nanosleep(32);
+    }
+}
+
+__global__ void k_root_flags(int32_t n, const int32_t* __restrict__ state, int32_t* __restrict__ flag) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) flag[i] = state[i] == kRoot ? 1 : 0;
+}
+
+// claim N[r] for every root r with id = #roots below r
+__global__ void k_claim(int32_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                        const int32_t* __restrict__ state, const int32_t* __restrict__ root_id, int32_t* __restrict__ own,
+                        int32_t* __restrict__ roots) {
+    const int32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n || state[r] != kRoot) return;
+    const int32_t id = root_id[r];
+    roots[id] = r;
+    own[r] = id;
+    for (int32_t p = rp[r]; p < rp[r + 1]; ++p) own[ci[p]] = id;
+}
+
+__global__ void k_pass2(int32_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                        const double* __restrict__ va, const int32_t* __restrict__ own, int32_t n_pass1,
+                        int32_t* __restrict__ joined) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    if (own[i] >= 0) {
+        joined[i] = own[i];
+        return;
+    }
+    double best = 0.0;
+    int32_t best_agg = -1;
+    for (int32_t p = rp[i]; p < rp[i + 1]; ++p) {
+        const int32_t j = ci[p];
+        if (j == i) continue;
+        const int32_t a = own[j];
+        if (a < 0 || a >= n_pass1) continue;
+        const double v = va[p];
+        if (v > best || (v == best && best_agg >= 0 && a < best_agg)) {
+            best = v;
+            best_agg = a;
+        }
+    }
+    joined[i] = best_agg;
+}
+
+__global__ void k_leftover_flags(int32_t n, const int32_t* __restrict__ joined, int32_t* __restrict__ flag) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) flag[i] = joined[i] < 0 ? 1 : 0;
+}
+
+__global__ void k_singletons(int32_t n, int32_t n_pass1, const int32_t* __restrict__ rank, int32_t* __restrict__ joined,
+                             int32_t* __restrict__ roots) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n || joined[i] >= 0) return;
+    const int32_t id = n_pass1 + rank[i];
+    joined[i] = id;
+    roots[id] = i;
+}
+
+__global__ void k_indicator(int32_t n, const int32_t* __restrict__ own, int32_t* __restrict__ rp,
+                            int32_t* __restrict__ ci, double* __restrict__ va) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i > n) return;
+    rp[i] = i;
+    if (i < n) {
+        ci[i] = own[i];
+        va[i] = 1.0;
+    }
+}
+
+}  // namespace
+
+void greedy_aggregate(Ctx& c, const DCsr& S, DAgg& agg) {
+    if (S.nr != S.nc) throw InvalidArgument("greedy_aggregate: square matrix required");
+    const int32_t n = S.nr;
+    {
+        DBuf<int32_t> bad(1, c.s);
+        AMG_CK(cudaMemsetAsync(bad.get(), 0, sizeof(int32_t), c.s));
+        launch(c, k_unit_diag_check, blocks_for(n, 256), 256, 0, n, S.rp.get(), S.ci.get(), S.va.get(), bad.get());
+        if (read_scalar(c, bad.get()))
+            throw InvalidArgument("greedy_aggregate: strength matrix must be normalized (unit diagonal)");
+    }
+    DCsr St;  // pattern of S^T (rows ascending) for the conflict sets
+    transpose(c, S, St);
+    DBuf<int32_t> state(static_cast<size_t>(n), c.s);
+    AMG_CK(cudaMemsetAsync(state.get(), 0, sizeof(int32_t) * n, c.s));
+    DBuf<unsigned int> ticket(1, c.s);
+    AMG_CK(cudaMemsetAsync(ticket.get(), 0, sizeof(unsigned int), c.s));
+    launch(c, k_lfmis, blocks_for(n, kMisThreads), kMisThreads, 0, n, S.rp.get(), S.ci.get(), St.rp.get(),
+           St.ci.get(), state.get(), ticket.get());
+    DBuf<int32_t> flag(static_cast<size_t>(n) + 1, c.s), rid(static_cast<size_t>(n) + 1, c.s);
+    launch(c, k_root_flags, blocks_for(n, 256), 256, 0, n, static_cast<const int32_t*>(state.get()), flag.get());
+    const int32_t n_pass1 = static_cast<int32_t>(exclusive_scan_i32(c, flag.get(), rid.get(), n));
+    DBuf<int32_t> own(static_cast<size_t>(n), c.s), roots(static_cast<size_t>(n), c.s);
+    fill_i32(c, own.get(), -1, n);
+    launch(c, k_claim, blocks_for(n, 256), 256, 0, n, S.rp.get(), S.ci.get(), static_cast<const int32_t*>(state.get()),
+           static_cast<const int32_t*>(rid.get()), own.get(), roots.get());
+    DBuf<int32_t> joined(static_cast<size_t>(n), c.s);
+    launch(c, k_pass2, blocks_for(n, 256), 256, 0, n, S.rp.get(), S.ci.get(), S.va.get(),
+           static_cast<const int32_t*>(own.get()), n_pass1, joined.get());
+    launch(c, k_leftover_flags, blocks_for(n, 256), 256, 0, n, static_cast<const int32_t*>(joined.get()), flag.get());
+    const int32_t n_left = static_cast<int32_t>(exclusive_scan_i32(c, flag.get(), rid.get(), n));
+    launch(c, k_singletons, blocks_for(n, 256), 256, 0, n, n_pass1, static_cast<const int32_t*>(rid.get()),
+           joined.get(), roots.get());
+    agg.n_nodes = n;
+    agg.n_agg = n_pass1 + n_left;
+    agg.owner = std::move(joined);
+    agg.roots = std::move(roots);
+}
+
+void aggregate_indicator(Ctx& c, const DAgg& agg, DCsr& Cm) {
+    Cm.alloc(c, agg.n_nodes, agg.n_agg, agg.n_nodes);
+    Cm.bs = 1;
+    launch(c, k_indicator, blocks_for(agg.n_nodes + 1, 256), 256, 0, agg.n_nodes, agg.owner.get(), Cm.rp.get(),
+           Cm.ci.get(), Cm.va.get());
+}
+
+}  // namespace amgcu

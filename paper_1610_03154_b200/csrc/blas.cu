@@ -1,0 +1,114 @@
+// BLAS-1 on device-resident scalars (sparse.hpp:309-323).
+//
+// dot: default = deterministic two-stage tree (fixed grid, fixed per-thread
+// order, last-block final sum in index order of the block partials), so the
+// same inputs always give the same bits.  With Ctx::seq the sum is taken in
+// the reference's order s = ((0 + x0 y0) + x1 y1) + ... by one warp
+// (parity-debug mode): bit-identical to the CPU, slower.
+#include <cub/block/block_reduce.cuh>
+
+#include <algorithm>
+
+#include "ops.cuh"
+
+namespace amgcu {
+
+namespace {
+
+constexpr int kDotThreads = 256;
+
+__global__ void k_dot_tree(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
+                           double* __restrict__ partials, unsigned int* __restrict__ done, double* __restrict__ out,
+                           bool take_sqrt) {
+    using BR = cub::BlockReduce<double, kDotThreads>;
+    __shared__ typename BR::TempStorage tmp;
+    __shared__ bool last;
+    double s = 0.0;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * kDotThreads;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * kDotThreads + threadIdx.x; i < n; i += stride)
+        s += x[i] * y[i];
+    const double b = BR(tmp).Sum(s);
+    if (threadIdx.x == 0) {
+        partials[blockIdx.x] = b;
+        __threadfence();
+        const unsigned prev = atomicAdd(done, 1u);
+        last = (prev == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        __threadfence();
+        double t = 0.0;
+        for (unsigned k = 0; k < gridDim.x; ++k) t += __ldcg(&partials[k]);
+        *out = take_sqrt ? sqrt(t) : t;
+        *done = 0u;  // reset for the next call on this stream
+    }
+}
+
+__global__ void k_dot_seq(const double* __restrict__ x, const double* __restrict__ y, int64_t n, double* __restrict__ out,
+                          bool take_sqrt) {
+    const int lane = threadIdx.x;
+    double s = 0.0;
+    for (int64_t base = 0; base < n; base += 32) {
+        const int64_t i = base + lane;
+        const double v = i < n ? x[i] * y[i] : 0.0;
+        const int cnt = static_cast<int>(n - base < 32 ? n - base : 32);
+        for (int t = 0; t < cnt; ++t) s += __shfl_sync(0xffffffffu, v, t);
+    }
+    if (lane == 0) *out = take_sqrt ? sqrt(s) : s;
+}
+
+__global__ void k_axpy_dev(const double* __restrict__ alpha, double sign, const double* __restrict__ x,
+                           double* __restrict__ y, int64_t n) {
+    const double a = sign * (*alpha);
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        y[i] += a * x[i];
+}
+
+__global__ void k_scale_recip(const double* __restrict__ denom, double* __restrict__ x, int64_t n) {
+    const double a = 1.0 / (*denom);
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        x[i] *= a;
+}
+
+__global__ void k_scale_const(double a, double* __restrict__ x, int64_t n) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        x[i] *= a;
+}
+
+unsigned stream_grid(Ctx& c, int64_t n) {
+    return std::max(1u, std::min<unsigned>(blocks_for(n, 256), 8u * c.sms));
+}
+
+void dot_impl(Ctx& c, const double* x, const double* y, int64_t n, double* out, bool take_sqrt) {
+    if (c.seq) {
+        launch(c, k_dot_seq, 1, 32, 0, x, y, n, out, take_sqrt);
+        return;
+    }
+    const unsigned g = std::max(1u, std::min<unsigned>(blocks_for(n, kDotThreads * 4), 2u * c.sms));
+    if (c.partials.size() < 4096) {
+        c.partials.alloc(4096, c.s);
+        c.tickets.alloc(64, c.s);
+        AMG_CK(cudaMemsetAsync(c.tickets.get(), 0, sizeof(unsigned int) * 64, c.s));
+    }
+    launch(c, k_dot_tree, g, kDotThreads, 0, x, y, n, c.partials.get(), c.tickets.get(), out, take_sqrt);
+}
+
+}  // namespace
+
+void dot(Ctx& c, const double* x, const double* y, int64_t n, double* out) { dot_impl(c, x, y, n, out, false); }
+void nrm2(Ctx& c, const double* x, int64_t n, double* out) { dot_impl(c, x, x, n, out, true); }
+
+void axpy_dev(Ctx& c, const double* alpha, double sign, const double* x, double* y, int64_t n) {
+    launch(c, k_axpy_dev, stream_grid(c, n), 256, 0, alpha, sign, x, y, n);
+}
+void scale_recip_dev(Ctx& c, const double* denom, double* x, int64_t n) {
+    launch(c, k_scale_recip, stream_grid(c, n), 256, 0, denom, x, n);
+}
+void scale_const(Ctx& c, double alpha, double* x, int64_t n) {
+    launch(c, k_scale_const, stream_grid(c, n), 256, 0, alpha, x, n);
+}
+
+}  // namespace amgcu

@@ -1,0 +1,533 @@
+// Solve phase on the GPU: V/W cycle (cycle.hpp:70-95) and the stationary /
+// PCG / FGMRES drivers (cycle.hpp:114-271).
+//
+// Level operators are mirrored into sliced ELL (32-row slices, column-major
+// inside a slice, rows kept in order) so one thread per row sums its row in CSR
+// order -- reference-exact -- while the warp's loads stay coalesced.  Fusions
+// (all reference-exact):
+//   * pre-relaxation from x = 0 (every cycle entry of the preconditioner and
+//     every coarse level) is x = (w D^-1) b, and is fused with the residual
+//     r = b - A x, recomputing neighbour x_j = (w D^-1)_j b_j in registers;
+//   * interpolate-and-correct t = x + P x_c is one pass;
+//   * post-relaxation x = t + (w D^-1)(b - A t) is one pass;
+//   * restriction b_c = R r is a gather over R's rows (no atomics).
+// Krylov scalars stay on the device; the host reads one small status record
+// per iteration (the residual norm decides termination, as in the reference).
+#include <cmath>
+
+#include "hier.cuh"
+
+namespace amgcu {
+
+namespace {
+
+constexpr int kSlice = 32;
+
+__global__ void k_slice_len(int32_t nr, const int32_t* __restrict__ rp, int64_t* __restrict__ slen) {
+    const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+    const int32_t nsl = (nr + kSlice - 1) / kSlice;
+    if (s >= nsl) return;
+    int32_t mx = 0;
+    for (int32_t r = s * kSlice; r < min(nr, s * kSlice + kSlice); ++r) mx = max(mx, rp[r + 1] - rp[r]);
+    slen[s] = static_cast<int64_t>(mx) * kSlice;
+}
+
+__global__ void k_sell_fill(int32_t nr, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                            const double* __restrict__ va, const int64_t* __restrict__ sptr, int32_t* __restrict__ sci,
+                            double* __restrict__ sva, int32_t* __restrict__ slen) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int32_t s = i / kSlice, lane = i % kSlice;
+    const int32_t nsl = (nr + kSlice - 1) / kSlice;
+    if (s >= nsl) return;
+    const int64_t base = sptr[s];
+    const int32_t width = static_cast<int32_t>((sptr[s + 1] - base) / kSlice);
+    if (lane == 0) slen[s] = width;
+    int32_t len = 0, lo = 0;
+    if (i < nr) {
+        lo = rp[i];
+        len = rp[i + 1] - lo;
+    }
+    for (int32_t e = 0; e < width; ++e) {
+        const int64_t at = base + static_cast<int64_t>(e) * kSlice + lane;
+        if (e < len) {
+            sci[at] = ci[lo + e];
+            sva[at] = va[lo + e];
+        } else {
+            sci[at] = -1;
+            sva[at] = 0.0;
+        }
+    }
+}
+
+__device__ __forceinline__ double sell_row(int32_t i, const int64_t* __restrict__ sptr, const int32_t* __restrict__ slen,
+                                           const int32_t* __restrict__ sci, const double* __restrict__ sva,
+                                           const double* __restrict__ x) {
+    const int32_t s = i / kSlice, lane = i % kSlice;
+    const int64_t base = sptr[s] + lane;
+    const int32_t w = slen[s];
+    double acc = 0.0;
+    for (int32_t e = 0; e < w; ++e) {
+        const int32_t j = sci[base + static_cast<int64_t>(e) * kSlice];
+        if (j < 0) break;
+        acc += sva[base + static_cast<int64_t>(e) * kSlice] * x[j];
+    }
+    return acc;
+}
+
+struct SellView {
+    int32_t nr;
+    const int64_t* sptr;
+    const int32_t* slen;
+    const int32_t* ci;
+    const double* va;
+};
+
+SellView view(const DSell& s) { return {s.nr, s.slice_ptr.get(), s.slice_len.get(), s.ci.get(), s.va.get()}; }
+
+__global__ void k_sell_spmv(SellView A, const double* __restrict__ x, double* __restrict__ y) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= A.nr) return;
+    y[i] = sell_row(i, A.sptr, A.slen, A.ci, A.va, x);
+}
+
+// r = b - A x
+__global__ void k_sell_residual(SellView A, const double* __restrict__ x, const double* __restrict__ b,
+                                double* __restrict__ r) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= A.nr) return;
+    const double s = sell_row(i, A.sptr, A.slen, A.ci, A.va, x);
+    r[i] = b[i] - s;
+}
+
+// pre-relaxation from zero fused with the residual: x = 0 + wd b, r = b - A x
+__global__ void k_relax0_residual(SellView A, const double* __restrict__ wd, const double* __restrict__ b,
+                                  double* __restrict__ x, double* __restrict__ r) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= A.nr) return;
+    const int32_t s = i / kSlice, lane = i % kSlice;
+    const int64_t base = A.sptr[s] + lane;
+    const int32_t w = A.slen[s];
+    double acc = 0.0;
+    for (int32_t e = 0; e < w; ++e) {
+        const int32_t j = A.ci[base + static_cast<int64_t>(e) * kSlice];
+        if (j < 0) break;
+        const double xj = 0.0 + wd[j] * b[j];
+        acc += A.va[base + static_cast<int64_t>(e) * kSlice] * xj;
+    }
+    x[i] = 0.0 + wd[i] * b[i];
+    r[i] = b[i] - acc;
+}
+
+// x = 0 + wd b (pre-relaxation from zero without the fused residual)
+__global__ void k_relax0(int32_t n, const double* __restrict__ wd, const double* __restrict__ b, double* __restrict__ x) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) x[i] = 0.0 + wd[i] * b[i];
+}
+
+// xout = xin + wd (b - A xin)
+__global__ void k_jacobi_sweep(SellView A, const double* __restrict__ wd, const double* __restrict__ b,
+                               const double* __restrict__ xin, double* __restrict__ xout) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= A.nr) return;
+    const double s = sell_row(i, A.sptr, A.slen, A.ci, A.va, xin);
+    xout[i] = xin[i] + wd[i] * (b[i] - s);
+}
+
+// t = x + P xc
+__global__ void k_prolong(SellView P, const double* __restrict__ xc, const double* __restrict__ x,
+                          double* __restrict__ t) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= P.nr) return;
+    const double s = sell_row(i, P.sptr, P.slen, P.ci, P.va, xc);
+    t[i] = x[i] + s;
+}
+
+// coarsest level: x = pinv b
+__global__ void k_dense_gemv(int32_t n, const double* __restrict__ M, const double* __restrict__ b,
+                             double* __restrict__ x) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double s = 0.0;
+    for (int32_t j = 0; j < n; ++j) s += M[static_cast<size_t>(i) * n + j] * b[j];
+    x[i] = s;
+}
+
+// PCG control: st = {rz, pq, alpha, rz_new, beta, rn}; flag: !(pq > 0)
+__global__ void k_pcg_alpha(double* __restrict__ st, int32_t* __restrict__ bad) {
+    const double pq = st[1];
+    if (!(pq > 0.0)) {
+        *bad = 1;
+        return;
+    }
+    *bad = 0;
+    st[2] = st[0] / pq;
+}
+
+__global__ void k_pcg_update(int64_t n, const double* __restrict__ st, const int32_t* __restrict__ bad,
+                             const double* __restrict__ p, const double* __restrict__ q, double* __restrict__ x,
+                             double* __restrict__ r) {
+    if (*bad) return;
+    const double a = st[2];
+    const double na = -a;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        x[i] += a * p[i];
+        r[i] += na * q[i];
+    }
+}
+
+__global__ void k_pcg_beta(double* __restrict__ st) {
+    st[4] = st[3] / st[0];
+    st[0] = st[3];
+}
+
+__global__ void k_pcg_dir(int64_t n, const double* __restrict__ st, const double* __restrict__ z, double* __restrict__ p) {
+    const double beta = st[4];
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        p[i] = z[i] + beta * p[i];
+}
+
+__global__ void k_axpy_c(int64_t n, double a, const double* __restrict__ x, double* __restrict__ y) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        y[i] += a * x[i];
+}
+
+void build_sell(Ctx& c, const DCsr& A, DSell& S) {
+    S.nr = A.nr;
+    S.nc = A.nc;
+    S.nslices = (A.nr + kSlice - 1) / kSlice;
+    DBuf<int64_t> slen(static_cast<size_t>(S.nslices) + 1, c.s);
+    S.slice_ptr.alloc(static_cast<size_t>(S.nslices) + 1, c.s);
+    launch(c, k_slice_len, blocks_for(S.nslices, 256), 256, 0, A.nr, A.rp.get(), slen.get());
+    S.stored = exclusive_scan_i64(c, slen.get(), S.slice_ptr.get(), S.nslices);
+    S.slice_len.alloc(static_cast<size_t>(S.nslices), c.s);
+    S.ci.alloc(static_cast<size_t>(S.stored), c.s);
+    S.va.alloc(static_cast<size_t>(S.stored), c.s);
+    launch(c, k_sell_fill, blocks_for(static_cast<int64_t>(S.nslices) * kSlice, 256), 256, 0, A.nr, A.rp.get(),
+           A.ci.get(), A.va.get(), static_cast<const int64_t*>(S.slice_ptr.get()), S.ci.get(), S.va.get(),
+           S.slice_len.get());
+}
+
+unsigned rows_grid(int32_t n) { return blocks_for(n, 128); }
+unsigned stream_grid(Ctx& c, int64_t n) { return std::max(1u, std::min<unsigned>(blocks_for(n, 256), 8u * c.sms)); }
+
+double relax_cost(int scheme, double nnz) { return scheme == 3 ? 2.0 * nnz : nnz; }
+
+struct Driver {
+    DHier& h;
+    Ctx& c;
+    double ops = 0.0;  // multiply-model count (cycle.hpp cost model)
+
+    // one cycle at `l`; x_zero: x is known to be all zeros on entry
+    void apply(size_t l, double* x, const double* b, int kind, bool x_zero) {
+        const size_t L = h.lv.size();
+        DLevel& lev = h.lv[l];
+        if (l == L - 1) {
+            launch(c, k_dense_gemv, blocks_for(h.coarse_n, 128), 128, 0, h.coarse_n,
+                   static_cast<const double*>(h.coarse_pinv.get()), b, x);
+            return;
+        }
+        const int32_t n = lev.A.nr;
+        const double nnz = static_cast<double>(lev.A.nnz);
+        const SellView A = view(lev.sA);
+        // pre-relaxation + residual
+        const int pre = h.o.pre_scheme;
+        int sweeps = h.o.pre_sweeps;
+        bool residual_done = false;
+        if (pre == 0) {
+            for (int s = 0; s < sweeps; ++s) {
+                if (s == 0 && x_zero) {
+                    if (sweeps == 1) {
+                        launch(c, k_relax0_residual, rows_grid(n), 128, 0, A, static_cast<const double*>(lev.wd_pre.get()),
+                               b, x, lev.r.get());
+                        residual_done = true;
+                    } else {
+                        launch(c, k_relax0, rows_grid(n), 128, 0, n, static_cast<const double*>(lev.wd_pre.get()), b, x);
+                    }
+                } else {
+                    launch(c, k_jacobi_sweep, rows_grid(n), 128, 0, A, static_cast<const double*>(lev.wd_pre.get()), b,
+                           static_cast<const double*>(x), lev.t.get());
+                    copy_d2d(c, x, lev.t.get(), n);
+                }
+                ops += relax_cost(pre, nnz);
+            }
+        } else {
+            if (x_zero) AMG_CK(cudaMemsetAsync(x, 0, sizeof(double) * n, c.s));
+            if (sweeps > 0) gauss_seidel(c, lev.A, lev.inv_diag.get(), x, b, 1, sweeps, pre == 2);
+            ops += sweeps * relax_cost(pre, nnz);
+        }
+        if (pre != 0 && x_zero && sweeps == 0) {
+            // x stays zero
+        }
+        if (!residual_done) {
+            if (pre == 0 && sweeps == 0 && x_zero) AMG_CK(cudaMemsetAsync(x, 0, sizeof(double) * n, c.s));
+            launch(c, k_sell_residual, rows_grid(n), 128, 0, A, static_cast<const double*>(x), b, lev.r.get());
+        }
+        ops += nnz;
+        // restriction
+        DLevel& nxt = h.lv[l + 1];
+        launch(c, k_sell_spmv, rows_grid(lev.sR.nr), 128, 0, view(lev.sR), static_cast<const double*>(lev.r.get()),
+               nxt.b.get());
+        ops += static_cast<double>(lev.R.nnz);
+        apply(l + 1, nxt.x.get(), nxt.b.get(), kind, true);
+        if (kind == 1 && l + 1 < L - 1) apply(l + 1, nxt.x.get(), nxt.b.get(), kind, false);
+        // interpolate and correct into t, then post-relax back into x
+        launch(c, k_prolong, rows_grid(n), 128, 0, view(lev.sP), static_cast<const double*>(nxt.x.get()),
+               static_cast<const double*>(x), lev.t.get());
+        ops += static_cast<double>(lev.P.nnz);
+        const int post = h.o.post_scheme;
+        sweeps = h.o.post_sweeps;
+        if (post == 0) {
+            if (sweeps == 0) {
+                copy_d2d(c, x, lev.t.get(), n);
+            } else {
+                for (int s = 0; s < sweeps; ++s) {
+                    if (s == 0) {
+                        launch(c, k_jacobi_sweep, rows_grid(n), 128, 0, A,
+                               static_cast<const double*>(lev.wd_post.get()), b, static_cast<const double*>(lev.t.get()),
+                               x);
+                    } else {
+                        launch(c, k_jacobi_sweep, rows_grid(n), 128, 0, A,
+                               static_cast<const double*>(lev.wd_post.get()), b, static_cast<const double*>(x),
+                               lev.t.get());
+                        copy_d2d(c, x, lev.t.get(), n);
+                    }
+                    ops += relax_cost(post, nnz);
+                }
+            }
+        } else {
+            copy_d2d(c, x, lev.t.get(), n);
+            if (sweeps > 0) gauss_seidel(c, lev.A, lev.inv_diag.get(), x, b, 1, sweeps, post == 2);
+            ops += sweeps * relax_cost(post, nnz);
+        }
+    }
+
+    void precond(const double* rhs, double* out, int kind) { apply(0, out, rhs, kind, true); }
+};
+
+double conv_factor(const std::vector<double>& hist, int window = 5) {  // cycle.hpp:39-46
+    if (hist.size() < 2) return 0.0;
+    const int w = std::min<int>(window, static_cast<int>(hist.size()) - 1);
+    const double head = hist[hist.size() - 1 - w];
+    const double tail = hist.back();
+    if (head <= 0.0) return 0.0;
+    return std::pow(tail / head, 1.0 / w);
+}
+
+}  // namespace
+
+void prepare_solve(DHier& h) {
+    Ctx& c = *h.ctx;
+    for (size_t l = 0; l < h.lv.size(); ++l) {
+        DLevel& L = h.lv[l];
+        const int32_t n = L.A.nr;
+        L.r.alloc(static_cast<size_t>(n), c.s);
+        L.t.alloc(static_cast<size_t>(n), c.s);
+        if (l > 0) {
+            L.b.alloc(static_cast<size_t>(n), c.s);
+            L.x.alloc(static_cast<size_t>(n), c.s);
+        }
+        build_sell(c, L.A, L.sA);
+        if (l + 1 < h.lv.size()) {
+            build_sell(c, L.P, L.sP);
+            build_sell(c, L.R, L.sR);
+        }
+    }
+    sync(c);
+    h.solve_ready = true;
+}
+
+double operator_complexity(const DHier& h) {  // complexity.hpp:15-20
+    const double base = static_cast<double>(h.lv.front().A.nnz);
+    double s = 0.0;
+    for (const DLevel& l : h.lv) s += static_cast<double>(l.A.nnz);
+    return s / base;
+}
+
+double cycle_complexity(const DHier& h) {  // complexity.hpp:25-36
+    const double base = static_cast<double>(h.lv.front().A.nnz);
+    double s = 0.0;
+    for (size_t l = 0; l + 1 < h.lv.size(); ++l) {
+        s += static_cast<double>(h.o.pre_sweeps + h.o.post_sweeps + 1) * h.lv[l].A.nnz;
+        s += static_cast<double>(h.lv[l].P.nnz) + static_cast<double>(h.lv[l].R.nnz);
+    }
+    return s / base;
+}
+
+void cycle(DHier& h, double* x, const double* b, int kind) {
+    Driver d{h, *h.ctx};
+    d.apply(0, x, b, kind, false);
+    sync(*h.ctx);
+}
+
+SolveResult solve(DHier& h, const double* b, double* x, const amgcu_solve_options& o) {
+    Ctx& c = *h.ctx;
+    if (o.max_iters < 1) throw InvalidArgument("solve: max_iters must be >= 1");
+    DLevel& L0 = h.lv.front();
+    const int32_t n = L0.A.nr;
+    const SellView A = view(L0.sA);
+    SolveResult rep;
+    rep.chi_oc = operator_complexity(h);
+    rep.chi_cc = cycle_complexity(h);
+    rep.wu_setup = h.wu[0] + h.wu[1] + h.wu[2] + h.wu[3];
+    Driver d{h, c};
+    auto finish = [&]() {
+        rep.rho = conv_factor(rep.history);
+        rep.wu_solve = d.ops / h.base_nnz;
+        h.wu[4] += d.ops / h.base_nnz;
+        return rep;
+    };
+    DBuf<double> r(static_cast<size_t>(n), c.s), st(16, c.s);
+    DBuf<int32_t> bad(1, c.s);
+    launch(c, k_sell_residual, rows_grid(n), 128, 0, A, static_cast<const double*>(x), b, r.get());
+    d.ops += static_cast<double>(L0.A.nnz);
+    double* S = st.get();
+    nrm2(c, r.get(), n, S + 10);  // r0
+    nrm2(c, b, n, S + 11);        // |b|
+    double h2[2];
+    copy_d2h(c, h2, S + 10, 2);
+    sync(c);
+    const double r0 = h2[0], bnorm = h2[1];
+    const double target = o.tol * (bnorm > 0.0 ? bnorm : r0);
+    rep.history.push_back(r0);
+    if (r0 <= target) {
+        rep.converged = true;
+        return finish();
+    }
+    const double blowup = 1e6 * r0;
+
+    if (o.method == 0) {  // stationary cycling
+        for (int it = 1; it <= o.max_iters; ++it) {
+            d.apply(0, x, b, o.cycle, false);
+            launch(c, k_sell_residual, rows_grid(n), 128, 0, A, static_cast<const double*>(x), b, r.get());
+            nrm2(c, r.get(), n, S + 5);
+            const double rn = read_scalar(c, S + 5);
+            rep.history.push_back(rn);
+            rep.iterations = it;
+            if (rn <= target) {
+                rep.converged = true;
+                break;
+            }
+            if (rn > blowup || !std::isfinite(rn)) {
+                rep.diverged = true;
+                break;
+            }
+        }
+        return finish();
+    }
+
+    if (o.method == 1) {  // PCG (cycle.hpp:174-209)
+        if (!L0.symmetric) throw InvalidArgument("solve: pcg requires a symmetric operator");
+        DBuf<double> z(static_cast<size_t>(n), c.s), p(static_cast<size_t>(n), c.s), q(static_cast<size_t>(n), c.s);
+        d.precond(r.get(), z.get(), o.cycle);
+        copy_d2d(c, p.get(), z.get(), n);
+        dot(c, r.get(), z.get(), n, S + 0);  // rz
+        for (int it = 1; it <= o.max_iters; ++it) {
+            launch(c, k_sell_spmv, rows_grid(n), 128, 0, A, static_cast<const double*>(p.get()), q.get());
+            d.ops += static_cast<double>(L0.A.nnz);
+            dot(c, p.get(), q.get(), n, S + 1);
+            launch(c, k_pcg_alpha, 1, 1, 0, S, bad.get());
+            launch(c, k_pcg_update, stream_grid(c, n), 256, 0, static_cast<int64_t>(n), static_cast<const double*>(S),
+                   static_cast<const int32_t*>(bad.get()), static_cast<const double*>(p.get()),
+                   static_cast<const double*>(q.get()), x, r.get());
+            nrm2(c, r.get(), n, S + 5);
+            struct {
+                double rn;
+                int32_t bad;
+            } hs;
+            copy_d2h(c, &hs.rn, S + 5, 1);
+            copy_d2h(c, &hs.bad, bad.get(), 1);
+            sync(c);
+            if (hs.bad) {
+                rep.diverged = true;
+                break;
+            }
+            const double rn = hs.rn;
+            rep.history.push_back(rn);
+            rep.iterations = it;
+            if (rn <= target) {
+                rep.converged = true;
+                break;
+            }
+            if (rn > blowup || !std::isfinite(rn)) {
+                rep.diverged = true;
+                break;
+            }
+            d.precond(r.get(), z.get(), o.cycle);
+            dot(c, r.get(), z.get(), n, S + 3);
+            launch(c, k_pcg_beta, 1, 1, 0, S);
+            launch(c, k_pcg_dir, stream_grid(c, n), 256, 0, static_cast<int64_t>(n), static_cast<const double*>(S),
+                   static_cast<const double*>(z.get()), p.get());
+        }
+        return finish();
+    }
+
+    // FGMRES, one cycle of max_iters steps (cycle.hpp:211-270)
+    const int m = o.max_iters;
+    DBuf<double> V(static_cast<size_t>(n) * (m + 1), c.s), Z(static_cast<size_t>(n) * m, c.s);
+    DBuf<double> Hcol(static_cast<size_t>(m) + 2, c.s);
+    copy_d2d(c, V.get(), r.get(), n);
+    scale_const(c, 1.0 / r0, V.get(), n);
+    std::vector<double> H(static_cast<size_t>(m + 1) * m, 0.0), cs(m, 0.0), sn(m, 0.0), g(m + 1, 0.0);
+    auto Hij = [&](int i, int j) -> double& { return H[static_cast<size_t>(i) * m + j]; };
+    g[0] = r0;
+    int built = 0;
+    for (int j = 0; j < m; ++j) {
+        double* zj = Z.get() + static_cast<size_t>(j) * n;
+        double* w = V.get() + static_cast<size_t>(j + 1) * n;
+        d.precond(V.get() + static_cast<size_t>(j) * n, zj, o.cycle);
+        launch(c, k_sell_spmv, rows_grid(n), 128, 0, A, static_cast<const double*>(zj), w);
+        d.ops += static_cast<double>(L0.A.nnz);
+        for (int t = 0; t <= j; ++t) {
+            dot(c, w, V.get() + static_cast<size_t>(t) * n, n, Hcol.get() + t);
+            axpy_dev(c, Hcol.get() + t, -1.0, V.get() + static_cast<size_t>(t) * n, w, n);
+        }
+        nrm2(c, w, n, Hcol.get() + j + 1);
+        std::vector<double> col(j + 2);
+        copy_d2h(c, col.data(), Hcol.get(), j + 2);
+        sync(c);
+        for (int t = 0; t <= j + 1; ++t) Hij(t, j) = col[t];
+        for (int t = 0; t < j; ++t) {
+            const double tmp = cs[t] * Hij(t, j) + sn[t] * Hij(t + 1, j);
+            Hij(t + 1, j) = -sn[t] * Hij(t, j) + cs[t] * Hij(t + 1, j);
+            Hij(t, j) = tmp;
+        }
+        const double den = std::hypot(Hij(j, j), Hij(j + 1, j));
+        cs[j] = den > 0.0 ? Hij(j, j) / den : 1.0;
+        sn[j] = den > 0.0 ? Hij(j + 1, j) / den : 0.0;
+        Hij(j, j) = den;
+        const double hlast = Hij(j + 1, j);
+        Hij(j + 1, j) = 0.0;
+        g[j + 1] = -sn[j] * g[j];
+        g[j] = cs[j] * g[j];
+        const double res = std::fabs(g[j + 1]);
+        rep.history.push_back(res);
+        rep.iterations = j + 1;
+        built = j + 1;
+        if (res <= target) {
+            rep.converged = true;
+            break;
+        }
+        if (res > blowup || !std::isfinite(res)) {
+            rep.diverged = true;
+            break;
+        }
+        if (hlast < 1e-300) break;
+        scale_const(c, 1.0 / hlast, w, n);
+    }
+    std::vector<double> y(built, 0.0);
+    for (int t = built - 1; t >= 0; --t) {
+        double s = g[t];
+        for (int u = t + 1; u < built; ++u) s -= Hij(t, u) * y[u];
+        y[t] = Hij(t, t) != 0.0 ? s / Hij(t, t) : 0.0;
+    }
+    for (int t = 0; t < built; ++t)
+        launch(c, k_axpy_c, stream_grid(c, n), 256, 0, static_cast<int64_t>(n), y[t],
+               static_cast<const double*>(Z.get() + static_cast<size_t>(t) * n), x);
+    sync(c);
+    return finish();
+}
+
+}  // namespace amgcu

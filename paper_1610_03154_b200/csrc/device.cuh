@@ -1,0 +1,161 @@
+// Device plumbing for libamgcu: stream-ordered buffers, the context, device
+// CSR, launch accounting and the few generic primitives (scan, fill, copy).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "host_common.h"
+
+namespace amgcu {
+
+#define AMG_CK(call)                                                                              \
+    do {                                                                                          \
+        cudaError_t e_ = (call);                                                                  \
+        if (e_ != cudaSuccess)                                                                    \
+            throw ::amgcu::CudaFailure(std::string(#call) + " failed: " + cudaGetErrorString(e_)); \
+    } while (0)
+
+// Stream-ordered device buffer (cudaMallocAsync on the context stream; the
+// pool keeps freed blocks for reuse, so per-level temporaries are cheap).
+template <typename T>
+class DBuf {
+public:
+    DBuf() = default;
+    DBuf(size_t n, cudaStream_t s) { alloc(n, s); }
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    DBuf(DBuf&& o) noexcept : p_(o.p_), n_(o.n_), s_(o.s_) {
+        o.p_ = nullptr;
+        o.n_ = 0;
+    }
+    DBuf& operator=(DBuf&& o) noexcept {
+        if (this != &o) {
+            release();
+            p_ = o.p_;
+            n_ = o.n_;
+            s_ = o.s_;
+            o.p_ = nullptr;
+            o.n_ = 0;
+        }
+        return *this;
+    }
+    ~DBuf() { release(); }
+
+    void alloc(size_t n, cudaStream_t s) {
+        release();
+        s_ = s;
+        n_ = n;
+        if (n) AMG_CK(cudaMallocAsync(reinterpret_cast<void**>(&p_), n * sizeof(T), s));
+    }
+    void release() {
+        if (p_) cudaFreeAsync(p_, s_);
+        p_ = nullptr;
+        n_ = 0;
+    }
+    T* get() const { return p_; }
+    size_t size() const { return n_; }
+    bool empty() const { return n_ == 0; }
+
+private:
+    T* p_ = nullptr;
+    size_t n_ = 0;
+    cudaStream_t s_ = nullptr;
+};
+
+struct Ctx {
+    int device = 0;
+    cudaStream_t s = nullptr;
+    int sms = 148;
+    bool seq = false;  // sequential (reference-order) global reductions
+    int64_t launches = 0;
+    std::string err;
+    DBuf<double> scal;         // device scalars for reductions/control
+    DBuf<double> partials;     // per-block partial sums
+    DBuf<unsigned int> tickets;  // sync-free wavefront tickets
+    double* hpin = nullptr;    // pinned host staging for scalars
+    // cached Arnoldi start vector 1 + U(-0.5, 0.5) from mt19937(20240911)
+    // (spectral.hpp:32-36); prefixes serve every smaller level.
+    DBuf<double> arnoldi_v0;
+    size_t arnoldi_v0_n = 0;
+};
+
+struct DCsr {
+    int32_t nr = 0, nc = 0, bs = 1;
+    int64_t nnz = 0;
+    DBuf<int32_t> rp, ci;
+    DBuf<double> va;
+    void alloc(Ctx& c, int32_t r, int32_t cols, int64_t nz) {
+        nr = r;
+        nc = cols;
+        nnz = nz;
+        rp.alloc(static_cast<size_t>(r) + 1, c.s);
+        ci.alloc(static_cast<size_t>(nz), c.s);
+        va.alloc(static_cast<size_t>(nz), c.s);
+    }
+};
+
+// Sliced-ELL (slice height 32, no row reordering) mirror of a CSR matrix for
+// the solve phase: column-major within each 32-row slice so the per-thread
+// row sums (CSR order, reference-exact) load coalesced.
+struct DSell {
+    int32_t nr = 0, nc = 0;
+    int32_t nslices = 0;
+    DBuf<int64_t> slice_ptr;   // nslices + 1, element offsets
+    DBuf<int32_t> slice_len;   // max row length per slice
+    DBuf<int32_t> ci;          // -1 marks padding
+    DBuf<double> va;
+    int64_t stored = 0;
+};
+
+template <typename Kern, typename... Args>
+inline void launch(Ctx& c, Kern k, unsigned grid, unsigned block, size_t smem, Args... args) {
+    if (grid == 0) return;
+    k<<<grid, block, smem, c.s>>>(args...);
+    ++c.launches;
+    AMG_CK(cudaGetLastError());
+}
+
+inline unsigned blocks_for(int64_t n, int per_block) {
+    return static_cast<unsigned>((n + per_block - 1) / per_block);
+}
+
+// ---- primitives (primitives.cu) ------------------------------------------
+// out[0..n] = exclusive prefix sum of in[0..n-1], out[n] = total.  Returns
+// the total (synchronising read).  in may alias out only if in == out is false.
+int64_t exclusive_scan_i32(Ctx& c, const int32_t* in, int32_t* out, int64_t n, bool read_total = true);
+int64_t exclusive_scan_i64(Ctx& c, const int64_t* in, int64_t* out, int64_t n, bool read_total = true);
+void fill_f64(Ctx& c, double* p, double v, int64_t n);
+void fill_i32(Ctx& c, int32_t* p, int32_t v, int64_t n);
+template <typename T>
+void copy_d2d(Ctx& c, T* dst, const T* src, int64_t n) {
+    if (n > 0) AMG_CK(cudaMemcpyAsync(dst, src, sizeof(T) * n, cudaMemcpyDeviceToDevice, c.s));
+}
+template <typename T>
+void copy_h2d(Ctx& c, T* dst, const T* src, int64_t n) {
+    if (n > 0) AMG_CK(cudaMemcpyAsync(dst, src, sizeof(T) * n, cudaMemcpyHostToDevice, c.s));
+}
+template <typename T>
+void copy_d2h(Ctx& c, T* dst, const T* src, int64_t n) {
+    if (n > 0) AMG_CK(cudaMemcpyAsync(dst, src, sizeof(T) * n, cudaMemcpyDeviceToHost, c.s));
+}
+inline void sync(Ctx& c) { AMG_CK(cudaStreamSynchronize(c.s)); }
+template <typename T>
+T read_scalar(Ctx& c, const T* dptr) {
+    T v;
+    AMG_CK(cudaMemcpyAsync(&v, dptr, sizeof(T), cudaMemcpyDeviceToHost, c.s));
+    sync(c);
+    return v;
+}
+
+// Device CSR <-> host CSR
+void upload_csr(Ctx& c, const amgcu_csr& h, DCsr& d);
+void upload_csr(Ctx& c, const HostCsr& h, DCsr& d);
+HostCsr download_csr(Ctx& c, const DCsr& d);
+void clone_csr(Ctx& c, const DCsr& src, DCsr& dst);
+
+}  // namespace amgcu

@@ -1,0 +1,1165 @@
+// Interpolation on the GPU: pattern fixes, tentative injection, constraint
+// projection, the pattern-masked product A X|_N, and energy minimisation with
+// the CG loop kept entirely on the device (scalars and stop/restart flags live
+// in device memory, so an iteration never waits on the host).
+// Reference: interpolation.hpp, hierarchy.hpp:98-154.
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstring>
+
+#include "interp.cuh"
+#include "small_dense.h"
+
+namespace amgcu {
+
+namespace {
+
+constexpr int kWarp = 32;
+constexpr int kKMax = 8;
+
+__device__ __forceinline__ int32_t lower_bound_i32(const int32_t* a, int32_t lo, int32_t hi, int32_t key) {
+    while (lo < hi) {
+        const int32_t mid = (lo + hi) >> 1;
+        if (a[mid] < key) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// ---------------------------------------------------------------------------------------
+// add_aggregate_entries: insert (i, owner(i), 1.0) where missing
+// ---------------------------------------------------------------------------------------
+__global__ void k_add_agg(int32_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                          const double* __restrict__ va, const int32_t* __restrict__ own,
+                          const int32_t* __restrict__ orp, int32_t* __restrict__ cnt, int32_t* __restrict__ oci,
+                          double* __restrict__ ova) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int32_t g = own[i];
+    const int32_t lo = rp[i], hi = rp[i + 1];
+    const int32_t pos = lower_bound_i32(ci, lo, hi, g);
+    const bool present = pos < hi && ci[pos] == g;
+    if (!orp) {
+        cnt[i] = (hi - lo) + (present ? 0 : 1);
+        return;
+    }
+    int32_t o = orp[i];
+    for (int32_t p = lo; p < hi; ++p) {
+        if (!present && p == pos) {
+            oci[o] = g;
+            ova[o] = 1.0;
+            ++o;
+        }
+        oci[o] = ci[p];
+        ova[o] = va[p];
+        ++o;
+    }
+    if (!present && pos == hi) {
+        oci[o] = g;
+        ova[o] = 1.0;
+    }
+}
+
+__global__ void k_any_missing(int32_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                              const int32_t* __restrict__ own, int32_t* __restrict__ flag) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int32_t pos = lower_bound_i32(ci, rp[i], rp[i + 1], own[i]);
+    if (!(pos < rp[i + 1] && ci[pos] == own[i])) atomicExch(flag, 1);
+}
+
+// ---------------------------------------------------------------------------------------
+// ensure_min_support (no Bc): re-add the largest dropped magnitudes (descending,
+// ties by position) until the row holds min(min_cols, |full row|) entries.
+// ---------------------------------------------------------------------------------------
+__global__ void k_min_support(int32_t n, const int32_t* __restrict__ frp, const int32_t* __restrict__ fci,
+                              const double* __restrict__ fva, const int32_t* __restrict__ grp,
+                              const int32_t* __restrict__ gci, const double* __restrict__ gva, int32_t min_cols,
+                              const int32_t* __restrict__ orp, int32_t* __restrict__ cnt, int32_t* __restrict__ oci,
+                              double* __restrict__ ova) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int32_t flo = frp[i], fhi = frp[i + 1], glo = grp[i], ghi = grp[i + 1];
+    const int32_t have = fhi - flo;
+    const int32_t target = min(min_cols, ghi - glo);
+    // candidate q (in full row) is chosen if its descending rank among candidates < need
+    const int32_t need = have >= target ? 0 : target - have;
+    auto is_candidate = [&](int32_t q) {
+        const int32_t pos = lower_bound_i32(fci, flo, fhi, gci[q]);
+        return !(pos < fhi && fci[pos] == gci[q]) && gva[q] != 0.0;
+    };
+    auto chosen = [&](int32_t q) {
+        if (need == 0 || !is_candidate(q)) return false;
+        const double m = fabs(gva[q]);
+        int32_t rank = 0;
+        for (int32_t r = glo; r < ghi; ++r) {
+            if (r == q || !is_candidate(r)) continue;
+            const double o = fabs(gva[r]);
+            rank += (o > m || (o == m && r < q)) ? 1 : 0;
+        }
+        return rank < need;
+    };
+    if (!orp) {
+        int32_t add = 0;
+        for (int32_t q = glo; q < ghi; ++q) add += chosen(q) ? 1 : 0;
+        cnt[i] = have + add;
+        return;
+    }
+    // merge filtered row with chosen entries, ascending column
+    int32_t o = orp[i], p = flo;
+    for (int32_t q = glo; q < ghi; ++q) {
+        if (!chosen(q)) continue;
+        while (p < fhi && fci[p] < gci[q]) {
+            oci[o] = fci[p];
+            ova[o] = fva[p];
+            ++o;
+            ++p;
+        }
+        oci[o] = gci[q];
+        ova[o] = gva[q];
+        ++o;
+    }
+    for (; p < fhi; ++p) {
+        oci[o] = fci[p];
+        ova[o] = fva[p];
+        ++o;
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// widen_deficient_rows: block per deficient row, whole-level BFS over S and S^T
+// ---------------------------------------------------------------------------------------
+constexpr int kWidenThreads = 256;
+constexpr int kWidenAggCap = 1024;
+
+__global__ void k_deficient(int32_t n, const int32_t* __restrict__ rp, int32_t min_aggs, int32_t* __restrict__ list,
+                            int32_t* __restrict__ count) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n && rp[i + 1] - rp[i] < min_aggs) list[atomicAdd(count, 1)] = i;
+}
+
+__global__ void __launch_bounds__(kWidenThreads)
+    k_widen(const int32_t* __restrict__ rows, int32_t nn, const int32_t* __restrict__ nrp, const int32_t* __restrict__ nci,
+            const int32_t* __restrict__ srp, const int32_t* __restrict__ sci, const int32_t* __restrict__ trp,
+            const int32_t* __restrict__ tci, const int32_t* __restrict__ own, int32_t min_aggs,
+            int32_t* __restrict__ gseen, int32_t* __restrict__ gfront, int32_t* __restrict__ xcols,
+            int32_t* __restrict__ xcnt, int32_t* __restrict__ xbase, int32_t b0, int32_t* __restrict__ err) {
+    const int32_t i = rows[blockIdx.x];
+    int32_t* seen = gseen + static_cast<int64_t>(blockIdx.x) * nn;
+    int32_t* fa = gfront + static_cast<int64_t>(blockIdx.x) * 2 * nn;
+    int32_t* fb = fa + nn;
+    __shared__ int32_t aggs[kWidenAggCap];
+    __shared__ int32_t naggs, nfront, nnext;
+    for (int32_t t = threadIdx.x; t < nn; t += blockDim.x) seen[t] = 0;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        naggs = 0;
+        for (int32_t p = nrp[i]; p < nrp[i + 1] && naggs < kWidenAggCap; ++p) aggs[naggs++] = nci[p];
+        seen[i] = 1;
+        fa[0] = i;
+        nfront = 1;
+    }
+    __syncthreads();
+    while (nfront > 0 && naggs < min_aggs) {
+        if (threadIdx.x == 0) nnext = 0;
+        __syncthreads();
+        for (int32_t f = 0; f < nfront; ++f) {
+            const int32_t u = fa[f];
+            for (int pass = 0; pass < 2; ++pass) {
+                const int32_t* rp = pass ? trp : srp;
+                const int32_t* cj = pass ? tci : sci;
+                for (int32_t p = rp[u] + threadIdx.x; p < rp[u + 1]; p += blockDim.x) {
+                    const int32_t j = cj[p];
+                    if (atomicCAS(&seen[j], 0, 1) != 0) continue;
+                    fb[atomicAdd(&nnext, 1)] = j;
+                    const int32_t at = atomicAdd(&naggs, 1);  // duplicates removed below
+                    if (at < kWidenAggCap) aggs[at] = own[j];
+                    else atomicExch(err, 1);
+                }
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            int32_t w = 0;
+            const int32_t m0 = min(naggs, kWidenAggCap);
+            for (int32_t t = 0; t < m0; ++t) {
+                bool dup = false;
+                for (int32_t u2 = 0; u2 < w; ++u2)
+                    if (aggs[u2] == aggs[t]) {
+                        dup = true;
+                        break;
+                    }
+                if (!dup) aggs[w++] = aggs[t];
+            }
+            naggs = w;
+            nfront = nnext;
+        }
+        __syncthreads();
+        int32_t* tmp = fa;
+        fa = fb;
+        fb = tmp;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const int32_t base = (b0 + blockIdx.x) * kWidenAggCap;
+        int32_t cnt = 0;
+        for (int32_t t = 0; t < naggs; ++t) {
+            const int32_t g = aggs[t];
+            const int32_t pos = lower_bound_i32(nci, nrp[i], nrp[i + 1], g);
+            if (pos < nrp[i + 1] && nci[pos] == g) continue;
+            // insertion keeps the extras of the row ascending
+            int32_t q = cnt++;
+            while (q > 0 && xcols[base + q - 1] > g) {
+                xcols[base + q] = xcols[base + q - 1];
+                --q;
+            }
+            xcols[base + q] = g;
+        }
+        xcnt[i] = cnt;
+        xbase[i] = base;
+    }
+}
+
+// N plus the extra (col, 1.0) entries of the widened rows, merged ascending
+__global__ void k_widen_merge(int32_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                              const double* __restrict__ va, const int32_t* __restrict__ xcols,
+                              const int32_t* __restrict__ xcnt, const int32_t* __restrict__ xbase,
+                              const int32_t* __restrict__ orp, int32_t* __restrict__ cnt, int32_t* __restrict__ oci,
+                              double* __restrict__ ova) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int32_t ne = xcnt[i];
+    if (!orp) {
+        cnt[i] = rp[i + 1] - rp[i] + ne;
+        return;
+    }
+    int32_t o = orp[i], p = rp[i], e = 0;
+    const int32_t* x = xcols + (ne ? xbase[i] : 0);
+    while (p < rp[i + 1] || e < ne) {
+        if (e < ne && (p == rp[i + 1] || x[e] < ci[p])) {
+            oci[o] = x[e];
+            ova[o] = 1.0;
+            ++e;
+        } else {
+            oci[o] = ci[p];
+            ova[o] = va[p];
+            ++p;
+        }
+        ++o;
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// unamalgamate (m > 1) and root_node_pattern
+// ---------------------------------------------------------------------------------------
+__global__ void k_unamalg_rp(int32_t nn, int32_t m, const int32_t* __restrict__ rp, int32_t* __restrict__ cnt) {
+    const int32_t d = blockIdx.x * blockDim.x + threadIdx.x;
+    if (d >= nn * m) return;
+    const int32_t i = d / m;
+    cnt[d] = (rp[i + 1] - rp[i]) * m;
+}
+
+__global__ void k_unamalg(int32_t nn, int32_t m, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                          const double* __restrict__ va, const int32_t* __restrict__ drp, int32_t* __restrict__ dci,
+                          double* __restrict__ dva) {
+    const int32_t d = blockIdx.x * blockDim.x + threadIdx.x;
+    if (d >= nn * m) return;
+    const int32_t i = d / m;
+    int32_t o = drp[d];
+    for (int32_t p = rp[i]; p < rp[i + 1]; ++p)
+        for (int32_t c = 0; c < m; ++c) {
+            dci[o] = ci[p] * m + c;
+            dva[o] = va[p];
+            ++o;
+        }
+}
+
+__global__ void k_droots(int32_t na, int32_t m, const int32_t* __restrict__ roots, int32_t* __restrict__ dr) {
+    const int32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= na) return;
+    for (int32_t c = 0; c < m; ++c) dr[g * m + c] = roots[g] * m + c;
+}
+
+__global__ void k_owner_of_root(int32_t nroots, const int32_t* __restrict__ roots, int32_t* __restrict__ owner,
+                                int32_t nrows, int32_t* __restrict__ err) {
+    const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= nroots) return;
+    const int32_t r = roots[j];
+    if (r < 0 || r >= nrows) {
+        atomicExch(err, 1);
+        return;
+    }
+    if (atomicCAS(&owner[r], -1, j) != -1) atomicExch(err, 2);
+}
+
+__global__ void k_rootpat(int32_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                          const double* __restrict__ va, const int32_t* __restrict__ owner,
+                          const int32_t* __restrict__ orp, int32_t* __restrict__ cnt, int32_t* __restrict__ oci,
+                          double* __restrict__ ova) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int32_t ow = owner[i];
+    if (!orp) {
+        cnt[i] = ow >= 0 ? 1 : rp[i + 1] - rp[i];
+        return;
+    }
+    int32_t o = orp[i];
+    if (ow >= 0) {
+        oci[o] = ow;
+        ova[o] = 1.0;
+        return;
+    }
+    for (int32_t p = rp[i]; p < rp[i + 1]; ++p) {
+        oci[o] = ci[p];
+        ova[o] = va[p];
+        ++o;
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// inject_tentative
+// ---------------------------------------------------------------------------------------
+__global__ void k_root_blocks(int32_t na, int32_t m, int32_t k, int32_t ndof, const int32_t* __restrict__ roots,
+                              const double* __restrict__ B, double* __restrict__ binv, double* __restrict__ Bc,
+                              int32_t nc, int32_t* __restrict__ degenerate) {
+    const int32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= na) return;
+    const int32_t root = roots[g];
+    double blk[64];
+    double mx = 0.0;
+    for (int r = 0; r < m; ++r)
+        for (int cc = 0; cc < m; ++cc) {
+            const double v = B[static_cast<size_t>(cc) * ndof + root * m + r];
+            blk[r * m + cc] = v;
+            const double a = fabs(v);
+            mx = (r == 0 && cc == 0) ? a : (mx < a ? a : mx);
+        }
+    sd::FullPivLU<8> lu;
+    lu.compute(m, blk);
+    const double scale_cut = 1e-10 * sd::dmax(mx, 1e-300);
+    double cut = 1.0;
+    for (int t = 0; t < m; ++t) cut *= scale_cut;  // pow(scale_cut, m)
+    if (m == 1) cut = scale_cut;
+    double* inv = binv + static_cast<size_t>(g) * m * m;
+    if (lu.rank() == m && mx > 0 && fabs(lu.determinant()) > cut) {
+        lu.inverse(inv);
+    } else if (m == 1) {
+        inv[0] = 0.0;  // COD pseudo-inverse of the zero 1x1 block
+    } else {
+        atomicAdd(degenerate, 1);
+        for (int t = 0; t < m * m; ++t) inv[t] = nan("");
+    }
+    for (int cc = 0; cc < m; ++cc)
+        for (int a = 0; a < k; ++a)
+            Bc[static_cast<size_t>(a) * nc + g * m + cc] = B[static_cast<size_t>(a) * ndof + root * m + cc];
+}
+
+__global__ void k_tentative_rows(int32_t nn, int32_t m, const int32_t* __restrict__ own,
+                                 const int32_t* __restrict__ roots, const double* __restrict__ B, int32_t ndof,
+                                 const double* __restrict__ binv, const int32_t* __restrict__ orp,
+                                 int32_t* __restrict__ cnt, int32_t* __restrict__ oci, double* __restrict__ ova) {
+    const int32_t d = blockIdx.x * blockDim.x + threadIdx.x;
+    if (d >= nn * m) return;
+    const int32_t i = d / m, r = d - i * m;
+    const int32_t g = own[i];
+    const bool is_root = roots[g] == i;
+    int32_t o = orp ? orp[d] : 0;
+    if (is_root) {
+        if (orp) {
+            oci[o] = g * m + r;
+            ova[o] = 1.0;
+        }
+        ++o;
+    } else {
+        const double* inv = binv + static_cast<size_t>(g) * m * m;
+        for (int32_t cc = 0; cc < m; ++cc) {
+            double v = 0.0;
+            for (int32_t s = 0; s < m; ++s) v += B[static_cast<size_t>(s) * ndof + d] * inv[s * m + cc];
+            if (v != 0.0) {
+                if (orp) {
+                    oci[o] = g * m + cc;
+                    ova[o] = v;
+                }
+                ++o;
+            }
+        }
+    }
+    if (!orp) cnt[d] = o;
+}
+
+// ---------------------------------------------------------------------------------------
+// scatter_into_pattern (interpolation.hpp:213-227)
+// ---------------------------------------------------------------------------------------
+__global__ void k_scatter_pattern(int32_t n, const int32_t* __restrict__ trp, const int32_t* __restrict__ tci,
+                                  const double* __restrict__ tva, const int32_t* __restrict__ nrp,
+                                  const int32_t* __restrict__ nci, double* __restrict__ vals, int32_t* __restrict__ err) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    for (int32_t p = nrp[i]; p < nrp[i + 1]; ++p) vals[p] = 0.0;
+    for (int32_t p = trp[i]; p < trp[i + 1]; ++p) {
+        const int32_t pos = lower_bound_i32(nci, nrp[i], nrp[i + 1], tci[p]);
+        if (pos == nrp[i + 1] || nci[pos] != tci[p]) {
+            atomicExch(err, 1);
+            return;
+        }
+        vals[pos] = tva[p];
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// enforce_constraints, thread per row (interpolation.hpp:467-518)
+// ---------------------------------------------------------------------------------------
+__global__ void k_enforce(int32_t n, int32_t k, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                          double* __restrict__ vals, const double* __restrict__ B, const double* __restrict__ Bc,
+                          int32_t nc) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int32_t lo = rp[i], hi = rp[i + 1];
+    if (lo == hi) return;
+    double G[kKMax * kKMax], y[kKMax], ev[kKMax], V[kKMax * kKMax], proj[kKMax], lv[kKMax];
+    for (int t = 0; t < k * k; ++t) G[t] = 0.0;
+    for (int a = 0; a < k; ++a) y[a] = 0.0;
+    for (int32_t p = lo; p < hi; ++p) {
+        const int32_t j = ci[p];
+        for (int a = 0; a < k; ++a) {
+            const double ba = Bc[static_cast<size_t>(a) * nc + j];
+            y[a] += ba * vals[p];
+            for (int b = a; b < k; ++b) G[a * k + b] += ba * Bc[static_cast<size_t>(b) * nc + j];
+        }
+    }
+    for (int a = 0; a < k; ++a)
+        for (int b = 0; b < a; ++b) G[a * k + b] = G[b * k + a];
+    for (int a = 0; a < k; ++a) y[a] = B[static_cast<size_t>(a) * n + i] - y[a];
+    sd::sym_eig<kKMax>(k, G, ev, V);
+    double mx = fabs(ev[0]);
+    for (int a = 0; a < k; ++a) mx = sd::dmax(mx, fabs(ev[a]));
+    const double cutoff = 1e-12 * sd::dmax(mx, 1e-300);
+    for (int t = 0; t < k; ++t) {
+        double s = 0.0;
+        for (int a = 0; a < k; ++a) s += V[a * k + t] * y[a];
+        proj[t] = s;
+    }
+    for (int a = 0; a < k; ++a) proj[a] = ev[a] > cutoff ? proj[a] / ev[a] : 0.0;
+    for (int a = 0; a < k; ++a) {
+        double s = 0.0;
+        for (int t = 0; t < k; ++t) s += V[a * k + t] * proj[t];
+        lv[a] = s;
+    }
+    for (int32_t p = lo; p < hi; ++p) {
+        double s = 0.0;
+        for (int a = 0; a < k; ++a) s += Bc[static_cast<size_t>(a) * nc + ci[p]] * lv[a];
+        vals[p] += s;
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// ConstraintWorkspace::build (interpolation.hpp:113-141): Gp per non-root row
+// ---------------------------------------------------------------------------------------
+__global__ void k_gram_pinv(int32_t n, int32_t k, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                            const double* __restrict__ Bc, int32_t nc, const unsigned char* __restrict__ is_root,
+                            double* __restrict__ gp) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double* out = gp + static_cast<size_t>(i) * k * k;
+    if (is_root[i]) {
+        for (int t = 0; t < k * k; ++t) out[t] = 0.0;
+        return;
+    }
+    double G[kKMax * kKMax];
+    for (int t = 0; t < k * k; ++t) G[t] = 0.0;
+    for (int32_t p = rp[i]; p < rp[i + 1]; ++p) {
+        const int32_t j = ci[p];
+        for (int a = 0; a < k; ++a)
+            for (int b = a; b < k; ++b)
+                G[a * k + b] += Bc[static_cast<size_t>(a) * nc + j] * Bc[static_cast<size_t>(b) * nc + j];
+    }
+    for (int a = 0; a < k; ++a)
+        for (int b = 0; b < a; ++b) G[a * k + b] = G[b * k + a];
+    sd::sym_pinv<kKMax>(k, G, out);
+}
+
+__global__ void k_root_mask(int32_t nroots, const int32_t* __restrict__ roots, unsigned char* __restrict__ mask) {
+    const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < nroots) mask[roots[j]] = 1;
+}
+
+// ---------------------------------------------------------------------------------------
+// Masked product Y = (A X)|_N (interpolation.hpp:186-210) with the constraint
+// projection (150-182) fused: warp per row, lane per pattern slot.  Each slot
+// accumulates over A's row in CSR order, looking its column up in N's row t.
+// Y (unprojected) and Yp (projected) are written when the pointer is non-null.
+// ---------------------------------------------------------------------------------------
+constexpr int kMpWarps = 4;
+constexpr int kMpSlots = 4;  // slots per lane per chunk -> 128 slots per chunk
+
+__device__ __forceinline__ void masked_row(int32_t i, int lane, const int32_t* __restrict__ arp,
+                                           const int32_t* __restrict__ aci, const double* __restrict__ ava,
+                                           const int32_t* __restrict__ nrp, const int32_t* __restrict__ nci,
+                                           const double* __restrict__ x, int32_t c0, int32_t L, double* acc,
+                                           int32_t* col) {
+    const int32_t lo = nrp[i];
+#pragma unroll
+    for (int s = 0; s < kMpSlots; ++s) {
+        const int32_t e = c0 + s * kWarp + lane;
+        acc[s] = 0.0;
+        col[s] = e < L ? nci[lo + e] : -1;
+    }
+    for (int32_t p = arp[i]; p < arp[i + 1]; ++p) {
+        const int32_t t = aci[p];
+        const double a = ava[p];
+        const int32_t tlo = nrp[t], thi = nrp[t + 1];
+#pragma unroll
+        for (int s = 0; s < kMpSlots; ++s) {
+            if (col[s] < 0) continue;
+            const int32_t q = lower_bound_i32(nci, tlo, thi, col[s]);
+            if (q < thi && nci[q] == col[s]) acc[s] += a * x[q];
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kMpWarps * kWarp)
+    k_masked_project(int32_t n, const int32_t* __restrict__ arp, const int32_t* __restrict__ aci,
+                     const double* __restrict__ ava, const int32_t* __restrict__ nrp, const int32_t* __restrict__ nci,
+                     const double* __restrict__ x, int32_t k, const double* __restrict__ Bc, int32_t nc,
+                     const double* __restrict__ gp, const unsigned char* __restrict__ is_root, double* __restrict__ y,
+                     double* __restrict__ yp, const int32_t* __restrict__ stop) {
+    if (stop && *stop) return;
+    const int w = threadIdx.x / kWarp, lane = threadIdx.x & (kWarp - 1);
+    const int32_t i = blockIdx.x * kMpWarps + w;
+    if (i >= n) return;
+    const int32_t lo = nrp[i], L = nrp[i + 1] - lo;
+    if (L == 0) return;
+    const bool root = yp && is_root[i];
+    const int32_t chunk = kMpSlots * kWarp;
+    if (L <= chunk) {
+        double acc[kMpSlots];
+        int32_t col[kMpSlots];
+        masked_row(i, lane, arp, aci, ava, nrp, nci, x, 0, L, acc, col);
+        if (y) {
+#pragma unroll
+            for (int s = 0; s < kMpSlots; ++s)
+                if (col[s] >= 0) y[lo + s * kWarp + lane] = acc[s];
+        }
+        if (!yp) return;
+        if (root) {
+#pragma unroll
+            for (int s = 0; s < kMpSlots; ++s)
+                if (col[s] >= 0) yp[lo + s * kWarp + lane] = 0.0;
+            return;
+        }
+        // y_a = sum_p Bc(col_p, a) * acc_p in slot order (sequential, warp-uniform)
+        double ya[kKMax];
+        for (int a = 0; a < k; ++a) ya[a] = 0.0;
+        for (int32_t e = 0; e < L; ++e) {
+            const int s = e / kWarp, src = e % kWarp;
+            double v = 0.0;
+            int32_t cj = 0;
+#pragma unroll
+            for (int ss = 0; ss < kMpSlots; ++ss)
+                if (ss == s) {
+                    v = __shfl_sync(0xffffffffu, acc[ss], src);
+                    cj = __shfl_sync(0xffffffffu, col[ss], src);
+                }
+            for (int a = 0; a < k; ++a) ya[a] += Bc[static_cast<size_t>(a) * nc + cj] * v;
+        }
+        const double* G = gp + static_cast<size_t>(i) * k * k;
+        double lam[kKMax];
+        for (int a = 0; a < k; ++a) {
+            double s = 0.0;
+            for (int b = 0; b < k; ++b) s += G[a * k + b] * ya[b];
+            lam[a] = s;
+        }
+#pragma unroll
+        for (int s = 0; s < kMpSlots; ++s) {
+            if (col[s] < 0) continue;
+            double t = 0.0;
+            for (int a = 0; a < k; ++a) t += Bc[static_cast<size_t>(a) * nc + col[s]] * lam[a];
+            yp[lo + s * kWarp + lane] = acc[s] - t;
+        }
+        return;
+    }
+    // long rows: chunked; Y is written first (into y, or yp as scratch), then projected
+    double* dst = y ? y : yp;
+    for (int32_t c0 = 0; c0 < L; c0 += chunk) {
+        double acc[kMpSlots];
+        int32_t col[kMpSlots];
+        masked_row(i, lane, arp, aci, ava, nrp, nci, x, c0, L, acc, col);
+#pragma unroll
+        for (int s = 0; s < kMpSlots; ++s)
+            if (col[s] >= 0) dst[lo + c0 + s * kWarp + lane] = acc[s];
+    }
+    __syncwarp();
+    if (!yp) return;
+    if (root) {
+        for (int32_t e = lane; e < L; e += kWarp) yp[lo + e] = 0.0;
+        return;
+    }
+    double ya[kKMax];
+    for (int a = 0; a < k; ++a) ya[a] = 0.0;
+    for (int32_t e = 0; e < L; ++e) {
+        const double v = dst[lo + e];
+        const int32_t cj = nci[lo + e];
+        for (int a = 0; a < k; ++a) ya[a] += Bc[static_cast<size_t>(a) * nc + cj] * v;
+    }
+    const double* G = gp + static_cast<size_t>(i) * k * k;
+    double lam[kKMax];
+    for (int a = 0; a < k; ++a) {
+        double s = 0.0;
+        for (int b = 0; b < k; ++b) s += G[a * k + b] * ya[b];
+        lam[a] = s;
+    }
+    __syncwarp();
+    for (int32_t e = lane; e < L; e += kWarp) {
+        double t = 0.0;
+        for (int a = 0; a < k; ++a) t += Bc[static_cast<size_t>(a) * nc + nci[lo + e]] * lam[a];
+        yp[lo + e] = dst[lo + e] - t;
+    }
+}
+
+// in-place projection of vals (project_to_constraints)
+__global__ void k_project(int32_t n, const int32_t* __restrict__ nrp, const int32_t* __restrict__ nci, int32_t k,
+                          const double* __restrict__ Bc, int32_t nc, const double* __restrict__ gp,
+                          const unsigned char* __restrict__ is_root, double* __restrict__ vals) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int32_t lo = nrp[i], hi = nrp[i + 1];
+    if (is_root[i]) {
+        for (int32_t p = lo; p < hi; ++p) vals[p] = 0.0;
+        return;
+    }
+    double ya[kKMax], lam[kKMax];
+    for (int a = 0; a < k; ++a) ya[a] = 0.0;
+    for (int32_t p = lo; p < hi; ++p)
+        for (int a = 0; a < k; ++a) ya[a] += Bc[static_cast<size_t>(a) * nc + nci[p]] * vals[p];
+    const double* G = gp + static_cast<size_t>(i) * k * k;
+    for (int a = 0; a < k; ++a) {
+        double s = 0.0;
+        for (int b = 0; b < k; ++b) s += G[a * k + b] * ya[b];
+        lam[a] = s;
+    }
+    for (int32_t p = lo; p < hi; ++p) {
+        double s = 0.0;
+        for (int a = 0; a < k; ++a) s += Bc[static_cast<size_t>(a) * nc + nci[p]] * lam[a];
+        vals[p] -= s;
+    }
+}
+
+__global__ void k_negate(int64_t n, const double* __restrict__ x, double* __restrict__ y) {
+    const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (p < n) y[p] = -x[p];
+}
+
+// ---------------------------------------------------------------------------------------
+// CG (interpolation.hpp:298-361) with device-side control
+//   st[0] newsum  st[1] oldsum  st[2] first  st[3] denom  st[4] alpha_cg
+//   st[5] alpha   st[6] beta    st[7] dot scratch
+//   flags: f[0] stop  f[1] restart  f[2] iterations  f[3] breakdown
+// ---------------------------------------------------------------------------------------
+__global__ void k_cg_z(int64_t nz, const int32_t* __restrict__ prow, const double* __restrict__ dinv,
+                       const double* __restrict__ R, double* __restrict__ Z, const int32_t* __restrict__ f) {
+    if (f[0]) return;
+    const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (p < nz) Z[p] = dinv[prow[p]] * R[p];
+}
+
+__global__ void k_cg_ctl_newsum(double* __restrict__ st, int32_t* __restrict__ f) {
+    if (f[0]) return;
+    const double newsum = st[7];
+    st[0] = newsum;
+    if (st[2] < 0.0) st[2] = newsum;
+    if (!(newsum > 1e-28 * sd::dmax(st[2], 1.0))) {
+        f[0] = 1;
+        return;
+    }
+    if (!f[1]) st[6] = newsum / st[1];
+}
+
+__global__ void k_cg_dir(int64_t nz, const double* __restrict__ Z, double* __restrict__ D,
+                         const double* __restrict__ st, const int32_t* __restrict__ f) {
+    if (f[0]) return;
+    const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (p >= nz) return;
+    if (f[1]) D[p] = Z[p];
+    else D[p] = Z[p] + st[6] * D[p];
+}
+
+__global__ void k_cg_ctl_denom(double* __restrict__ st, int32_t* __restrict__ f,
+                               unsigned long long* __restrict__ alpha_bits) {
+    if (f[0]) return;
+    const double denom = st[7];
+    st[3] = denom;
+    if (!(denom > 0.0)) {
+        f[0] = 1;
+        return;
+    }
+    st[4] = st[0] / denom;
+    *alpha_bits = static_cast<unsigned long long>(__double_as_longlong(st[4]));
+}
+
+// per column j, entries in increasing row order (CSC positions): e, g, h and the
+// safe step (column_safe_step, interpolation.hpp:247-260), min-reduced into alpha_bits
+__global__ void k_cg_columns(int32_t nc, const int32_t* __restrict__ colptr, const int32_t* __restrict__ pos,
+                             const double* __restrict__ P, const double* __restrict__ APm, const double* __restrict__ D,
+                             const double* __restrict__ ADm, unsigned long long* __restrict__ alpha_bits,
+                             const int32_t* __restrict__ f) {
+    if (f[0]) return;
+    const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= nc) return;
+    double e = 0.0, g = 0.0, h = 0.0;
+    for (int32_t q = colptr[j]; q < colptr[j + 1]; ++q) {
+        const int32_t p = pos[q];
+        e += P[p] * APm[p];
+        g += D[p] * APm[p];
+        h += D[p] * ADm[p];
+    }
+    if (h <= 0.0) return;
+    const double norm_j = sqrt(sd::dmax(e, 0.0));
+    const double tol = 2.5e-13 * sd::dmax(norm_j, 1.0e-30);
+    const double budget = tol * (2.0 * norm_j + tol);
+    const double disc = g * g + h * budget;
+    const double beta = (-g + sqrt(sd::dmax(disc, 0.0))) / h;
+    if (beta >= 0.0)  // all finite steps are >= 0; NaN never wins (std::min semantics)
+        atomicMin(alpha_bits, static_cast<unsigned long long>(__double_as_longlong(beta)));
+}
+
+__global__ void k_cg_ctl_alpha(double* __restrict__ st, int32_t* __restrict__ f,
+                               const unsigned long long* __restrict__ alpha_bits, int s) {
+    if (f[0]) return;
+    const double alpha = __longlong_as_double(static_cast<long long>(*alpha_bits));
+    const double alpha_cg = st[4];
+    st[5] = alpha;
+    if (!(alpha > 1e-14 * alpha_cg)) {
+        f[3] = 1;
+        f[0] = 1;
+        return;
+    }
+    f[1] = alpha < alpha_cg * (1.0 - 1e-12) ? 1 : 0;
+    st[1] = st[0];
+    f[2] = s + 1;
+}
+
+__global__ void k_cg_update(int64_t nz, double* __restrict__ P, double* __restrict__ APm, double* __restrict__ R,
+                            const double* __restrict__ D, const double* __restrict__ ADm,
+                            const double* __restrict__ ADp, const double* __restrict__ st,
+                            const int32_t* __restrict__ f, int s) {
+    if (f[3] || f[2] != s + 1) return;  // only when iteration s completed its step
+    const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (p >= nz) return;
+    const double alpha = st[5];
+    P[p] += alpha * D[p];
+    APm[p] += alpha * ADm[p];
+    R[p] -= alpha * ADp[p];
+}
+
+// ---------------------------------------------------------------------------------------
+// GMRES clipping sums (interpolation.hpp:417-435): per column j over AT / AU entries
+// in increasing row order
+// ---------------------------------------------------------------------------------------
+__global__ void k_gm_columns(int32_t nc, const int32_t* __restrict__ tcp, const int32_t* __restrict__ tpos,
+                             const double* __restrict__ atv, const int32_t* __restrict__ ucp,
+                             const int32_t* __restrict__ upos, const int32_t* __restrict__ urow,
+                             const double* __restrict__ auv, const int32_t* __restrict__ atrp,
+                             const int32_t* __restrict__ atci, double* __restrict__ e, double* __restrict__ g,
+                             double* __restrict__ h) {
+    const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= nc) return;
+    double ej = 0.0, gj = 0.0, hj = 0.0;
+    for (int32_t q = tcp[j]; q < tcp[j + 1]; ++q) {
+        const double v = atv[tpos[q]];
+        ej += v * v;
+    }
+    for (int32_t q = ucp[j]; q < ucp[j + 1]; ++q) {
+        const int32_t p = upos[q];
+        const double v = auv[p];
+        hj += v * v;
+        const int32_t i = urow[p];
+        const int32_t at = lower_bound_i32(atci, atrp[i], atrp[i + 1], j);
+        if (at < atrp[i + 1] && atci[at] == j) gj += v * atv[at];
+    }
+    e[j] = ej;
+    g[j] = gj;
+    h[j] = hj;
+}
+
+__global__ void k_axpy_host(int64_t n, double a, const double* __restrict__ x, double* __restrict__ y) {
+    const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (p < n) y[p] += a * x[p];
+}
+
+// two-pass helper for row kernels with (..., orp, cnt, oci, ova) tails
+template <typename K, typename... Args>
+void build_rows(Ctx& c, int32_t nr, int32_t nc, int32_t bs, DCsr& out, K k, unsigned grid, unsigned block,
+                Args... args) {
+    DBuf<int32_t> cnt(static_cast<size_t>(nr) + 1, c.s);
+    launch(c, k, grid, block, 0, args..., static_cast<const int32_t*>(nullptr), cnt.get(),
+           static_cast<int32_t*>(nullptr), static_cast<double*>(nullptr));
+    out.nr = nr;
+    out.nc = nc;
+    out.bs = bs;
+    out.rp.alloc(static_cast<size_t>(nr) + 1, c.s);
+    out.nnz = exclusive_scan_i32(c, cnt.get(), out.rp.get(), nr);
+    out.ci.alloc(static_cast<size_t>(out.nnz), c.s);
+    out.va.alloc(static_cast<size_t>(out.nnz), c.s);
+    launch(c, k, grid, block, 0, args..., static_cast<const int32_t*>(out.rp.get()), cnt.get(), out.ci.get(),
+           out.va.get());
+}
+
+}  // namespace
+
+void add_aggregate_entries(Ctx& c, const DCsr& N, const DAgg& agg, DCsr& out) {
+    DBuf<int32_t> flag(1, c.s);
+    AMG_CK(cudaMemsetAsync(flag.get(), 0, sizeof(int32_t), c.s));
+    launch(c, k_any_missing, blocks_for(N.nr, 256), 256, 0, N.nr, N.rp.get(), N.ci.get(), agg.owner.get(), flag.get());
+    if (!read_scalar(c, flag.get())) {
+        clone_csr(c, N, out);
+        return;
+    }
+    build_rows(c, N.nr, N.nc, 1, out, k_add_agg, blocks_for(N.nr, 128), 128, N.nr, N.rp.get(), N.ci.get(), N.va.get(),
+               static_cast<const int32_t*>(agg.owner.get()));
+}
+
+void ensure_min_support(Ctx& c, const DCsr& filtered, const DCsr& full, int32_t min_cols, DCsr& out) {
+    if (filtered.nr != full.nr || filtered.nc != full.nc) throw InvalidArgument("ensure_min_support: shape mismatch");
+    build_rows(c, filtered.nr, filtered.nc, filtered.bs, out, k_min_support, blocks_for(filtered.nr, 128), 128,
+               filtered.nr, filtered.rp.get(), filtered.ci.get(), filtered.va.get(), full.rp.get(), full.ci.get(),
+               full.va.get(), min_cols);
+}
+
+void widen_deficient_rows(Ctx& c, const DCsr& N, const DCsr& S, const DAgg& agg, int32_t min_aggs, DCsr& out) {
+    if (min_aggs <= 1) {
+        clone_csr(c, N, out);
+        return;
+    }
+    const int32_t n = N.nr;
+    DBuf<int32_t> list(static_cast<size_t>(n), c.s), count(1, c.s);
+    AMG_CK(cudaMemsetAsync(count.get(), 0, sizeof(int32_t), c.s));
+    launch(c, k_deficient, blocks_for(n, 256), 256, 0, n, N.rp.get(), min_aggs, list.get(), count.get());
+    const int32_t nd = read_scalar(c, count.get());
+    if (nd == 0) {
+        clone_csr(c, N, out);
+        return;
+    }
+    DCsr St;
+    transpose(c, S, St);
+    const int32_t conc = std::min<int32_t>(nd, 32);
+    DBuf<int32_t> seen(static_cast<size_t>(conc) * S.nr, c.s), front(static_cast<size_t>(conc) * 2 * S.nr, c.s);
+    DBuf<int32_t> xcols(static_cast<size_t>(nd) * kWidenAggCap, c.s), xcnt(static_cast<size_t>(n), c.s),
+        xbase(static_cast<size_t>(n), c.s), err(1, c.s);
+    AMG_CK(cudaMemsetAsync(xcnt.get(), 0, sizeof(int32_t) * n, c.s));
+    AMG_CK(cudaMemsetAsync(xbase.get(), 0, sizeof(int32_t) * n, c.s));
+    AMG_CK(cudaMemsetAsync(err.get(), 0, sizeof(int32_t), c.s));
+    for (int32_t b0 = 0; b0 < nd; b0 += conc) {
+        const int32_t nb = std::min(conc, nd - b0);
+        launch(c, k_widen, static_cast<unsigned>(nb), kWidenThreads, 0, static_cast<const int32_t*>(list.get() + b0),
+               S.nr, N.rp.get(), N.ci.get(), S.rp.get(), S.ci.get(), St.rp.get(), St.ci.get(), agg.owner.get(),
+               min_aggs, seen.get(), front.get(), xcols.get(), xcnt.get(), xbase.get(), b0, err.get());
+    }
+    if (read_scalar(c, err.get())) throw RuntimeError("widen_deficient_rows: GPU aggregate-set capacity exceeded");
+    build_rows(c, N.nr, N.nc, N.bs, out, k_widen_merge, blocks_for(n, 128), 128, n, N.rp.get(), N.ci.get(),
+               N.va.get(), static_cast<const int32_t*>(xcols.get()), static_cast<const int32_t*>(xcnt.get()),
+               static_cast<const int32_t*>(xbase.get()));
+}
+
+void unamalgamate(Ctx& c, const DCsr& N, const DAgg& agg, int32_t m, DCsr& Nd, DBuf<int32_t>& droots) {
+    if (m < 1) throw InvalidArgument("unamalgamate: block size must be >= 1");
+    droots.alloc(static_cast<size_t>(agg.n_agg) * m, c.s);
+    if (m == 1) {
+        clone_csr(c, N, Nd);
+        copy_d2d(c, droots.get(), agg.roots.get(), agg.n_agg);
+        return;
+    }
+    const int32_t nd = N.nr * m;
+    DBuf<int32_t> cnt(static_cast<size_t>(nd) + 1, c.s);
+    launch(c, k_unamalg_rp, blocks_for(nd, 256), 256, 0, N.nr, m, N.rp.get(), cnt.get());
+    Nd.nr = nd;
+    Nd.nc = N.nc * m;
+    Nd.bs = 1;
+    Nd.rp.alloc(static_cast<size_t>(nd) + 1, c.s);
+    Nd.nnz = exclusive_scan_i32(c, cnt.get(), Nd.rp.get(), nd);
+    Nd.ci.alloc(static_cast<size_t>(Nd.nnz), c.s);
+    Nd.va.alloc(static_cast<size_t>(Nd.nnz), c.s);
+    launch(c, k_unamalg, blocks_for(nd, 256), 256, 0, N.nr, m, N.rp.get(), N.ci.get(), N.va.get(),
+           static_cast<const int32_t*>(Nd.rp.get()), Nd.ci.get(), Nd.va.get());
+    launch(c, k_droots, blocks_for(agg.n_agg, 256), 256, 0, agg.n_agg, m, agg.roots.get(), droots.get());
+}
+
+void root_node_pattern(Ctx& c, const DCsr& N, const int32_t* roots, int32_t n_roots, DCsr& out) {
+    if (n_roots != N.nc) throw InvalidArgument("root_node_pattern: need one root per coarse column");
+    DBuf<int32_t> owner(static_cast<size_t>(N.nr), c.s), err(1, c.s);
+    fill_i32(c, owner.get(), -1, N.nr);
+    AMG_CK(cudaMemsetAsync(err.get(), 0, sizeof(int32_t), c.s));
+    launch(c, k_owner_of_root, blocks_for(n_roots, 256), 256, 0, n_roots, roots, owner.get(), N.nr, err.get());
+    const int32_t e = read_scalar(c, err.get());
+    if (e == 1) throw InvalidArgument("root_node_pattern: root out of range");
+    if (e == 2) throw InvalidArgument("root_node_pattern: duplicate root row");
+    build_rows(c, N.nr, N.nc, N.bs, out, k_rootpat, blocks_for(N.nr, 128), 128, N.nr, N.rp.get(), N.ci.get(),
+               N.va.get(), static_cast<const int32_t*>(owner.get()));
+}
+
+void enforce_constraints(Ctx& c, const DCsr& P, const double* B, const double* Bc, int32_t k, const DCsr* allowed,
+                         DCsr& out) {
+    const DCsr& N = allowed ? *allowed : P;
+    if (P.nr != N.nr || P.nc != N.nc) throw InvalidArgument("enforce_constraints: dimension mismatch");
+    if (k > kKMax) throw InvalidArgument("enforce_constraints: at most 8 candidates on the GPU path");
+    DBuf<double> vals(static_cast<size_t>(N.nnz), c.s);
+    DBuf<int32_t> err(1, c.s);
+    AMG_CK(cudaMemsetAsync(err.get(), 0, sizeof(int32_t), c.s));
+    launch(c, k_scatter_pattern, blocks_for(N.nr, 256), 256, 0, N.nr, P.rp.get(), P.ci.get(), P.va.get(), N.rp.get(),
+           N.ci.get(), vals.get(), err.get());
+    if (read_scalar(c, err.get())) throw InvalidArgument("energy_minimize: T has an entry outside the pattern");
+    launch(c, k_enforce, blocks_for(N.nr, 64), 64, 0, N.nr, k, N.rp.get(), N.ci.get(), vals.get(), B, Bc, N.nc);
+    compact_pattern(c, N, vals.get(), P.bs, out);
+}
+
+void inject_tentative(Ctx& c, const DAgg& agg, const DCsr& N, const double* B, int32_t k, int32_t m, DCsr& T,
+                      DBuf<double>& Bc) {
+    if (m < 1) throw InvalidArgument("inject_tentative: block size must be >= 1");
+    if (k < m) throw InvalidArgument("inject_tentative: need at least m candidates");
+    if (m > 8) throw InvalidArgument("inject_tentative: block size above 8 on the GPU path");
+    const int32_t ndof = agg.n_nodes * m, nc = agg.n_agg * m;
+    if (N.nr != ndof || N.nc != nc) throw InvalidArgument("inject_tentative: pattern dimensions mismatch");
+    Bc.alloc(static_cast<size_t>(nc) * k, c.s);
+    DBuf<double> binv(static_cast<size_t>(agg.n_agg) * m * m, c.s);
+    DBuf<int32_t> degenerate(1, c.s);
+    AMG_CK(cudaMemsetAsync(degenerate.get(), 0, sizeof(int32_t), c.s));
+    launch(c, k_root_blocks, blocks_for(agg.n_agg, 128), 128, 0, agg.n_agg, m, k, ndof, agg.roots.get(), B, binv.get(),
+           Bc.get(), nc, degenerate.get());
+    if (m > 1 && read_scalar(c, degenerate.get()) > 0) {
+        // degenerate m x m root blocks: COD pseudo-inverse (threshold 1e-10) on the host,
+        // interpolation.hpp:550-553 -- rare, tiny
+        std::vector<double> hb(static_cast<size_t>(agg.n_agg) * m * m);
+        copy_d2h(c, hb.data(), binv.get(), static_cast<int64_t>(hb.size()));
+        std::vector<int32_t> hroots(agg.n_agg);
+        copy_d2h(c, hroots.data(), agg.roots.get(), agg.n_agg);
+        std::vector<double> hB(static_cast<size_t>(ndof) * k);
+        copy_d2h(c, hB.data(), B, static_cast<int64_t>(hB.size()));
+        sync(c);
+        for (int32_t g = 0; g < agg.n_agg; ++g) {
+            double* inv = hb.data() + static_cast<size_t>(g) * m * m;
+            if (!std::isnan(inv[0])) continue;
+            std::vector<double> blk(static_cast<size_t>(m) * m);
+            for (int r = 0; r < m; ++r)
+                for (int cc = 0; cc < m; ++cc) blk[r * m + cc] = hB[static_cast<size_t>(cc) * ndof + hroots[g] * m + r];
+            sd::COD cod;
+            cod.threshold = 1e-10;
+            cod.compute(m, m, blk.data());
+            cod.pseudo_inverse(inv);
+        }
+        copy_h2d(c, binv.get(), hb.data(), static_cast<int64_t>(hb.size()));
+        sync(c);
+    }
+    DCsr T0;
+    build_rows(c, ndof, nc, m, T0, k_tentative_rows, blocks_for(ndof, 256), 256, agg.n_nodes, m, agg.owner.get(),
+               agg.roots.get(), B, ndof, static_cast<const double*>(binv.get()));
+    T0.bs = m;
+    if (k > m) {
+        enforce_constraints(c, T0, B, Bc.get(), k, &N, T);
+        T.bs = m;
+    } else {
+        T = std::move(T0);
+    }
+}
+
+void energy_minimize(Ctx& c, const DCsr& A, const DCsr& T, const double* B, const double* Bc, int32_t k,
+                     const DCsr& N, int iters, int krylov, const int32_t* roots, int32_t n_roots, DCsr& Pout,
+                     EnergyMinStats* stats) {
+    (void)B;
+    if (A.nr != A.nc || A.nr != N.nr) throw InvalidArgument("energy_minimize: dimension mismatch");
+    if (k > kKMax) throw InvalidArgument("energy_minimize: at most 8 candidates on the GPU path");
+    const int32_t n = N.nr, nc = N.nc;
+    const int64_t nz = N.nnz;
+    EnergyMinStats local;
+    EnergyMinStats& st = stats ? *stats : local;
+    st = EnergyMinStats{};
+    // constraint workspace
+    DBuf<unsigned char> is_root(static_cast<size_t>(n), c.s);
+    AMG_CK(cudaMemsetAsync(is_root.get(), 0, static_cast<size_t>(n), c.s));
+    launch(c, k_root_mask, blocks_for(n_roots, 256), 256, 0, n_roots, roots, is_root.get());
+    DBuf<double> gp(static_cast<size_t>(n) * k * k, c.s);
+    launch(c, k_gram_pinv, blocks_for(n, 64), 64, 0, n, k, N.rp.get(), N.ci.get(), Bc, nc,
+           static_cast<const unsigned char*>(is_root.get()), gp.get());
+    DBuf<double> P(static_cast<size_t>(nz), c.s);
+    {
+        DBuf<int32_t> err(1, c.s);
+        AMG_CK(cudaMemsetAsync(err.get(), 0, sizeof(int32_t), c.s));
+        launch(c, k_scatter_pattern, blocks_for(n, 256), 256, 0, n, T.rp.get(), T.ci.get(), T.va.get(), N.rp.get(),
+               N.ci.get(), P.get(), err.get());
+        if (read_scalar(c, err.get())) throw InvalidArgument("energy_minimize: T has an entry outside the pattern");
+    }
+    const unsigned mp_grid = blocks_for(n, kMpWarps);
+    const unsigned mp_block = kMpWarps * kWarp;
+    const unsigned ew = blocks_for(nz, 256);
+
+    if (krylov == 0) {
+        DBuf<double> dinv(static_cast<size_t>(n), c.s);
+        inverse_diagonal(c, A, dinv.get(), "energy_minimize: zero diagonal at row ");
+        DBuf<int32_t> prow(static_cast<size_t>(nz), c.s);
+        entry_rows(c, N, prow.get());
+        DBuf<int32_t> colptr, pos;
+        transpose_positions(c, N, colptr, pos, nullptr);
+        DBuf<double> APm(static_cast<size_t>(nz), c.s), R(static_cast<size_t>(nz), c.s), Z(static_cast<size_t>(nz), c.s),
+            D(static_cast<size_t>(nz), c.s), ADm(static_cast<size_t>(nz), c.s), ADp(static_cast<size_t>(nz), c.s);
+        AMG_CK(cudaMemsetAsync(D.get(), 0, sizeof(double) * nz, c.s));
+        launch(c, k_masked_project, mp_grid, mp_block, 0, n, A.rp.get(), A.ci.get(), A.va.get(), N.rp.get(),
+               N.ci.get(), static_cast<const double*>(P.get()), k, Bc, nc, static_cast<const double*>(gp.get()),
+               static_cast<const unsigned char*>(is_root.get()), APm.get(), static_cast<double*>(nullptr),
+               static_cast<const int32_t*>(nullptr));
+        launch(c, k_negate, ew, 256, 0, nz, static_cast<const double*>(APm.get()), R.get());
+        launch(c, k_project, blocks_for(n, 128), 128, 0, n, N.rp.get(), N.ci.get(), k, Bc, nc,
+               static_cast<const double*>(gp.get()), static_cast<const unsigned char*>(is_root.get()), R.get());
+        DBuf<double> scal(8, c.s);
+        DBuf<int32_t> flags(4, c.s);
+        DBuf<unsigned long long> abits(1, c.s);
+        const double init[8] = {0.0, 0.0, -1.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        const int32_t finit[4] = {0, 1, 0, 0};
+        copy_h2d(c, scal.get(), init, 8);
+        copy_h2d(c, flags.get(), finit, 4);
+        double* S = scal.get();
+        int32_t* F = flags.get();
+        for (int s = 0; s < iters; ++s) {
+            launch(c, k_cg_z, ew, 256, 0, nz, static_cast<const int32_t*>(prow.get()),
+                   static_cast<const double*>(dinv.get()), static_cast<const double*>(R.get()), Z.get(),
+                   static_cast<const int32_t*>(F));
+            dot(c, R.get(), Z.get(), nz, S + 7);
+            launch(c, k_cg_ctl_newsum, 1, 1, 0, S, F);
+            launch(c, k_cg_dir, ew, 256, 0, nz, static_cast<const double*>(Z.get()), D.get(),
+                   static_cast<const double*>(S), static_cast<const int32_t*>(F));
+            launch(c, k_masked_project, mp_grid, mp_block, 0, n, A.rp.get(), A.ci.get(), A.va.get(), N.rp.get(),
+                   N.ci.get(), static_cast<const double*>(D.get()), k, Bc, nc, static_cast<const double*>(gp.get()),
+                   static_cast<const unsigned char*>(is_root.get()), ADm.get(), ADp.get(),
+                   static_cast<const int32_t*>(F));
+            dot(c, D.get(), ADm.get(), nz, S + 7);
+            launch(c, k_cg_ctl_denom, 1, 1, 0, S, F, abits.get());
+            launch(c, k_cg_columns, blocks_for(nc, 128), 128, 0, nc, static_cast<const int32_t*>(colptr.get()),
+                   static_cast<const int32_t*>(pos.get()), static_cast<const double*>(P.get()),
+                   static_cast<const double*>(APm.get()), static_cast<const double*>(D.get()),
+                   static_cast<const double*>(ADm.get()), abits.get(), static_cast<const int32_t*>(F));
+            launch(c, k_cg_ctl_alpha, 1, 1, 0, S, F, static_cast<const unsigned long long*>(abits.get()), s);
+            launch(c, k_cg_update, ew, 256, 0, nz, P.get(), APm.get(), R.get(), static_cast<const double*>(D.get()),
+                   static_cast<const double*>(ADm.get()), static_cast<const double*>(ADp.get()),
+                   static_cast<const double*>(S), static_cast<const int32_t*>(F), s);
+        }
+        int32_t fh[4];
+        copy_d2h(c, fh, F, 4);
+        sync(c);
+        st.iterations = fh[2];
+        st.breakdown = fh[3] != 0;
+        compact_pattern(c, N, P.get(), T.bs, Pout);
+        return;
+    }
+
+    // ---- GMRES branch (interpolation.hpp:363-441) ----
+    DCsr At, AtA;
+    transpose(c, A, At);
+    spgemm(c, At, A, AtA);
+    DBuf<double> R0(static_cast<size_t>(nz), c.s);
+    launch(c, k_masked_project, mp_grid, mp_block, 0, n, AtA.rp.get(), AtA.ci.get(), AtA.va.get(), N.rp.get(),
+           N.ci.get(), static_cast<const double*>(P.get()), k, Bc, nc, static_cast<const double*>(gp.get()),
+           static_cast<const unsigned char*>(is_root.get()), R0.get(), static_cast<double*>(nullptr),
+           static_cast<const int32_t*>(nullptr));
+    launch(c, k_negate, ew, 256, 0, nz, static_cast<const double*>(R0.get()), R0.get());
+    launch(c, k_project, blocks_for(n, 128), 128, 0, n, N.rp.get(), N.ci.get(), k, Bc, nc,
+           static_cast<const double*>(gp.get()), static_cast<const unsigned char*>(is_root.get()), R0.get());
+    DBuf<double> scal(2, c.s);
+    nrm2(c, R0.get(), nz, scal.get());
+    const double beta = read_scalar(c, scal.get());
+    if (beta < 1e-300) {
+        compact_pattern(c, N, P.get(), T.bs, Pout);
+        return;
+    }
+    const int m = iters;
+    DBuf<double> V(static_cast<size_t>(nz) * (m + 1), c.s);
+    DBuf<double> Hd(static_cast<size_t>(m + 1) * m, c.s);
+    AMG_CK(cudaMemsetAsync(Hd.get(), 0, sizeof(double) * (m + 1) * m, c.s));
+    copy_d2d(c, V.get(), R0.get(), nz);
+    scale_const(c, 1.0 / beta, V.get(), nz);
+    int built = 0;
+    for (int s = 0; s < m; ++s) {
+        double* W = V.get() + static_cast<size_t>(s + 1) * nz;
+        launch(c, k_masked_project, mp_grid, mp_block, 0, n, AtA.rp.get(), AtA.ci.get(), AtA.va.get(), N.rp.get(),
+               N.ci.get(), static_cast<const double*>(V.get() + static_cast<size_t>(s) * nz), k, Bc, nc,
+               static_cast<const double*>(gp.get()), static_cast<const unsigned char*>(is_root.get()),
+               static_cast<double*>(nullptr), W, static_cast<const int32_t*>(nullptr));
+        for (int t = 0; t <= s; ++t) {
+            double* h = Hd.get() + t * m + s;
+            dot(c, W, V.get() + static_cast<size_t>(t) * nz, nz, h);
+            axpy_dev(c, h, -1.0, V.get() + static_cast<size_t>(t) * nz, W, nz);
+        }
+        double* hn_d = Hd.get() + (s + 1) * m + s;
+        nrm2(c, W, nz, hn_d);
+        const double hn = read_scalar(c, hn_d);
+        built = s + 1;
+        st.iterations = s + 1;
+        if (hn < 1e-14 * beta) break;
+        scale_recip_dev(c, hn_d, W, nz);
+    }
+    std::vector<double> H(static_cast<size_t>(m + 1) * m);
+    copy_d2h(c, H.data(), Hd.get(), static_cast<int64_t>(H.size()));
+    sync(c);
+    if (built > 64) throw RuntimeError("energy_minimize: Krylov dimension above 64");
+    std::vector<double> Hs(static_cast<size_t>(built) * built), ev(built), EV(static_cast<size_t>(built) * built);
+    for (int i = 0; i < built; ++i)
+        for (int j = 0; j < built; ++j) Hs[i * built + j] = 0.5 * (H[i * m + j] + H[j * m + i]);
+    sd::sym_eig<64>(built, Hs.data(), ev.data(), EV.data());
+    double mx = std::fabs(ev[0]);
+    for (double v : ev) mx = std::max(mx, std::fabs(v));
+    const double cutoff = 1e-14 * std::max(mx, 1e-300);
+    std::vector<double> rhs(built, 0.0), z(built), y(built);
+    rhs[0] = beta;
+    for (int t = 0; t < built; ++t) {
+        double s2 = 0.0;
+        for (int i = 0; i < built; ++i) s2 += EV[i * built + t] * rhs[i];
+        z[t] = s2;
+    }
+    for (int t = 0; t < built; ++t) z[t] = ev[t] > cutoff ? z[t] / ev[t] : 0.0;
+    for (int i = 0; i < built; ++i) {
+        double s2 = 0.0;
+        for (int t = 0; t < built; ++t) s2 += EV[i * built + t] * z[t];
+        y[i] = s2;
+    }
+    DBuf<double> U(static_cast<size_t>(nz), c.s);
+    AMG_CK(cudaMemsetAsync(U.get(), 0, sizeof(double) * nz, c.s));
+    // V holds built+1 vectors only up to the last normalised one (V[s+1] is filled
+    // in place while building); the reference combines V[0..built-1]
+    for (int t = 0; t < built; ++t)
+        launch(c, k_axpy_host, ew, 256, 0, nz, y[t], static_cast<const double*>(V.get() + static_cast<size_t>(t) * nz),
+               U.get());
+    DCsr Tc, Uc, AT, AU;
+    compact_pattern(c, N, P.get(), T.bs, Tc);
+    compact_pattern(c, N, U.get(), T.bs, Uc);
+    spgemm(c, A, Tc, AT);
+    spgemm(c, A, Uc, AU);
+    DBuf<int32_t> tcp, tpos, ucp, upos, urow;
+    transpose_positions(c, AT, tcp, tpos, nullptr);
+    transpose_positions(c, AU, ucp, upos, &urow);
+    DBuf<double> e(static_cast<size_t>(nc), c.s), g(static_cast<size_t>(nc), c.s), h(static_cast<size_t>(nc), c.s);
+    launch(c, k_gm_columns, blocks_for(nc, 128), 128, 0, nc, static_cast<const int32_t*>(tcp.get()),
+           static_cast<const int32_t*>(tpos.get()), AT.va.get(), static_cast<const int32_t*>(ucp.get()),
+           static_cast<const int32_t*>(upos.get()), static_cast<const int32_t*>(urow.get()), AU.va.get(), AT.rp.get(),
+           AT.ci.get(), e.get(), g.get(), h.get());
+    std::vector<double> he(nc), hg(nc), hh(nc);
+    copy_d2h(c, he.data(), e.get(), nc);
+    copy_d2h(c, hg.data(), g.get(), nc);
+    copy_d2h(c, hh.data(), h.get(), nc);
+    sync(c);
+    double tau = 1.0;  // column_safe_step(e, g, h, 1.0), host: n_c scalars
+    for (int32_t j = 0; j < nc; ++j) {
+        if (hh[j] <= 0.0) continue;
+        const double norm_j = std::sqrt(std::max(he[j], 0.0));
+        const double tol = 2.5e-13 * std::max(norm_j, 1.0e-30);
+        const double budget = tol * (2.0 * norm_j + tol);
+        const double disc = hg[j] * hg[j] + hh[j] * budget;
+        const double bj = (-hg[j] + std::sqrt(std::max(disc, 0.0))) / hh[j];
+        tau = std::min(tau, bj);
+    }
+    if (!(tau > 0.0)) {
+        st.breakdown = true;
+        Pout = std::move(Tc);
+        return;
+    }
+    launch(c, k_axpy_host, ew, 256, 0, nz, tau, static_cast<const double*>(U.get()), P.get());
+    compact_pattern(c, N, P.get(), T.bs, Pout);
+}
+
+}  // namespace amgcu

@@ -1,0 +1,77 @@
+// Declarations of the sm_100a kernel families of libamgcu (host launchers).
+// Every launcher reproduces one reference routine with the reference's
+// per-entry operation order (compiled with --fmad=false), so the integer
+// structure it emits is bit-identical and the fp64 values are bit-identical
+// given bit-identical inputs (SURVEY.md §7 hard part 1).
+#pragma once
+
+#include "device.cuh"
+
+namespace amgcu {
+
+// ---- sparse core (sparse_core.cu) -----------------------------------------------------
+// y = A x, sequential row sums in CSR order (sparse.hpp:141-152)
+void spmv(Ctx& c, const DCsr& A, const double* x, double* y);
+// transpose with rows ascending inside each column (sparse.hpp:161-179)
+void transpose(Ctx& c, const DCsr& A, DCsr& T);
+// positions of A's entries in transposed (CSC) order: colptr (nc+1), pos (nnz)
+void transpose_positions(Ctx& c, const DCsr& A, DBuf<int32_t>& colptr, DBuf<int32_t>& pos, DBuf<int32_t>* src_row);
+// C = A B, per-entry sums in A-row then B-row order, exact zeros dropped
+// (sparse.hpp:183-217); *ops receives the multiply-model count.
+void spgemm(Ctx& c, const DCsr& A, const DCsr& B, DCsr& C, double* ops = nullptr);
+// R (A P) (sparse.hpp:220-228)
+void galerkin(Ctx& c, const DCsr& R, const DCsr& A, const DCsr& P, DCsr& C, double* ops = nullptr);
+// filter_matrix (sparse.hpp:236-272); k <= 0 means unset
+void filter_matrix(Ctx& c, const DCsr& G, bool theta_set, double theta, int32_t k, DCsr& F);
+// is_symmetric (sparse.hpp:288-305)
+bool is_symmetric(Ctx& c, const DCsr& A, double tol);
+// dinv[i] = 1 / A(i,i); throws RuntimeError(prefix + row) for the lowest zero diagonal
+void inverse_diagonal(Ctx& c, const DCsr& A, double* dinv, const char* prefix);
+void diagonal(Ctx& c, const DCsr& A, double* d);
+// max_i |v_i| (exact)
+double max_abs(Ctx& c, const double* v, int64_t n);
+// drop entries with vals[p] == 0 from pattern N (from_pattern_values, interpolation.hpp:229-243)
+void compact_pattern(Ctx& c, const DCsr& N, const double* vals, int32_t bs, DCsr& out);
+// row index of every stored entry
+void entry_rows(Ctx& c, const DCsr& A, int32_t* rows);
+
+// ---- BLAS-1 with device-resident scalars (blas.cu) -----------------------------------
+// *out = sum_i x_i y_i.  seq mode: reference order (sparse.hpp:309-313);
+// otherwise a deterministic two-stage tree.
+void dot(Ctx& c, const double* x, const double* y, int64_t n, double* out);
+// *out = sqrt(dot(x, x))
+void nrm2(Ctx& c, const double* x, int64_t n, double* out);
+// y += s * x with s = sign * (*alpha)   (axpy, sparse.hpp:317-319)
+void axpy_dev(Ctx& c, const double* alpha, double sign, const double* x, double* y, int64_t n);
+// x *= 1 / (*denom)                      (scale(1.0 / h, v))
+void scale_recip_dev(Ctx& c, const double* denom, double* x, int64_t n);
+void scale_const(Ctx& c, double alpha, double* x, int64_t n);
+
+// ---- strength / aggregation (strength.cu, aggregate.cu) --------------------------------
+void symmetric_strength(Ctx& c, const DCsr& A, double theta, DCsr& S);
+void classical_strength(Ctx& c, const DCsr& A, double theta, DCsr& S);
+// evolution strength (strength.hpp:116-238); winv per row
+void evolution_strength(Ctx& c, const DCsr& A, const DCsr& At, const double* winv, double drop_tol, int steps,
+                        DCsr& S);
+void normalize_strength(Ctx& c, const DCsr& S, DCsr& N);
+void amalgamate(Ctx& c, const DCsr& S, int32_t m, DCsr& N);
+struct DAgg {
+    int32_t n_nodes = 0, n_agg = 0;
+    DBuf<int32_t> owner;  // node_to_agg
+    DBuf<int32_t> roots;
+};
+void greedy_aggregate(Ctx& c, const DCsr& S, DAgg& agg);
+void aggregate_indicator(Ctx& c, const DAgg& agg, DCsr& Cm);
+
+// ---- spectral radius (arnoldi.cu) ----------------------------------------------------
+double spectral_radius(Ctx& c, const DCsr& A, int steps, const double* dinv);
+
+// ---- relaxation (relax.cu) -----------------------------------------------------------
+// sync-free wavefront Gauss-Seidel sweeps (relaxation.hpp:115-127) over k columns
+// (column-major x of size n*k; b n*k or nullptr for b = 0)
+void gauss_seidel(Ctx& c, const DCsr& A, const double* inv_diag, double* x, const double* b, int k, int sweeps,
+                  bool symmetric_sweep);
+// weighted Jacobi sweeps x += (w dinv) (b - A x) (relaxation.hpp:107-113); b may be nullptr (0)
+void jacobi(Ctx& c, const DCsr& A, const double* wdinv, double* x, const double* b, int k, int sweeps);
+
+}  // namespace amgcu

@@ -1,0 +1,159 @@
+// Generic device primitives: tile-based exclusive scan (3 launches, deterministic),
+// fills, CSR upload/download.
+#include <cub/block/block_reduce.cuh>
+#include <cub/block/block_scan.cuh>
+
+#include "device.cuh"
+
+namespace amgcu {
+
+namespace {
+
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 16;
+constexpr int kTile = kScanThreads * kScanItems;
+
+template <typename T>
+__global__ void k_tile_reduce(const T* __restrict__ in, int64_t n, T* __restrict__ tile_sums) {
+    using BR = cub::BlockReduce<T, kScanThreads>;
+    __shared__ typename BR::TempStorage tmp;
+    const int64_t base = static_cast<int64_t>(blockIdx.x) * kTile;
+    T s = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        const int64_t i = base + static_cast<int64_t>(k) * kScanThreads + threadIdx.x;
+        if (i < n) s += in[i];
+    }
+    T tot = BR(tmp).Sum(s);
+    if (threadIdx.x == 0) tile_sums[blockIdx.x] = tot;
+}
+
+// single block: exclusive scan of the tile sums in place; total -> tile_sums[ntiles]
+template <typename T>
+__global__ void k_scan_tile_sums(T* __restrict__ sums, int64_t ntiles) {
+    using BS = cub::BlockScan<T, kScanThreads>;
+    __shared__ typename BS::TempStorage tmp;
+    __shared__ T carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int64_t base = 0; base < ntiles; base += kTile) {
+        T v[kScanItems];
+#pragma unroll
+        for (int k = 0; k < kScanItems; ++k) {
+            const int64_t i = base + threadIdx.x * kScanItems + k;
+            v[k] = i < ntiles ? sums[i] : T(0);
+        }
+        T agg;
+        BS(tmp).ExclusiveSum(v, v, agg);
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < kScanItems; ++k) {
+            const int64_t i = base + threadIdx.x * kScanItems + k;
+            if (i < ntiles) sums[i] = v[k] + carry;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) carry += agg;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) sums[ntiles] = carry;
+}
+
+template <typename T>
+__global__ void k_tile_scan(const T* __restrict__ in, T* __restrict__ out, int64_t n, const T* __restrict__ offs,
+                            int64_t ntiles) {
+    using BS = cub::BlockScan<T, kScanThreads>;
+    __shared__ typename BS::TempStorage tmp;
+    const int64_t base = static_cast<int64_t>(blockIdx.x) * kTile;
+    T v[kScanItems];
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        const int64_t i = base + threadIdx.x * kScanItems + k;
+        v[k] = i < n ? in[i] : T(0);
+    }
+    BS(tmp).ExclusiveSum(v, v);
+    const T off = offs[blockIdx.x];
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        const int64_t i = base + threadIdx.x * kScanItems + k;
+        if (i < n) out[i] = v[k] + off;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) out[n] = offs[ntiles];
+}
+
+template <typename T>
+int64_t scan_impl(Ctx& c, const T* in, T* out, int64_t n, bool read_total) {
+    if (n == 0) {
+        AMG_CK(cudaMemsetAsync(out, 0, sizeof(T), c.s));
+        return 0;
+    }
+    const int64_t ntiles = (n + kTile - 1) / kTile;
+    DBuf<T> sums(static_cast<size_t>(ntiles) + 1, c.s);
+    launch(c, k_tile_reduce<T>, static_cast<unsigned>(ntiles), kScanThreads, 0, in, n, sums.get());
+    launch(c, k_scan_tile_sums<T>, 1, kScanThreads, 0, sums.get(), ntiles);
+    launch(c, k_tile_scan<T>, static_cast<unsigned>(ntiles), kScanThreads, 0, in, out, n,
+           static_cast<const T*>(sums.get()), ntiles);
+    if (!read_total) return -1;
+    return static_cast<int64_t>(read_scalar(c, out + n));
+}
+
+template <typename T>
+__global__ void k_fill(T* p, T v, int64_t n) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+
+}  // namespace
+
+int64_t exclusive_scan_i32(Ctx& c, const int32_t* in, int32_t* out, int64_t n, bool read_total) {
+    return scan_impl<int32_t>(c, in, out, n, read_total);
+}
+int64_t exclusive_scan_i64(Ctx& c, const int64_t* in, int64_t* out, int64_t n, bool read_total) {
+    return scan_impl<int64_t>(c, in, out, n, read_total);
+}
+void fill_f64(Ctx& c, double* p, double v, int64_t n) { launch(c, k_fill<double>, blocks_for(n, 256), 256, 0, p, v, n); }
+void fill_i32(Ctx& c, int32_t* p, int32_t v, int64_t n) {
+    launch(c, k_fill<int32_t>, blocks_for(n, 256), 256, 0, p, v, n);
+}
+
+void upload_csr(Ctx& c, const amgcu_csr& h, DCsr& d) {
+    const int64_t nnz = h.row_offsets[h.n_rows];
+    d.alloc(c, h.n_rows, h.n_cols, nnz);
+    d.bs = h.block_size;
+    copy_h2d(c, d.rp.get(), h.row_offsets, h.n_rows + 1);
+    copy_h2d(c, d.ci.get(), h.col_indices, nnz);
+    copy_h2d(c, d.va.get(), h.values, nnz);
+}
+
+void upload_csr(Ctx& c, const HostCsr& h, DCsr& d) {
+    d.alloc(c, h.n_rows, h.n_cols, h.nnz());
+    d.bs = h.block_size;
+    copy_h2d(c, d.rp.get(), h.row_offsets.data(), h.n_rows + 1);
+    copy_h2d(c, d.ci.get(), h.col_indices.data(), h.nnz());
+    copy_h2d(c, d.va.get(), h.values.data(), h.nnz());
+    sync(c);  // host vectors may go out of scope
+}
+
+HostCsr download_csr(Ctx& c, const DCsr& d) {
+    HostCsr h;
+    h.n_rows = d.nr;
+    h.n_cols = d.nc;
+    h.block_size = d.bs;
+    h.row_offsets.resize(static_cast<size_t>(d.nr) + 1);
+    h.col_indices.resize(static_cast<size_t>(d.nnz));
+    h.values.resize(static_cast<size_t>(d.nnz));
+    copy_d2h(c, h.row_offsets.data(), d.rp.get(), d.nr + 1);
+    copy_d2h(c, h.col_indices.data(), d.ci.get(), d.nnz);
+    copy_d2h(c, h.values.data(), d.va.get(), d.nnz);
+    sync(c);
+    return h;
+}
+
+void clone_csr(Ctx& c, const DCsr& src, DCsr& dst) {
+    dst.alloc(c, src.nr, src.nc, src.nnz);
+    dst.bs = src.bs;
+    copy_d2d(c, dst.rp.get(), src.rp.get(), src.nr + 1);
+    copy_d2d(c, dst.ci.get(), src.ci.get(), src.nnz);
+    copy_d2d(c, dst.va.get(), src.va.get(), src.nnz);
+}
+
+}  // namespace amgcu

@@ -1,0 +1,323 @@
+// Root-node setup on the GPU: rn_setup / rn_coarsen_once (hierarchy.hpp:183-287)
+// orchestrated on the host, every data-parallel step a kernel from ops.cuh /
+// interp.cuh, level data resident in HBM.  Sizes cross to the host only where
+// an allocation depends on them (scan totals) and for the scalar decisions the
+// reference takes on the host (stagnation, symmetry, rho).
+#include <cmath>
+#include <string>
+
+#include "hier.cuh"
+#include "small_dense.h"
+
+namespace amgcu {
+
+namespace {
+
+__global__ void k_evolution_weights(int32_t n, const double* __restrict__ d, double omega, double* __restrict__ winv,
+                                    int32_t* __restrict__ bad) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    if (d[i] == 0.0) atomicMin(bad, i);
+    winv[i] = omega / d[i];
+}
+
+__global__ void k_l1_weights(int32_t n, const int32_t* __restrict__ rp, const double* __restrict__ va,
+                             double* __restrict__ winv, int32_t* __restrict__ bad) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double s = 0.0;
+    for (int32_t p = rp[i]; p < rp[i + 1]; ++p) s += fabs(va[p]);
+    if (s == 0.0) atomicMin(bad, i);
+    winv[i] = 1.0 / s;
+}
+
+__global__ void k_scale_by(int32_t n, double w, const double* __restrict__ d, double* __restrict__ out) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = w * d[i];
+}
+
+__global__ void k_scale_if_positive(int64_t n, const double* __restrict__ s, double* __restrict__ x) {
+    const double nrm = *s;
+    if (!(nrm > 0.0)) return;
+    const double a = 1.0 / nrm;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        x[i] *= a;
+}
+
+int energy_iterations(const amgcu_setup_options& o) {  // interpolation.hpp:34-37
+    if (o.energy_iters > 0) return o.energy_iters;
+    return std::max(1, static_cast<int>(std::ceil(1.5 * o.degree)));
+}
+
+struct Coarsened {
+    DCsr P, R, Ac;
+    DBuf<double> Bf, Bcoarse, Bhc;
+};
+
+void strength_of(Ctx& c, DLevel& L, const amgcu_setup_options& o, DCsr& S) {
+    const DCsr& A = L.A;
+    switch (o.strength_measure) {
+        case 0: classical_strength(c, A, o.drop_tol, S); return;
+        case 1: symmetric_strength(c, A, o.drop_tol, S); return;
+        case 2: {
+            if (A.nr != A.nc) throw InvalidArgument("evolution_strength: square matrix required");
+            if (o.drop_tol <= 0.0) throw InvalidArgument("evolution_strength: drop_tol must be positive");
+            if (o.evolution_steps < 1) throw InvalidArgument("evolution_strength: steps must be >= 1");
+            const int32_t n = A.nr;
+            DBuf<double> winv(static_cast<size_t>(n), c.s);
+            DBuf<int32_t> bad(1, c.s);
+            fill_i32(c, bad.get(), INT32_MAX, 1);
+            if (o.weighting == 0) {
+                const double rho = level_rho(c, L);
+                if (rho <= 0.0) throw RuntimeError("evolution_strength: spectral radius estimate failed");
+                DBuf<double> d(static_cast<size_t>(n), c.s);
+                diagonal(c, A, d.get());
+                launch(c, k_evolution_weights, blocks_for(n, 256), 256, 0, n, static_cast<const double*>(d.get()),
+                       1.0 / rho, winv.get(), bad.get());
+                const int32_t b = read_scalar(c, bad.get());
+                if (b != INT32_MAX)
+                    throw RuntimeError("evolution_strength: zero diagonal at row " + std::to_string(b));
+            } else {
+                launch(c, k_l1_weights, blocks_for(n, 256), 256, 0, n, A.rp.get(), A.va.get(), winv.get(), bad.get());
+                const int32_t b = read_scalar(c, bad.get());
+                if (b != INT32_MAX) throw RuntimeError("evolution_strength: zero row at " + std::to_string(b));
+            }
+            DCsr At;
+            transpose(c, A, At);
+            evolution_strength(c, A, At, winv.get(), o.drop_tol, o.evolution_steps, S);
+            return;
+        }
+    }
+    throw InvalidArgument("strength: unknown measure");
+}
+
+bool coarsen(Ctx& c, DHier& H, int level, const double* Bhat, Coarsened& out) {
+    const amgcu_setup_options& o = H.o;
+    DLevel& L = H.lv[level];
+    const DCsr& A = L.A;
+    const int32_t k = L.k;
+    const int32_t m = std::max<int32_t>(1, A.bs);
+
+    DCsr S0, Sa, S;
+    strength_of(c, L, o, S0);
+    amalgamate(c, S0, m, Sa);
+    normalize_strength(c, Sa, S);
+    DAgg agg;
+    greedy_aggregate(c, S, agg);
+    if (agg.n_agg >= agg.n_nodes) return false;
+
+    DCsr N;
+    aggregate_indicator(c, agg, N);
+    for (int t = 0; t < o.degree; ++t) {
+        DCsr next;
+        spgemm(c, S, N, next);
+        N = std::move(next);
+    }
+    const int32_t min_aggs = (k + m - 1) / m;
+    if (o.prefilter_set) {
+        DCsr F, Fa, Fm;
+        filter_matrix(c, N, o.prefilter_theta_set != 0, o.prefilter_theta, o.prefilter_k, F);
+        add_aggregate_entries(c, F, agg, Fa);
+        ensure_min_support(c, Fa, N, min_aggs, Fm);
+        N = std::move(Fm);
+    }
+    {
+        DCsr W;
+        widen_deficient_rows(c, N, S, agg, min_aggs, W);
+        N = std::move(W);
+    }
+    DCsr Nd0, Nd;
+    DBuf<int32_t> droots;
+    unamalgamate(c, N, agg, m, Nd0, droots);
+    root_node_pattern(c, Nd0, droots.get(), agg.n_agg * m, Nd);
+
+    const int32_t n = A.nr;
+    DBuf<double> Bimp(static_cast<size_t>(n) * k, c.s);
+    copy_d2d(c, Bimp.get(), L.B.get(), static_cast<int64_t>(n) * k);
+    improve_candidates(c, A, Bimp.get(), k, o.candidate_sweeps, o.cand_scheme, o.cand_weight, &L);
+    DCsr T;
+    DBuf<double> Bc;
+    inject_tentative(c, agg, Nd, Bimp.get(), k, m, T, Bc);
+
+    int kry = o.krylov;
+    if (!L.symmetric && kry == 0) kry = 1;
+    const int iters = energy_iterations(o);
+    if (o.postfilter_set) throw InvalidArgument("rn_setup: post-filtering is not on the GPU path yet");
+    energy_minimize(c, A, T, Bimp.get(), Bc.get(), k, Nd, iters, kry, droots.get(), agg.n_agg * m, out.P, nullptr);
+    out.P.bs = T.bs;
+
+    if (L.symmetric) {
+        transpose(c, out.P, out.R);
+        out.Bhc.alloc(Bc.size(), c.s);
+        copy_d2d(c, out.Bhc.get(), Bc.get(), static_cast<int64_t>(Bc.size()));
+    } else {
+        DCsr At;
+        transpose(c, A, At);
+        DBuf<double> Bh(static_cast<size_t>(n) * k, c.s);
+        copy_d2d(c, Bh.get(), Bhat, static_cast<int64_t>(n) * k);
+        improve_candidates(c, At, Bh.get(), k, o.candidate_sweeps, o.cand_scheme, o.cand_weight, nullptr);
+        DCsr That, Rt;
+        DBuf<double> Bhc;
+        inject_tentative(c, agg, Nd, Bh.get(), k, m, That, Bhc);
+        energy_minimize(c, At, That, Bh.get(), Bhc.get(), k, Nd, iters, 1, droots.get(), agg.n_agg * m, Rt, nullptr);
+        Rt.bs = That.bs;
+        transpose(c, Rt, out.R);
+        out.Bhc = std::move(Bhc);
+    }
+    galerkin(c, out.R, A, out.P, out.Ac);
+    out.Bf = std::move(Bimp);
+    out.Bcoarse = std::move(Bc);
+    return true;
+}
+
+}  // namespace
+
+void require_supported_relax(int scheme, const char* who) {
+    if (scheme == 0 || scheme == 1 || scheme == 2) return;
+    throw InvalidArgument(std::string(who) +
+                          ": relaxation scheme not available on the GPU path (jacobi, gauss_seidel, sym_gauss_seidel)");
+}
+
+double level_rho(Ctx& c, DLevel& L) {
+    if (!std::isnan(L.rho)) return L.rho;
+    if (L.inv_diag.empty()) {
+        L.inv_diag.alloc(static_cast<size_t>(L.A.nr), c.s);
+        inverse_diagonal(c, L.A, L.inv_diag.get(), "spectral_radius_estimate: zero diagonal at row ");
+    }
+    L.rho = spectral_radius(c, L.A, 15, L.inv_diag.get());
+    return L.rho;
+}
+
+void improve_candidates(Ctx& c, const DCsr& A, double* B, int32_t k, int sweeps, int scheme, double weight,
+                        DLevel* cache) {
+    if (A.nr != A.nc) throw InvalidArgument("improve_candidates: dimension mismatch");
+    if (sweeps < 0) throw InvalidArgument("improve_candidates: sweeps must be >= 0");
+    const int32_t n = A.nr;
+    if (sweeps > 0) {
+        require_supported_relax(scheme, "improve_candidates");
+        DBuf<double> dinv(static_cast<size_t>(n), c.s);
+        inverse_diagonal(c, A, dinv.get(), "relax: zero diagonal at row ");
+        if (scheme == 0) {
+            double w = weight;
+            if (w == 0.0) {
+                double rho;
+                if (cache) {
+                    rho = level_rho(c, *cache);
+                } else {
+                    rho = spectral_radius(c, A, 15, dinv.get());
+                }
+                w = 4.0 / (3.0 * rho);
+            }
+            DBuf<double> wd(static_cast<size_t>(n), c.s);
+            launch(c, k_scale_by, blocks_for(n, 256), 256, 0, n, w, static_cast<const double*>(dinv.get()), wd.get());
+            jacobi(c, A, wd.get(), B, nullptr, k, sweeps);
+        } else {
+            gauss_seidel(c, A, dinv.get(), B, nullptr, k, sweeps, scheme == 2);
+        }
+    }
+    DBuf<double> nrm(static_cast<size_t>(k), c.s);
+    for (int32_t j = 0; j < k; ++j) {
+        double* col = B + static_cast<size_t>(j) * n;
+        nrm2(c, col, n, nrm.get() + j);
+        launch(c, k_scale_if_positive, std::max(1u, std::min<unsigned>(blocks_for(n, 256), 4u * c.sms)), 256, 0,
+               static_cast<int64_t>(n), static_cast<const double*>(nrm.get() + j), col);
+    }
+}
+
+std::unique_ptr<DHier> rn_setup(Ctx& c, const DCsr& A, const double* B, int32_t k, const double* left,
+                                const amgcu_setup_options& o) {
+    if (o.method != 0) throw InvalidArgument("setup: only the rn method runs on the GPU path");
+    if (A.nr != A.nc || A.nr == 0) throw InvalidArgument("rn_setup: square nonempty matrix required");
+    if (k < 1) throw InvalidArgument("CandidateSet: need n >= 0, k >= 1");
+    const int32_t m = std::max<int32_t>(1, A.bs);
+    if (A.nr % m != 0) throw InvalidArgument("rn_setup: block size must divide the dimension");
+    if (k < m) throw InvalidArgument("rn_setup: need at least block_size candidates");
+    require_supported_relax(o.pre_scheme, "rn_setup");
+    require_supported_relax(o.post_scheme, "rn_setup");
+    auto H = std::make_unique<DHier>();
+    H->ctx = &c;
+    H->o = o;
+    if (!(A.nnz > 0)) throw InvalidArgument("WorkLedger: base nnz must be positive");
+    H->base_nnz = static_cast<double>(A.nnz);
+    H->lv.emplace_back();
+    {
+        DLevel& L0 = H->lv.back();
+        clone_csr(c, A, L0.A);
+        L0.k = k;
+        L0.B.alloc(static_cast<size_t>(A.nr) * k, c.s);
+        copy_d2d(c, L0.B.get(), B, static_cast<int64_t>(A.nr) * k);
+        L0.symmetric = is_symmetric(c, L0.A, 1e-12);
+    }
+    DBuf<double> Bhat(static_cast<size_t>(A.nr) * k, c.s);
+    copy_d2d(c, Bhat.get(), left ? left : B, static_cast<int64_t>(A.nr) * k);
+
+    while (static_cast<int>(H->lv.size()) < o.max_levels && H->lv.back().A.nr > o.max_size) {
+        const int l = static_cast<int>(H->lv.size()) - 1;
+        Coarsened step;
+        if (!coarsen(c, *H, l, Bhat.get(), step)) {
+            H->stagnated = true;
+            break;
+        }
+        DLevel& fine = H->lv[l];
+        fine.P = std::move(step.P);
+        fine.R = std::move(step.R);
+        fine.B = std::move(step.Bf);
+        fine.Bc.alloc(step.Bcoarse.size(), c.s);
+        copy_d2d(c, fine.Bc.get(), step.Bcoarse.get(), static_cast<int64_t>(step.Bcoarse.size()));
+        Bhat = std::move(step.Bhc);
+        DLevel next;
+        next.A = std::move(step.Ac);
+        next.k = k;
+        next.B = std::move(step.Bcoarse);
+        next.symmetric = is_symmetric(c, next.A, 1e-12);
+        H->lv.push_back(std::move(next));
+    }
+    // finalize_hierarchy (hierarchy.hpp:164-172): relaxation workspaces and the
+    // coarsest-level factorisation
+    for (size_t l = 0; l + 1 < H->lv.size(); ++l) {
+        DLevel& L = H->lv[l];
+        const int32_t n = L.A.nr;
+        if (L.inv_diag.empty()) {
+            L.inv_diag.alloc(static_cast<size_t>(n), c.s);
+            inverse_diagonal(c, L.A, L.inv_diag.get(), "relax: zero diagonal at row ");
+        }
+        auto weight = [&](int scheme, double w) {
+            if (scheme != 0) return 0.0;
+            return w != 0.0 ? w : 4.0 / (3.0 * level_rho(c, L));
+        };
+        L.w_pre = weight(o.pre_scheme, o.pre_weight);
+        L.w_post = weight(o.post_scheme, o.post_weight);
+        if (o.pre_scheme == 0) {
+            L.wd_pre.alloc(static_cast<size_t>(n), c.s);
+            launch(c, k_scale_by, blocks_for(n, 256), 256, 0, n, L.w_pre, static_cast<const double*>(L.inv_diag.get()),
+                   L.wd_pre.get());
+        }
+        if (o.post_scheme == 0) {
+            L.wd_post.alloc(static_cast<size_t>(n), c.s);
+            launch(c, k_scale_by, blocks_for(n, 256), 256, 0, n, L.w_post,
+                   static_cast<const double*>(L.inv_diag.get()), L.wd_post.get());
+        }
+    }
+    {
+        const DLevel& Lc = H->lv.back();
+        HostCsr hc = download_csr(c, Lc.A);
+        const int32_t nL = hc.n_rows;
+        std::vector<double> D(static_cast<size_t>(nL) * hc.n_cols, 0.0);
+        for (int32_t i = 0; i < nL; ++i)
+            for (int32_t p = hc.row_offsets[i]; p < hc.row_offsets[i + 1]; ++p)
+                D[static_cast<size_t>(i) * hc.n_cols + hc.col_indices[p]] = hc.values[p];
+        sd::COD cod;
+        cod.compute(nL, hc.n_cols, D.data());
+        std::vector<double> pinv(static_cast<size_t>(hc.n_cols) * nL);
+        cod.pseudo_inverse(pinv.data());
+        H->coarse_pinv.alloc(pinv.size(), c.s);
+        copy_h2d(c, H->coarse_pinv.get(), pinv.data(), static_cast<int64_t>(pinv.size()));
+        H->coarse_n = nL;
+        sync(c);
+    }
+    prepare_solve(*H);
+    return H;
+}
+
+}  // namespace amgcu

@@ -1,0 +1,649 @@
+// Sparse core kernels: SpMV, deterministic transpose, SpGEMM, filter,
+// symmetry test, diagonal, pattern compaction.  Reference: core/sparse.hpp.
+#include <cub/block/block_reduce.cuh>
+
+#include <algorithm>
+#include <climits>
+#include <cstring>
+#include <string>
+
+#include "ops.cuh"
+
+namespace amgcu {
+
+namespace {
+
+constexpr int kWarp = 32;
+
+// ---------------------------------------------------------------------------------
+// SpMV: one thread per row, CSR order (sparse.hpp:145-150).  The solve phase uses
+// the sliced-ELL variant in cycle.cu; this one serves setup (Arnoldi, checks).
+// ---------------------------------------------------------------------------------
+__global__ void k_spmv(int32_t nr, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                       const double* __restrict__ va, const double* __restrict__ x, double* __restrict__ y) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nr) return;
+    double s = 0.0;
+    for (int32_t p = rp[i]; p < rp[i + 1]; ++p) s += va[p] * x[ci[p]];
+    y[i] = s;
+}
+
+// ---------------------------------------------------------------------------------
+// Transpose: count -> scan -> atomic scatter -> per-column rank sort by source
+// position (keys unique), which restores the ascending-row order of sparse.hpp:169-177.
+// ---------------------------------------------------------------------------------
+__global__ void k_col_count(int64_t nnz, const int32_t* __restrict__ ci, int32_t* __restrict__ cnt) {
+    const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (p < nnz) atomicAdd(&cnt[ci[p]], 1);
+}
+
+__global__ void k_scatter_positions(int32_t nr, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                    const int32_t* __restrict__ colptr, int32_t* __restrict__ cursor,
+                                    int32_t* __restrict__ pos_tmp) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nr) return;
+    for (int32_t p = rp[i]; p < rp[i + 1]; ++p) {
+        const int32_t j = ci[p];
+        const int32_t slot = colptr[j] + atomicAdd(&cursor[j], 1);
+        pos_tmp[slot] = p;
+    }
+}
+
+// warp per segment: rank = #keys smaller (keys unique) -> sorted positions
+__global__ void k_segment_rank_sort(int32_t nseg, const int32_t* __restrict__ segptr, const int32_t* __restrict__ in,
+                                    int32_t* __restrict__ out) {
+    const int32_t seg = (blockIdx.x * blockDim.x + threadIdx.x) / kWarp;
+    const int lane = threadIdx.x & (kWarp - 1);
+    if (seg >= nseg) return;
+    const int32_t lo = segptr[seg], hi = segptr[seg + 1], len = hi - lo;
+    if (len == 1) {
+        if (lane == 0) out[lo] = in[lo];
+        return;
+    }
+    for (int32_t e0 = 0; e0 < len; e0 += kWarp) {
+        const int32_t e = e0 + lane;
+        const int32_t key = e < len ? in[lo + e] : INT_MAX;
+        int32_t rank = 0;
+        for (int32_t c0 = 0; c0 < len; c0 += kWarp) {
+            const int32_t other = (c0 + lane) < len ? in[lo + c0 + lane] : INT_MAX;
+            const int cnt = min(kWarp, len - c0);
+            for (int t = 0; t < cnt; ++t) {
+                const int32_t o = __shfl_sync(0xffffffffu, other, t);
+                rank += (o < key) ? 1 : 0;
+            }
+        }
+        if (e < len) out[lo + rank] = key;
+    }
+}
+
+__global__ void k_rows_of_entries(int32_t nr, const int32_t* __restrict__ rp, int32_t* __restrict__ rows) {
+    const int32_t i = (blockIdx.x * blockDim.x + threadIdx.x) / kWarp;
+    const int lane = threadIdx.x & (kWarp - 1);
+    if (i >= nr) return;
+    for (int32_t p = rp[i] + lane; p < rp[i + 1]; p += kWarp) rows[p] = i;
+}
+
+__global__ void k_gather_transpose(int64_t nnz, const int32_t* __restrict__ pos, const int32_t* __restrict__ rows,
+                                   const double* __restrict__ va, int32_t* __restrict__ tci, double* __restrict__ tva) {
+    const int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (q >= nnz) return;
+    const int32_t p = pos[q];
+    tci[q] = rows[p];
+    tva[q] = va[p];
+}
+
+// ---------------------------------------------------------------------------------
+// SpGEMM (sparse.hpp:183-217).  Products are expanded in the reference order
+// (A-row entry t, then B-row entry q); key = (col << 32) | seq; a bitonic sort by
+// key groups each output column with its contributions still in sequence order,
+// and one lane sums each group from 0.0 in that order.  Exact zeros are dropped.
+// Rows with up to kSmallCap products: one warp, shared memory.  Larger rows:
+// one block over a global scratch region.
+// ---------------------------------------------------------------------------------
+constexpr int kSmallCap = 512;
+constexpr int kGemmWarps = 4;
+
+__global__ void k_product_count(int32_t nr, const int32_t* __restrict__ arp, const int32_t* __restrict__ aci,
+                                const int32_t* __restrict__ brp, int64_t* __restrict__ np) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nr) return;
+    int64_t s = 0;
+    for (int32_t p = arp[i]; p < arp[i + 1]; ++p) {
+        const int32_t t = aci[p];
+        s += brp[t + 1] - brp[t];
+    }
+    np[i] = s;
+}
+
+__global__ void k_collect_big(int32_t nr, const int64_t* __restrict__ np, int32_t* __restrict__ list,
+                              int32_t* __restrict__ count) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nr) return;
+    if (np[i] > kSmallCap) list[atomicAdd(count, 1)] = i;
+}
+
+__device__ __forceinline__ unsigned next_pow2(unsigned v) {
+    v--;
+    v |= v >> 1;
+    v |= v >> 2;
+    v |= v >> 4;
+    v |= v >> 8;
+    v |= v >> 16;
+    return v + 1;
+}
+
+// expand row i of A*B into keys/vals (shared or global), cooperative over a group of `gsize` threads
+__device__ __forceinline__ void expand_row(int32_t i, const int32_t* __restrict__ arp, const int32_t* __restrict__ aci,
+                                           const double* __restrict__ ava, const int32_t* __restrict__ brp,
+                                           const int32_t* __restrict__ bci, const double* __restrict__ bva,
+                                           unsigned long long* keys, double* vals, int tid, int gsize) {
+    int64_t base = 0;
+    for (int32_t p = arp[i]; p < arp[i + 1]; ++p) {
+        const int32_t t = aci[p];
+        const double a = ava[p];
+        const int32_t lo = brp[t], len = brp[t + 1] - lo;
+        for (int32_t q = tid; q < len; q += gsize) {
+            const int64_t seq = base + q;
+            keys[seq] = (static_cast<unsigned long long>(static_cast<uint32_t>(bci[lo + q])) << 32) |
+                        static_cast<unsigned long long>(seq);
+            vals[seq] = a * bva[lo + q];
+        }
+        base += len;
+    }
+}
+
+__global__ void __launch_bounds__(kGemmWarps * kWarp)
+    k_spgemm_small(int32_t nr, const int32_t* __restrict__ arp, const int32_t* __restrict__ aci,
+                   const double* __restrict__ ava, const int32_t* __restrict__ brp, const int32_t* __restrict__ bci,
+                   const double* __restrict__ bva, const int64_t* __restrict__ poff, int32_t* __restrict__ tcol,
+                   double* __restrict__ tval, int32_t* __restrict__ cnt) {
+    __shared__ unsigned long long skeys[kGemmWarps][kSmallCap];
+    __shared__ double svals[kGemmWarps][kSmallCap];
+    const int w = threadIdx.x / kWarp;
+    const int lane = threadIdx.x & (kWarp - 1);
+    const int32_t i = blockIdx.x * kGemmWarps + w;
+    if (i >= nr) return;
+    const int64_t np = poff[i + 1] - poff[i];
+    if (np > kSmallCap) return;  // handled by the block kernel
+    if (np == 0) {
+        if (lane == 0) cnt[i] = 0;
+        return;
+    }
+    unsigned long long* keys = skeys[w];
+    double* vals = svals[w];
+    expand_row(i, arp, aci, ava, brp, bci, bva, keys, vals, lane, kWarp);
+    const unsigned n2 = max(next_pow2(static_cast<unsigned>(np)), 2u);
+    for (unsigned e = static_cast<unsigned>(np) + lane; e < n2; e += kWarp) keys[e] = ~0ull;
+    __syncwarp();
+    // bitonic sort, ascending
+    for (unsigned k = 2; k <= n2; k <<= 1) {
+        for (unsigned j = k >> 1; j > 0; j >>= 1) {
+            for (unsigned e = lane; e < n2 / 2; e += kWarp) {
+                const unsigned lo = 2 * e - (e & (j - 1));
+                const unsigned hi = lo + j;
+                const bool up = ((lo & k) == 0);
+                const unsigned long long a = keys[lo], b = keys[hi];
+                if ((a > b) == up) {
+                    keys[lo] = b;
+                    keys[hi] = a;
+                }
+            }
+            __syncwarp();
+        }
+    }
+    // ordered segment sums; compacted write in column order
+    int32_t written = 0;
+    int32_t* ocol = tcol + poff[i];
+    double* oval = tval + poff[i];
+    for (int32_t e0 = 0; e0 < np; e0 += kWarp) {
+        const int32_t e = e0 + lane;
+        bool emit = false;
+        uint32_t col = 0;
+        double acc = 0.0;
+        if (e < np) {
+            const unsigned long long key = keys[e];
+            col = static_cast<uint32_t>(key >> 32);
+            const bool start = (e == 0) || (static_cast<uint32_t>(keys[e - 1] >> 32) != col);
+            if (start) {
+                for (int32_t r = e; r < np; ++r) {
+                    const unsigned long long kr = keys[r];
+                    if (static_cast<uint32_t>(kr >> 32) != col) break;
+                    acc += vals[static_cast<uint32_t>(kr & 0xffffffffull)];
+                }
+                emit = (acc != 0.0);
+            }
+        }
+        const unsigned ballot = __ballot_sync(0xffffffffu, emit);
+        if (emit) {
+            const int32_t at = written + __popc(ballot & ((1u << lane) - 1u));
+            ocol[at] = static_cast<int32_t>(col);
+            oval[at] = acc;
+        }
+        written += __popc(ballot);
+    }
+    if (lane == 0) cnt[i] = written;
+}
+
+constexpr int kBigThreads = 512;
+
+__global__ void __launch_bounds__(kBigThreads)
+    k_spgemm_big(const int32_t* __restrict__ list, const int32_t* __restrict__ arp, const int32_t* __restrict__ aci,
+                 const double* __restrict__ ava, const int32_t* __restrict__ brp, const int32_t* __restrict__ bci,
+                 const double* __restrict__ bva, const int64_t* __restrict__ poff,
+                 const int64_t* __restrict__ scratch_off, unsigned long long* __restrict__ gkeys,
+                 double* __restrict__ gvals, int32_t* __restrict__ tcol, double* __restrict__ tval,
+                 int32_t* __restrict__ cnt) {
+    const int32_t i = list[blockIdx.x];
+    const int64_t np = poff[i + 1] - poff[i];
+    unsigned long long* keys = gkeys + scratch_off[blockIdx.x];
+    double* vals = gvals + poff[i];
+    expand_row(i, arp, aci, ava, brp, bci, bva, keys, vals, threadIdx.x, blockDim.x);
+    int64_t n2 = 1;
+    while (n2 < np) n2 <<= 1;
+    for (int64_t e = np + threadIdx.x; e < n2; e += blockDim.x) keys[e] = ~0ull;
+    __syncthreads();
+    for (int64_t k = 2; k <= n2; k <<= 1) {
+        for (int64_t j = k >> 1; j > 0; j >>= 1) {
+            for (int64_t e = threadIdx.x; e < n2 / 2; e += blockDim.x) {
+                const int64_t lo = 2 * e - (e & (j - 1));
+                const int64_t hi = lo + j;
+                const bool up = ((lo & k) == 0);
+                const unsigned long long a = keys[lo], b = keys[hi];
+                if ((a > b) == up) {
+                    keys[lo] = b;
+                    keys[hi] = a;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    __shared__ int32_t s_written;
+    __shared__ int32_t s_warp[kBigThreads / kWarp];
+    if (threadIdx.x == 0) s_written = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & (kWarp - 1), wid = threadIdx.x / kWarp;
+    int32_t* ocol = tcol + poff[i];
+    double* oval = tval + poff[i];
+    for (int64_t e0 = 0; e0 < np; e0 += blockDim.x) {
+        const int64_t e = e0 + threadIdx.x;
+        bool emit = false;
+        uint32_t col = 0;
+        double acc = 0.0;
+        if (e < np) {
+            const unsigned long long key = keys[e];
+            col = static_cast<uint32_t>(key >> 32);
+            const bool start = (e == 0) || (static_cast<uint32_t>(keys[e - 1] >> 32) != col);
+            if (start) {
+                for (int64_t r = e; r < np; ++r) {
+                    const unsigned long long kr = keys[r];
+                    if (static_cast<uint32_t>(kr >> 32) != col) break;
+                    acc += vals[static_cast<uint32_t>(kr & 0xffffffffull)];
+                }
+                emit = (acc != 0.0);
+            }
+        }
+        const unsigned ballot = __ballot_sync(0xffffffffu, emit);
+        if (lane == 0) s_warp[wid] = __popc(ballot);
+        __syncthreads();
+        int32_t before = s_written;
+        for (int t = 0; t < wid; ++t) before += s_warp[t];
+        if (emit) {
+            const int32_t at = before + __popc(ballot & ((1u << lane) - 1u));
+            ocol[at] = static_cast<int32_t>(col);
+            oval[at] = acc;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int32_t tot = 0;
+            for (int t = 0; t < static_cast<int>(blockDim.x / kWarp); ++t) tot += s_warp[t];
+            s_written += tot;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) cnt[i] = s_written;
+}
+
+__global__ void k_copy_rows(int32_t nr, const int64_t* __restrict__ poff, const int32_t* __restrict__ tcol,
+                            const double* __restrict__ tval, const int32_t* __restrict__ crp, int32_t* __restrict__ cci,
+                            double* __restrict__ cva) {
+    const int32_t i = (blockIdx.x * blockDim.x + threadIdx.x) / kWarp;
+    const int lane = threadIdx.x & (kWarp - 1);
+    if (i >= nr) return;
+    const int64_t src = poff[i];
+    const int32_t dst = crp[i], len = crp[i + 1] - dst;
+    for (int32_t e = lane; e < len; e += kWarp) {
+        cci[dst + e] = tcol[src + e];
+        cva[dst + e] = tval[src + e];
+    }
+}
+
+// ---------------------------------------------------------------------------------
+// filter_matrix (sparse.hpp:236-272), thread per row, two passes.
+// ---------------------------------------------------------------------------------
+__device__ void filter_thresholds(int32_t i, bool square, const int32_t* rp, const int32_t* ci, const double* va,
+                                  bool theta_set, double theta, int32_t k, double* kth_out, double* tmax_out) {
+    const int32_t lo = rp[i], hi = rp[i + 1];
+    int32_t nm = 0;
+    double mx = 0.0;
+    bool any = false;
+    for (int32_t p = lo; p < hi; ++p) {
+        if (square && ci[p] == i) continue;
+        const double m = fabs(va[p]);
+        mx = any ? (m > mx ? m : mx) : m;
+        any = true;
+        ++nm;
+    }
+    double kth = 0.0;
+    if (k > 0 && k < nm) {
+        // k-th largest magnitude (duplicates counted): the m whose descending
+        // rank range [#greater, #greater + #equal) contains k-1
+        for (int32_t p = lo; p < hi; ++p) {
+            if (square && ci[p] == i) continue;
+            const double m = fabs(va[p]);
+            int32_t greater = 0, equal = 0;
+            for (int32_t q = lo; q < hi; ++q) {
+                if (square && ci[q] == i) continue;
+                const double o = fabs(va[q]);
+                greater += (o > m) ? 1 : 0;
+                equal += (o == m) ? 1 : 0;
+            }
+            if (greater <= k - 1 && k - 1 < greater + equal) {
+                kth = m;
+                break;
+            }
+        }
+    }
+    *kth_out = kth;
+    *tmax_out = (theta_set && any) ? theta * mx : 0.0;
+}
+
+__device__ __forceinline__ bool filter_keep(int32_t i, int32_t j, double v, bool square, bool theta_set, int32_t k,
+                                            double kth, double tmax) {
+    const double mag = fabs(v);
+    const bool diag = square && j == i;
+    const bool keep = diag || ((k <= 0 || mag >= kth) && (!theta_set || mag >= tmax));
+    return keep && v != 0.0;
+}
+
+__global__ void k_filter_count(int32_t nr, bool square, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                               const double* __restrict__ va, bool theta_set, double theta, int32_t k,
+                               int32_t* __restrict__ cnt) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nr) return;
+    double kth, tmax;
+    filter_thresholds(i, square, rp, ci, va, theta_set, theta, k, &kth, &tmax);
+    int32_t c = 0;
+    for (int32_t p = rp[i]; p < rp[i + 1]; ++p) c += filter_keep(i, ci[p], va[p], square, theta_set, k, kth, tmax);
+    cnt[i] = c;
+}
+
+__global__ void k_filter_write(int32_t nr, bool square, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                               const double* __restrict__ va, bool theta_set, double theta, int32_t k,
+                               const int32_t* __restrict__ frp, int32_t* __restrict__ fci, double* __restrict__ fva) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nr) return;
+    double kth, tmax;
+    filter_thresholds(i, square, rp, ci, va, theta_set, theta, k, &kth, &tmax);
+    int32_t o = frp[i];
+    for (int32_t p = rp[i]; p < rp[i + 1]; ++p)
+        if (filter_keep(i, ci[p], va[p], square, theta_set, k, kth, tmax)) {
+            fci[o] = ci[p];
+            fva[o] = va[p];
+            ++o;
+        }
+}
+
+// ---------------------------------------------------------------------------------
+// symmetry: for every stored (i, j): |A(i,j) - A(j,i)| <= tol * max|A| (the fast and
+// fallback branches of sparse.hpp:288-305 test exactly this set of pairs)
+// ---------------------------------------------------------------------------------
+__device__ __forceinline__ double coeff_at(const int32_t* rp, const int32_t* ci, const double* va, int32_t i, int32_t j) {
+    int32_t lo = rp[i], hi = rp[i + 1];
+    while (lo < hi) {
+        const int32_t mid = (lo + hi) >> 1;
+        if (ci[mid] < j) lo = mid + 1;
+        else hi = mid;
+    }
+    return (lo < rp[i + 1] && ci[lo] == j) ? va[lo] : 0.0;
+}
+
+__global__ void k_asym(int32_t nr, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                       const double* __restrict__ va, double bound, int32_t* __restrict__ bad) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nr) return;
+    for (int32_t p = rp[i]; p < rp[i + 1]; ++p) {
+        const double t = coeff_at(rp, ci, va, ci[p], i);
+        if (fabs(va[p] - t) > bound) {
+            atomicExch(bad, 1);
+            return;
+        }
+    }
+}
+
+__global__ void k_max_abs(int64_t n, const double* __restrict__ v, unsigned long long* __restrict__ out) {
+    using BR = cub::BlockReduce<double, 256>;
+    __shared__ typename BR::TempStorage tmp;
+    double m = 0.0;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        m = fmax(m, fabs(v[i]));
+    const double bm = BR(tmp).Reduce(m, [](double a, double b) { return fmax(a, b); });
+    if (threadIdx.x == 0) atomicMax(out, static_cast<unsigned long long>(__double_as_longlong(bm)));
+}
+
+__global__ void k_diag(int32_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                       const double* __restrict__ va, double* __restrict__ d, bool invert, int32_t* __restrict__ bad) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double v = coeff_at(rp, ci, va, i, i);
+    if (invert) {
+        if (v == 0.0) atomicMin(bad, i);
+        d[i] = 1.0 / v;
+    } else {
+        d[i] = v;
+    }
+}
+
+__global__ void k_nonzero_count(int32_t nr, const int32_t* __restrict__ rp, const double* __restrict__ vals,
+                                int32_t* __restrict__ cnt) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nr) return;
+    int32_t c = 0;
+    for (int32_t p = rp[i]; p < rp[i + 1]; ++p) c += vals[p] != 0.0;
+    cnt[i] = c;
+}
+
+__global__ void k_nonzero_write(int32_t nr, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                const double* __restrict__ vals, const int32_t* __restrict__ orp,
+                                int32_t* __restrict__ oci, double* __restrict__ ova) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nr) return;
+    int32_t o = orp[i];
+    for (int32_t p = rp[i]; p < rp[i + 1]; ++p)
+        if (vals[p] != 0.0) {
+            oci[o] = ci[p];
+            ova[o] = vals[p];
+            ++o;
+        }
+}
+
+}  // namespace
+
+void spmv(Ctx& c, const DCsr& A, const double* x, double* y) {
+    launch(c, k_spmv, blocks_for(A.nr, 256), 256, 0, A.nr, A.rp.get(), A.ci.get(), A.va.get(), x, y);
+}
+
+void entry_rows(Ctx& c, const DCsr& A, int32_t* rows) {
+    launch(c, k_rows_of_entries, blocks_for(static_cast<int64_t>(A.nr) * kWarp, 256), 256, 0, A.nr, A.rp.get(), rows);
+}
+
+void transpose_positions(Ctx& c, const DCsr& A, DBuf<int32_t>& colptr, DBuf<int32_t>& pos, DBuf<int32_t>* src_row) {
+    DBuf<int32_t> cnt(static_cast<size_t>(A.nc) + 1, c.s);
+    AMG_CK(cudaMemsetAsync(cnt.get(), 0, sizeof(int32_t) * (A.nc + 1), c.s));
+    launch(c, k_col_count, blocks_for(A.nnz, 256), 256, 0, A.nnz, A.ci.get(), cnt.get());
+    colptr.alloc(static_cast<size_t>(A.nc) + 1, c.s);
+    exclusive_scan_i32(c, cnt.get(), colptr.get(), A.nc, false);
+    AMG_CK(cudaMemsetAsync(cnt.get(), 0, sizeof(int32_t) * (A.nc + 1), c.s));
+    DBuf<int32_t> tmp(static_cast<size_t>(A.nnz), c.s);
+    launch(c, k_scatter_positions, blocks_for(A.nr, 256), 256, 0, A.nr, A.rp.get(), A.ci.get(),
+           static_cast<const int32_t*>(colptr.get()), cnt.get(), tmp.get());
+    pos.alloc(static_cast<size_t>(A.nnz), c.s);
+    launch(c, k_segment_rank_sort, blocks_for(static_cast<int64_t>(A.nc) * kWarp, 256), 256, 0, A.nc,
+           static_cast<const int32_t*>(colptr.get()), static_cast<const int32_t*>(tmp.get()), pos.get());
+    if (src_row) {
+        src_row->alloc(static_cast<size_t>(A.nnz), c.s);
+        entry_rows(c, A, src_row->get());
+    }
+}
+
+void transpose(Ctx& c, const DCsr& A, DCsr& T) {
+    DBuf<int32_t> colptr, pos, rows;
+    transpose_positions(c, A, colptr, pos, &rows);
+    T.nr = A.nc;
+    T.nc = A.nr;
+    T.bs = A.bs;
+    T.nnz = A.nnz;
+    T.rp = std::move(colptr);
+    T.ci.alloc(static_cast<size_t>(A.nnz), c.s);
+    T.va.alloc(static_cast<size_t>(A.nnz), c.s);
+    launch(c, k_gather_transpose, blocks_for(A.nnz, 256), 256, 0, A.nnz, static_cast<const int32_t*>(pos.get()),
+           static_cast<const int32_t*>(rows.get()), A.va.get(), T.ci.get(), T.va.get());
+}
+
+void spgemm(Ctx& c, const DCsr& A, const DCsr& B, DCsr& C, double* ops) {
+    if (A.nc != B.nr) throw InvalidArgument("matmul: dimension mismatch");
+    const int32_t nr = A.nr;
+    DBuf<int64_t> np(static_cast<size_t>(nr) + 1, c.s), poff(static_cast<size_t>(nr) + 1, c.s);
+    launch(c, k_product_count, blocks_for(nr, 256), 256, 0, nr, A.rp.get(), A.ci.get(), B.rp.get(), np.get());
+    const int64_t total = exclusive_scan_i64(c, np.get(), poff.get(), nr);
+    if (ops) *ops = static_cast<double>(total);
+    DBuf<int32_t> tcol(static_cast<size_t>(total), c.s), cnt(static_cast<size_t>(nr) + 1, c.s);
+    DBuf<double> tval(static_cast<size_t>(total), c.s);
+    launch(c, k_spgemm_small, blocks_for(nr, kGemmWarps), kGemmWarps * kWarp, 0, nr, A.rp.get(), A.ci.get(),
+           A.va.get(), B.rp.get(), B.ci.get(), B.va.get(), static_cast<const int64_t*>(poff.get()), tcol.get(),
+           tval.get(), cnt.get());
+    // rows above the shared-memory capacity
+    DBuf<int32_t> big_list(static_cast<size_t>(nr), c.s), big_count(1, c.s);
+    AMG_CK(cudaMemsetAsync(big_count.get(), 0, sizeof(int32_t), c.s));
+    launch(c, k_collect_big, blocks_for(nr, 256), 256, 0, nr, static_cast<const int64_t*>(np.get()), big_list.get(),
+           big_count.get());
+    const int32_t nbig = read_scalar(c, big_count.get());
+    if (nbig > 0) {
+        std::vector<int32_t> hl(nbig);
+        copy_d2h(c, hl.data(), big_list.get(), nbig);
+        std::vector<int64_t> hpoff(static_cast<size_t>(nr) + 1);
+        copy_d2h(c, hpoff.data(), poff.get(), nr + 1);
+        sync(c);
+        std::sort(hl.begin(), hl.end());
+        std::vector<int64_t> soff(nbig);
+        int64_t acc = 0;
+        for (int32_t b = 0; b < nbig; ++b) {
+            soff[b] = acc;
+            int64_t np2 = 1;
+            while (np2 < hpoff[hl[b] + 1] - hpoff[hl[b]]) np2 <<= 1;
+            acc += np2;
+        }
+        DBuf<int32_t> dl(static_cast<size_t>(nbig), c.s);
+        DBuf<int64_t> doff(static_cast<size_t>(nbig), c.s);
+        DBuf<unsigned long long> gkeys(static_cast<size_t>(acc), c.s);
+        DBuf<double> gvals(static_cast<size_t>(total), c.s);
+        copy_h2d(c, dl.get(), hl.data(), nbig);
+        copy_h2d(c, doff.get(), soff.data(), nbig);
+        launch(c, k_spgemm_big, static_cast<unsigned>(nbig), kBigThreads, 0, static_cast<const int32_t*>(dl.get()),
+               A.rp.get(), A.ci.get(), A.va.get(), B.rp.get(), B.ci.get(), B.va.get(),
+               static_cast<const int64_t*>(poff.get()), static_cast<const int64_t*>(doff.get()), gkeys.get(),
+               gvals.get(), tcol.get(), tval.get(), cnt.get());
+        sync(c);
+    }
+    C.nr = nr;
+    C.nc = B.nc;
+    C.bs = 1;
+    C.rp.alloc(static_cast<size_t>(nr) + 1, c.s);
+    const int64_t nnz = exclusive_scan_i32(c, cnt.get(), C.rp.get(), nr);
+    C.nnz = nnz;
+    C.ci.alloc(static_cast<size_t>(nnz), c.s);
+    C.va.alloc(static_cast<size_t>(nnz), c.s);
+    launch(c, k_copy_rows, blocks_for(static_cast<int64_t>(nr) * kWarp, 256), 256, 0, nr,
+           static_cast<const int64_t*>(poff.get()), static_cast<const int32_t*>(tcol.get()),
+           static_cast<const double*>(tval.get()), static_cast<const int32_t*>(C.rp.get()), C.ci.get(), C.va.get());
+}
+
+void galerkin(Ctx& c, const DCsr& R, const DCsr& A, const DCsr& P, DCsr& C, double* ops) {
+    if (R.nc != A.nr || A.nc != P.nr) throw InvalidArgument("galerkin_product: dimension mismatch");
+    DCsr AP;
+    double o1 = 0.0, o2 = 0.0;
+    spgemm(c, A, P, AP, &o1);
+    spgemm(c, R, AP, C, &o2);
+    C.bs = P.bs;
+    if (ops) *ops = o1 + o2;
+}
+
+void filter_matrix(Ctx& c, const DCsr& G, bool theta_set, double theta, int32_t k, DCsr& F) {
+    if (theta_set && (theta < 0.0 || theta > 1.0)) throw InvalidArgument("filter_matrix: theta must lie in [0, 1]");
+    if (k < 0) throw InvalidArgument("filter_matrix: k must be >= 1");
+    const bool square = G.nr == G.nc;
+    DBuf<int32_t> cnt(static_cast<size_t>(G.nr) + 1, c.s);
+    launch(c, k_filter_count, blocks_for(G.nr, 128), 128, 0, G.nr, square, G.rp.get(), G.ci.get(), G.va.get(),
+           theta_set, theta, k, cnt.get());
+    F.nr = G.nr;
+    F.nc = G.nc;
+    F.bs = G.bs;
+    F.rp.alloc(static_cast<size_t>(G.nr) + 1, c.s);
+    F.nnz = exclusive_scan_i32(c, cnt.get(), F.rp.get(), G.nr);
+    F.ci.alloc(static_cast<size_t>(F.nnz), c.s);
+    F.va.alloc(static_cast<size_t>(F.nnz), c.s);
+    launch(c, k_filter_write, blocks_for(G.nr, 128), 128, 0, G.nr, square, G.rp.get(), G.ci.get(), G.va.get(),
+           theta_set, theta, k, static_cast<const int32_t*>(F.rp.get()), F.ci.get(), F.va.get());
+}
+
+double max_abs(Ctx& c, const double* v, int64_t n) {
+    DBuf<unsigned long long> out(1, c.s);
+    AMG_CK(cudaMemsetAsync(out.get(), 0, sizeof(unsigned long long), c.s));
+    const unsigned g = std::min<unsigned>(blocks_for(n, 256), 4u * c.sms);
+    launch(c, k_max_abs, std::max(g, 1u), 256, 0, n, v, out.get());
+    const unsigned long long bits = read_scalar(c, out.get());
+    double r;
+    std::memcpy(&r, &bits, sizeof(r));
+    return r;
+}
+
+bool is_symmetric(Ctx& c, const DCsr& A, double tol) {
+    if (A.nr != A.nc) return false;
+    const double scale = max_abs(c, A.va.get(), A.nnz);
+    DBuf<int32_t> bad(1, c.s);
+    AMG_CK(cudaMemsetAsync(bad.get(), 0, sizeof(int32_t), c.s));
+    launch(c, k_asym, blocks_for(A.nr, 256), 256, 0, A.nr, A.rp.get(), A.ci.get(), A.va.get(), tol * scale,
+           bad.get());
+    return read_scalar(c, bad.get()) == 0;
+}
+
+void inverse_diagonal(Ctx& c, const DCsr& A, double* dinv, const char* prefix) {
+    const int32_t n = std::min(A.nr, A.nc);
+    DBuf<int32_t> bad(1, c.s);
+    fill_i32(c, bad.get(), INT_MAX, 1);
+    launch(c, k_diag, blocks_for(n, 256), 256, 0, n, A.rp.get(), A.ci.get(), A.va.get(), dinv, true, bad.get());
+    const int32_t b = read_scalar(c, bad.get());
+    if (b != INT_MAX) throw RuntimeError(std::string(prefix) + std::to_string(b));
+}
+
+void diagonal(Ctx& c, const DCsr& A, double* d) {
+    const int32_t n = std::min(A.nr, A.nc);
+    launch(c, k_diag, blocks_for(n, 256), 256, 0, n, A.rp.get(), A.ci.get(), A.va.get(), d, false,
+           static_cast<int32_t*>(nullptr));
+}
+
+void compact_pattern(Ctx& c, const DCsr& N, const double* vals, int32_t bs, DCsr& out) {
+    DBuf<int32_t> cnt(static_cast<size_t>(N.nr) + 1, c.s);
+    launch(c, k_nonzero_count, blocks_for(N.nr, 256), 256, 0, N.nr, N.rp.get(), vals, cnt.get());
+    out.nr = N.nr;
+    out.nc = N.nc;
+    out.bs = bs;
+    out.rp.alloc(static_cast<size_t>(N.nr) + 1, c.s);
+    out.nnz = exclusive_scan_i32(c, cnt.get(), out.rp.get(), N.nr);
+    out.ci.alloc(static_cast<size_t>(out.nnz), c.s);
+    out.va.alloc(static_cast<size_t>(out.nnz), c.s);
+    launch(c, k_nonzero_write, blocks_for(N.nr, 256), 256, 0, N.nr, N.rp.get(), N.ci.get(), vals,
+           static_cast<const int32_t*>(out.rp.get()), out.ci.get(), out.va.get());
+}
+
+}  // namespace amgcu

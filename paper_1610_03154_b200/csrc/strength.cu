@@ -1,0 +1,627 @@
+// Strength of connection on the GPU (strength.hpp).
+//  symmetric / classical: thread per row, count + scan + write.
+//  evolution: one warp per row; the distance-`steps` neighbourhood in A + A^T
+//  lives in a shared-memory hash (global id -> local slot), the local Jacobi
+//  evolution z <- z - W^{-1} (A z) runs lane-parallel over the neighbourhood
+//  with each row sum in CSR order (strength.hpp:179-194), and the ring decision
+//  (strength.hpp:199-231) is taken over the merged A / A^T row.  Rows whose
+//  neighbourhood exceeds the shared capacity fall back to a block-per-row
+//  kernel over a direct-mapped global scratch.
+#include <climits>
+
+#include "ops.cuh"
+
+namespace amgcu {
+
+namespace {
+
+constexpr int kWarp = 32;
+
+__device__ __forceinline__ double diag_of(const int32_t* rp, const int32_t* ci, const double* va, int32_t i) {
+    int32_t lo = rp[i], hi = rp[i + 1];
+    while (lo < hi) {
+        const int32_t mid = (lo + hi) >> 1;
+        if (ci[mid] < i) lo = mid + 1;
+        else hi = mid;
+    }
+    return (lo < rp[i + 1] && ci[lo] == i) ? va[lo] : 0.0;
+}
+
+// ---- symmetric (strength.hpp:70-107) / classical (29-66) --------------------------------
+template <bool kSym>
+__device__ __forceinline__ bool strong(const double* d, int32_t i, int32_t j, double v, double theta, double mx,
+                                       double* val) {
+    if (kSym) {
+        const double raw = fabs(v) / sqrt(fabs(d[i]) * fabs(d[j]));
+        *val = raw;
+        return raw >= theta && raw > 0.0;
+    } else {
+        const double raw = -v;
+        *val = raw;
+        return mx > 0.0 && raw > 0.0 && raw >= theta * mx;
+    }
+}
+
+template <bool kSym>
+__global__ void k_soc(int32_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                      const double* __restrict__ va, const double* __restrict__ d, double theta,
+                      const int32_t* __restrict__ orp, int32_t* __restrict__ cnt, int32_t* __restrict__ oci,
+                      double* __restrict__ ova) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double mx = 0.0;
+    if (!kSym)
+        for (int32_t p = rp[i]; p < rp[i + 1]; ++p)
+            if (ci[p] != i && mx < -va[p]) mx = -va[p];  // std::max(mx, -a_ip)
+    int32_t o = orp ? orp[i] : 0;
+    bool dd = false;
+    for (int32_t p = rp[i]; p < rp[i + 1]; ++p) {
+        const int32_t j = ci[p];
+        if (j == i) continue;
+        double val;
+        if (strong<kSym>(d, i, j, va[p], theta, mx, &val)) {
+            if (!dd && j > i) {
+                if (orp) {
+                    oci[o] = i;
+                    ova[o] = 1.0;
+                }
+                ++o;
+                dd = true;
+            }
+            if (orp) {
+                oci[o] = j;
+                ova[o] = val;
+            }
+            ++o;
+        }
+    }
+    if (!dd) {  // diagonal goes last (every emitted column is < i)
+        if (orp) {
+            oci[o] = i;
+            ova[o] = 1.0;
+        }
+        ++o;
+    }
+    if (!orp) cnt[i] = o;
+}
+
+// ---- normalize_strength (strength.hpp:252-288) --------------------------------------------
+__global__ void k_normalize(int32_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                            const double* __restrict__ va, const int32_t* __restrict__ orp, int32_t* __restrict__ cnt,
+                            int32_t* __restrict__ oci, double* __restrict__ ova) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double mx = 0.0;
+    for (int32_t p = rp[i]; p < rp[i + 1]; ++p)
+        if (ci[p] != i && va[p] > mx) mx = va[p];
+    int32_t o = orp ? orp[i] : 0;
+    bool dd = false;
+    for (int32_t p = rp[i]; p < rp[i + 1]; ++p) {
+        const int32_t j = ci[p];
+        if (j == i || mx <= 0.0) continue;
+        const double v = va[p] / mx;
+        if (v == 0.0) continue;
+        if (!dd && j > i) {
+            if (orp) {
+                oci[o] = i;
+                ova[o] = 1.0;
+            }
+            ++o;
+            dd = true;
+        }
+        if (orp) {
+            oci[o] = j;
+            ova[o] = v;
+        }
+        ++o;
+    }
+    if (!dd) {
+        if (orp) {
+            oci[o] = i;
+            ova[o] = 1.0;
+        }
+        ++o;
+    }
+    if (!orp) cnt[i] = o;
+}
+
+__global__ void k_negative_check(int64_t nnz, const double* __restrict__ va, int32_t* __restrict__ bad) {
+    const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (p < nnz && va[p] < 0.0) atomicExch(bad, 1);
+}
+
+// ---- amalgamate (strength.hpp:292-324): node row = max |s| per block column ----------------
+__global__ void k_amalgamate(int32_t nn, int32_t m, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                             const double* __restrict__ va, const int32_t* __restrict__ orp, int32_t* __restrict__ cnt,
+                             int32_t* __restrict__ oci, double* __restrict__ ova) {
+    const int32_t bi = blockIdx.x * blockDim.x + threadIdx.x;
+    if (bi >= nn) return;
+    const int32_t lo = rp[bi * m], hi = rp[bi * m + m];
+    int32_t o = 0;
+    for (int32_t p = lo; p < hi; ++p) {
+        const int32_t bc = ci[p] / m;
+        bool first = true;  // first occurrence of this block column in the node row
+        for (int32_t q = lo; q < p; ++q)
+            if (ci[q] / m == bc) {
+                first = false;
+                break;
+            }
+        if (!first) continue;
+        double mx = 0.0;
+        for (int32_t q = p; q < hi; ++q)
+            if (ci[q] / m == bc) mx = fmax(mx, fabs(va[q]));
+        if (mx == 0.0) continue;
+        if (orp) {
+            int32_t rank = 0;  // distinct nonzero block columns smaller than bc
+            for (int32_t q = lo; q < hi; ++q) {
+                const int32_t oc = ci[q] / m;
+                if (oc >= bc) continue;
+                bool f = true;
+                for (int32_t r = lo; r < q; ++r)
+                    if (ci[r] / m == oc) {
+                        f = false;
+                        break;
+                    }
+                if (!f) continue;
+                double om = 0.0;
+                for (int32_t r = q; r < hi; ++r)
+                    if (ci[r] / m == oc) om = fmax(om, fabs(va[r]));
+                rank += (om != 0.0);
+            }
+            oci[orp[bi] + rank] = bc;
+            ova[orp[bi] + rank] = mx;
+        }
+        ++o;
+    }
+    if (!orp) cnt[bi] = o;
+}
+
+// ---- evolution (strength.hpp:116-238) -------------------------------------------------------
+constexpr int kEvWarps = 4;
+constexpr int kEvCap = 256;    // neighbourhood capacity per warp
+constexpr int kEvHash = 512;   // power of two
+
+struct EvShared {
+    int32_t nodes[kEvCap];
+    double z[kEvCap];
+    double zn[kEvCap];
+    int32_t hkey[kEvHash];
+    int32_t hval[kEvHash];
+    int32_t count;
+    int32_t overflow;
+};
+
+__device__ __forceinline__ uint32_t hslot(int32_t key) { return (static_cast<uint32_t>(key) * 2654435761u) & (kEvHash - 1); }
+
+__device__ __forceinline__ int32_t h_lookup(const EvShared& sh, int32_t key) {
+    uint32_t s = hslot(key);
+    for (int probe = 0; probe < kEvHash; ++probe) {
+        const int32_t k = sh.hkey[s];
+        if (k == key) return sh.hval[s];
+        if (k < 0) return -1;
+        s = (s + 1) & (kEvHash - 1);
+    }
+    return -1;
+}
+
+// insert; returns the new local id if this call inserted, -1 if present, -2 on overflow
+__device__ __forceinline__ int32_t h_insert(EvShared& sh, int32_t key) {
+    uint32_t s = hslot(key);
+    for (int probe = 0; probe < kEvHash; ++probe) {
+        const int32_t prev = atomicCAS(&sh.hkey[s], -1, key);
+        if (prev == -1) {
+            const int32_t id = atomicAdd(&sh.count, 1);
+            if (id >= kEvCap) {
+                sh.overflow = 1;
+                sh.hval[s] = -1;
+                return -2;
+            }
+            sh.nodes[id] = key;
+            sh.hval[s] = id;
+            return id;
+        }
+        if (prev == key) return -1;
+        s = (s + 1) & (kEvHash - 1);
+    }
+    sh.overflow = 1;
+    return -2;
+}
+
+__device__ __forceinline__ int32_t lower_bound_i32(const int32_t* a, int32_t lo, int32_t hi, int32_t key) {
+    while (lo < hi) {
+        const int32_t mid = (lo + hi) >> 1;
+        if (a[mid] < key) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+__global__ void __launch_bounds__(kEvWarps * kWarp)
+    k_evolution(int32_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci, const double* __restrict__ va,
+                const int32_t* __restrict__ trp, const int32_t* __restrict__ tci, const double* __restrict__ winv,
+                double drop_tol, int steps, const int64_t* __restrict__ ooff, int32_t* __restrict__ cnt,
+                int32_t* __restrict__ tcol, double* __restrict__ tval, int32_t* __restrict__ overflow_rows,
+                int32_t* __restrict__ n_overflow) {
+    __shared__ EvShared shm[kEvWarps];
+    const int w = threadIdx.x / kWarp, lane = threadIdx.x & (kWarp - 1);
+    const int32_t i = blockIdx.x * kEvWarps + w;
+    if (i >= n) return;
+    EvShared& sh = shm[w];
+    for (int s = lane; s < kEvHash; s += kWarp) sh.hkey[s] = -1;
+    if (lane == 0) {
+        sh.count = 0;
+        sh.overflow = 0;
+    }
+    __syncwarp();
+    if (lane == 0) h_insert(sh, i);
+    __syncwarp();
+    int32_t lo = 0;
+    for (int st = 0; st < steps; ++st) {
+        const int32_t hi = min(sh.count, kEvCap);
+        for (int32_t f = lo; f < hi; ++f) {
+            const int32_t u = sh.nodes[f];
+            for (int32_t p = rp[u] + lane; p < rp[u + 1]; p += kWarp) h_insert(sh, ci[p]);
+            for (int32_t p = trp[u] + lane; p < trp[u + 1]; p += kWarp) h_insert(sh, tci[p]);
+        }
+        __syncwarp();
+        lo = hi;
+        if (sh.overflow) break;
+    }
+    __syncwarp();
+    if (sh.overflow) {
+        if (lane == 0) overflow_rows[atomicAdd(n_overflow, 1)] = i;
+        return;
+    }
+    const int32_t nb = sh.count;
+    for (int32_t t = lane; t < nb; t += kWarp) sh.z[t] = (t == 0) ? 1.0 : 0.0;
+    __syncwarp();
+    double* z = sh.z;
+    double* zn = sh.zn;
+    for (int st = 0; st < steps; ++st) {
+        for (int32_t t = lane; t < nb; t += kWarp) {
+            const int32_t u = sh.nodes[t];
+            double az = 0.0;
+            for (int32_t p = rp[u]; p < rp[u + 1]; ++p) {
+                const int32_t lj = h_lookup(sh, ci[p]);
+                if (lj >= 0) az += va[p] * z[lj];
+            }
+            zn[t] = z[t] - winv[u] * az;
+        }
+        __syncwarp();
+        double* tmp = z;
+        z = zn;
+        zn = tmp;
+    }
+    // ring: A row i followed by the A^T entries not in A row i, each ranked in the union
+    const int32_t alo = rp[i], ahi = rp[i + 1], tlo = trp[i], thi = trp[i + 1];
+    const int32_t na = ahi - alo, nt = thi - tlo;
+    double mx = 0.0;
+    for (int32_t e = lane; e < na + nt; e += kWarp) {
+        int32_t j;
+        if (e < na) {
+            j = ci[alo + e];
+        } else {
+            j = tci[tlo + e - na];
+            const int32_t pos = lower_bound_i32(ci, alo, ahi, j);
+            if (pos < ahi && ci[pos] == j) continue;
+        }
+        if (j == i) continue;
+        const int32_t lj = h_lookup(sh, j);
+        if (lj >= 0) mx = fmax(mx, fabs(z[lj]));
+    }
+    for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    const double cutoff = mx / drop_tol;
+    const double zi = fabs(z[0]);
+    const double dval = zi > 0.0 ? zi : 1.0;
+    int32_t* ocol = tcol + ooff[i];
+    double* oval = tval + ooff[i];
+    // emitted entries: rank among emitted = #emitted ring entries with smaller column,
+    // +1 if the diagonal precedes it
+    int32_t emitted_total = 0;
+    int32_t below_i = 0;  // emitted columns < i
+    for (int32_t e0 = 0; e0 < na + nt; e0 += kWarp) {
+        const int32_t e = e0 + lane;
+        bool emit = false;
+        int32_t j = -1;
+        double mag = 0.0;
+        if (e < na + nt) {
+            bool dup = false;
+            if (e < na) {
+                j = ci[alo + e];
+            } else {
+                j = tci[tlo + e - na];
+                const int32_t pos = lower_bound_i32(ci, alo, ahi, j);
+                dup = (pos < ahi && ci[pos] == j);
+            }
+            if (!dup && j != i) {
+                const int32_t lj = h_lookup(sh, j);
+                mag = lj >= 0 ? fabs(z[lj]) : 0.0;
+                emit = mx > 0.0 && mag >= cutoff && mag > 0.0;
+            }
+        }
+        const unsigned b = __ballot_sync(0xffffffffu, emit);
+        emitted_total += __popc(b);
+        const unsigned bl = __ballot_sync(0xffffffffu, emit && j < i);
+        below_i += __popc(bl);
+        if (emit) {
+            // rank among emitted: count emitted ring entries with smaller column
+            int32_t rank = 0;
+            for (int32_t f = 0; f < na + nt; ++f) {
+                int32_t jf;
+                if (f < na) {
+                    jf = ci[alo + f];
+                } else {
+                    jf = tci[tlo + f - na];
+                    const int32_t pos = lower_bound_i32(ci, alo, ahi, jf);
+                    if (pos < ahi && ci[pos] == jf) continue;
+                }
+                if (jf >= j || jf == i) continue;
+                const int32_t lf = h_lookup(sh, jf);
+                const double mf = lf >= 0 ? fabs(z[lf]) : 0.0;
+                rank += (mx > 0.0 && mf >= cutoff && mf > 0.0) ? 1 : 0;
+            }
+            const int32_t at = rank + (j > i ? 1 : 0);
+            ocol[at] = j;
+            oval[at] = mag;
+        }
+    }
+    if (lane == 0) {
+        ocol[below_i] = i;
+        oval[below_i] = dval;
+        cnt[i] = emitted_total + 1;
+    }
+}
+
+// Fallback: block per row over a direct-mapped global scratch (local id per node).
+constexpr int kEvBigThreads = 256;
+
+__global__ void __launch_bounds__(kEvBigThreads)
+    k_evolution_big(const int32_t* __restrict__ rows, int32_t n, const int32_t* __restrict__ rp,
+                    const int32_t* __restrict__ ci, const double* __restrict__ va, const int32_t* __restrict__ trp,
+                    const int32_t* __restrict__ tci, const double* __restrict__ winv, double drop_tol, int steps,
+                    const int64_t* __restrict__ ooff, int32_t* __restrict__ cnt, int32_t* __restrict__ tcol,
+                    double* __restrict__ tval, int32_t* __restrict__ gslot, int32_t* __restrict__ gnodes,
+                    double* __restrict__ gz, double* __restrict__ gzn) {
+    const int32_t i = rows[blockIdx.x];
+    int32_t* slot = gslot + static_cast<int64_t>(blockIdx.x) * n;
+    int32_t* nodes = gnodes + static_cast<int64_t>(blockIdx.x) * n;
+    double* z = gz + static_cast<int64_t>(blockIdx.x) * n;
+    double* zn = gzn + static_cast<int64_t>(blockIdx.x) * n;
+    __shared__ int32_t count;
+    __shared__ double red[kEvBigThreads / 32];
+    for (int32_t t = threadIdx.x; t < n; t += blockDim.x) slot[t] = -1;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        slot[i] = 0;
+        nodes[0] = i;
+        count = 1;
+    }
+    __syncthreads();
+    int32_t lo = 0;
+    for (int st = 0; st < steps; ++st) {
+        const int32_t hi = count;
+        __syncthreads();
+        for (int32_t f = lo; f < hi; ++f) {
+            const int32_t u = nodes[f];
+            for (int32_t p = rp[u] + threadIdx.x; p < rp[u + 1]; p += blockDim.x) {
+                const int32_t j = ci[p];
+                if (atomicCAS(&slot[j], -1, -2) == -1) {
+                    const int32_t id = atomicAdd(&count, 1);
+                    nodes[id] = j;
+                    atomicExch(&slot[j], id);
+                }
+            }
+            for (int32_t p = trp[u] + threadIdx.x; p < trp[u + 1]; p += blockDim.x) {
+                const int32_t j = tci[p];
+                if (atomicCAS(&slot[j], -1, -2) == -1) {
+                    const int32_t id = atomicAdd(&count, 1);
+                    nodes[id] = j;
+                    atomicExch(&slot[j], id);
+                }
+            }
+            __syncthreads();
+        }
+        lo = hi;
+    }
+    __syncthreads();
+    const int32_t nb = count;
+    for (int32_t t = threadIdx.x; t < nb; t += blockDim.x) z[t] = (t == 0) ? 1.0 : 0.0;
+    __syncthreads();
+    for (int st = 0; st < steps; ++st) {
+        for (int32_t t = threadIdx.x; t < nb; t += blockDim.x) {
+            const int32_t u = nodes[t];
+            double az = 0.0;
+            for (int32_t p = rp[u]; p < rp[u + 1]; ++p) {
+                const int32_t lj = slot[ci[p]];
+                if (lj >= 0) az += va[p] * z[lj];
+            }
+            zn[t] = z[t] - winv[u] * az;
+        }
+        __syncthreads();
+        double* tmp = z;
+        z = zn;
+        zn = tmp;
+    }
+    const int32_t alo = rp[i], ahi = rp[i + 1], tlo = trp[i], thi = trp[i + 1];
+    const int32_t na = ahi - alo, nt = thi - tlo;
+    auto ring_at = [&](int32_t e, bool* dup) -> int32_t {
+        if (e < na) {
+            *dup = false;
+            return ci[alo + e];
+        }
+        const int32_t j = tci[tlo + e - na];
+        const int32_t pos = lower_bound_i32(ci, alo, ahi, j);
+        *dup = (pos < ahi && ci[pos] == j);
+        return j;
+    };
+    double mx = 0.0;
+    for (int32_t e = threadIdx.x; e < na + nt; e += blockDim.x) {
+        bool dup;
+        const int32_t j = ring_at(e, &dup);
+        if (dup || j == i) continue;
+        const int32_t lj = slot[j];
+        if (lj >= 0) mx = fmax(mx, fabs(z[lj]));
+    }
+    for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x / 32] = mx;
+    __syncthreads();
+    mx = 0.0;
+    for (int t = 0; t < static_cast<int>(blockDim.x / 32); ++t) mx = fmax(mx, red[t]);
+    const double cutoff = mx / drop_tol;
+    const double zi = fabs(z[0]);
+    const double dval = zi > 0.0 ? zi : 1.0;
+    int32_t* ocol = tcol + ooff[i];
+    double* oval = tval + ooff[i];
+    __shared__ int32_t s_tot, s_below;
+    if (threadIdx.x == 0) {
+        s_tot = 0;
+        s_below = 0;
+    }
+    __syncthreads();
+    for (int32_t e = threadIdx.x; e < na + nt; e += blockDim.x) {
+        bool dup;
+        const int32_t j = ring_at(e, &dup);
+        if (dup || j == i) continue;
+        const int32_t lj = slot[j];
+        const double mag = lj >= 0 ? fabs(z[lj]) : 0.0;
+        if (!(mx > 0.0 && mag >= cutoff && mag > 0.0)) continue;
+        atomicAdd(&s_tot, 1);
+        if (j < i) atomicAdd(&s_below, 1);
+        int32_t rank = 0;
+        for (int32_t f = 0; f < na + nt; ++f) {
+            bool d2;
+            const int32_t jf = ring_at(f, &d2);
+            if (d2 || jf >= j || jf == i) continue;
+            const int32_t lf = slot[jf];
+            const double mf = lf >= 0 ? fabs(z[lf]) : 0.0;
+            rank += (mx > 0.0 && mf >= cutoff && mf > 0.0) ? 1 : 0;
+        }
+        const int32_t at = rank + (j > i ? 1 : 0);
+        ocol[at] = j;
+        oval[at] = mag;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        ocol[s_below] = i;
+        oval[s_below] = dval;
+        cnt[i] = s_tot + 1;
+    }
+}
+
+__global__ void k_ring_capacity(int32_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ trp,
+                                int64_t* __restrict__ cap) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    cap[i] = (rp[i + 1] - rp[i]) + (trp[i + 1] - trp[i]) + 1;
+}
+
+__global__ void k_copy_rows64(int32_t nr, const int64_t* __restrict__ off, const int32_t* __restrict__ tcol,
+                              const double* __restrict__ tval, const int32_t* __restrict__ orp, int32_t* __restrict__ oci,
+                              double* __restrict__ ova) {
+    const int32_t i = (blockIdx.x * blockDim.x + threadIdx.x) / kWarp;
+    const int lane = threadIdx.x & (kWarp - 1);
+    if (i >= nr) return;
+    const int64_t src = off[i];
+    const int32_t dst = orp[i], len = orp[i + 1] - dst;
+    for (int32_t e = lane; e < len; e += kWarp) {
+        oci[dst + e] = tcol[src + e];
+        ova[dst + e] = tval[src + e];
+    }
+}
+
+template <typename CountK, typename... Args>
+void two_pass(Ctx& c, int32_t n_out_rows, int32_t nc, int32_t bs, DCsr& S, CountK k, unsigned grid, unsigned block,
+              Args... args) {
+    DBuf<int32_t> cnt(static_cast<size_t>(n_out_rows) + 1, c.s);
+    launch(c, k, grid, block, 0, args..., static_cast<const int32_t*>(nullptr), cnt.get(), static_cast<int32_t*>(nullptr),
+           static_cast<double*>(nullptr));
+    S.nr = n_out_rows;
+    S.nc = nc;
+    S.bs = bs;
+    S.rp.alloc(static_cast<size_t>(n_out_rows) + 1, c.s);
+    S.nnz = exclusive_scan_i32(c, cnt.get(), S.rp.get(), n_out_rows);
+    S.ci.alloc(static_cast<size_t>(S.nnz), c.s);
+    S.va.alloc(static_cast<size_t>(S.nnz), c.s);
+    launch(c, k, grid, block, 0, args..., static_cast<const int32_t*>(S.rp.get()), cnt.get(), S.ci.get(), S.va.get());
+}
+
+}  // namespace
+
+void symmetric_strength(Ctx& c, const DCsr& A, double theta, DCsr& S) {
+    if (A.nr != A.nc) throw InvalidArgument("symmetric_strength: square matrix required");
+    if (theta < 0.0 || theta > 1.0) throw InvalidArgument("symmetric_strength: theta must lie in [0, 1]");
+    DBuf<double> d(static_cast<size_t>(A.nr), c.s);
+    diagonal(c, A, d.get());
+    // zero diagonal -> runtime_error with the lowest such row (strength.hpp:75-77)
+    DBuf<double> dinv(static_cast<size_t>(A.nr), c.s);
+    inverse_diagonal(c, A, dinv.get(), "symmetric_strength: zero diagonal at row ");
+    two_pass(c, A.nr, A.nc, A.bs, S, k_soc<true>, blocks_for(A.nr, 128), 128, A.nr, A.rp.get(), A.ci.get(), A.va.get(),
+             static_cast<const double*>(d.get()), theta);
+}
+
+void classical_strength(Ctx& c, const DCsr& A, double theta, DCsr& S) {
+    if (A.nr != A.nc) throw InvalidArgument("classical_strength: square matrix required");
+    if (theta < 0.0 || theta > 1.0) throw InvalidArgument("classical_strength: theta must lie in [0, 1]");
+    two_pass(c, A.nr, A.nc, A.bs, S, k_soc<false>, blocks_for(A.nr, 128), 128, A.nr, A.rp.get(), A.ci.get(),
+             A.va.get(), static_cast<const double*>(nullptr), theta);
+}
+
+void normalize_strength(Ctx& c, const DCsr& S, DCsr& N) {
+    if (S.nr != S.nc) throw InvalidArgument("normalize_strength: square matrix required");
+    DBuf<int32_t> bad(1, c.s);
+    AMG_CK(cudaMemsetAsync(bad.get(), 0, sizeof(int32_t), c.s));
+    launch(c, k_negative_check, blocks_for(S.nnz, 256), 256, 0, S.nnz, S.va.get(), bad.get());
+    if (read_scalar(c, bad.get())) throw InvalidArgument("normalize_strength: negative strength value");
+    two_pass(c, S.nr, S.nc, S.bs, N, k_normalize, blocks_for(S.nr, 128), 128, S.nr, S.rp.get(), S.ci.get(), S.va.get());
+}
+
+void amalgamate(Ctx& c, const DCsr& S, int32_t m, DCsr& N) {
+    if (m < 1) throw InvalidArgument("amalgamate: block size must be >= 1");
+    if (m == 1) {
+        clone_csr(c, S, N);
+        return;
+    }
+    if (S.nr % m != 0 || S.nc % m != 0) throw InvalidArgument("amalgamate: dimensions not divisible by block size");
+    const int32_t nn = S.nr / m;
+    two_pass(c, nn, S.nc / m, 1, N, k_amalgamate, blocks_for(nn, 128), 128, nn, m, S.rp.get(), S.ci.get(), S.va.get());
+}
+
+void evolution_strength(Ctx& c, const DCsr& A, const DCsr& At, const double* winv, double drop_tol, int steps,
+                        DCsr& S) {
+    const int32_t n = A.nr;
+    DBuf<int64_t> cap(static_cast<size_t>(n) + 1, c.s), off(static_cast<size_t>(n) + 1, c.s);
+    launch(c, k_ring_capacity, blocks_for(n, 256), 256, 0, n, A.rp.get(), At.rp.get(), cap.get());
+    const int64_t total = exclusive_scan_i64(c, cap.get(), off.get(), n);
+    DBuf<int32_t> tcol(static_cast<size_t>(total), c.s), cnt(static_cast<size_t>(n) + 1, c.s);
+    DBuf<double> tval(static_cast<size_t>(total), c.s);
+    DBuf<int32_t> ovf(static_cast<size_t>(n), c.s), novf(1, c.s);
+    AMG_CK(cudaMemsetAsync(novf.get(), 0, sizeof(int32_t), c.s));
+    launch(c, k_evolution, blocks_for(n, kEvWarps), kEvWarps * kWarp, 0, n, A.rp.get(), A.ci.get(), A.va.get(),
+           At.rp.get(), At.ci.get(), winv, drop_tol, steps, static_cast<const int64_t*>(off.get()), cnt.get(),
+           tcol.get(), tval.get(), ovf.get(), novf.get());
+    const int32_t nbig = read_scalar(c, novf.get());
+    if (nbig > 0) {
+        const int32_t conc = std::min<int32_t>(nbig, 64);
+        DBuf<int32_t> gslot(static_cast<size_t>(conc) * n, c.s), gnodes(static_cast<size_t>(conc) * n, c.s);
+        DBuf<double> gz(static_cast<size_t>(conc) * n, c.s), gzn(static_cast<size_t>(conc) * n, c.s);
+        for (int32_t b0 = 0; b0 < nbig; b0 += conc) {
+            const int32_t nb = std::min(conc, nbig - b0);
+            launch(c, k_evolution_big, static_cast<unsigned>(nb), kEvBigThreads, 0,
+                   static_cast<const int32_t*>(ovf.get() + b0), n, A.rp.get(), A.ci.get(), A.va.get(), At.rp.get(),
+                   At.ci.get(), winv, drop_tol, steps, static_cast<const int64_t*>(off.get()), cnt.get(), tcol.get(),
+                   tval.get(), gslot.get(), gnodes.get(), gz.get(), gzn.get());
+        }
+    }
+    S.nr = n;
+    S.nc = n;
+    S.bs = A.bs;
+    S.rp.alloc(static_cast<size_t>(n) + 1, c.s);
+    S.nnz = exclusive_scan_i32(c, cnt.get(), S.rp.get(), n);
+    S.ci.alloc(static_cast<size_t>(S.nnz), c.s);
+    S.va.alloc(static_cast<size_t>(S.nnz), c.s);
+    launch(c, k_copy_rows64, blocks_for(static_cast<int64_t>(n) * kWarp, 256), 256, 0, n,
+           static_cast<const int64_t*>(off.get()), static_cast<const int32_t*>(tcol.get()),
+           static_cast<const double*>(tval.get()), static_cast<const int32_t*>(S.rp.get()), S.ci.get(), S.va.get());
+}
+
+}  // namespace amgcu

@@ -1,0 +1,158 @@
+"""GPU kernel parity: each libamgcu entry point against the CPU oracle on the
+same inputs.  Integer structure and every fp64 value must be bit-identical
+(the kernels keep the reference's per-entry operation order, --fmad=false);
+reductions that the reference takes sequentially are bit-identical in the
+sequential-reduction context (gpu_seq) and within 1e-12 otherwise."""
+import numpy as np
+import pytest
+
+import paper_1610_03154_b200.api as api
+from paper_1610_03154_b200.types import (CandidateSet, StrengthConfig, StrengthMeasure, constant_candidates,
+                                         from_triplets, identity)
+from tests.helpers import aniso2d, poisson1d, random_sparse, random_spd_sparse, rel_max_err, tridiag
+
+pytestmark = pytest.mark.gpu
+
+
+def bitwise(a, b):
+    return a == b
+
+
+def test_spmv_bitwise(gpu, port):
+    rng = np.random.default_rng(42)
+    for _ in range(20):
+        n, m = rng.integers(2, 80, size=2)
+        A = random_sparse(int(n), int(m), 0.3, rng)
+        x = rng.uniform(-1, 1, int(m))
+        assert api.spmv(A, x, ctx=gpu).tobytes() == port.spmv(A, x).tobytes()
+
+
+def test_transpose_bitwise(gpu, port):
+    rng = np.random.default_rng(7)
+    for _ in range(20):
+        n, m = rng.integers(1, 90, size=2)
+        A = random_sparse(int(n), int(m), 0.25, rng)
+        assert bitwise(api.transpose(A, ctx=gpu), port.transpose(A))
+    assert api.transpose(identity(4), ctx=gpu) == identity(4)
+
+
+def test_matmul_bitwise_random(gpu, port):
+    """test_sparse_core.cpp:70-96 shapes (100 random instances)"""
+    rng = np.random.default_rng(42)
+    for _ in range(100):
+        n, m, k = (int(v) for v in rng.integers(2, 65, size=3))
+        A = random_sparse(n, m, 0.3, rng)
+        B = random_sparse(m, k, 0.3, rng)
+        assert api.matmul(A, B, ctx=gpu) == port.matmul(A, B)
+        R = random_sparse(k, n, 0.3, rng)
+        assert api.galerkin_product(R, A, B, ctx=gpu) == port.galerkin_product(R, A, B)
+
+
+def test_matmul_long_rows_and_cancellation(gpu, port):
+    """rows above the shared-memory capacity and exact-zero drops (sparse.hpp:208)"""
+    rng = np.random.default_rng(3)
+    A = random_sparse(30, 400, 0.9, rng)
+    B = random_sparse(400, 300, 0.5, rng)
+    assert api.matmul(A, B, ctx=gpu) == port.matmul(A, B)
+    # exact cancellation: (1, -1) . (x, x) = 0 is dropped
+    A2 = from_triplets(2, 2, [(0, 0, 1.0), (0, 1, -1.0), (1, 1, 2.0)])
+    B2 = from_triplets(2, 1, [(0, 0, 3.0), (1, 0, 3.0)])
+    C = api.matmul(A2, B2, ctx=gpu)
+    assert C == port.matmul(A2, B2)
+    assert C.nnz() == 1
+
+
+def test_filter_matrix(gpu, port):
+    rng = np.random.default_rng(17)
+    for _ in range(20):
+        G = random_sparse(12, 12, 0.45, rng)
+        for theta, k in [(0.3, 2), (0.0, None), (None, 1), (0.1, None), (None, 3)]:
+            assert api.filter_matrix(G, theta, k, ctx=gpu) == port.filter_matrix(G, theta, k)
+        R = random_sparse(9, 5, 0.6, rng)
+        assert api.filter_matrix(R, 0.4, 2, ctx=gpu) == port.filter_matrix(R, 0.4, 2)
+
+
+def test_is_symmetric(gpu, port):
+    rng = np.random.default_rng(5)
+    A = random_spd_sparse(24, 0.3, rng)
+    assert api.is_symmetric(A, ctx=gpu) and port.is_symmetric(A)
+    B = random_sparse(20, 20, 0.3, rng)
+    assert api.is_symmetric(B, ctx=gpu) == port.is_symmetric(B)
+    U = from_triplets(3, 3, [(0, 0, 1.0), (0, 1, 1e-20), (1, 1, 1.0), (2, 2, 1.0)])
+    assert api.is_symmetric(U, ctx=gpu) == port.is_symmetric(U)
+
+
+def test_spectral_radius(gpu_seq, gpu, port):
+    for A in (poisson1d(32), aniso2d(12, 0.1), aniso2d(20, 1.0)):
+        want = port.spectral_radius_estimate(A)
+        assert api.spectral_radius_estimate(A, ctx=gpu_seq) == want
+        assert abs(api.spectral_radius_estimate(A, ctx=gpu) - want) <= 1e-12 * want
+
+
+@pytest.mark.parametrize("measure,tol", [(StrengthMeasure.symmetric, 0.25), (StrengthMeasure.symmetric, 0.0),
+                                         (StrengthMeasure.classical, 0.25), (StrengthMeasure.evolution, 4.0)])
+def test_strength(gpu_seq, port, measure, tol):
+    for A in (poisson1d(16), aniso2d(10, 0.001), aniso2d(9, 1.0), tridiag(12, -1.0, 4.0, -2.0)):
+        cfg = StrengthConfig(measure, tol)
+        S = api.strength(A, cfg, ctx=gpu_seq)
+        assert S == port.strength(A, cfg)
+        N = api.normalize_strength(S, ctx=gpu_seq)
+        assert N == port.normalize_strength(S)
+        n, own, roots = api.greedy_aggregate(N, ctx=gpu_seq)
+        n2, own2, roots2 = port.greedy_aggregate(N)
+        assert n == n2 and np.array_equal(own, own2) and np.array_equal(roots, roots2)
+
+
+def test_amalgamate(gpu, port):
+    rng = np.random.default_rng(29)
+    R = random_sparse(12, 12, 0.3, rng)
+    for m in (1, 2, 3):
+        assert api.amalgamate(R, m, ctx=gpu) == port.amalgamate(R, m)
+
+
+def test_aggregation_known_answers(gpu):
+    """test_aggregation.cpp:18-49"""
+    def path(n):
+        return api.normalize_strength(api.strength(poisson1d(n), StrengthConfig(StrengthMeasure.symmetric, 0.0),
+                                                   ctx=gpu), ctx=gpu)
+    n, own, roots = api.greedy_aggregate(path(8), ctx=gpu)
+    assert n == 3 and list(roots) == [0, 3, 6] and list(own) == [0, 0, 1, 1, 1, 2, 2, 2]
+    n, own, roots = api.greedy_aggregate(path(5), ctx=gpu)
+    assert n == 2 and list(roots) == [0, 3] and list(own) == [0, 0, 1, 1, 1]
+    n, own, roots = api.greedy_aggregate(identity(5), ctx=gpu)
+    assert n == 5 and list(roots) == list(range(5))
+    n, own, roots = api.greedy_aggregate(path(3), ctx=gpu)
+    assert n == 1 and list(roots) == [0] and list(own) == [0, 0, 0]
+
+
+def test_aggregation_random(gpu, port):
+    rng = np.random.default_rng(31)
+    for _ in range(10):
+        R = random_sparse(200, 200, 0.02, rng)
+        R.values = np.abs(R.values)
+        S = port.normalize_strength(R)
+        a = api.greedy_aggregate(S, ctx=gpu)
+        b = port.greedy_aggregate(S)
+        assert a[0] == b[0] and np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2])
+
+
+def test_improve_candidates(gpu_seq, port):
+    rng = np.random.default_rng(19)
+    A = random_spd_sparse(40, 0.2, rng)
+    for A_ in (A, poisson1d(30), aniso2d(8, 0.1)):
+        B = constant_candidates(A_.n_rows)
+        for scheme, w in ((1, 0.0), (2, 0.0), (0, 0.6), (0, 0.0)):
+            got = api.improve_candidates(A_, B, 4, scheme, w, ctx=gpu_seq)
+            want = port.improve_candidates(A_, B, 4, scheme, w)
+            assert got.data.tobytes() == want.data.tobytes(), (scheme, w)
+
+
+def test_relax(gpu_seq, port):
+    rng = np.random.default_rng(3)
+    A = random_spd_sparse(20, 0.25, rng)
+    b = rng.uniform(-1, 1, 20)
+    x0 = rng.uniform(-1, 1, 20)
+    for scheme, w, sw in ((0, 1.0, 3), (1, 0.0, 2), (2, 0.0, 2), (0, 0.0, 1)):
+        got = api.relax(A, scheme, w, sw, x0, b, ctx=gpu_seq)
+        want = port.relax(A, scheme, w, sw, x0, b)
+        assert got.tobytes() == want.tobytes(), (scheme, w, sw)

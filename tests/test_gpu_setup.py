@@ -1,0 +1,157 @@
+"""GPU rn_setup + solve against the CPU oracle on small problems covering every
+branch of the path: symmetric SOC + CG (C1-like), evolution SOC + prefilter
+(C2-like), nonsymmetric GMRES with separate restriction (C3/C4-like), and
+block elasticity with k = 3 > m = 2 (C5-like).
+
+Parity classes: in the sequential-reduction context every
+level's A, P, R, B, Bc must be bit-identical; in the default context the
+structure (row offsets, column indices, aggregates) must be identical and the
+values within 1e-10 relative.  Solve: residual histories within 1e-10
+relative (the coarsest solve is a pseudo-inverse product on the GPU and a COD
+solve on the CPU), iteration counts equal."""
+import numpy as np
+import pytest
+
+import paper_1610_03154_b200.api as api
+from paper_1610_03154_b200.types import (FilterRule, KrylovKind, RelaxConfig, RelaxScheme, SetupOptions,
+                                         SolveMethod, SolveOptions, StrengthConfig, StrengthMeasure,
+                                         constant_candidates)
+from tests.helpers import aniso2d, poisson1d, rel_max_err, same_structure
+
+pytestmark = pytest.mark.gpu
+
+JAC = RelaxConfig(RelaxScheme.jacobi, 0.0, 1)
+
+
+def _cases():
+    cases = []
+    # C1-like: 5-point Poisson, symmetric SOC 0.25, degree 2, 4 CG iterations
+    cases.append(("poisson", lambda: api.generate_config(1, 24),
+                  SetupOptions(strength=StrengthConfig(StrengthMeasure.symmetric, 0.25), pre_relax=JAC, post_relax=JAC,
+                               max_size=30), SolveOptions(SolveMethod.pcg)))
+    # C2-like: rotated anisotropic Q1, evolution SOC, prefilter 0.1, 6 CG iterations
+    so = SetupOptions(pre_relax=JAC, post_relax=JAC, max_size=40)
+    so.interp.prefilter = FilterRule(0.1, None)
+    so.interp.energy_iters = 6
+    cases.append(("rotated", lambda: api.generate_config(2, 25), so, SolveOptions(SolveMethod.pcg)))
+    # C3-like: recirculating convection-diffusion, GMRES energy-min, FGMRES
+    so = SetupOptions(pre_relax=JAC, post_relax=JAC, max_size=40)
+    so.interp.krylov = KrylovKind.gmres
+    so.interp.energy_iters = 4
+    cases.append(("recirc", lambda: api.generate_config(3, 24), so, SolveOptions(SolveMethod.fgmres, max_iters=30)))
+    # C4-like: upwind transport, degree 3, no candidate sweeps
+    so = SetupOptions(pre_relax=JAC, post_relax=JAC, max_size=40, candidate_sweeps=0)
+    so.interp.krylov = KrylovKind.gmres
+    so.interp.degree = 3
+    so.interp.energy_iters = 4
+    cases.append(("transport", lambda: api.generate_config(4, 24), so, SolveOptions(SolveMethod.fgmres, max_iters=30)))
+    # C5-like: Q1 plane strain, k = 3 rigid-body modes, block size 2
+    so = SetupOptions(strength=StrengthConfig(StrengthMeasure.symmetric, 0.1), pre_relax=JAC, post_relax=JAC,
+                      max_size=40)
+    so.interp.energy_iters = 4
+    cases.append(("elasticity", lambda: api.generate_config(5, 10), so, SolveOptions(SolveMethod.pcg)))
+    return cases
+
+
+CASES = _cases()
+
+
+def compare(hg, ho, bitwise):
+    assert hg.n_levels() == ho.n_levels()
+    assert hg.stagnated == ho.stagnated
+    L = hg.n_levels()
+    for l in range(L):
+        assert hg.symmetric(l) == ho.symmetric(l), l
+        for which in ((0, 1, 2) if l < L - 1 else (0,)):
+            a, b = hg.matrix(l, which), ho.matrix(l, which)
+            assert same_structure(a, b), (l, which)
+            if bitwise:
+                assert a.values.tobytes() == b.values.tobytes(), (l, which)
+            else:
+                assert rel_max_err(a.values, b.values) <= 1e-10, (l, which)
+        ca, cb = hg.candidates(l, 0), ho.candidates(l, 0)
+        if bitwise:
+            assert ca.data.tobytes() == cb.data.tobytes(), l
+        else:
+            assert rel_max_err(ca.data, cb.data) <= 1e-10, l
+
+
+@pytest.mark.parametrize("name,gen,so,vo", CASES, ids=[c[0] for c in CASES])
+def test_setup_bitwise_sequential(gpu_seq, port, name, gen, so, vo):
+    A, B, Bh, b = gen()
+    hg = api.setup(A, B, so, Bh, ctx=gpu_seq)
+    ho = port.setup(A, B, so, Bh)
+    compare(hg, ho, bitwise=True)
+    for l in range(hg.n_levels() - 1):
+        assert hg.relax_weights(l) == ho.relax_weights(l)
+    xg, rg = api.solve(hg, b, None, vo)
+    xo, ro = port.solve(ho, b, None, vo)
+    assert rg.iterations == ro.iterations and rg.converged == ro.converged
+    assert rel_max_err(rg.residual_history, ro.residual_history) <= 1e-10
+    assert rel_max_err(xg, xo) <= 1e-10
+    assert rg.chi_oc == ro.chi_oc and rg.chi_cc == ro.chi_cc
+
+
+@pytest.mark.parametrize("name,gen,so,vo", CASES, ids=[c[0] for c in CASES])
+def test_setup_parallel_reductions(gpu, port, name, gen, so, vo):
+    A, B, Bh, b = gen()
+    hg = api.setup(A, B, so, Bh, ctx=gpu)
+    ho = port.setup(A, B, so, Bh)
+    compare(hg, ho, bitwise=False)
+    xg, rg = api.solve(hg, b, None, vo)
+    xo, ro = port.solve(ho, b, None, vo)
+    assert rg.iterations == ro.iterations
+    assert rel_max_err(rg.residual_history, ro.residual_history) <= 1e-10
+
+
+def test_line_hierarchy_known_answers(gpu):
+    """test_hierarchy.cpp:23-34: 8-point line -> 3 coarse rows, R == P^T, A1 == RAP bitwise"""
+    A = poisson1d(8)
+    so = SetupOptions(strength=StrengthConfig(StrengthMeasure.symmetric, 0.0), max_size=2)
+    h = api.setup(A, constant_candidates(8), so, ctx=gpu)
+    assert h.n_levels() >= 2
+    assert h.matrix(1, 0).n_rows == 3
+    assert h.symmetric(0)
+    P, R = h.matrix(0, 1), h.matrix(0, 2)
+    assert R == api.transpose(P, ctx=gpu)
+    assert h.matrix(1, 0) == api.galerkin_product(R, A, P, ctx=gpu)
+
+
+def test_solve_zero_rhs(gpu):
+    """test_cycle.cpp:44-54"""
+    A = poisson1d(16)
+    h = api.setup(A, constant_candidates(16), SetupOptions(max_size=4, pre_relax=JAC, post_relax=JAC), ctx=gpu)
+    x, rep = api.solve(h, np.zeros(16))
+    assert rep.converged and rep.iterations == 0 and not np.any(x)
+
+
+def test_single_level_direct(gpu):
+    """test_cycle.cpp:28-42"""
+    A = poisson1d(12)
+    h = api.setup(A, constant_candidates(12), SetupOptions(max_size=20), ctx=gpu)
+    assert h.n_levels() == 1
+    rng = np.random.default_rng(7)
+    want = rng.uniform(-1, 1, 12)
+    b = api.spmv(A, want, ctx=gpu)
+    x, rep = api.solve(h, b)
+    assert rep.converged and rep.iterations == 1
+    assert np.max(np.abs(x - want)) < 1e-12
+
+
+def test_stationary_vcycle_contracts(gpu):
+    """test_cycle.cpp:75-88 with weighted Jacobi smoothing"""
+    A = aniso2d(32, 1.0)
+    h = api.setup(A, constant_candidates(A.n_rows), SetupOptions(pre_relax=JAC, post_relax=JAC), ctx=gpu)
+    rng = np.random.default_rng(3)
+    b = rng.uniform(-1, 1, A.n_rows)
+    x, rep = api.solve(h, b, None, SolveOptions(tol=1e-10, max_iters=60))
+    assert rep.converged
+
+
+def test_errors_map_to_reference_exceptions(gpu):
+    with pytest.raises(ValueError):
+        api.setup(poisson1d(4), constant_candidates(5), SetupOptions(), ctx=gpu)
+    from paper_1610_03154_b200.types import from_triplets
+    Z = from_triplets(2, 2, [(0, 1, 1.0), (1, 1, 1.0)])
+    with pytest.raises(RuntimeError, match="zero diagonal at row 0"):
+        api.strength(Z, StrengthConfig(StrengthMeasure.symmetric, 0.1), ctx=gpu)
