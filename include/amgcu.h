@@ -135,6 +135,18 @@ amgcu_status amgcu_ctx_set_sequential_reductions(amgcu_ctx ctx, int on);
 amgcu_status amgcu_ctx_synchronize(amgcu_ctx ctx);
 /* Kernel launch counter (all kernels this library launched on the context). */
 amgcu_status amgcu_ctx_launch_count(amgcu_ctx ctx, int64_t* launches);
+/* Device timer on the context stream: CUDA events recorded at start and stop
+ * (the stop call synchronises).  Used by bench.py for device-side timing. */
+amgcu_status amgcu_ctx_timer_start(amgcu_ctx ctx);
+amgcu_status amgcu_ctx_timer_stop(amgcu_ctx ctx, double* ms);
+/* Per-kernel-family profiling (CUDA events around each launch of the family,
+ * plus its algorithmic bytes = compulsory I/O of that launch). */
+amgcu_status amgcu_ctx_set_profiling(amgcu_ctx ctx, int on);
+amgcu_status amgcu_ctx_set_profile_mask(amgcu_ctx ctx, uint32_t family_mask);
+amgcu_status amgcu_ctx_profile_reset(amgcu_ctx ctx);
+amgcu_status amgcu_ctx_profile_query(amgcu_ctx ctx, int32_t family, int64_t* launches, double* ms, double* bytes);
+int32_t amgcu_profile_family_count(void);
+const char* amgcu_profile_family_name(int32_t family);
 void amgcu_free(void* p);
 void amgcu_csr_free(amgcu_csr* m);
 

@@ -74,7 +74,7 @@ def build_lib(force=False, jobs=8, verbose=False):
                     sys.stderr.write(err)
     tmp = LIB + ".tmp"
     if tasks or not os.path.exists(LIB) or force:
-        _run([NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-lcudart_static"])
+        _run([NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-lcudart_static", "-L" + os.path.join(CUDA_HOME, "lib64"), "-lcusolver"])
         os.replace(tmp, LIB)
     return LIB
 

@@ -158,7 +158,8 @@ void greedy_aggregate(Ctx& c, const DCsr& S, DAgg& agg) {
     AMG_CK(cudaMemsetAsync(state.get(), 0, sizeof(int32_t) * n, c.s));
     DBuf<unsigned int> ticket(1, c.s);
     AMG_CK(cudaMemsetAsync(ticket.get(), 0, sizeof(unsigned int), c.s));
-    launch(c, k_lfmis, blocks_for(n, kMisThreads), kMisThreads, 0, n, S.rp.get(), S.ci.get(), St.rp.get(),
+    launch_prof(c, kProfAggregate, 8.0 * S.nnz + 8.0 * (n + 1) + 4.0 * n, k_lfmis, blocks_for(n, kMisThreads),
+                kMisThreads, 0, n, S.rp.get(), S.ci.get(), St.rp.get(),
            St.ci.get(), state.get(), ticket.get());
     DBuf<int32_t> flag(static_cast<size_t>(n) + 1, c.s), rid(static_cast<size_t>(n) + 1, c.s);
     launch(c, k_root_flags, blocks_for(n, 256), 256, 0, n, static_cast<const int32_t*>(state.get()), flag.get());

@@ -13,6 +13,7 @@ using namespace amgcu;
 
 struct amgcu_ctx_s {
     Ctx c;
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
 };
 
 struct amgcu_hier_s {
@@ -161,6 +162,66 @@ amgcu_status amgcu_ctx_synchronize(amgcu_ctx ctx) {
 
 amgcu_status amgcu_ctx_launch_count(amgcu_ctx ctx, int64_t* launches) {
     return guarded(ctx, [&] { *launches = ctx->c.launches; });
+}
+
+amgcu_status amgcu_ctx_timer_start(amgcu_ctx ctx) {
+    return guarded(ctx, [&] {
+        Ctx& c = ctx->c;
+        if (!ctx->t0) AMG_CK(cudaEventCreate(&ctx->t0));
+        if (!ctx->t1) AMG_CK(cudaEventCreate(&ctx->t1));
+        AMG_CK(cudaEventRecord(ctx->t0, c.s));
+    });
+}
+
+amgcu_status amgcu_ctx_timer_stop(amgcu_ctx ctx, double* ms) {
+    return guarded(ctx, [&] {
+        Ctx& c = ctx->c;
+        AMG_CK(cudaEventRecord(ctx->t1, c.s));
+        AMG_CK(cudaEventSynchronize(ctx->t1));
+        float f = 0.f;
+        AMG_CK(cudaEventElapsedTime(&f, ctx->t0, ctx->t1));
+        *ms = f;
+    });
+}
+
+amgcu_status amgcu_ctx_set_profiling(amgcu_ctx ctx, int on) {
+    return guarded(ctx, [&] { ctx->c.profile = on != 0; });
+}
+
+amgcu_status amgcu_ctx_set_profile_mask(amgcu_ctx ctx, uint32_t family_mask) {
+    return guarded(ctx, [&] { ctx->c.prof_mask = family_mask; });
+}
+
+amgcu_status amgcu_ctx_profile_reset(amgcu_ctx ctx) {
+    return guarded(ctx, [&] {
+        prof_collect(ctx->c);
+        for (auto& r : ctx->c.prof) {
+            r.launches = 0;
+            r.bytes = 0.0;
+            r.ms = 0.0;
+        }
+    });
+}
+
+amgcu_status amgcu_ctx_profile_query(amgcu_ctx ctx, int32_t family, int64_t* launches, double* ms, double* bytes) {
+    return guarded(ctx, [&] {
+        if (family < 0 || family >= kProfFamilies) throw InvalidArgument("profile family out of range");
+        prof_collect(ctx->c);
+        const ProfRecord& r = ctx->c.prof[family];
+        *launches = r.launches;
+        *ms = r.ms;
+        *bytes = r.bytes;
+    });
+}
+
+int32_t amgcu_profile_family_count(void) { return kProfFamilies; }
+
+const char* amgcu_profile_family_name(int32_t family) {
+    static const char* names[kProfFamilies] = {"vcycle_relax0_residual", "vcycle_restrict", "vcycle_prolong",
+                                               "vcycle_post_relax",      "krylov_spmv",     "emin_masked_product",
+                                               "spgemm",                 "evolution_soc",   "gauss_seidel_wavefront",
+                                               "aggregate_lfmis",        "coarse_solve"};
+    return (family >= 0 && family < kProfFamilies) ? names[family] : "";
 }
 
 void amgcu_free(void* p) { std::free(p); }

@@ -152,6 +152,20 @@ __global__ void k_dense_gemv(int32_t n, const double* __restrict__ M, const doub
     x[i] = s;
 }
 
+// large coarsest level: one warp per row, coalesced row reads, warp-tree sum
+// (the coarsest solve is a tolerance-level step either way)
+__global__ void k_dense_gemv_warp(int32_t n, const double* __restrict__ M, const double* __restrict__ b,
+                                  double* __restrict__ x) {
+    const int32_t i = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
+    const int lane = threadIdx.x & 31;
+    if (i >= n) return;
+    const double* row = M + static_cast<size_t>(i) * n;
+    double s = 0.0;
+    for (int32_t j = lane; j < n; j += 32) s += row[j] * b[j];
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if (lane == 0) x[i] = s;
+}
+
 // PCG control: st = {rz, pq, alpha, rz_new, beta, rn}; flag: !(pq > 0)
 __global__ void k_pcg_alpha(double* __restrict__ st, int32_t* __restrict__ bad) {
     const double pq = st[1];
@@ -225,8 +239,13 @@ struct Driver {
         const size_t L = h.lv.size();
         DLevel& lev = h.lv[l];
         if (l == L - 1) {
-            launch(c, k_dense_gemv, blocks_for(h.coarse_n, 128), 128, 0, h.coarse_n,
-                   static_cast<const double*>(h.coarse_pinv.get()), b, x);
+            const double cb = 8.0 * h.coarse_n * h.coarse_n + 16.0 * h.coarse_n;
+            if (h.coarse_n <= 256)
+                launch_prof(c, kProfCoarseSolve, cb, k_dense_gemv, blocks_for(h.coarse_n, 128), 128, 0, h.coarse_n,
+                       static_cast<const double*>(h.coarse_pinv.get()), b, x);
+            else
+                launch_prof(c, kProfCoarseSolve, cb, k_dense_gemv_warp, blocks_for(static_cast<int64_t>(h.coarse_n) * 32, 256), 256, 0,
+                       h.coarse_n, static_cast<const double*>(h.coarse_pinv.get()), b, x);
             return;
         }
         const int32_t n = lev.A.nr;
@@ -240,8 +259,9 @@ struct Driver {
             for (int s = 0; s < sweeps; ++s) {
                 if (s == 0 && x_zero) {
                     if (sweeps == 1) {
-                        launch(c, k_relax0_residual, rows_grid(n), 128, 0, A, static_cast<const double*>(lev.wd_pre.get()),
-                               b, x, lev.r.get());
+                        launch_prof(c, kProfVcycleRelax0Residual, 12.0 * nnz + 4.0 * (n + 1) + 32.0 * n,
+                                    k_relax0_residual, rows_grid(n), 128, 0, A,
+                                    static_cast<const double*>(lev.wd_pre.get()), b, x, lev.r.get());
                         residual_done = true;
                     } else {
                         launch(c, k_relax0, rows_grid(n), 128, 0, n, static_cast<const double*>(lev.wd_pre.get()), b, x);
@@ -268,14 +288,16 @@ struct Driver {
         ops += nnz;
         // restriction
         DLevel& nxt = h.lv[l + 1];
-        launch(c, k_sell_spmv, rows_grid(lev.sR.nr), 128, 0, view(lev.sR), static_cast<const double*>(lev.r.get()),
-               nxt.b.get());
+        launch_prof(c, kProfVcycleRestrict,
+                    12.0 * lev.R.nnz + 4.0 * (lev.R.nr + 1) + 8.0 * n + 8.0 * lev.R.nr, k_sell_spmv,
+                    rows_grid(lev.sR.nr), 128, 0, view(lev.sR), static_cast<const double*>(lev.r.get()), nxt.b.get());
         ops += static_cast<double>(lev.R.nnz);
         apply(l + 1, nxt.x.get(), nxt.b.get(), kind, true);
         if (kind == 1 && l + 1 < L - 1) apply(l + 1, nxt.x.get(), nxt.b.get(), kind, false);
         // interpolate and correct into t, then post-relax back into x
-        launch(c, k_prolong, rows_grid(n), 128, 0, view(lev.sP), static_cast<const double*>(nxt.x.get()),
-               static_cast<const double*>(x), lev.t.get());
+        launch_prof(c, kProfVcycleProlong, 12.0 * lev.P.nnz + 4.0 * (n + 1) + 8.0 * lev.P.nc + 16.0 * n, k_prolong,
+                    rows_grid(n), 128, 0, view(lev.sP), static_cast<const double*>(nxt.x.get()),
+                    static_cast<const double*>(x), lev.t.get());
         ops += static_cast<double>(lev.P.nnz);
         const int post = h.o.post_scheme;
         sweeps = h.o.post_sweeps;
@@ -285,9 +307,9 @@ struct Driver {
             } else {
                 for (int s = 0; s < sweeps; ++s) {
                     if (s == 0) {
-                        launch(c, k_jacobi_sweep, rows_grid(n), 128, 0, A,
-                               static_cast<const double*>(lev.wd_post.get()), b, static_cast<const double*>(lev.t.get()),
-                               x);
+                        launch_prof(c, kProfVcyclePostRelax, 12.0 * nnz + 4.0 * (n + 1) + 32.0 * n, k_jacobi_sweep,
+                                    rows_grid(n), 128, 0, A, static_cast<const double*>(lev.wd_post.get()), b,
+                                    static_cast<const double*>(lev.t.get()), x);
                     } else {
                         launch(c, k_jacobi_sweep, rows_grid(n), 128, 0, A,
                                static_cast<const double*>(lev.wd_post.get()), b, static_cast<const double*>(x),
@@ -425,7 +447,8 @@ SolveResult solve(DHier& h, const double* b, double* x, const amgcu_solve_option
         copy_d2d(c, p.get(), z.get(), n);
         dot(c, r.get(), z.get(), n, S + 0);  // rz
         for (int it = 1; it <= o.max_iters; ++it) {
-            launch(c, k_sell_spmv, rows_grid(n), 128, 0, A, static_cast<const double*>(p.get()), q.get());
+            launch_prof(c, kProfKrylovSpmv, 12.0 * L0.A.nnz + 4.0 * (n + 1) + 16.0 * n, k_sell_spmv, rows_grid(n), 128,
+                        0, A, static_cast<const double*>(p.get()), q.get());
             d.ops += static_cast<double>(L0.A.nnz);
             dot(c, p.get(), q.get(), n, S + 1);
             launch(c, k_pcg_alpha, 1, 1, 0, S, bad.get());
@@ -478,7 +501,8 @@ SolveResult solve(DHier& h, const double* b, double* x, const amgcu_solve_option
         double* zj = Z.get() + static_cast<size_t>(j) * n;
         double* w = V.get() + static_cast<size_t>(j + 1) * n;
         d.precond(V.get() + static_cast<size_t>(j) * n, zj, o.cycle);
-        launch(c, k_sell_spmv, rows_grid(n), 128, 0, A, static_cast<const double*>(zj), w);
+        launch_prof(c, kProfKrylovSpmv, 12.0 * L0.A.nnz + 4.0 * (n + 1) + 16.0 * n, k_sell_spmv, rows_grid(n), 128, 0,
+                    A, static_cast<const double*>(zj), w);
         d.ops += static_cast<double>(L0.A.nnz);
         for (int t = 0; t <= j; ++t) {
             dot(c, w, V.get() + static_cast<size_t>(t) * n, n, Hcol.get() + t);

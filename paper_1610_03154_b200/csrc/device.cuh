@@ -67,7 +67,36 @@ private:
     cudaStream_t s_ = nullptr;
 };
 
+// Per-kernel-family timing with CUDA events on the context stream (bench.py's
+// live roofline).  Off by default; when on, every tagged launch is bracketed by
+// two events and its algorithmic bytes (the kernel's compulsory I/O) recorded.
+enum ProfFamily : int {
+    kProfVcycleRelax0Residual = 0,
+    kProfVcycleRestrict,
+    kProfVcycleProlong,
+    kProfVcyclePostRelax,
+    kProfKrylovSpmv,
+    kProfMaskedProduct,
+    kProfSpgemm,
+    kProfEvolution,
+    kProfGaussSeidel,
+    kProfAggregate,
+    kProfCoarseSolve,
+    kProfFamilies
+};
+
+struct ProfRecord {
+    int64_t launches = 0;
+    double bytes = 0.0;
+    double ms = 0.0;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending;
+};
+
 struct Ctx {
+    bool profile = false;
+    uint32_t prof_mask = 0xffffffffu;  // families timed while profile is on
+    ProfRecord prof[kProfFamilies];
+    std::vector<cudaEvent_t> event_pool;
     int device = 0;
     cudaStream_t s = nullptr;
     int sms = 148;
@@ -118,6 +147,51 @@ inline void launch(Ctx& c, Kern k, unsigned grid, unsigned block, size_t smem, A
     k<<<grid, block, smem, c.s>>>(args...);
     ++c.launches;
     AMG_CK(cudaGetLastError());
+}
+
+inline cudaEvent_t prof_event(Ctx& c) {
+    if (!c.event_pool.empty()) {
+        cudaEvent_t e = c.event_pool.back();
+        c.event_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    AMG_CK(cudaEventCreate(&e));
+    return e;
+}
+
+// launch with timing attribution to a profile family
+template <typename Kern, typename... Args>
+inline void launch_prof(Ctx& c, int family, double bytes, Kern k, unsigned grid, unsigned block, size_t smem,
+                        Args... args) {
+    if (grid == 0) return;
+    if (!c.profile || !((c.prof_mask >> family) & 1u)) {
+        launch(c, k, grid, block, smem, args...);
+        return;
+    }
+    cudaEvent_t e0 = prof_event(c), e1 = prof_event(c);
+    AMG_CK(cudaEventRecord(e0, c.s));
+    launch(c, k, grid, block, smem, args...);
+    AMG_CK(cudaEventRecord(e1, c.s));
+    ProfRecord& r = c.prof[family];
+    r.launches += 1;
+    r.bytes += bytes;
+    r.pending.emplace_back(e0, e1);
+}
+
+// resolve pending event pairs into milliseconds (synchronises)
+inline void prof_collect(Ctx& c) {
+    AMG_CK(cudaStreamSynchronize(c.s));
+    for (auto& r : c.prof) {
+        for (auto& pr : r.pending) {
+            float ms = 0.f;
+            AMG_CK(cudaEventElapsedTime(&ms, pr.first, pr.second));
+            r.ms += ms;
+            c.event_pool.push_back(pr.first);
+            c.event_pool.push_back(pr.second);
+        }
+        r.pending.clear();
+    }
 }
 
 inline unsigned blocks_for(int64_t n, int per_block) {

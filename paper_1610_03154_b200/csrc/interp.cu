@@ -988,6 +988,10 @@ void energy_minimize(Ctx& c, const DCsr& A, const DCsr& T, const double* B, cons
         if (read_scalar(c, err.get())) throw InvalidArgument("energy_minimize: T has an entry outside the pattern");
     }
     const unsigned mp_grid = blocks_for(n, kMpWarps);
+    auto mp_bytes = [&](const DCsr& M, int outs) {
+        return 12.0 * M.nnz + 4.0 * (M.nr + 1) + 4.0 * nz + 4.0 * (n + 1) + 8.0 * nz * (1 + outs) + 8.0 * k * nc +
+               8.0 * k * k * n;
+    };
     const unsigned mp_block = kMpWarps * kWarp;
     const unsigned ew = blocks_for(nz, 256);
 
@@ -1025,7 +1029,8 @@ void energy_minimize(Ctx& c, const DCsr& A, const DCsr& T, const double* B, cons
             launch(c, k_cg_ctl_newsum, 1, 1, 0, S, F);
             launch(c, k_cg_dir, ew, 256, 0, nz, static_cast<const double*>(Z.get()), D.get(),
                    static_cast<const double*>(S), static_cast<const int32_t*>(F));
-            launch(c, k_masked_project, mp_grid, mp_block, 0, n, A.rp.get(), A.ci.get(), A.va.get(), N.rp.get(),
+            launch_prof(c, kProfMaskedProduct, mp_bytes(A, 2), k_masked_project, mp_grid, mp_block, 0, n, A.rp.get(),
+                   A.ci.get(), A.va.get(), N.rp.get(),
                    N.ci.get(), static_cast<const double*>(D.get()), k, Bc, nc, static_cast<const double*>(gp.get()),
                    static_cast<const unsigned char*>(is_root.get()), ADm.get(), ADp.get(),
                    static_cast<const int32_t*>(F));
@@ -1077,7 +1082,8 @@ void energy_minimize(Ctx& c, const DCsr& A, const DCsr& T, const double* B, cons
     int built = 0;
     for (int s = 0; s < m; ++s) {
         double* W = V.get() + static_cast<size_t>(s + 1) * nz;
-        launch(c, k_masked_project, mp_grid, mp_block, 0, n, AtA.rp.get(), AtA.ci.get(), AtA.va.get(), N.rp.get(),
+        launch_prof(c, kProfMaskedProduct, mp_bytes(AtA, 1), k_masked_project, mp_grid, mp_block, 0, n, AtA.rp.get(),
+               AtA.ci.get(), AtA.va.get(), N.rp.get(),
                N.ci.get(), static_cast<const double*>(V.get() + static_cast<size_t>(s) * nz), k, Bc, nc,
                static_cast<const double*>(gp.get()), static_cast<const unsigned char*>(is_root.get()),
                static_cast<double*>(nullptr), W, static_cast<const int32_t*>(nullptr));

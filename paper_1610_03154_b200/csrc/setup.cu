@@ -6,6 +6,8 @@
 #include <cmath>
 #include <string>
 
+#include <cusolverDn.h>
+
 #include "hier.cuh"
 #include "small_dense.h"
 
@@ -171,6 +173,48 @@ bool coarsen(Ctx& c, DHier& H, int level, const double* Bhat, Coarsened& out) {
     return true;
 }
 
+
+__global__ void k_densify(int32_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                          const double* __restrict__ va, double* __restrict__ D) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    for (int32_t p = rp[i]; p < rp[i + 1]; ++p) D[static_cast<size_t>(i) * n + ci[p]] = va[p];
+}
+
+__global__ void k_identity(int32_t n, double* __restrict__ I) {
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= static_cast<int64_t>(n) * n) return;
+    I[t] = (t / n == t % n) ? 1.0 : 0.0;
+}
+
+constexpr int32_t kCoarseGpuThreshold = 512;
+
+// inverse of the row-major D (n x n) into inv (row-major).  Reading D as
+// column-major gives D^T; solving D^T X = I column-major yields X = D^-T,
+// i.e. D^-1 in row-major.  Returns false when the LU is singular.
+bool dense_inverse_gpu(Ctx& c, double* D, int32_t n, double* inv) {
+    cusolverDnHandle_t hs;
+    if (cusolverDnCreate(&hs) != CUSOLVER_STATUS_SUCCESS) throw CudaFailure("cusolverDnCreate failed");
+    struct Guard {
+        cusolverDnHandle_t h;
+        ~Guard() { cusolverDnDestroy(h); }
+    } guard{hs};
+    cusolverDnSetStream(hs, c.s);
+    int lwork = 0;
+    if (cusolverDnDgetrf_bufferSize(hs, n, n, D, n, &lwork) != CUSOLVER_STATUS_SUCCESS)
+        throw CudaFailure("cusolverDnDgetrf_bufferSize failed");
+    DBuf<double> work(static_cast<size_t>(lwork) + 1, c.s);
+    DBuf<int> piv(static_cast<size_t>(n), c.s), info(1, c.s);
+    if (cusolverDnDgetrf(hs, n, n, D, n, work.get(), piv.get(), info.get()) != CUSOLVER_STATUS_SUCCESS)
+        throw CudaFailure("cusolverDnDgetrf failed");
+    if (read_scalar(c, info.get()) != 0) return false;
+    launch(c, k_identity, blocks_for(static_cast<int64_t>(n) * n, 256), 256, 0, n, inv);
+    if (cusolverDnDgetrs(hs, CUBLAS_OP_N, n, n, D, n, piv.get(), inv, n, info.get()) != CUSOLVER_STATUS_SUCCESS)
+        throw CudaFailure("cusolverDnDgetrs failed");
+    if (read_scalar(c, info.get()) != 0) return false;
+    return true;
+}
+
 }  // namespace
 
 void require_supported_relax(int scheme, const char* who) {
@@ -223,6 +267,33 @@ void improve_candidates(Ctx& c, const DCsr& A, double* B, int32_t k, int sweeps,
         launch(c, k_scale_if_positive, std::max(1u, std::min<unsigned>(blocks_for(n, 256), 4u * c.sms)), 256, 0,
                static_cast<int64_t>(n), static_cast<const double*>(nrm.get() + j), col);
     }
+}
+
+// CoarseSolver::factor (hierarchy.hpp:59-68).  The coarsest operator is
+// inverted once; each cycle then applies the inverse with one dense GEMV.
+// Small levels: complete orthogonal decomposition on the host (the reference's
+// algorithm, also valid for singular operators).  Large levels (a stagnated
+// hierarchy can stop at ~10^4 rows): LU with partial pivoting on the GPU
+// (cuSOLVER getrf/getrs), falling back to the COD if the LU is singular.
+void coarse_factor(Ctx& c, DHier& H) {
+    const DLevel& Lc = H.lv.back();
+    const int32_t nL = Lc.A.nr;
+    H.coarse_n = nL;
+    H.coarse_pinv.alloc(static_cast<size_t>(nL) * nL, c.s);
+    // dense row-major copy of A_L
+    DBuf<double> D(static_cast<size_t>(nL) * nL, c.s);
+    AMG_CK(cudaMemsetAsync(D.get(), 0, sizeof(double) * nL * nL, c.s));
+    launch(c, k_densify, blocks_for(nL, 128), 128, 0, nL, Lc.A.rp.get(), Lc.A.ci.get(), Lc.A.va.get(), D.get());
+    if (nL > kCoarseGpuThreshold && dense_inverse_gpu(c, D.get(), nL, H.coarse_pinv.get())) return;
+    std::vector<double> hD(static_cast<size_t>(nL) * nL);
+    copy_d2h(c, hD.data(), D.get(), static_cast<int64_t>(hD.size()));
+    sync(c);
+    sd::COD cod;
+    cod.compute(nL, nL, hD.data());
+    std::vector<double> pinv(static_cast<size_t>(nL) * nL);
+    cod.pseudo_inverse(pinv.data());
+    copy_h2d(c, H.coarse_pinv.get(), pinv.data(), static_cast<int64_t>(pinv.size()));
+    sync(c);
 }
 
 std::unique_ptr<DHier> rn_setup(Ctx& c, const DCsr& A, const double* B, int32_t k, const double* left,
@@ -299,23 +370,7 @@ std::unique_ptr<DHier> rn_setup(Ctx& c, const DCsr& A, const double* B, int32_t 
                    static_cast<const double*>(L.inv_diag.get()), L.wd_post.get());
         }
     }
-    {
-        const DLevel& Lc = H->lv.back();
-        HostCsr hc = download_csr(c, Lc.A);
-        const int32_t nL = hc.n_rows;
-        std::vector<double> D(static_cast<size_t>(nL) * hc.n_cols, 0.0);
-        for (int32_t i = 0; i < nL; ++i)
-            for (int32_t p = hc.row_offsets[i]; p < hc.row_offsets[i + 1]; ++p)
-                D[static_cast<size_t>(i) * hc.n_cols + hc.col_indices[p]] = hc.values[p];
-        sd::COD cod;
-        cod.compute(nL, hc.n_cols, D.data());
-        std::vector<double> pinv(static_cast<size_t>(hc.n_cols) * nL);
-        cod.pseudo_inverse(pinv.data());
-        H->coarse_pinv.alloc(pinv.size(), c.s);
-        copy_h2d(c, H->coarse_pinv.get(), pinv.data(), static_cast<int64_t>(pinv.size()));
-        H->coarse_n = nL;
-        sync(c);
-    }
+    coarse_factor(c, *H);
     prepare_solve(*H);
     return H;
 }

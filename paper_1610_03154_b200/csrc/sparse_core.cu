@@ -519,7 +519,10 @@ void spgemm(Ctx& c, const DCsr& A, const DCsr& B, DCsr& C, double* ops) {
     if (ops) *ops = static_cast<double>(total);
     DBuf<int32_t> tcol(static_cast<size_t>(total), c.s), cnt(static_cast<size_t>(nr) + 1, c.s);
     DBuf<double> tval(static_cast<size_t>(total), c.s);
-    launch(c, k_spgemm_small, blocks_for(nr, kGemmWarps), kGemmWarps * kWarp, 0, nr, A.rp.get(), A.ci.get(),
+    launch_prof(c, kProfSpgemm,
+                12.0 * A.nnz + 4.0 * (A.nr + 1) + 12.0 * B.nnz + 4.0 * (B.nr + 1) + 12.0 * static_cast<double>(total) +
+                    4.0 * nr,
+                k_spgemm_small, blocks_for(nr, kGemmWarps), kGemmWarps * kWarp, 0, nr, A.rp.get(), A.ci.get(),
            A.va.get(), B.rp.get(), B.ci.get(), B.va.get(), static_cast<const int64_t*>(poff.get()), tcol.get(),
            tval.get(), cnt.get());
     // rows above the shared-memory capacity

@@ -596,7 +596,8 @@ void evolution_strength(Ctx& c, const DCsr& A, const DCsr& At, const double* win
     DBuf<double> tval(static_cast<size_t>(total), c.s);
     DBuf<int32_t> ovf(static_cast<size_t>(n), c.s), novf(1, c.s);
     AMG_CK(cudaMemsetAsync(novf.get(), 0, sizeof(int32_t), c.s));
-    launch(c, k_evolution, blocks_for(n, kEvWarps), kEvWarps * kWarp, 0, n, A.rp.get(), A.ci.get(), A.va.get(),
+    launch_prof(c, kProfEvolution, 12.0 * A.nnz + 8.0 * (n + 1) + 4.0 * At.nnz + 8.0 * n + 12.0 * total, k_evolution,
+                blocks_for(n, kEvWarps), kEvWarps * kWarp, 0, n, A.rp.get(), A.ci.get(), A.va.get(),
            At.rp.get(), At.ci.get(), winv, drop_tol, steps, static_cast<const int64_t*>(off.get()), cnt.get(),
            tcol.get(), tval.get(), ovf.get(), novf.get());
     const int32_t nbig = read_scalar(c, novf.get());
