@@ -65,12 +65,14 @@ __device__ __forceinline__ double wait_bits(const double* p, unsigned long long 
 // entry classes in sweep order
 enum : int { kSelf = 0, kInBlock = 1, kReady = 2, kPoll = 3 };
 
-// Per warp, dynamic shared memory: cache[32][kSegMaxE][k] prefetched bits,
-// xb[32][k] values published in the current block.
+// Per warp, dynamic shared memory: cache[32][kSegMaxE][K] prefetched bits,
+// xb[32][K] values published in the current block.  K = number of candidate
+// columns (compile-time so the per-entry arrays stay in registers).
+template <int K>
 __global__ void __launch_bounds__(kSegWarps * 32)
     k_gs_segments(int32_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
                   const double* __restrict__ va, const double* __restrict__ inv_diag, const double* __restrict__ b,
-                  int k, int nsweeps, const unsigned char* __restrict__ backward, const int32_t* __restrict__ item_base,
+                  int nsweeps, const unsigned char* __restrict__ backward, const int32_t* __restrict__ item_base,
                   const int32_t* __restrict__ seg_fwd, const int32_t* __restrict__ seg_bwd, double* __restrict__ X,
                   unsigned int* __restrict__ ticket) {
     extern __shared__ unsigned long long smem[];
@@ -86,12 +88,12 @@ __global__ void __launch_bounds__(kSegWarps * 32)
     const int32_t* segs = bwd ? seg_bwd : seg_fwd;
     const int32_t g = item - item_base[s];
     const int32_t q0 = segs[g], q1 = segs[g + 1];
-    const size_t stride = static_cast<size_t>(n) * k;
+    const size_t stride = static_cast<size_t>(n) * K;
     const double* xin = X + static_cast<size_t>(s) * stride;
     double* xout = X + static_cast<size_t>(s + 1) * stride;
-    unsigned long long* cache = smem + static_cast<size_t>(wl) * 32 * (kSegMaxE + 1) * k;  // [32][kSegMaxE][k]
-    double* xb = reinterpret_cast<double*>(cache + 32 * kSegMaxE * k);                   // [32][k]
-    unsigned long long* mycache = cache + static_cast<size_t>(lane) * kSegMaxE * k;
+    unsigned long long* cache = smem + static_cast<size_t>(wl) * 32 * (kSegMaxE + 1) * K;
+    double* xb = reinterpret_cast<double*>(cache + 32 * kSegMaxE * K);
+    unsigned long long* mycache = cache + static_cast<size_t>(lane) * kSegMaxE * K;
     for (int32_t qb = q0; qb < q1; qb += 32) {
         const int32_t q = qb + lane;
         const bool active = q < q1;
@@ -101,21 +103,25 @@ __global__ void __launch_bounds__(kSegWarps * 32)
             lo = rp[i];
             hi = rp[i + 1];
         }
-        // ---- phase A: issue every independent load of the row, no waiting ----
-        int32_t cols[kSegMaxE];
+        // ---- phase A: every independent load of the row, issued without waiting ----
+        int32_t ref[kSegMaxE];  // in-block: lane index of the producer; otherwise the column
         unsigned char cls[kSegMaxE];
+        double a[kSegMaxE];
 #pragma unroll
         for (int e = 0; e < kSegMaxE; ++e) {
             cls[e] = kSelf;
-            cols[e] = i;
+            ref[e] = 0;
+            a[e] = 0.0;
             if (lo + e < hi) {
                 const int32_t j = ci[lo + e];
-                cols[e] = j;
+                a[e] = va[lo + e];
+                ref[e] = j;
                 if (j != i) {
                     const int32_t qj = bwd ? n - 1 - j : j;
                     const bool fresh = qj < q;
                     if (fresh && qj >= qb) {
                         cls[e] = kInBlock;
+                        ref[e] = qj - qb;
                     } else {
                         const bool own = fresh && qj >= q0;  // earlier block of this warp's segment
                         cls[e] = (own || (!fresh && s == 0)) ? kReady : kPoll;
@@ -126,70 +132,94 @@ __global__ void __launch_bounds__(kSegWarps * 32)
 #pragma unroll
         for (int e = 0; e < kSegMaxE; ++e) {
             if (cls[e] == kReady || cls[e] == kPoll) {
-                const int32_t j = cols[e];
+                const int32_t j = ref[e];
                 const int32_t qj = bwd ? n - 1 - j : j;
                 const double* src = (qj < q) ? xout : xin;
-                for (int c = 0; c < k; ++c) {
+#pragma unroll
+                for (int c = 0; c < K; ++c) {
                     const double* addr = &src[static_cast<size_t>(c) * n + j];
-                    mycache[e * k + c] = cls[e] == kReady
+                    mycache[e * K + c] = cls[e] == kReady
                                              ? static_cast<unsigned long long>(__double_as_longlong(__ldcg(addr)))
                                              : load_relaxed_bits(addr);
                 }
             }
         }
-        // prefix of the CSR sum that needs no in-block value and no pending poll
-        double acc[kMaxK];
+        // CSR prefix that needs neither an in-block value nor a pending one
+        double acc[K];
+#pragma unroll
+        for (int c = 0; c < K; ++c) acc[c] = (active && b) ? b[static_cast<size_t>(c) * n + i] : 0.0;
+        bool open = active;
         int32_t e_stop = 0;
-        if (active) {
-            for (int c = 0; c < k; ++c) acc[c] = b ? b[static_cast<size_t>(c) * n + i] : 0.0;
-            const int32_t ne = min(hi - lo, kSegMaxE);
-            for (; e_stop < ne; ++e_stop) {
-                const int ce = cls[e_stop];
-                if (ce == kSelf) continue;
-                if (ce == kInBlock) break;
-                bool pending = false;
-                for (int c = 0; c < k; ++c) pending = pending || mycache[e_stop * k + c] == kPending;
-                if (pending) break;
-                const double a = va[lo + e_stop];
-                for (int c = 0; c < k; ++c)
-                    acc[c] -= a * __longlong_as_double(static_cast<long long>(mycache[e_stop * k + c]));
+#pragma unroll
+        for (int e = 0; e < kSegMaxE; ++e) {
+            if (open && lo + e < hi) {
+                if (cls[e] == kInBlock) {
+                    open = false;
+                } else if (cls[e] != kSelf) {
+                    bool pending = false;
+#pragma unroll
+                    for (int c = 0; c < K; ++c) pending = pending || mycache[e * K + c] == kPending;
+                    if (pending) {
+                        open = false;
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < K; ++c)
+                            acc[c] -= a[e] * __longlong_as_double(static_cast<long long>(mycache[e * K + c]));
+                    }
+                }
+                if (open) e_stop = e + 1;
             }
         }
         __syncwarp();
-        // ---- phase B: lanes finish in order, polling only what is still pending ----
+        // ---- phase B: lanes finish in order; arithmetic on registers, polls only if pending ----
         const int32_t cnt = min(32, q1 - qb);
         for (int32_t t = 0; t < cnt; ++t) {
             if (lane == t) {
-                for (int32_t p = lo + e_stop; p < hi; ++p) {
-                    const int32_t e = p - lo;
+#pragma unroll
+                for (int e = 0; e < kSegMaxE; ++e) {
+                    if (e >= e_stop && lo + e < hi) {
+                        if (cls[e] == kInBlock) {
+#pragma unroll
+                            for (int c = 0; c < K; ++c) acc[c] -= a[e] * xb[ref[e] * K + c];
+                        } else if (cls[e] != kSelf) {
+                            const int32_t j = ref[e];
+                            const int32_t qj = bwd ? n - 1 - j : j;
+                            const double* src = (qj < q) ? xout : xin;
+#pragma unroll
+                            for (int c = 0; c < K; ++c)
+                                acc[c] -= a[e] * wait_bits(&src[static_cast<size_t>(c) * n + j], mycache[e * K + c]);
+                        }
+                    }
+                }
+                // entries beyond the prefetch window, in CSR order
+                for (int32_t p = lo + kSegMaxE; p < hi; ++p) {
                     const int32_t j = ci[p];
                     if (j == i) continue;
                     const int32_t qj = bwd ? n - 1 - j : j;
                     const bool fresh = qj < q;
-                    const double a = va[p];
+                    const double av = va[p];
                     if (fresh && qj >= qb) {
-                        for (int c = 0; c < k; ++c) acc[c] -= a * xb[(qj - qb) * k + c];
+#pragma unroll
+                        for (int c = 0; c < K; ++c) acc[c] -= av * xb[(qj - qb) * K + c];
                         continue;
                     }
                     const double* src = fresh ? xout : xin;
-                    for (int c = 0; c < k; ++c) {
+                    const bool own = fresh && qj >= q0;
+#pragma unroll
+                    for (int c = 0; c < K; ++c) {
                         const double* addr = &src[static_cast<size_t>(c) * n + j];
-                        unsigned long long bits;
-                        if (e < kSegMaxE) {
-                            bits = mycache[e * k + c];
-                        } else {
-                            const bool own = fresh && qj >= q0;
-                            bits = (own || (!fresh && s == 0))
-                                       ? static_cast<unsigned long long>(__double_as_longlong(__ldcg(addr)))
-                                       : load_relaxed_bits(addr);
-                        }
-                        acc[c] -= a * wait_bits(addr, bits);
+                        const unsigned long long bits =
+                            (own || (!fresh && s == 0))
+                                ? static_cast<unsigned long long>(__double_as_longlong(__ldcg(addr)))
+                                : load_relaxed_bits(addr);
+                        acc[c] -= av * wait_bits(addr, bits);
                     }
                 }
                 const double d = inv_diag[i];
-                for (int c = 0; c < k; ++c) {
+#pragma unroll
+                for (int c = 0; c < K; ++c) {
                     const double xi = acc[c] * d;
-                    xb[t * k + c] = xi;
+                    xb[t * K + c] = xi;
                     cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> out(
                         *reinterpret_cast<unsigned long long*>(&xout[static_cast<size_t>(c) * n + i]));
                     out.store(static_cast<unsigned long long>(__double_as_longlong(xi)), cuda::memory_order_relaxed);
@@ -288,13 +318,25 @@ void gauss_seidel(Ctx& c, const DCsr& A, const double* inv_diag, double* x, cons
     DBuf<unsigned int> ticket(1, c.s);
     AMG_CK(cudaMemsetAsync(ticket.get(), 0, sizeof(unsigned int), c.s));
     const size_t smem = static_cast<size_t>(kSegWarps) * 32 * (kSegMaxE + 1) * k * sizeof(unsigned long long);
-    if (smem > 48 * 1024)
-        AMG_CK(cudaFuncSetAttribute(k_gs_segments, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    launch_prof(c, kProfGaussSeidel, nsw * (12.0 * A.nnz + 4.0 * (n + 1) + 8.0 * n + 16.0 * n * k), k_gs_segments,
-                blocks_for(base[nsw], kSegWarps), kSegWarps * 32, smem, n, A.rp.get(), A.ci.get(), A.va.get(), inv_diag,
-                b, k, nsw, static_cast<const unsigned char*>(bwd.get()), static_cast<const int32_t*>(dbase.get()),
-                static_cast<const int32_t*>(segf.get()),
-                static_cast<const int32_t*>(symmetric_sweep ? segb.get() : segf.get()), X.get(), ticket.get());
+    const double bytes = nsw * (12.0 * A.nnz + 4.0 * (n + 1) + 8.0 * n + 16.0 * n * k);
+    auto run = [&](auto kern) {
+        if (smem > 48 * 1024)
+            AMG_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        launch_prof(c, kProfGaussSeidel, bytes, kern, blocks_for(base[nsw], kSegWarps), kSegWarps * 32, smem, n,
+                    A.rp.get(), A.ci.get(), A.va.get(), inv_diag, b, nsw, static_cast<const unsigned char*>(bwd.get()),
+                    static_cast<const int32_t*>(dbase.get()), static_cast<const int32_t*>(segf.get()),
+                    static_cast<const int32_t*>(symmetric_sweep ? segb.get() : segf.get()), X.get(), ticket.get());
+    };
+    switch (k) {
+        case 1: run(k_gs_segments<1>); break;
+        case 2: run(k_gs_segments<2>); break;
+        case 3: run(k_gs_segments<3>); break;
+        case 4: run(k_gs_segments<4>); break;
+        case 5: run(k_gs_segments<5>); break;
+        case 6: run(k_gs_segments<6>); break;
+        case 7: run(k_gs_segments<7>); break;
+        default: run(k_gs_segments<8>); break;
+    }
     copy_d2d(c, x, X.get() + stride * nsw, static_cast<int64_t>(stride));
     sync(c);
 }
