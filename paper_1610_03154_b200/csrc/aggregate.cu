@@ -45,31 +45,47 @@ __global__ void __launch_bounds__(kMisThreads)
     __syncthreads();
     const int32_t i = static_cast<int32_t>(blk) * kMisThreads + threadIdx.x;
     if (i >= n) return;
-    // The decision is published inside the loop: a lane that exits a spin loop
+    // Scan the lower conflict neighbours once, in order; on the first one still
+    // undecided, wait on that single state with exponential back-off (one
+    // address polled per waiting node), then resume the scan where it stopped.
+    // The decision is published inside the loop: a lane leaving a spin loop
     // before storing could wait at the warp's reconvergence point while its
-    // neighbours spin on the value it has not yet written.
+    // neighbours spin on the value it has not written yet.
     cuda::atomic_ref<int32_t, cuda::thread_scope_device> me(state[i]);
+    int32_t p = rp[i];
+    int32_t q = p < rp[i + 1] ? trp[ci[p]] : 0;
+    unsigned ns = 32;
     while (true) {
-        bool pending = false, hit_root = false;
-        for (int32_t p = rp[i]; p < rp[i + 1] && !hit_root; ++p) {
+        bool hit_root = false, pending = false;
+        for (; p < rp[i + 1]; ++p) {
             const int32_t x = ci[p];
-            for (int32_t q = trp[x]; q < trp[x + 1]; ++q) {
+            if (q < trp[x]) q = trp[x];
+            for (; q < trp[x + 1]; ++q) {
                 const int32_t r = tci[q];
-                if (r >= i) break;  // rows of S^T are ascending
+                if (r >= i) {  // rows of S^T are ascending: nothing lower remains in this column
+                    q = trp[x + 1];
+                    break;
+                }
                 cuda::atomic_ref<int32_t, cuda::thread_scope_device> st(state[r]);
                 const int32_t v = st.load(cuda::memory_order_relaxed);
                 if (v == kRoot) {
                     hit_root = true;
                     break;
                 }
-                if (v == kUndecided) pending = true;
+                if (v == kUndecided) {
+                    pending = true;
+                    break;
+                }
             }
+            if (hit_root || pending) break;
+            if (p + 1 < rp[i + 1]) q = trp[ci[p + 1]];
         }
         if (hit_root || !pending) {
             me.store(hit_root ? kOut : kRoot, cuda::memory_order_relaxed);
             break;
         }
-        __nanosleep(32);
+        __nanosleep(ns);
+        ns = ns < 1024 ? 2 * ns : 1024;
     }
 }
 

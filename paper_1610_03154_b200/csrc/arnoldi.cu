@@ -60,13 +60,18 @@ double spectral_radius(Ctx& c, const DCsr& A, int steps, const double* dinv) {
         double* w = V.get() + static_cast<size_t>(j + 1) * n;
         launch(c, k_spmv_dinv, blocks_for(n, 256), 256, 0, n, A.rp.get(), A.ci.get(), A.va.get(),
                static_cast<const double*>(V.get() + static_cast<size_t>(j) * n), dinv, w);
-        for (int t = 0; t <= j; ++t) {
-            double* h = Hd.get() + t * m + j;
-            dot(c, w, V.get() + static_cast<size_t>(t) * n, n, h);
-            axpy_dev(c, h, -1.0, V.get() + static_cast<size_t>(t) * n, w, n);
-        }
+        // modified Gram-Schmidt: h_t = (w, v_t); w -= h_t v_t; the axpy of step t is
+        // fused with the dot of step t + 1 (and the last one with the norm)
         double* hsub = Hd.get() + (j + 1) * m + j;
-        nrm2(c, w, n, hsub);
+        dot(c, w, V.get(), n, Hd.get() + j);
+        for (int t = 0; t <= j; ++t) {
+            const double* vt = V.get() + static_cast<size_t>(t) * n;
+            if (t < j)
+                axpy_dot(c, Hd.get() + t * m + j, -1.0, vt, w, V.get() + static_cast<size_t>(t + 1) * n, n,
+                         Hd.get() + (t + 1) * m + j, false);
+            else
+                axpy_dot(c, Hd.get() + t * m + j, -1.0, vt, w, nullptr, n, hsub, true);
+        }
         const double h = read_scalar(c, hsub);
         built = j + 1;
         if (h < 1e-14) break;

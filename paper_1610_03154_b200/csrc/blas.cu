@@ -44,6 +44,41 @@ __global__ void k_dot_tree(const double* __restrict__ x, const double* __restric
     }
 }
 
+// y += sign * (*alpha) * x, then *out = dot(y, z) (z == nullptr: dot(y, y),
+// optionally square-rooted) -- one pass for a modified Gram-Schmidt step
+// (the reference's axpy followed by the next dot, spectral.hpp:47-51).
+__global__ void k_axpy_dot_tree(const double* __restrict__ alpha, double sign, const double* __restrict__ x,
+                                double* __restrict__ y, const double* __restrict__ z, int64_t n,
+                                double* __restrict__ partials, unsigned int* __restrict__ done,
+                                double* __restrict__ out, bool take_sqrt) {
+    using BR = cub::BlockReduce<double, kDotThreads>;
+    __shared__ typename BR::TempStorage tmp;
+    __shared__ bool last;
+    const double a = sign * (*alpha);
+    double s = 0.0;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * kDotThreads;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * kDotThreads + threadIdx.x; i < n; i += stride) {
+        const double yi = y[i] + a * x[i];
+        y[i] = yi;
+        s += yi * (z ? z[i] : yi);
+    }
+    const double b = BR(tmp).Sum(s);
+    if (threadIdx.x == 0) {
+        partials[blockIdx.x] = b;
+        __threadfence();
+        const unsigned prev = atomicAdd(done, 1u);
+        last = (prev == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        __threadfence();
+        double t = 0.0;
+        for (unsigned k = 0; k < gridDim.x; ++k) t += __ldcg(&partials[k]);
+        *out = take_sqrt ? sqrt(t) : t;
+        *done = 0u;
+    }
+}
+
 __global__ void k_dot_seq(const double* __restrict__ x, const double* __restrict__ y, int64_t n, double* __restrict__ out,
                           bool take_sqrt) {
     const int lane = threadIdx.x;
@@ -97,6 +132,23 @@ void dot_impl(Ctx& c, const double* x, const double* y, int64_t n, double* out, 
 }
 
 }  // namespace
+
+void axpy_dot(Ctx& c, const double* alpha, double sign, const double* x, double* y, const double* z, int64_t n,
+              double* out, bool take_sqrt) {
+    if (c.seq) {
+        axpy_dev(c, alpha, sign, x, y, n);
+        dot_impl(c, y, z ? z : y, n, out, take_sqrt);
+        return;
+    }
+    const unsigned g = std::max(1u, std::min<unsigned>(blocks_for(n, kDotThreads * 4), 2u * c.sms));
+    if (c.partials.size() < 4096) {
+        c.partials.alloc(4096, c.s);
+        c.tickets.alloc(64, c.s);
+        AMG_CK(cudaMemsetAsync(c.tickets.get(), 0, sizeof(unsigned int) * 64, c.s));
+    }
+    launch(c, k_axpy_dot_tree, g, kDotThreads, 0, alpha, sign, x, y, z, n, c.partials.get(), c.tickets.get(), out,
+           take_sqrt);
+}
 
 void dot(Ctx& c, const double* x, const double* y, int64_t n, double* out) { dot_impl(c, x, y, n, out, false); }
 void nrm2(Ctx& c, const double* x, int64_t n, double* out) { dot_impl(c, x, x, n, out, true); }

@@ -504,11 +504,11 @@ SolveResult solve(DHier& h, const double* b, double* x, const amgcu_solve_option
         launch_prof(c, kProfKrylovSpmv, 12.0 * L0.A.nnz + 4.0 * (n + 1) + 16.0 * n, k_sell_spmv, rows_grid(n), 128, 0,
                     A, static_cast<const double*>(zj), w);
         d.ops += static_cast<double>(L0.A.nnz);
-        for (int t = 0; t <= j; ++t) {
-            dot(c, w, V.get() + static_cast<size_t>(t) * n, n, Hcol.get() + t);
-            axpy_dev(c, Hcol.get() + t, -1.0, V.get() + static_cast<size_t>(t) * n, w, n);
-        }
-        nrm2(c, w, n, Hcol.get() + j + 1);
+        // modified Gram-Schmidt (cycle.hpp:228-231); axpy of step t fused with the dot of t + 1
+        dot(c, w, V.get(), n, Hcol.get());
+        for (int t = 0; t <= j; ++t)
+            axpy_dot(c, Hcol.get() + t, -1.0, V.get() + static_cast<size_t>(t) * n, w,
+                     t < j ? V.get() + static_cast<size_t>(t + 1) * n : nullptr, n, Hcol.get() + t + 1, t == j);
         std::vector<double> col(j + 2);
         copy_d2h(c, col.data(), Hcol.get(), j + 2);
         sync(c);

@@ -15,7 +15,6 @@ namespace amgcu {
 
 namespace {
 
-constexpr int kWarp = 32;
 constexpr int kKMax = 8;
 
 __device__ __forceinline__ int32_t lower_bound_i32(const int32_t* a, int32_t lo, int32_t hi, int32_t key) {
@@ -486,134 +485,97 @@ __global__ void k_root_mask(int32_t nroots, const int32_t* __restrict__ roots, u
 
 // ---------------------------------------------------------------------------------------
 // Masked product Y = (A X)|_N (interpolation.hpp:186-210) with the constraint
-// projection (150-182) fused: warp per row, lane per pattern slot.  Each slot
-// accumulates over A's row in CSR order, looking its column up in N's row t.
-// Y (unprojected) and Yp (projected) are written when the pointer is non-null.
+// projection (150-182) fused.  Y (unprojected) and Yp (projected) are written
+// when the pointer is non-null.
 // ---------------------------------------------------------------------------------------
-constexpr int kMpWarps = 4;
-constexpr int kMpSlots = 4;  // slots per lane per chunk -> 128 slots per chunk
+// Thread-per-row masked product + projection (reference arithmetic): the row's pattern slots are taken in chunks of kMrChunk
+// held in registers; for every A entry (CSR order) the slot columns are merged
+// against the sorted row N_t with two pointers.  Rows of N are short (3-8
+// slots on the BASELINE configs), so one thread per row keeps every lane busy.
+constexpr int kMrChunk = 8;
 
-__device__ __forceinline__ void masked_row(int32_t i, int lane, const int32_t* __restrict__ arp,
-                                           const int32_t* __restrict__ aci, const double* __restrict__ ava,
-                                           const int32_t* __restrict__ nrp, const int32_t* __restrict__ nci,
-                                           const double* __restrict__ x, int32_t c0, int32_t L, double* acc,
-                                           int32_t* col) {
-    const int32_t lo = nrp[i];
-#pragma unroll
-    for (int s = 0; s < kMpSlots; ++s) {
-        const int32_t e = c0 + s * kWarp + lane;
-        acc[s] = 0.0;
-        col[s] = e < L ? nci[lo + e] : -1;
-    }
-    for (int32_t p = arp[i]; p < arp[i + 1]; ++p) {
-        const int32_t t = aci[p];
-        const double a = ava[p];
-        const int32_t tlo = nrp[t], thi = nrp[t + 1];
-#pragma unroll
-        for (int s = 0; s < kMpSlots; ++s) {
-            if (col[s] < 0) continue;
-            const int32_t q = lower_bound_i32(nci, tlo, thi, col[s]);
-            if (q < thi && nci[q] == col[s]) acc[s] += a * x[q];
-        }
-    }
-}
-
-__global__ void __launch_bounds__(kMpWarps * kWarp)
-    k_masked_project(int32_t n, const int32_t* __restrict__ arp, const int32_t* __restrict__ aci,
-                     const double* __restrict__ ava, const int32_t* __restrict__ nrp, const int32_t* __restrict__ nci,
-                     const double* __restrict__ x, int32_t k, const double* __restrict__ Bc, int32_t nc,
-                     const double* __restrict__ gp, const unsigned char* __restrict__ is_root, double* __restrict__ y,
-                     double* __restrict__ yp, const int32_t* __restrict__ stop) {
+__global__ void __launch_bounds__(128)
+    k_masked_rows(int32_t n, const int32_t* __restrict__ arp, const int32_t* __restrict__ aci,
+                  const double* __restrict__ ava, const int32_t* __restrict__ nrp, const int32_t* __restrict__ nci,
+                  const double* __restrict__ x, int32_t k, const double* __restrict__ Bc, int32_t nc,
+                  const double* __restrict__ gp, const unsigned char* __restrict__ is_root, double* __restrict__ y,
+                  double* __restrict__ yp, const int32_t* __restrict__ stop) {
     if (stop && *stop) return;
-    const int w = threadIdx.x / kWarp, lane = threadIdx.x & (kWarp - 1);
-    const int32_t i = blockIdx.x * kMpWarps + w;
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int32_t lo = nrp[i], L = nrp[i + 1] - lo;
     if (L == 0) return;
-    const bool root = yp && is_root[i];
-    const int32_t chunk = kMpSlots * kWarp;
-    if (L <= chunk) {
-        double acc[kMpSlots];
-        int32_t col[kMpSlots];
-        masked_row(i, lane, arp, aci, ava, nrp, nci, x, 0, L, acc, col);
-        if (y) {
+    const int32_t alo = arp[i], ahi = arp[i + 1];
+    double* dst = y ? y : yp;  // unprojected values (scratch in yp when y is not wanted)
+    double keep[kMrChunk];     // last chunk's values, reused by the projection when L <= kMrChunk
+    for (int32_t c0 = 0; c0 < L; c0 += kMrChunk) {
+        const int32_t m = min(kMrChunk, L - c0);
+        int32_t cols[kMrChunk];
+        double acc[kMrChunk];
 #pragma unroll
-            for (int s = 0; s < kMpSlots; ++s)
-                if (col[s] >= 0) y[lo + s * kWarp + lane] = acc[s];
+        for (int s = 0; s < kMrChunk; ++s) {
+            cols[s] = s < m ? nci[lo + c0 + s] : 0x7fffffff;
+            acc[s] = 0.0;
         }
-        if (!yp) return;
-        if (root) {
+        for (int32_t p = alo; p < ahi; ++p) {
+            const int32_t t = aci[p];
+            const double a = ava[p];
+            int32_t q = nrp[t];
+            const int32_t qe = nrp[t + 1];
 #pragma unroll
-            for (int s = 0; s < kMpSlots; ++s)
-                if (col[s] >= 0) yp[lo + s * kWarp + lane] = 0.0;
-            return;
-        }
-        // y_a = sum_p Bc(col_p, a) * acc_p in slot order (sequential, warp-uniform)
-        double ya[kKMax];
-        for (int a = 0; a < k; ++a) ya[a] = 0.0;
-        for (int32_t e = 0; e < L; ++e) {
-            const int s = e / kWarp, src = e % kWarp;
-            double v = 0.0;
-            int32_t cj = 0;
-#pragma unroll
-            for (int ss = 0; ss < kMpSlots; ++ss)
-                if (ss == s) {
-                    v = __shfl_sync(0xffffffffu, acc[ss], src);
-                    cj = __shfl_sync(0xffffffffu, col[ss], src);
+            for (int s = 0; s < kMrChunk; ++s) {
+                if (s < m) {
+                    while (q < qe && nci[q] < cols[s]) ++q;
+                    if (q < qe && nci[q] == cols[s]) acc[s] += a * x[q];
                 }
-            for (int a = 0; a < k; ++a) ya[a] += Bc[static_cast<size_t>(a) * nc + cj] * v;
-        }
-        const double* G = gp + static_cast<size_t>(i) * k * k;
-        double lam[kKMax];
-        for (int a = 0; a < k; ++a) {
-            double s = 0.0;
-            for (int b = 0; b < k; ++b) s += G[a * k + b] * ya[b];
-            lam[a] = s;
+            }
         }
 #pragma unroll
-        for (int s = 0; s < kMpSlots; ++s) {
-            if (col[s] < 0) continue;
-            double t = 0.0;
-            for (int a = 0; a < k; ++a) t += Bc[static_cast<size_t>(a) * nc + col[s]] * lam[a];
-            yp[lo + s * kWarp + lane] = acc[s] - t;
-        }
-        return;
+        for (int s = 0; s < kMrChunk; ++s)
+            if (s < m) {
+                dst[lo + c0 + s] = acc[s];
+                keep[s] = acc[s];
+            }
     }
-    // long rows: chunked; Y is written first (into y, or yp as scratch), then projected
-    double* dst = y ? y : yp;
-    for (int32_t c0 = 0; c0 < L; c0 += chunk) {
-        double acc[kMpSlots];
-        int32_t col[kMpSlots];
-        masked_row(i, lane, arp, aci, ava, nrp, nci, x, c0, L, acc, col);
-#pragma unroll
-        for (int s = 0; s < kMpSlots; ++s)
-            if (col[s] >= 0) dst[lo + c0 + s * kWarp + lane] = acc[s];
-    }
-    __syncwarp();
     if (!yp) return;
-    if (root) {
-        for (int32_t e = lane; e < L; e += kWarp) yp[lo + e] = 0.0;
+    if (is_root[i]) {
+        for (int32_t e = 0; e < L; ++e) yp[lo + e] = 0.0;
         return;
     }
-    double ya[kKMax];
+    double ya[kKMax], lam[kKMax];
     for (int a = 0; a < k; ++a) ya[a] = 0.0;
+    const bool in_regs = L <= kMrChunk;
     for (int32_t e = 0; e < L; ++e) {
-        const double v = dst[lo + e];
+        double v = 0.0;
+        if (in_regs) {
+#pragma unroll
+            for (int s = 0; s < kMrChunk; ++s)
+                if (s == e) v = keep[s];
+        } else {
+            v = dst[lo + e];
+        }
         const int32_t cj = nci[lo + e];
         for (int a = 0; a < k; ++a) ya[a] += Bc[static_cast<size_t>(a) * nc + cj] * v;
     }
     const double* G = gp + static_cast<size_t>(i) * k * k;
-    double lam[kKMax];
     for (int a = 0; a < k; ++a) {
-        double s = 0.0;
-        for (int b = 0; b < k; ++b) s += G[a * k + b] * ya[b];
-        lam[a] = s;
+        double s2 = 0.0;
+        for (int b2 = 0; b2 < k; ++b2) s2 += G[a * k + b2] * ya[b2];
+        lam[a] = s2;
     }
-    __syncwarp();
-    for (int32_t e = lane; e < L; e += kWarp) {
-        double t = 0.0;
-        for (int a = 0; a < k; ++a) t += Bc[static_cast<size_t>(a) * nc + nci[lo + e]] * lam[a];
-        yp[lo + e] = dst[lo + e] - t;
+    for (int32_t e = 0; e < L; ++e) {
+        double v = 0.0;
+        if (in_regs) {
+#pragma unroll
+            for (int s = 0; s < kMrChunk; ++s)
+                if (s == e) v = keep[s];
+        } else {
+            v = dst[lo + e];
+        }
+        const int32_t cj = nci[lo + e];
+        double t2 = 0.0;
+        for (int a = 0; a < k; ++a) t2 += Bc[static_cast<size_t>(a) * nc + cj] * lam[a];
+        yp[lo + e] = v - t2;
     }
 }
 
@@ -987,12 +949,12 @@ void energy_minimize(Ctx& c, const DCsr& A, const DCsr& T, const double* B, cons
                N.ci.get(), P.get(), err.get());
         if (read_scalar(c, err.get())) throw InvalidArgument("energy_minimize: T has an entry outside the pattern");
     }
-    const unsigned mp_grid = blocks_for(n, kMpWarps);
+    const unsigned mp_grid = blocks_for(n, 128);
     auto mp_bytes = [&](const DCsr& M, int outs) {
         return 12.0 * M.nnz + 4.0 * (M.nr + 1) + 4.0 * nz + 4.0 * (n + 1) + 8.0 * nz * (1 + outs) + 8.0 * k * nc +
                8.0 * k * k * n;
     };
-    const unsigned mp_block = kMpWarps * kWarp;
+    const unsigned mp_block = 128;
     const unsigned ew = blocks_for(nz, 256);
 
     if (krylov == 0) {
@@ -1005,7 +967,7 @@ void energy_minimize(Ctx& c, const DCsr& A, const DCsr& T, const double* B, cons
         DBuf<double> APm(static_cast<size_t>(nz), c.s), R(static_cast<size_t>(nz), c.s), Z(static_cast<size_t>(nz), c.s),
             D(static_cast<size_t>(nz), c.s), ADm(static_cast<size_t>(nz), c.s), ADp(static_cast<size_t>(nz), c.s);
         AMG_CK(cudaMemsetAsync(D.get(), 0, sizeof(double) * nz, c.s));
-        launch(c, k_masked_project, mp_grid, mp_block, 0, n, A.rp.get(), A.ci.get(), A.va.get(), N.rp.get(),
+        launch(c, k_masked_rows, mp_grid, mp_block, 0, n, A.rp.get(), A.ci.get(), A.va.get(), N.rp.get(),
                N.ci.get(), static_cast<const double*>(P.get()), k, Bc, nc, static_cast<const double*>(gp.get()),
                static_cast<const unsigned char*>(is_root.get()), APm.get(), static_cast<double*>(nullptr),
                static_cast<const int32_t*>(nullptr));
@@ -1029,7 +991,7 @@ void energy_minimize(Ctx& c, const DCsr& A, const DCsr& T, const double* B, cons
             launch(c, k_cg_ctl_newsum, 1, 1, 0, S, F);
             launch(c, k_cg_dir, ew, 256, 0, nz, static_cast<const double*>(Z.get()), D.get(),
                    static_cast<const double*>(S), static_cast<const int32_t*>(F));
-            launch_prof(c, kProfMaskedProduct, mp_bytes(A, 2), k_masked_project, mp_grid, mp_block, 0, n, A.rp.get(),
+            launch_prof(c, kProfMaskedProduct, mp_bytes(A, 2), k_masked_rows, mp_grid, mp_block, 0, n, A.rp.get(),
                    A.ci.get(), A.va.get(), N.rp.get(),
                    N.ci.get(), static_cast<const double*>(D.get()), k, Bc, nc, static_cast<const double*>(gp.get()),
                    static_cast<const unsigned char*>(is_root.get()), ADm.get(), ADp.get(),
@@ -1059,7 +1021,7 @@ void energy_minimize(Ctx& c, const DCsr& A, const DCsr& T, const double* B, cons
     transpose(c, A, At);
     spgemm(c, At, A, AtA);
     DBuf<double> R0(static_cast<size_t>(nz), c.s);
-    launch(c, k_masked_project, mp_grid, mp_block, 0, n, AtA.rp.get(), AtA.ci.get(), AtA.va.get(), N.rp.get(),
+    launch(c, k_masked_rows, mp_grid, mp_block, 0, n, AtA.rp.get(), AtA.ci.get(), AtA.va.get(), N.rp.get(),
            N.ci.get(), static_cast<const double*>(P.get()), k, Bc, nc, static_cast<const double*>(gp.get()),
            static_cast<const unsigned char*>(is_root.get()), R0.get(), static_cast<double*>(nullptr),
            static_cast<const int32_t*>(nullptr));
@@ -1082,18 +1044,17 @@ void energy_minimize(Ctx& c, const DCsr& A, const DCsr& T, const double* B, cons
     int built = 0;
     for (int s = 0; s < m; ++s) {
         double* W = V.get() + static_cast<size_t>(s + 1) * nz;
-        launch_prof(c, kProfMaskedProduct, mp_bytes(AtA, 1), k_masked_project, mp_grid, mp_block, 0, n, AtA.rp.get(),
+        launch_prof(c, kProfMaskedProduct, mp_bytes(AtA, 1), k_masked_rows, mp_grid, mp_block, 0, n, AtA.rp.get(),
                AtA.ci.get(), AtA.va.get(), N.rp.get(),
                N.ci.get(), static_cast<const double*>(V.get() + static_cast<size_t>(s) * nz), k, Bc, nc,
                static_cast<const double*>(gp.get()), static_cast<const unsigned char*>(is_root.get()),
                static_cast<double*>(nullptr), W, static_cast<const int32_t*>(nullptr));
-        for (int t = 0; t <= s; ++t) {
-            double* h = Hd.get() + t * m + s;
-            dot(c, W, V.get() + static_cast<size_t>(t) * nz, nz, h);
-            axpy_dev(c, h, -1.0, V.get() + static_cast<size_t>(t) * nz, W, nz);
-        }
         double* hn_d = Hd.get() + (s + 1) * m + s;
-        nrm2(c, W, nz, hn_d);
+        dot(c, W, V.get(), nz, Hd.get() + s);
+        for (int t = 0; t <= s; ++t)
+            axpy_dot(c, Hd.get() + t * m + s, -1.0, V.get() + static_cast<size_t>(t) * nz, W,
+                     t < s ? V.get() + static_cast<size_t>(t + 1) * nz : nullptr, nz,
+                     t < s ? Hd.get() + (t + 1) * m + s : hn_d, t == s);
         const double hn = read_scalar(c, hn_d);
         built = s + 1;
         st.iterations = s + 1;

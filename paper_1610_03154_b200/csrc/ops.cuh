@@ -45,6 +45,9 @@ void nrm2(Ctx& c, const double* x, int64_t n, double* out);
 void axpy_dev(Ctx& c, const double* alpha, double sign, const double* x, double* y, int64_t n);
 // x *= 1 / (*denom)                      (scale(1.0 / h, v))
 void scale_recip_dev(Ctx& c, const double* denom, double* x, int64_t n);
+// y += sign * (*alpha) * x; *out = dot(y, z) (z null: dot(y, y), sqrt if take_sqrt) -- one pass
+void axpy_dot(Ctx& c, const double* alpha, double sign, const double* x, double* y, const double* z, int64_t n,
+              double* out, bool take_sqrt);
 void scale_const(Ctx& c, double alpha, double* x, int64_t n);
 
 // ---- strength / aggregation (strength.cu, aggregate.cu) --------------------------------

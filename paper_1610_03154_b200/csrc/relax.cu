@@ -9,6 +9,8 @@
 #include <cuda/atomic>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include "ops.cuh"
 
@@ -339,6 +341,15 @@ void gauss_seidel(Ctx& c, const DCsr& A, const double* inv_diag, double* x, cons
     }
     copy_d2d(c, x, X.get() + stride * nsw, static_cast<int64_t>(stride));
     sync(c);
+    if (std::getenv("AMGCU_DEBUG_GS")) {
+        std::vector<int32_t> hs(static_cast<size_t>(nf) + 1);
+        copy_d2h(c, hs.data(), segf.get(), nf + 1);
+        sync(c);
+        int32_t longest = 0;
+        for (int32_t g = 0; g < nf; ++g) longest = std::max(longest, hs[g + 1] - hs[g]);
+        std::fprintf(stderr, "[gs] n=%d nnz=%lld k=%d sweeps=%d segments=%d longest=%d\n", n,
+                     static_cast<long long>(A.nnz), k, nsw, nf, longest);
+    }
 }
 
 void jacobi(Ctx& c, const DCsr& A, const double* wdinv, double* x, const double* b, int k, int sweeps) {
