@@ -113,6 +113,24 @@ class Context:
         self._chk(lib.amgcu_ctx_launch_count(self.handle, C.byref(v)))
         return v.value
 
+    def set_profiling(self, on: bool, mask: int = 0xFFFFFFFF):
+        """Per-kernel-family CUDA-event timing (two events per launch of a masked family)."""
+        self._chk(lib.amgcu_ctx_set_profiling(self.handle, 1 if on else 0))
+        self._chk(lib.amgcu_ctx_set_profile_mask(self.handle, C.c_uint32(mask)))
+        if on:
+            self._chk(lib.amgcu_ctx_profile_reset(self.handle))
+
+    def profile(self) -> dict:
+        """{family: (launches, ms, algorithmic_bytes)} since the last reset."""
+        lib.amgcu_profile_family_name.restype = C.c_char_p
+        out = {}
+        for f in range(lib.amgcu_profile_family_count()):
+            n, ms, by = C.c_int64(), C.c_double(), C.c_double()
+            self._chk(lib.amgcu_ctx_profile_query(self.handle, f, C.byref(n), C.byref(ms), C.byref(by)))
+            if n.value:
+                out[lib.amgcu_profile_family_name(f).decode()] = (n.value, ms.value, by.value)
+        return out
+
     def _chk(self, code):
         if code != 0:
             raise_for(code if code in (1, 2, 3) else 2, lib.amgcu_last_error(self.handle).decode())

@@ -44,8 +44,9 @@ constexpr int kMaxK = 8;
 // Items (sweep, segment) draw tickets in (sweep, position) order; segments are
 // contiguous, so any unfinished row that an item waits on belongs to an item
 // with a smaller ticket, which is already running: the launch cannot deadlock.
-constexpr int kSegWarps = 4;
-constexpr int kSegMaxE = 16;  // entries per row handled from the prefetch cache
+constexpr int kSegMaxE = 32;  // entries per row handled from the prefetch records
+constexpr int kChunk = 8;     // prefetcher: entries loaded per batch
+constexpr int kRegTerms = 16; // solver: terms held in registers
 constexpr unsigned long long kPending = 0x7FF4A11CE5EEDULL;
 
 __device__ __forceinline__ unsigned long long load_relaxed_bits(const double* p) {
@@ -54,35 +55,106 @@ __device__ __forceinline__ unsigned long long load_relaxed_bits(const double* p)
     return r.load(cuda::memory_order_relaxed);
 }
 
-__device__ __forceinline__ double wait_bits(const double* p, unsigned long long bits) {
-    unsigned ns = 16;
+__device__ __forceinline__ double wait_bits(const double* p, unsigned long long bits, unsigned max_ns) {
+    unsigned ns = 8;
     while (bits == kPending) {
-        __nanosleep(ns);
-        ns = ns < 512 ? 2 * ns : 512;
+        if (max_ns) __nanosleep(ns);
+        ns = ns < max_ns ? 2 * ns : max_ns;
         bits = load_relaxed_bits(p);
     }
     return __longlong_as_double(static_cast<long long>(bits));
 }
 
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
 // entry classes in sweep order
 enum : int { kSelf = 0, kInBlock = 1, kReady = 2, kPoll = 3 };
 
-// Per warp, dynamic shared memory: cache[32][kSegMaxE][K] prefetched bits,
-// xb[32][K] values published in the current block.  K = number of candidate
-// columns (compile-time so the per-entry arrays stay in registers).
+__device__ __forceinline__ unsigned long long vload(const unsigned long long* p) {
+    return *reinterpret_cast<const volatile unsigned long long*>(p);
+}
+__device__ __forceinline__ void vstore(unsigned long long* p, unsigned long long v) {
+    *reinterpret_cast<volatile unsigned long long*>(p) = v;
+}
+__device__ __forceinline__ int vload(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
+__device__ __forceinline__ void vstore(int* p, int v) { *reinterpret_cast<volatile int*>(p) = v; }
+
+// Each segment is served by THREE warps of one CTA:
+//   prefetcher: phase A for the block AHEAD of the solver (double-buffered):
+//     loads every entry and every independent x in batches, sums the CSR
+//     prefix that needs no new value, and compiles the rest of the row into a
+//     dense TERM list (a, shared-memory slot) -- a slot is the value's record
+//     (ready now, or filled in by the poller) or the producer lane's xb entry
+//     (this block or the previous one of the own segment);
+//   poller:     keeps loading the pending values of the solver's current and
+//     next block (lane l for row l, all of the row's loads in flight) and
+//     writes each resolved one into its slot;
+//   solver:     phase B -- lanes finish their rows in order: for every term,
+//     wait until the slot is no longer kPending, then acc -= a * x.  The step
+//     is a short branch-free loop over registers (the i-cache matters here:
+//     the three roles run side by side on the SM).
+// Rows whose entries do not fit the records (more than kSegMaxE, or more
+// pending values than the poll list) take a rolled slow path that polls
+// global memory directly.
+// Hand-shakes (shared memory, volatile): ready[b] = block sequence number the
+// buffer b holds; done = last block the solver finished; step = rows of block
+// done + 1 finished; plo = lowest block the poller may still touch (the
+// prefetcher refills a buffer only when neither the solver nor the poller
+// can still use it).  Arrays are stored [.][lane] (conflict-free).
+constexpr int kMaxPoll = 16;  // pending (entry, column) values tracked per row
+
 template <int K>
-__global__ void __launch_bounds__(kSegWarps * 32)
+struct GsBuf {
+    unsigned long long bits[kSegMaxE][K][32];  // value slots (c stride = 32 words)
+    double ta[kSegMaxE][32];                   // term: matrix value
+    int32_t toff[kSegMaxE][32];                // term: slot offset (bytes from the segment base)
+    const double* paddr[kMaxPoll][32];         // poll list: address
+    int32_t pslot[kMaxPoll][32];               // poll list: word offset of the slot in bits
+    double acc0[K][32];
+    double dinv[32];
+    int32_t nterm[32];  // -1: slow path
+    int32_t npoll[32];
+};
+
+template <int K>
+constexpr int gs_segs_per_cta() {
+    return K <= 3 ? 2 : 1;
+}
+
+template <int K>
+constexpr size_t gs_seg_bytes() {
+    return (2 * sizeof(GsBuf<K>) + 64 * K * sizeof(double) + 15) / 16 * 16;
+}
+
+template <int K>
+__global__ void __launch_bounds__(3 * gs_segs_per_cta<K>() * 32)
     k_gs_segments(int32_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
                   const double* __restrict__ va, const double* __restrict__ inv_diag, const double* __restrict__ b,
                   int nsweeps, const unsigned char* __restrict__ backward, const int32_t* __restrict__ item_base,
                   const int32_t* __restrict__ seg_fwd, const int32_t* __restrict__ seg_bwd, double* __restrict__ X,
-                  unsigned int* __restrict__ ticket) {
+                  unsigned int* __restrict__ ticket, unsigned max_ns, unsigned long long* __restrict__ trace,
+                  int poll_window) {
+    constexpr int S = gs_segs_per_cta<K>();
     extern __shared__ unsigned long long smem[];
     __shared__ unsigned int blk;
+    __shared__ int sh_ready[S][2], sh_done[S], sh_step[S], sh_plo[S];
     if (threadIdx.x == 0) blk = atomicAdd(ticket, 1u);
+    if (threadIdx.x < S) {
+        sh_ready[threadIdx.x][0] = sh_ready[threadIdx.x][1] = -1;
+        sh_done[threadIdx.x] = -1;
+        sh_step[threadIdx.x] = 0;
+        sh_plo[threadIdx.x] = 0;
+    }
     __syncthreads();
-    const int lane = threadIdx.x & 31, wl = threadIdx.x / 32;
-    const int32_t item = static_cast<int32_t>(blk) * kSegWarps + wl;
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x / 32;
+    const int role = warp / S;  // 0 solver, 1 poller, 2 prefetcher
+    const int wl = warp % S;
+    const int32_t item = static_cast<int32_t>(blk) * S + wl;
     if (item >= item_base[nsweeps]) return;
     int s = 0;
     while (item >= item_base[s + 1]) ++s;
@@ -90,144 +162,310 @@ __global__ void __launch_bounds__(kSegWarps * 32)
     const int32_t* segs = bwd ? seg_bwd : seg_fwd;
     const int32_t g = item - item_base[s];
     const int32_t q0 = segs[g], q1 = segs[g + 1];
+    const int nblocks = (q1 - q0 + 31) / 32;
     const size_t stride = static_cast<size_t>(n) * K;
     const double* xin = X + static_cast<size_t>(s) * stride;
     double* xout = X + static_cast<size_t>(s + 1) * stride;
-    unsigned long long* cache = smem + static_cast<size_t>(wl) * 32 * (kSegMaxE + 1) * K;
-    double* xb = reinterpret_cast<double*>(cache + 32 * kSegMaxE * K);
-    unsigned long long* mycache = cache + static_cast<size_t>(lane) * kSegMaxE * K;
-    for (int32_t qb = q0; qb < q1; qb += 32) {
-        const int32_t q = qb + lane;
-        const bool active = q < q1;
-        const int32_t i = active ? (bwd ? n - 1 - q : q) : 0;
-        int32_t lo = 0, hi = 0;
-        if (active) {
-            lo = rp[i];
-            hi = rp[i + 1];
-        }
-        // ---- phase A: every independent load of the row, issued without waiting ----
-        int32_t ref[kSegMaxE];  // in-block: lane index of the producer; otherwise the column
-        unsigned char cls[kSegMaxE];
-        double a[kSegMaxE];
+    unsigned char* segmem = reinterpret_cast<unsigned char*>(smem) + static_cast<size_t>(wl) * gs_seg_bytes<K>();
+    GsBuf<K>* buf = reinterpret_cast<GsBuf<K>*>(segmem);
+    // values published by the solver: xb[block & 1][c][lane]
+    unsigned long long* xb = reinterpret_cast<unsigned long long*>(segmem + 2 * sizeof(GsBuf<K>));
+    const int32_t xb_off = static_cast<int32_t>(2 * sizeof(GsBuf<K>));
+
+    if (role == 2) {
+        // ---------------- prefetcher ----------------
+        for (int seq = 0; seq < nblocks; ++seq) {
+            if (seq >= 2)
+                while (vload(&sh_done[wl]) < seq - 2 || vload(&sh_plo[wl]) < seq - 1) __nanosleep(32);
+            __threadfence_block();
+            GsBuf<K>& B = buf[seq & 1];
+            const int32_t buf_off = static_cast<int32_t>((seq & 1) * sizeof(GsBuf<K>));
+            const int32_t qb = q0 + 32 * seq;
+            const int32_t q = qb + lane;
+            const bool active = q < q1;
+            const int32_t i = active ? (bwd ? n - 1 - q : q) : 0;
+            int32_t lo = 0, hi = 0;
+            double dinv_i = 0.0;
+            double acc[K];
 #pragma unroll
-        for (int e = 0; e < kSegMaxE; ++e) {
-            cls[e] = kSelf;
-            ref[e] = 0;
-            a[e] = 0.0;
-            if (lo + e < hi) {
-                const int32_t j = ci[lo + e];
-                a[e] = va[lo + e];
-                ref[e] = j;
-                if (j != i) {
+            for (int c = 0; c < K; ++c) acc[c] = 0.0;
+            if (active) {
+                lo = rp[i];
+                hi = rp[i + 1];
+                dinv_i = inv_diag[i];
+                if (b) {
+#pragma unroll
+                    for (int c = 0; c < K; ++c) acc[c] = b[static_cast<size_t>(c) * n + i];
+                }
+            }
+            const int32_t ne = min(hi - lo, kSegMaxE);
+            int np = 0;
+            bool slow = active && hi - lo > kSegMaxE;
+            // pass 1, kChunk entries at a time: class, slot and every independent value.
+            // Staging: ta[e] = a, toff[e] = class | xb offset << 2.
+            for (int e0 = 0; e0 < ne; e0 += kChunk) {
+                int32_t jj[kChunk];
+                double aa[kChunk];
+#pragma unroll
+                for (int u = 0; u < kChunk; ++u) {
+                    jj[u] = i;
+                    aa[u] = 0.0;
+                    if (e0 + u < ne) {
+                        jj[u] = ci[lo + e0 + u];
+                        aa[u] = va[lo + e0 + u];
+                    }
+                }
+                int cls[kChunk], xslot[kChunk];
+#pragma unroll
+                for (int u = 0; u < kChunk; ++u) {
+                    const int32_t j = jj[u];
                     const int32_t qj = bwd ? n - 1 - j : j;
                     const bool fresh = qj < q;
-                    if (fresh && qj >= qb) {
-                        cls[e] = kInBlock;
-                        ref[e] = qj - qb;
-                    } else {
-                        const bool own = fresh && qj >= q0;  // earlier block of this warp's segment
-                        cls[e] = (own || (!fresh && s == 0)) ? kReady : kPoll;
+                    int cl = kSelf, xs = 0;
+                    if (e0 + u < ne && j != i) {
+                        if (fresh && qj >= qb) {
+                            cl = kInBlock;
+                            xs = xb_off + 8 * ((seq & 1) * 32 * K + (qj - qb));
+                        } else if (fresh && qj >= q0 && qj >= qb - 32) {
+                            cl = kInBlock;
+                            xs = xb_off + 8 * (((seq + 1) & 1) * 32 * K + (qj - qb + 32));
+                        } else {
+                            cl = ((fresh && qj >= q0) || (!fresh && s == 0)) ? kReady : kPoll;
+                        }
                     }
+                    cls[u] = cl;
+                    xslot[u] = xs;
                 }
-            }
-        }
-#pragma unroll
-        for (int e = 0; e < kSegMaxE; ++e) {
-            if (cls[e] == kReady || cls[e] == kPoll) {
-                const int32_t j = ref[e];
-                const int32_t qj = bwd ? n - 1 - j : j;
-                const double* src = (qj < q) ? xout : xin;
 #pragma unroll
                 for (int c = 0; c < K; ++c) {
-                    const double* addr = &src[static_cast<size_t>(c) * n + j];
-                    mycache[e * K + c] = cls[e] == kReady
-                                             ? static_cast<unsigned long long>(__double_as_longlong(__ldcg(addr)))
-                                             : load_relaxed_bits(addr);
-                }
-            }
-        }
-        // CSR prefix that needs neither an in-block value nor a pending one
-        double acc[K];
+                    unsigned long long xv[kChunk];
 #pragma unroll
-        for (int c = 0; c < K; ++c) acc[c] = (active && b) ? b[static_cast<size_t>(c) * n + i] : 0.0;
-        bool open = active;
-        int32_t e_stop = 0;
-#pragma unroll
-        for (int e = 0; e < kSegMaxE; ++e) {
-            if (open && lo + e < hi) {
-                if (cls[e] == kInBlock) {
-                    open = false;
-                } else if (cls[e] != kSelf) {
-                    bool pending = false;
-#pragma unroll
-                    for (int c = 0; c < K; ++c) pending = pending || mycache[e * K + c] == kPending;
-                    if (pending) {
-                        open = false;
-                    } else {
-#pragma unroll
-                        for (int c = 0; c < K; ++c)
-                            acc[c] -= a[e] * __longlong_as_double(static_cast<long long>(mycache[e * K + c]));
-                    }
-                }
-                if (open) e_stop = e + 1;
-            }
-        }
-        __syncwarp();
-        // ---- phase B: lanes finish in order; arithmetic on registers, polls only if pending ----
-        const int32_t cnt = min(32, q1 - qb);
-        for (int32_t t = 0; t < cnt; ++t) {
-            if (lane == t) {
-#pragma unroll
-                for (int e = 0; e < kSegMaxE; ++e) {
-                    if (e >= e_stop && lo + e < hi) {
-                        if (cls[e] == kInBlock) {
-#pragma unroll
-                            for (int c = 0; c < K; ++c) acc[c] -= a[e] * xb[ref[e] * K + c];
-                        } else if (cls[e] != kSelf) {
-                            const int32_t j = ref[e];
+                    for (int u = 0; u < kChunk; ++u) {
+                        xv[u] = kPending;
+                        if (cls[u] >= kReady) {
+                            const int32_t j = jj[u];
                             const int32_t qj = bwd ? n - 1 - j : j;
-                            const double* src = (qj < q) ? xout : xin;
+                            const double* addr = &((qj < q) ? xout : xin)[static_cast<size_t>(c) * n + j];
+                            xv[u] = cls[u] == kReady
+                                        ? static_cast<unsigned long long>(__double_as_longlong(__ldcg(addr)))
+                                        : load_relaxed_bits(addr);
+                        }
+                    }
 #pragma unroll
-                            for (int c = 0; c < K; ++c)
-                                acc[c] -= a[e] * wait_bits(&src[static_cast<size_t>(c) * n + j], mycache[e * K + c]);
+                    for (int u = 0; u < kChunk; ++u) {
+                        if (cls[u] >= kReady) {
+                            const int e = e0 + u;
+                            B.bits[e][c][lane] = xv[u];
+                            if (xv[u] == kPending) {
+                                if (np < kMaxPoll) {
+                                    const int32_t j = jj[u];
+                                    const int32_t qj = bwd ? n - 1 - j : j;
+                                    B.paddr[np][lane] = &((qj < q) ? xout : xin)[static_cast<size_t>(c) * n + j];
+                                    B.pslot[np][lane] = (e * K + c) * 32 + lane;
+                                    ++np;
+                                } else {
+                                    slow = true;
+                                }
+                            }
                         }
                     }
                 }
-                // entries beyond the prefetch window, in CSR order
-                for (int32_t p = lo + kSegMaxE; p < hi; ++p) {
-                    const int32_t j = ci[p];
-                    if (j == i) continue;
-                    const int32_t qj = bwd ? n - 1 - j : j;
-                    const bool fresh = qj < q;
-                    const double av = va[p];
-                    if (fresh && qj >= qb) {
 #pragma unroll
-                        for (int c = 0; c < K; ++c) acc[c] -= av * xb[(qj - qb) * K + c];
-                        continue;
+                for (int u = 0; u < kChunk; ++u) {
+                    if (e0 + u < ne) {
+                        B.ta[e0 + u][lane] = aa[u];
+                        B.toff[e0 + u][lane] = cls[u] | (xslot[u] << 2);
                     }
-                    const double* src = fresh ? xout : xin;
-                    const bool own = fresh && qj >= q0;
-#pragma unroll
-                    for (int c = 0; c < K; ++c) {
-                        const double* addr = &src[static_cast<size_t>(c) * n + j];
-                        const unsigned long long bits =
-                            (own || (!fresh && s == 0))
-                                ? static_cast<unsigned long long>(__double_as_longlong(__ldcg(addr)))
-                                : load_relaxed_bits(addr);
-                        acc[c] -= av * wait_bits(addr, bits);
-                    }
-                }
-                const double d = inv_diag[i];
-#pragma unroll
-                for (int c = 0; c < K; ++c) {
-                    const double xi = acc[c] * d;
-                    xb[t * K + c] = xi;
-                    cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> out(
-                        *reinterpret_cast<unsigned long long*>(&xout[static_cast<size_t>(c) * n + i]));
-                    out.store(static_cast<unsigned long long>(__double_as_longlong(xi)), cuda::memory_order_relaxed);
                 }
             }
+            // pass 2 (in place, nt <= e): the CSR prefix that needs neither an xb value nor a
+            // pending one, then the term list
+            bool stopped = false;
+            int nt = 0;
+            for (int e = 0; e < ne; ++e) {
+                const int code = B.toff[e][lane];
+                const int cl = code & 3;
+                if (cl == kSelf) continue;
+                const double ae = B.ta[e][lane];
+                if (!stopped) {
+                    bool pending = cl == kInBlock;
+#pragma unroll
+                    for (int c = 0; c < K; ++c) pending = pending || B.bits[e][c][lane] == kPending;
+                    stopped = pending;
+                }
+                if (!stopped) {
+#pragma unroll
+                    for (int c = 0; c < K; ++c)
+                        acc[c] -= ae * __longlong_as_double(static_cast<long long>(B.bits[e][c][lane]));
+                } else {
+                    B.ta[nt][lane] = ae;
+                    B.toff[nt][lane] =
+                        cl == kInBlock ? (code >> 2) : buf_off + static_cast<int32_t>(8 * (e * K * 32 + lane));
+                    ++nt;
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < K; ++c) B.acc0[c][lane] = acc[c];
+            B.dinv[lane] = dinv_i;
+            B.nterm[lane] = slow ? -1 : nt;
+            B.npoll[lane] = slow ? 0 : np;
             __syncwarp();
+            __threadfence_block();
+            if (lane == 0) vstore(&sh_ready[wl][seq & 1], seq);
+        }
+        return;
+    }
+
+    if (role == 1) {
+        // ---------------- poller ----------------
+        int mblk[2] = {-1, -1};
+        unsigned mask[2] = {0u, 0u};
+        unsigned ns = 0;
+        unsigned long long* bits_base[2] = {&buf[0].bits[0][0][0], &buf[1].bits[0][0][0]};
+        while (true) {
+            const int cur = vload(&sh_done[wl]) + 1;
+            if (cur >= nblocks) break;
+            vstore(&sh_plo[wl], cur);
+            __threadfence_block();
+            const int step = vload(&sh_step[wl]);
+            bool progress = false, more = false;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int bq = cur + h;
+                const int sl = bq & 1;
+                if (bq >= nblocks) continue;
+                if (mblk[sl] != bq) {
+                    if (vload(&sh_ready[wl][sl]) != bq) continue;
+                    __threadfence_block();
+                    mblk[sl] = bq;
+                    const int np = q0 + 32 * bq + lane < q1 ? buf[sl].npoll[lane] : 0;
+                    mask[sl] = np >= 32 ? 0xffffffffu : ((1u << np) - 1u);
+                }
+                const int rel = h * 32 + lane - step;  // rows ahead of the solver
+                const unsigned m = (rel < 0 || rel >= poll_window) ? 0u : mask[sl];
+                if (!m) continue;
+                GsBuf<K>& B = buf[sl];
+                unsigned long long got[kMaxPoll];
+#pragma unroll
+                for (int u = 0; u < kMaxPoll; ++u) got[u] = (m >> u) & 1u ? load_relaxed_bits(B.paddr[u][lane]) : kPending;
+#pragma unroll
+                for (int u = 0; u < kMaxPoll; ++u) {
+                    if (((m >> u) & 1u) && got[u] != kPending) {
+                        vstore(bits_base[sl] + B.pslot[u][lane], got[u]);
+                        mask[sl] &= ~(1u << u);
+                        progress = true;
+                    }
+                }
+                if (mask[sl]) more = true;
+            }
+            if (__any_sync(0xffffffffu, progress)) {
+                ns = 0;
+            } else {
+                // nothing resolved: back off (longer when nothing is pending at all)
+                const bool any_more = __any_sync(0xffffffffu, more);
+                ns = ns ? min(2 * ns, any_more ? 64u : 512u) : 16u;
+                __nanosleep(ns);
+            }
+        }
+        return;
+    }
+
+    // ---------------- solver ----------------
+    for (int seq = 0; seq < nblocks; ++seq) {
+        const int32_t qb = q0 + 32 * seq;
+        unsigned long long* tr = trace ? trace + (static_cast<size_t>(s) * n + qb) * 4 : nullptr;
+        if (tr && lane == 0) tr[0] = globaltimer_ns();
+        // this block's xb slots become pending (the previous block's stay readable)
+#pragma unroll
+        for (int c = 0; c < K; ++c) xb[((seq & 1) * K + c) * 32 + lane] = kPending;
+        while (vload(&sh_ready[wl][seq & 1]) != seq) __nanosleep(32);
+        __threadfence_block();
+        GsBuf<K>& B = buf[seq & 1];
+        const int32_t q = qb + lane;
+        const int32_t i = q < q1 ? (bwd ? n - 1 - q : q) : 0;
+        double acc[K];
+#pragma unroll
+        for (int c = 0; c < K; ++c) acc[c] = B.acc0[c][lane];
+        const double dinv_i = B.dinv[lane];
+        const int32_t nt = B.nterm[lane];
+        // the first kRegTerms terms live in registers for the step (the rest: shared memory)
+        double rta[kRegTerms];
+        int32_t rtoff[kRegTerms];
+#pragma unroll
+        for (int k = 0; k < kRegTerms; ++k) {
+            rta[k] = B.ta[k][lane];
+            rtoff[k] = B.toff[k][lane];
+        }
+        if (tr && lane == 0) tr[1] = globaltimer_ns();
+        const int32_t cnt = min(32, q1 - qb);
+        for (int32_t t = 0; t < cnt; ++t) {
+            if (lane == t) {
+                if (nt >= 0) {
+#pragma unroll
+                    for (int k = 0; k < kSegMaxE; ++k) {
+                        if (k < nt) {
+                            const double ak = k < kRegTerms ? rta[k] : B.ta[k][lane];
+                            const unsigned char* sp = segmem + (k < kRegTerms ? rtoff[k] : B.toff[k][lane]);
+#pragma unroll
+                            for (int c = 0; c < K; ++c) {
+                                const unsigned long long* slot = reinterpret_cast<const unsigned long long*>(sp) + 32 * c;
+                                unsigned long long v = vload(slot);
+                                while (v == kPending) v = vload(slot);
+                                acc[c] -= ak * __longlong_as_double(static_cast<long long>(v));
+                            }
+                        }
+                    }
+                } else {
+                    // slow path: the whole row in CSR order, values from xb or global memory
+#pragma unroll
+                    for (int c = 0; c < K; ++c) acc[c] = b ? b[static_cast<size_t>(c) * n + i] : 0.0;
+                    const int32_t lo = rp[i], hi = rp[i + 1];
+                    for (int32_t p = lo; p < hi; ++p) {
+                        const int32_t j = ci[p];
+                        if (j == i) continue;
+                        const int32_t qj = bwd ? n - 1 - j : j;
+                        const bool fresh = qj < q;
+                        const double av = va[p];
+                        if (fresh && qj >= qb) {
+#pragma unroll
+                            for (int c = 0; c < K; ++c)
+                                acc[c] -= av * __longlong_as_double(static_cast<long long>(
+                                                   xb[((seq & 1) * K + c) * 32 + (qj - qb)]));
+                            continue;
+                        }
+                        const double* src = fresh ? xout : xin;
+                        const bool own = fresh && qj >= q0;  // earlier blocks of the own segment: published
+#pragma unroll
+                        for (int c = 0; c < K; ++c) {
+                            const double* addr = &src[static_cast<size_t>(c) * n + j];
+                            const unsigned long long bb =
+                                (own || (!fresh && s == 0))
+                                    ? static_cast<unsigned long long>(__double_as_longlong(__ldcg(addr)))
+                                    : load_relaxed_bits(addr);
+                            acc[c] -= av * wait_bits(addr, bb, max_ns);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int c = 0; c < K; ++c) {
+                    const double xi = acc[c] * dinv_i;
+                    const unsigned long long xbits = static_cast<unsigned long long>(__double_as_longlong(xi));
+                    vstore(&xb[((seq & 1) * K + c) * 32 + t], xbits);
+                    cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> out(
+                        *reinterpret_cast<unsigned long long*>(&xout[static_cast<size_t>(c) * n + i]));
+                    out.store(xbits, cuda::memory_order_relaxed);
+                }
+                vstore(&sh_step[wl], t + 1);
+                if (trace) trace[(static_cast<size_t>(s) * n + q) * 4 + 3] = globaltimer_ns();
+            }
+            __syncwarp();
+        }
+        if (tr && lane == 0) tr[2] = globaltimer_ns();
+        __syncwarp();
+        __threadfence_block();
+        if (lane == 0) {
+            vstore(&sh_step[wl], 0);
+            vstore(&sh_done[wl], seq);
         }
     }
 }
@@ -263,6 +501,24 @@ __global__ void k_segment_starts(int32_t n, const int32_t* __restrict__ head, co
 __global__ void k_fill_pending(int64_t count, double* __restrict__ p) {
     const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (t < count) reinterpret_cast<unsigned long long*>(p)[t] = kPending;
+}
+
+// poll back-off cap in ns (AMGCU_GS_NS overrides; 0 = spin)
+unsigned gs_max_ns() {
+    static const unsigned v = [] {
+        const char* e = std::getenv("AMGCU_GS_NS");
+        return e ? static_cast<unsigned>(std::atoi(e)) : 512u;
+    }();
+    return v;
+}
+
+// rows ahead of the solver whose pending values the poller keeps loading (AMGCU_GS_PW)
+int gs_poll_window() {
+    static const int v = [] {
+        const char* e = std::getenv("AMGCU_GS_PW");
+        return e ? std::atoi(e) : 8;
+    }();
+    return v;
 }
 
 int32_t build_segments(Ctx& c, const DCsr& A, bool bwd, DBuf<int32_t>& starts) {
@@ -319,28 +575,56 @@ void gauss_seidel(Ctx& c, const DCsr& A, const double* inv_diag, double* x, cons
     copy_h2d(c, dbase.get(), base.data(), nsw + 1);
     DBuf<unsigned int> ticket(1, c.s);
     AMG_CK(cudaMemsetAsync(ticket.get(), 0, sizeof(unsigned int), c.s));
-    const size_t smem = static_cast<size_t>(kSegWarps) * 32 * (kSegMaxE + 1) * k * sizeof(unsigned long long);
+    // AMGCU_GS_TRACE=<file>: per (sweep, block) globaltimer stamps for the timeline tool
+    const char* trace_path = std::getenv("AMGCU_GS_TRACE");
+    DBuf<unsigned long long> trace;
+    if (trace_path) {
+        trace.alloc(static_cast<size_t>(nsw) * n * 4, c.s);
+        AMG_CK(cudaMemsetAsync(trace.get(), 0, sizeof(unsigned long long) * nsw * n * 4, c.s));
+    }
     const double bytes = nsw * (12.0 * A.nnz + 4.0 * (n + 1) + 8.0 * n + 16.0 * n * k);
-    auto run = [&](auto kern) {
+    auto run = [&](auto kern, int segs, size_t seg_bytes) {
+        // AMGCU_GS_SMEM: request at least this much shared memory per CTA (caps CTAs per SM)
+        static const size_t smem_floor = [] {
+            const char* e = std::getenv("AMGCU_GS_SMEM");
+            return e ? static_cast<size_t>(std::atol(e)) : size_t(0);
+        }();
+        const size_t smem = std::max(seg_bytes * segs, smem_floor);
         if (smem > 48 * 1024)
             AMG_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        launch_prof(c, kProfGaussSeidel, bytes, kern, blocks_for(base[nsw], kSegWarps), kSegWarps * 32, smem, n,
+        launch_prof(c, kProfGaussSeidel, bytes, kern, blocks_for(base[nsw], segs), 3 * segs * 32, smem, n,
                     A.rp.get(), A.ci.get(), A.va.get(), inv_diag, b, nsw, static_cast<const unsigned char*>(bwd.get()),
                     static_cast<const int32_t*>(dbase.get()), static_cast<const int32_t*>(segf.get()),
-                    static_cast<const int32_t*>(symmetric_sweep ? segb.get() : segf.get()), X.get(), ticket.get());
+                    static_cast<const int32_t*>(symmetric_sweep ? segb.get() : segf.get()), X.get(), ticket.get(),
+                    gs_max_ns(), trace.get(), gs_poll_window());
     };
+#define AMGCU_GS_RUN(KK) run(k_gs_segments<KK>, gs_segs_per_cta<KK>(), gs_seg_bytes<KK>())
     switch (k) {
-        case 1: run(k_gs_segments<1>); break;
-        case 2: run(k_gs_segments<2>); break;
-        case 3: run(k_gs_segments<3>); break;
-        case 4: run(k_gs_segments<4>); break;
-        case 5: run(k_gs_segments<5>); break;
-        case 6: run(k_gs_segments<6>); break;
-        case 7: run(k_gs_segments<7>); break;
-        default: run(k_gs_segments<8>); break;
+        case 1: AMGCU_GS_RUN(1); break;
+        case 2: AMGCU_GS_RUN(2); break;
+        case 3: AMGCU_GS_RUN(3); break;
+        case 4: AMGCU_GS_RUN(4); break;
+        case 5: AMGCU_GS_RUN(5); break;
+        case 6: AMGCU_GS_RUN(6); break;
+        case 7: AMGCU_GS_RUN(7); break;
+        default: AMGCU_GS_RUN(8); break;
     }
+#undef AMGCU_GS_RUN
     copy_d2d(c, x, X.get() + stride * nsw, static_cast<int64_t>(stride));
     sync(c);
+    if (trace_path) {
+        std::vector<unsigned long long> ht(static_cast<size_t>(nsw) * n * 4);
+        std::vector<int32_t> hs(static_cast<size_t>(nf) + 1);
+        AMG_CK(cudaMemcpy(ht.data(), trace.get(), ht.size() * 8, cudaMemcpyDeviceToHost));
+        AMG_CK(cudaMemcpy(hs.data(), segf.get(), hs.size() * 4, cudaMemcpyDeviceToHost));
+        if (FILE* f = std::fopen(trace_path, "ab")) {
+            const int32_t hdr[3] = {n, nsw, nf};
+            std::fwrite(hdr, 4, 3, f);
+            std::fwrite(hs.data(), 4, hs.size(), f);
+            std::fwrite(ht.data(), 8, ht.size(), f);
+            std::fclose(f);
+        }
+    }
     if (std::getenv("AMGCU_DEBUG_GS")) {
         std::vector<int32_t> hs(static_cast<size_t>(nf) + 1);
         copy_d2h(c, hs.data(), segf.get(), nf + 1);

@@ -147,6 +147,19 @@ def test_improve_candidates(gpu_seq, port):
             assert got.data.tobytes() == want.data.tobytes(), (scheme, w)
 
 
+def test_gauss_seidel_long_segments(gpu_seq, port):
+    """Segments of many 32-row blocks (the solver / prefetcher / poller hand-offs
+    across blocks), forward, symmetric and multi-column sweeps."""
+    for A_ in (poisson1d(1000), aniso2d(70, 0.1), aniso2d(33, 1.0)):
+        for k in (1, 3):
+            rng = np.random.default_rng(k)
+            B = CandidateSet(A_.n_rows, k, rng.uniform(0.5, 1.5, A_.n_rows * k))
+            for scheme in (1, 2):
+                got = api.improve_candidates(A_, B, 3, scheme, 0.0, ctx=gpu_seq)
+                want = port.improve_candidates(A_, B, 3, scheme, 0.0)
+                assert got.data.tobytes() == want.data.tobytes(), (A_.n_rows, k, scheme)
+
+
 def test_relax(gpu_seq, port):
     rng = np.random.default_rng(3)
     A = random_spd_sparse(20, 0.25, rng)

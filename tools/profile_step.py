@@ -14,6 +14,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=2)
 ap.add_argument("--size", type=int, default=1024)
 ap.add_argument("--reps", type=int, default=2)
+ap.add_argument("--max-restarts", type=int, default=20)
 a = ap.parse_args()
 A, B, Bh, b = api.generate_config(a.config, a.size)
 so, vo = api.config_options(a.config)
@@ -22,8 +23,10 @@ for r in range(a.reps):
     t0 = time.perf_counter()
     h = api.setup(A, B, so, Bh, ctx=ctx)
     x, rep = api.solve(h, b, None, vo)
-    while vo.method == 2 and not rep.converged and not rep.diverged:
+    restarts = 0
+    while vo.method == 2 and not rep.converged and not rep.diverged and restarts < a.max_restarts:
         x, rep = api.solve(h, b, x, vo)
+        restarts += 1
     print(f"rep {r}: levels {h.n_levels()} its {rep.iterations} conv {rep.converged} "
           f"wall {time.perf_counter() - t0:.3f}s launches {ctx.launch_count()}", flush=True)
     del h
