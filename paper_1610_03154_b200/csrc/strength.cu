@@ -241,11 +241,12 @@ __global__ void __launch_bounds__(kEvWarps * kWarp)
                 const int32_t* __restrict__ trp, const int32_t* __restrict__ tci, const double* __restrict__ winv,
                 double drop_tol, int steps, const int64_t* __restrict__ ooff, int32_t* __restrict__ cnt,
                 int32_t* __restrict__ tcol, double* __restrict__ tval, int32_t* __restrict__ overflow_rows,
-                int32_t* __restrict__ n_overflow) {
+                int32_t* __restrict__ n_overflow, const int32_t* __restrict__ rows, int32_t nrows) {
     __shared__ EvShared shm[kEvWarps];
     const int w = threadIdx.x / kWarp, lane = threadIdx.x & (kWarp - 1);
-    const int32_t i = blockIdx.x * kEvWarps + w;
-    if (i >= n) return;
+    const int32_t r = blockIdx.x * kEvWarps + w;
+    if (r >= nrows) return;
+    const int32_t i = rows ? rows[r] : r;
     EvShared& sh = shm[w];
     for (int s = lane; s < kEvHash; s += kWarp) sh.hkey[s] = -1;
     if (lane == 0) {
@@ -369,6 +370,164 @@ __global__ void __launch_bounds__(kEvWarps * kWarp)
         ocol[below_i] = i;
         oval[below_i] = dval;
         cnt[i] = emitted_total + 1;
+    }
+}
+
+// Two evolution steps (the BASELINE configurations), without a neighbourhood.
+// z1 = z0 - W^-1 A z0 with z0 = e_i is non-zero only on column i's pattern
+// (A^T row i) and at i:  z1[j] = [j == i] - winv[j] * A(j, i)  -- exactly the
+// reference's value, its row sum having one non-zero term.  Every row of a
+// ring node u (A row i U A^T row i) lies inside the distance-2 ball, so the
+// second step needs no truncation:
+//   z2[u] = z1[u] - winv[u] * sum_{p in row u, CSR order} a_p z1[c_p],
+// where the terms with z1 = +0 are skipped (the sum starts at +0 and adding
+// +-0 never changes it; matrices holding inf/NaN are outside this argument).
+// One warp per row; A row i and column i's pattern are staged in shared
+// memory and looked up by binary search.  Rows with more than kEv2Cap entries
+// in either list go to the generic kernel.
+constexpr int kEv2Warps = 8;
+constexpr int kEv2Cap = 64;
+
+struct Ev2Shared {
+    int32_t acol[kEv2Cap];       // A row i
+    int32_t tcol[kEv2Cap];       // A^T row i (column i's pattern)
+    double z1[kEv2Cap];          // z1 on column i's pattern
+    int32_t tonly[kEv2Cap];      // A^T entries absent from A row i: exclusive prefix
+    int32_t aemit[kEv2Cap];      // emitted-flag prefix over A row i
+    int32_t temit[kEv2Cap];      // emitted-flag prefix over the A^T-only entries (by A^T index)
+    double amag[kEv2Cap];
+    double tmag[kEv2Cap];
+};
+
+__device__ __forceinline__ int32_t find_sorted(const int32_t* a, int32_t n, int32_t key) {
+    int32_t lo = lower_bound_i32(a, 0, n, key);
+    return (lo < n && a[lo] == key) ? lo : -1;
+}
+
+// exclusive warp prefix of flags[0..n) (in place), returns the total
+__device__ __forceinline__ int32_t warp_prefix(int32_t* flags, int32_t n, int lane) {
+    int32_t base = 0;
+    for (int32_t e0 = 0; e0 < n; e0 += kWarp) {
+        const int32_t e = e0 + lane;
+        const int32_t f = e < n ? flags[e] : 0;
+        const unsigned bal = __ballot_sync(0xffffffffu, f != 0);
+        if (e < n) flags[e] = base + __popc(bal & ((1u << lane) - 1u));
+        base += __popc(bal);
+    }
+    return base;
+}
+
+__global__ void __launch_bounds__(kEv2Warps * kWarp)
+    k_evolution2(int32_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                 const double* __restrict__ va, const int32_t* __restrict__ trp, const int32_t* __restrict__ tci,
+                 const double* __restrict__ tva, const double* __restrict__ winv, double drop_tol,
+                 const int64_t* __restrict__ ooff, int32_t* __restrict__ cnt, int32_t* __restrict__ tcol,
+                 double* __restrict__ tval, int32_t* __restrict__ overflow_rows, int32_t* __restrict__ n_overflow) {
+    __shared__ Ev2Shared shm[kEv2Warps];
+    const int w = threadIdx.x / kWarp, lane = threadIdx.x & (kWarp - 1);
+    const int32_t i = blockIdx.x * kEv2Warps + w;
+    if (i >= n) return;
+    Ev2Shared& sh = shm[w];
+    const int32_t alo = rp[i], na = rp[i + 1] - alo, tlo = trp[i], nt = trp[i + 1] - tlo;
+    if (na > kEv2Cap || nt > kEv2Cap) {
+        if (lane == 0) overflow_rows[atomicAdd(n_overflow, 1)] = i;
+        return;
+    }
+    const double wi = winv[i];
+    for (int32_t e = lane; e < na; e += kWarp) sh.acol[e] = ci[alo + e];
+    for (int32_t e = lane; e < nt; e += kWarp) {
+        const int32_t j = tci[tlo + e];
+        sh.tcol[e] = j;
+        sh.z1[e] = (j == i ? 1.0 : 0.0) - winv[j] * tva[tlo + e];
+    }
+    __syncwarp();
+    // z1 at i when A(i, i) is not stored: 1 - winv_i * (+0)
+    const int32_t ti = find_sorted(sh.tcol, nt, i);
+    const double z1_i = ti >= 0 ? sh.z1[ti] : 1.0 - wi * 0.0;
+    // z2 at a node u (rows in CSR order, z1 looked up on column i's pattern)
+    auto z2_at = [&](int32_t u) -> double {
+        const int32_t tu = u == i ? -2 : find_sorted(sh.tcol, nt, u);
+        const double z1u = u == i ? z1_i : (tu >= 0 ? sh.z1[tu] : 0.0);
+        double az = 0.0;
+        const int32_t lo = rp[u], hi = rp[u + 1];
+        for (int32_t p = lo; p < hi; ++p) {
+            const int32_t j = ci[p];
+            double zj;
+            if (j == i) {
+                zj = z1_i;
+            } else {
+                const int32_t k = find_sorted(sh.tcol, nt, j);
+                if (k < 0) continue;
+                zj = sh.z1[k];
+            }
+            az += va[p] * zj;
+        }
+        return z1u - winv[u] * az;
+    };
+    // ring = A row i U (A^T row i \ A row i); magnitudes |z2|, i excluded
+    double mx = 0.0;
+    for (int32_t e = lane; e < na; e += kWarp) {
+        const int32_t j = sh.acol[e];
+        const double m = j == i ? 0.0 : fabs(z2_at(j));
+        sh.amag[e] = m;
+        mx = fmax(mx, m);
+    }
+    for (int32_t e = lane; e < nt; e += kWarp) {
+        const int32_t j = sh.tcol[e];
+        const bool only = find_sorted(sh.acol, na, j) < 0;
+        sh.tonly[e] = only ? 1 : 0;
+        const double m = (only && j != i) ? fabs(z2_at(j)) : 0.0;
+        sh.tmag[e] = m;
+        mx = fmax(mx, m);
+    }
+    for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    const double cutoff = mx / drop_tol;
+    __syncwarp();
+    for (int32_t e = lane; e < na; e += kWarp) {
+        const double m = sh.amag[e];
+        sh.aemit[e] = (sh.acol[e] != i && mx > 0.0 && m >= cutoff && m > 0.0) ? 1 : 0;
+    }
+    for (int32_t e = lane; e < nt; e += kWarp) {
+        const double m = sh.tmag[e];
+        sh.temit[e] = (sh.tonly[e] && sh.tcol[e] != i && mx > 0.0 && m >= cutoff && m > 0.0) ? 1 : 0;
+    }
+    __syncwarp();
+    // flags -> positions: keep the flags in registers, prefix in place
+    const int32_t a_tot = warp_prefix(sh.aemit, na, lane);
+    const int32_t t_tot = warp_prefix(sh.temit, nt, lane);
+    __syncwarp();
+    // emitted count with column < key, over both lists (prefix arrays are exclusive)
+    auto emitted_below = [&](int32_t key) -> int32_t {
+        const int32_t pa = lower_bound_i32(sh.acol, 0, na, key);
+        const int32_t pt = lower_bound_i32(sh.tcol, 0, nt, key);
+        return (pa < na ? sh.aemit[pa] : a_tot) + (pt < nt ? sh.temit[pt] : t_tot);
+    };
+    int32_t* ocol = tcol + ooff[i];
+    double* oval = tval + ooff[i];
+    for (int32_t e = lane; e < na; e += kWarp) {
+        const int32_t nxt = e + 1 < na ? sh.aemit[e + 1] : a_tot;
+        if (nxt != sh.aemit[e]) {  // emitted
+            const int32_t j = sh.acol[e];
+            const int32_t at = emitted_below(j) + (j > i ? 1 : 0);
+            ocol[at] = j;
+            oval[at] = sh.amag[e];
+        }
+    }
+    for (int32_t e = lane; e < nt; e += kWarp) {
+        const int32_t nxt = e + 1 < nt ? sh.temit[e + 1] : t_tot;
+        if (nxt != sh.temit[e]) {
+            const int32_t j = sh.tcol[e];
+            const int32_t at = emitted_below(j) + (j > i ? 1 : 0);
+            ocol[at] = j;
+            oval[at] = sh.tmag[e];
+        }
+    }
+    if (lane == 0) {
+        const double zi = fabs(z2_at(i));
+        const int32_t at = emitted_below(i);
+        ocol[at] = i;
+        oval[at] = zi > 0.0 ? zi : 1.0;
+        cnt[i] = a_tot + t_tot + 1;
     }
 }
 
@@ -596,10 +755,27 @@ void evolution_strength(Ctx& c, const DCsr& A, const DCsr& At, const double* win
     DBuf<double> tval(static_cast<size_t>(total), c.s);
     DBuf<int32_t> ovf(static_cast<size_t>(n), c.s), novf(1, c.s);
     AMG_CK(cudaMemsetAsync(novf.get(), 0, sizeof(int32_t), c.s));
-    launch_prof(c, kProfEvolution, 12.0 * A.nnz + 8.0 * (n + 1) + 4.0 * At.nnz + 8.0 * n + 12.0 * total, k_evolution,
-                blocks_for(n, kEvWarps), kEvWarps * kWarp, 0, n, A.rp.get(), A.ci.get(), A.va.get(),
-           At.rp.get(), At.ci.get(), winv, drop_tol, steps, static_cast<const int64_t*>(off.get()), cnt.get(),
-           tcol.get(), tval.get(), ovf.get(), novf.get());
+    const double ev_bytes = 12.0 * A.nnz + 8.0 * (n + 1) + 4.0 * At.nnz + 8.0 * n + 12.0 * total;
+    if (steps == 2) {
+        // hash-free two-step kernel; rows beyond its capacity go to the generic one
+        DBuf<int32_t> ovf2(static_cast<size_t>(n), c.s), novf2(1, c.s);
+        AMG_CK(cudaMemsetAsync(novf2.get(), 0, sizeof(int32_t), c.s));
+        launch_prof(c, kProfEvolution, ev_bytes, k_evolution2, blocks_for(n, kEv2Warps), kEv2Warps * kWarp, 0, n,
+                    A.rp.get(), A.ci.get(), A.va.get(), At.rp.get(), At.ci.get(), At.va.get(), winv, drop_tol,
+                    static_cast<const int64_t*>(off.get()), cnt.get(), tcol.get(), tval.get(), ovf2.get(),
+                    novf2.get());
+        const int32_t n2 = read_scalar(c, novf2.get());
+        if (n2 > 0)
+            launch(c, k_evolution, blocks_for(n2, kEvWarps), kEvWarps * kWarp, 0, n, A.rp.get(), A.ci.get(),
+                   A.va.get(), At.rp.get(), At.ci.get(), winv, drop_tol, steps,
+                   static_cast<const int64_t*>(off.get()), cnt.get(), tcol.get(), tval.get(), ovf.get(), novf.get(),
+                   static_cast<const int32_t*>(ovf2.get()), n2);
+    } else {
+        launch_prof(c, kProfEvolution, ev_bytes, k_evolution, blocks_for(n, kEvWarps), kEvWarps * kWarp, 0, n,
+                    A.rp.get(), A.ci.get(), A.va.get(), At.rp.get(), At.ci.get(), winv, drop_tol, steps,
+                    static_cast<const int64_t*>(off.get()), cnt.get(), tcol.get(), tval.get(), ovf.get(), novf.get(),
+                    static_cast<const int32_t*>(nullptr), n);
+    }
     const int32_t nbig = read_scalar(c, novf.get());
     if (nbig > 0) {
         const int32_t conc = std::min<int32_t>(nbig, 64);

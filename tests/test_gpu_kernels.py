@@ -7,7 +7,8 @@ import numpy as np
 import pytest
 
 import paper_1610_03154_b200.api as api
-from paper_1610_03154_b200.types import (CandidateSet, StrengthConfig, StrengthMeasure, constant_candidates,
+from paper_1610_03154_b200.types import (CandidateSet, EvolutionWeighting, StrengthConfig, StrengthMeasure,
+                                         constant_candidates,
                                          from_triplets, identity)
 from tests.helpers import aniso2d, poisson1d, random_sparse, random_spd_sparse, rel_max_err, tridiag
 
@@ -101,6 +102,51 @@ def test_strength(gpu_seq, port, measure, tol):
         n, own, roots = api.greedy_aggregate(N, ctx=gpu_seq)
         n2, own2, roots2 = port.greedy_aggregate(N)
         assert n == n2 and np.array_equal(own, own2) and np.array_equal(roots, roots2)
+
+
+def _dense(D):
+    return from_triplets(D.shape[0], D.shape[1],
+                         [(i, j, float(D[i, j])) for i in range(D.shape[0]) for j in range(D.shape[1]) if D[i, j] != 0.0])
+
+
+def _evolution_cases(rng):
+    cases = []
+    # non-symmetric pattern with a full diagonal
+    R = random_sparse(60, 60, 0.08, rng)
+    D = R.to_dense() + np.diag(rng.uniform(2.0, 3.0, 60))
+    cases.append(_dense(D))
+    # one-sided (upwind, lower bidiagonal) operator: mass lands on column neighbours only
+    U = np.diag(np.full(40, 2.0)) + np.diag(np.full(39, -1.0), -1)
+    cases.append(_dense(U))
+    # a dense row and column (> 64 entries: the generic neighbourhood kernel)
+    n = 90
+    H = np.diag(np.full(n, 4.0)) + np.diag(np.full(n - 1, -1.0), 1) + np.diag(np.full(n - 1, -1.0), -1)
+    H[0, :] = -0.5
+    H[:, 0] = -0.25
+    H[0, 0] = 50.0
+    cases.append(_dense(H))
+    # a row without a stored diagonal
+    M = aniso2d(6, 0.5).to_dense()
+    M[7, 7] = 0.0
+    cases.append(_dense(M))
+    return cases
+
+
+@pytest.mark.parametrize("steps", [1, 2, 3])
+@pytest.mark.parametrize("weighting", [EvolutionWeighting.spectral, EvolutionWeighting.l1jacobi])
+def test_evolution_variants(gpu_seq, port, steps, weighting):
+    """Evolution SOC on patterns the structured configs do not exercise: non-symmetric,
+    one-sided, rows beyond the two-step kernel's capacity, a missing diagonal."""
+    rng = np.random.default_rng(41)
+    for A in _evolution_cases(rng):
+        cfg = StrengthConfig(StrengthMeasure.evolution, 4.0, steps, weighting)
+        try:
+            want = port.strength(A, cfg)
+        except RuntimeError as e:  # zero diagonal under spectral weighting
+            with pytest.raises(RuntimeError, match=str(e).split(" at row")[0]):
+                api.strength(A, cfg, ctx=gpu_seq)
+            continue
+        assert api.strength(A, cfg, ctx=gpu_seq) == want, (A.n_rows, steps, weighting)
 
 
 def test_amalgamate(gpu, port):
