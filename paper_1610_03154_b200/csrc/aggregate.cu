@@ -14,6 +14,9 @@
 // and scans.
 #include <cuda/atomic>
 
+#include <climits>
+#include <cstdlib>
+
 #include "ops.cuh"
 
 namespace amgcu {
@@ -39,7 +42,8 @@ __global__ void k_unit_diag_check(int32_t n, const int32_t* __restrict__ rp, con
 
 __global__ void __launch_bounds__(kMisThreads)
     k_lfmis(int32_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci, const int32_t* __restrict__ trp,
-            const int32_t* __restrict__ tci, int32_t* __restrict__ state, unsigned int* __restrict__ ticket) {
+            const int32_t* __restrict__ tci, int32_t* __restrict__ state, unsigned int* __restrict__ ticket,
+            unsigned max_ns) {
     __shared__ unsigned int blk;
     if (threadIdx.x == 0) blk = atomicAdd(ticket, 1u);
     __syncthreads();
@@ -54,7 +58,7 @@ __global__ void __launch_bounds__(kMisThreads)
     cuda::atomic_ref<int32_t, cuda::thread_scope_device> me(state[i]);
     int32_t p = rp[i];
     int32_t q = p < rp[i + 1] ? trp[ci[p]] : 0;
-    unsigned ns = 32;
+    unsigned ns = 16;
     while (true) {
         bool hit_root = false, pending = false;
         for (; p < rp[i + 1]; ++p) {
@@ -85,7 +89,106 @@ __global__ void __launch_bounds__(kMisThreads)
             break;
         }
         __nanosleep(ns);
-        ns = ns < 1024 ? 2 * ns : 1024;
+        ns = ns < max_ns ? 2 * ns : max_ns;
+    }
+}
+
+// Lower conflict lists: for node i, every r < i with N[r] ∩ N[i] ≠ ∅, i.e.
+// r in S^T row x for x in S row i (duplicates kept; the decision is a set test:
+// OUT iff some listed node is a root, ROOT iff all are OUT).
+__global__ void k_conf_count(int32_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                             const int32_t* __restrict__ trp, const int32_t* __restrict__ tci, int32_t* __restrict__ cnt) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int32_t c = 0;
+    for (int32_t p = rp[i]; p < rp[i + 1]; ++p) {
+        const int32_t x = ci[p];
+        int32_t lo = trp[x], hi = trp[x + 1];
+        const int32_t b = lo;
+        while (lo < hi) {  // rows of S^T ascend: count entries < i
+            const int32_t mid = (lo + hi) >> 1;
+            if (tci[mid] < i) lo = mid + 1;
+            else hi = mid;
+        }
+        c += lo - b;
+    }
+    cnt[i] = c;
+}
+
+__global__ void k_conf_fill(int32_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                            const int32_t* __restrict__ trp, const int32_t* __restrict__ tci,
+                            const int32_t* __restrict__ off, int32_t* __restrict__ list) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int32_t at = off[i];
+    for (int32_t p = rp[i]; p < rp[i + 1]; ++p) {
+        const int32_t x = ci[p];
+        for (int32_t q = trp[x]; q < trp[x + 1]; ++q) {
+            const int32_t r = tci[q];
+            if (r >= i) break;
+            list[at++] = r;
+        }
+    }
+}
+
+// Sync-free wavefront over the lists: a node loads all listed states at once
+// (kMisBatch loads in flight), decides OUT on a root, ROOT when all are OUT,
+// otherwise waits on one undecided state and re-checks only the undecided ones.
+constexpr int kMisBatch = 8;
+
+__global__ void __launch_bounds__(kMisThreads)
+    k_lfmis_lists(int32_t n, const int32_t* __restrict__ off, const int32_t* __restrict__ list,
+                  int32_t* __restrict__ state, unsigned int* __restrict__ ticket, unsigned max_ns) {
+    __shared__ unsigned int blk;
+    if (threadIdx.x == 0) blk = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const int32_t i = static_cast<int32_t>(blk) * kMisThreads + threadIdx.x;
+    if (i >= n) return;
+    cuda::atomic_ref<int32_t, cuda::thread_scope_device> me(state[i]);
+    const int32_t lo = off[i], hi = off[i + 1];
+    int32_t first = lo;  // entries before `first` are known OUT
+    unsigned ns = 16;
+    while (true) {
+        bool root_seen = false;
+        int32_t undecided_at = -1;
+        for (int32_t e0 = first; e0 < hi && !root_seen; e0 += kMisBatch) {
+            int32_t r[kMisBatch];
+#pragma unroll
+            for (int u = 0; u < kMisBatch; ++u) r[u] = e0 + u < hi ? __ldg(&list[e0 + u]) : -1;
+            int32_t v[kMisBatch];
+#pragma unroll
+            for (int u = 0; u < kMisBatch; ++u) {
+                v[u] = kOut;
+                if (r[u] >= 0) {
+                    cuda::atomic_ref<int32_t, cuda::thread_scope_device> st(state[r[u]]);
+                    v[u] = st.load(cuda::memory_order_relaxed);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kMisBatch; ++u) {
+                if (v[u] == kRoot) root_seen = true;
+                if (v[u] == kUndecided && undecided_at < 0) undecided_at = e0 + u;
+            }
+        }
+        if (root_seen || undecided_at < 0) {
+            me.store(root_seen ? kOut : kRoot, cuda::memory_order_relaxed);
+            break;
+        }
+        // everything before the first undecided entry is OUT; wait on it, then re-check from there
+        first = undecided_at;
+        cuda::atomic_ref<int32_t, cuda::thread_scope_device> w(state[list[undecided_at]]);
+        int32_t v = w.load(cuda::memory_order_relaxed);
+        while (v == kUndecided) {
+            __nanosleep(ns);
+            ns = ns < max_ns ? 2 * ns : max_ns;
+            v = w.load(cuda::memory_order_relaxed);
+        }
+        if (v == kRoot) {
+            me.store(kOut, cuda::memory_order_relaxed);
+            break;
+        }
+        first = undecided_at + 1;
+        ns = 16;
     }
 }
 
@@ -156,6 +259,15 @@ __global__ void k_indicator(int32_t n, const int32_t* __restrict__ own, int32_t*
     }
 }
 
+// poll back-off cap in ns (AMGCU_MIS_NS overrides)
+unsigned lfmis_max_ns() {
+    static const unsigned v = [] {
+        const char* e = std::getenv("AMGCU_MIS_NS");
+        return e ? static_cast<unsigned>(std::atoi(e)) : 1024u;
+    }();
+    return v;
+}
+
 }  // namespace
 
 void greedy_aggregate(Ctx& c, const DCsr& S, DAgg& agg) {
@@ -174,9 +286,26 @@ void greedy_aggregate(Ctx& c, const DCsr& S, DAgg& agg) {
     AMG_CK(cudaMemsetAsync(state.get(), 0, sizeof(int32_t) * n, c.s));
     DBuf<unsigned int> ticket(1, c.s);
     AMG_CK(cudaMemsetAsync(ticket.get(), 0, sizeof(unsigned int), c.s));
-    launch_prof(c, kProfAggregate, 8.0 * S.nnz + 8.0 * (n + 1) + 4.0 * n, k_lfmis, blocks_for(n, kMisThreads),
-                kMisThreads, 0, n, S.rp.get(), S.ci.get(), St.rp.get(),
-           St.ci.get(), state.get(), ticket.get());
+    {
+        DBuf<int32_t> cnt(static_cast<size_t>(n) + 1, c.s), off(static_cast<size_t>(n) + 1, c.s);
+        launch(c, k_conf_count, blocks_for(n, 256), 256, 0, n, S.rp.get(), S.ci.get(), St.rp.get(), St.ci.get(),
+               cnt.get());
+        const int64_t total = exclusive_scan_i32(c, cnt.get(), off.get(), n);
+        if (total > INT32_MAX - 1) {
+            // lists would overflow 32-bit offsets: scan S and S^T on the fly
+            launch_prof(c, kProfAggregate, 8.0 * S.nnz + 8.0 * (n + 1) + 4.0 * n, k_lfmis, blocks_for(n, kMisThreads),
+                        kMisThreads, 0, n, S.rp.get(), S.ci.get(), St.rp.get(), St.ci.get(), state.get(),
+                        ticket.get(), lfmis_max_ns());
+        } else {
+            DBuf<int32_t> list(static_cast<size_t>(std::max<int64_t>(total, 1)), c.s);
+            launch(c, k_conf_fill, blocks_for(n, 256), 256, 0, n, S.rp.get(), S.ci.get(), St.rp.get(), St.ci.get(),
+                   static_cast<const int32_t*>(off.get()), list.get());
+            launch_prof(c, kProfAggregate, 8.0 * static_cast<double>(total) + 4.0 * (n + 1) + 4.0 * n,
+                        k_lfmis_lists, blocks_for(n, kMisThreads), kMisThreads, 0, n,
+                        static_cast<const int32_t*>(off.get()), static_cast<const int32_t*>(list.get()), state.get(),
+                        ticket.get(), lfmis_max_ns());
+        }
+    }
     DBuf<int32_t> flag(static_cast<size_t>(n) + 1, c.s), rid(static_cast<size_t>(n) + 1, c.s);
     launch(c, k_root_flags, blocks_for(n, 256), 256, 0, n, static_cast<const int32_t*>(state.get()), flag.get());
     const int32_t n_pass1 = static_cast<int32_t>(exclusive_scan_i32(c, flag.get(), rid.get(), n));

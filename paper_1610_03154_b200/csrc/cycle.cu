@@ -59,19 +59,45 @@ __global__ void k_sell_fill(int32_t nr, const int32_t* __restrict__ rp, const in
     }
 }
 
+// Row sum over a SELL row in stored (CSR) order.  Entries are loaded kBatch at a
+// time with predication instead of stopping at the first padding slot, so a
+// thread keeps kBatch column/value loads and then kBatch gathers in flight;
+// padding (column -1, always after the row's entries) is skipped by predicate,
+// so the sum is the reference's sequential one.
+constexpr int kBatch = 8;
+
+template <typename Gather>
+__device__ __forceinline__ double sell_row_sum(int64_t base, int32_t w, const int32_t* __restrict__ sci,
+                                               const double* __restrict__ sva, Gather gx) {
+    double acc = 0.0;
+    for (int32_t e0 = 0; e0 < w; e0 += kBatch) {
+        int32_t j[kBatch];
+        double a[kBatch];
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) {
+            const int32_t e = e0 + u;
+            j[u] = -1;
+            a[u] = 0.0;
+            if (e < w) {
+                j[u] = __ldg(&sci[base + static_cast<int64_t>(e) * kSlice]);
+                a[u] = __ldg(&sva[base + static_cast<int64_t>(e) * kSlice]);
+            }
+        }
+        double xv[kBatch];
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) xv[u] = j[u] >= 0 ? gx(j[u]) : 0.0;
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u)
+            if (j[u] >= 0) acc += a[u] * xv[u];
+    }
+    return acc;
+}
+
 __device__ __forceinline__ double sell_row(int32_t i, const int64_t* __restrict__ sptr, const int32_t* __restrict__ slen,
                                            const int32_t* __restrict__ sci, const double* __restrict__ sva,
                                            const double* __restrict__ x) {
     const int32_t s = i / kSlice, lane = i % kSlice;
-    const int64_t base = sptr[s] + lane;
-    const int32_t w = slen[s];
-    double acc = 0.0;
-    for (int32_t e = 0; e < w; ++e) {
-        const int32_t j = sci[base + static_cast<int64_t>(e) * kSlice];
-        if (j < 0) break;
-        acc += sva[base + static_cast<int64_t>(e) * kSlice] * x[j];
-    }
-    return acc;
+    return sell_row_sum(sptr[s] + lane, slen[s], sci, sva, [&](int32_t j) { return __ldg(&x[j]); });
 }
 
 struct SellView {
@@ -105,15 +131,8 @@ __global__ void k_relax0_residual(SellView A, const double* __restrict__ wd, con
     const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= A.nr) return;
     const int32_t s = i / kSlice, lane = i % kSlice;
-    const int64_t base = A.sptr[s] + lane;
-    const int32_t w = A.slen[s];
-    double acc = 0.0;
-    for (int32_t e = 0; e < w; ++e) {
-        const int32_t j = A.ci[base + static_cast<int64_t>(e) * kSlice];
-        if (j < 0) break;
-        const double xj = 0.0 + wd[j] * b[j];
-        acc += A.va[base + static_cast<int64_t>(e) * kSlice] * xj;
-    }
+    const double acc = sell_row_sum(A.sptr[s] + lane, A.slen[s], A.ci, A.va,
+                                    [&](int32_t j) { return 0.0 + __ldg(&wd[j]) * __ldg(&b[j]); });
     x[i] = 0.0 + wd[i] * b[i];
     r[i] = b[i] - acc;
 }

@@ -152,6 +152,43 @@ __device__ __forceinline__ void expand_row(int32_t i, const int32_t* __restrict_
     }
 }
 
+// Warp-cooperative expansion: lanes take A entries (32 at a time), a warp scan
+// of their B-row lengths gives each product's sequence number, and each lane
+// writes its B row's products -- the A-entry loop is no longer a chain of
+// dependent loads.
+__device__ __forceinline__ void expand_row_warp(int32_t i, const int32_t* __restrict__ arp,
+                                                const int32_t* __restrict__ aci, const double* __restrict__ ava,
+                                                const int32_t* __restrict__ brp, const int32_t* __restrict__ bci,
+                                                const double* __restrict__ bva, unsigned long long* keys, double* vals,
+                                                int lane) {
+    const int32_t alo = arp[i], ahi = arp[i + 1];
+    int64_t base = 0;
+    for (int32_t p0 = alo; p0 < ahi; p0 += kWarp) {
+        const int32_t p = p0 + lane;
+        int32_t lo = 0, len = 0;
+        double a = 0.0;
+        if (p < ahi) {
+            const int32_t t = aci[p];
+            a = ava[p];
+            lo = brp[t];
+            len = brp[t + 1] - lo;
+        }
+        int32_t incl = len;
+        for (int off = 1; off < kWarp; off <<= 1) {
+            const int32_t v = __shfl_up_sync(0xffffffffu, incl, off);
+            if (lane >= off) incl += v;
+        }
+        const int64_t my = base + incl - len;
+        for (int32_t q = 0; q < len; ++q) {
+            const int64_t seq = my + q;
+            keys[seq] = (static_cast<unsigned long long>(static_cast<uint32_t>(__ldg(&bci[lo + q]))) << 32) |
+                        static_cast<unsigned long long>(seq);
+            vals[seq] = a * __ldg(&bva[lo + q]);
+        }
+        base += __shfl_sync(0xffffffffu, incl, kWarp - 1);
+    }
+}
+
 __global__ void __launch_bounds__(kGemmWarps * kWarp)
     k_spgemm_small(int32_t nr, const int32_t* __restrict__ arp, const int32_t* __restrict__ aci,
                    const double* __restrict__ ava, const int32_t* __restrict__ brp, const int32_t* __restrict__ bci,
@@ -171,7 +208,7 @@ __global__ void __launch_bounds__(kGemmWarps * kWarp)
     }
     unsigned long long* keys = skeys[w];
     double* vals = svals[w];
-    expand_row(i, arp, aci, ava, brp, bci, bva, keys, vals, lane, kWarp);
+    expand_row_warp(i, arp, aci, ava, brp, bci, bva, keys, vals, lane);
     const unsigned n2 = max(next_pow2(static_cast<unsigned>(np)), 2u);
     for (unsigned e = static_cast<unsigned>(np) + lane; e < n2; e += kWarp) keys[e] = ~0ull;
     __syncwarp();

@@ -25,5 +25,5 @@ for r in range(a.reps):
     ctx.set_profiling(False)
     del h
 tot = sum(v[1] for v in prof.values())
-fams = " ".join(f"{k}={v[1]:.2f}" for k, v in sorted(prof.items(), key=lambda kv: -kv[1][1]))
+fams = " ".join(f"{k}={v[1]:.2f}({v[2] / v[1] / 1e6:.0f}GB/s)" for k, v in sorted(prof.items(), key=lambda kv: -kv[1][1]))
 print(f"[{a.tag}] C{a.config}/{a.size} its {rep.iterations} total {tot:.1f} ms :: {fams}", flush=True)
