@@ -17,17 +17,13 @@ namespace {
 
 constexpr int kDotThreads = 256;
 
-__global__ void k_dot_tree(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
-                           double* __restrict__ partials, unsigned int* __restrict__ done, double* __restrict__ out,
-                           bool take_sqrt) {
+// Final stage shared by the tree reductions: the last block to finish sums the
+// block partials with a block-wide (fixed-shape, hence deterministic) reduction.
+__device__ __forceinline__ void finish_tree(double b, double* __restrict__ partials, unsigned int* __restrict__ done,
+                                            double* __restrict__ out, bool take_sqrt) {
     using BR = cub::BlockReduce<double, kDotThreads>;
-    __shared__ typename BR::TempStorage tmp;
+    __shared__ typename BR::TempStorage tmp2;
     __shared__ bool last;
-    double s = 0.0;
-    const int64_t stride = static_cast<int64_t>(gridDim.x) * kDotThreads;
-    for (int64_t i = static_cast<int64_t>(blockIdx.x) * kDotThreads + threadIdx.x; i < n; i += stride)
-        s += x[i] * y[i];
-    const double b = BR(tmp).Sum(s);
     if (threadIdx.x == 0) {
         partials[blockIdx.x] = b;
         __threadfence();
@@ -35,48 +31,78 @@ __global__ void k_dot_tree(const double* __restrict__ x, const double* __restric
         last = (prev == gridDim.x - 1);
     }
     __syncthreads();
-    if (last && threadIdx.x == 0) {
-        __threadfence();
-        double t = 0.0;
-        for (unsigned k = 0; k < gridDim.x; ++k) t += __ldcg(&partials[k]);
+    if (!last) return;
+    __threadfence();
+    double t = 0.0;
+    for (unsigned k = threadIdx.x; k < gridDim.x; k += kDotThreads) t += __ldcg(&partials[k]);
+    t = BR(tmp2).Sum(t);
+    if (threadIdx.x == 0) {
         *out = take_sqrt ? sqrt(t) : t;
         *done = 0u;  // reset for the next call on this stream
     }
 }
 
+// per-thread partial over a grid-stride range, kUnroll independent loads in flight
+constexpr int kUnroll = 4;
+
+__global__ void __launch_bounds__(kDotThreads)
+    k_dot_tree(const double* __restrict__ x, const double* __restrict__ y, int64_t n, double* __restrict__ partials,
+               unsigned int* __restrict__ done, double* __restrict__ out, bool take_sqrt) {
+    using BR = cub::BlockReduce<double, kDotThreads>;
+    __shared__ typename BR::TempStorage tmp;
+    double s = 0.0;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * kDotThreads;
+    int64_t i = static_cast<int64_t>(blockIdx.x) * kDotThreads + threadIdx.x;
+    for (; i + (kUnroll - 1) * stride < n; i += kUnroll * stride) {
+        double xv[kUnroll], yv[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            xv[u] = __ldg(&x[i + u * stride]);
+            yv[u] = __ldg(&y[i + u * stride]);
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) s += xv[u] * yv[u];
+    }
+    for (; i < n; i += stride) s += x[i] * y[i];
+    const double b = BR(tmp).Sum(s);
+    finish_tree(b, partials, done, out, take_sqrt);
+}
+
 // y += sign * (*alpha) * x, then *out = dot(y, z) (z == nullptr: dot(y, y),
 // optionally square-rooted) -- one pass for a modified Gram-Schmidt step
 // (the reference's axpy followed by the next dot, spectral.hpp:47-51).
-__global__ void k_axpy_dot_tree(const double* __restrict__ alpha, double sign, const double* __restrict__ x,
-                                double* __restrict__ y, const double* __restrict__ z, int64_t n,
-                                double* __restrict__ partials, unsigned int* __restrict__ done,
-                                double* __restrict__ out, bool take_sqrt) {
+__global__ void __launch_bounds__(kDotThreads)
+    k_axpy_dot_tree(const double* __restrict__ alpha, double sign, const double* __restrict__ x,
+                    double* __restrict__ y, const double* __restrict__ z, int64_t n, double* __restrict__ partials,
+                    unsigned int* __restrict__ done, double* __restrict__ out, bool take_sqrt) {
     using BR = cub::BlockReduce<double, kDotThreads>;
     __shared__ typename BR::TempStorage tmp;
-    __shared__ bool last;
     const double a = sign * (*alpha);
     double s = 0.0;
     const int64_t stride = static_cast<int64_t>(gridDim.x) * kDotThreads;
-    for (int64_t i = static_cast<int64_t>(blockIdx.x) * kDotThreads + threadIdx.x; i < n; i += stride) {
+    int64_t i = static_cast<int64_t>(blockIdx.x) * kDotThreads + threadIdx.x;
+    for (; i + (kUnroll - 1) * stride < n; i += kUnroll * stride) {
+        double yv[kUnroll], xv[kUnroll], zv[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            yv[u] = y[i + u * stride];
+            xv[u] = __ldg(&x[i + u * stride]);
+            zv[u] = z ? __ldg(&z[i + u * stride]) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            const double yi = yv[u] + a * xv[u];
+            y[i + u * stride] = yi;
+            s += yi * (z ? zv[u] : yi);
+        }
+    }
+    for (; i < n; i += stride) {
         const double yi = y[i] + a * x[i];
         y[i] = yi;
         s += yi * (z ? z[i] : yi);
     }
     const double b = BR(tmp).Sum(s);
-    if (threadIdx.x == 0) {
-        partials[blockIdx.x] = b;
-        __threadfence();
-        const unsigned prev = atomicAdd(done, 1u);
-        last = (prev == gridDim.x - 1);
-    }
-    __syncthreads();
-    if (last && threadIdx.x == 0) {
-        __threadfence();
-        double t = 0.0;
-        for (unsigned k = 0; k < gridDim.x; ++k) t += __ldcg(&partials[k]);
-        *out = take_sqrt ? sqrt(t) : t;
-        *done = 0u;
-    }
+    finish_tree(b, partials, done, out, take_sqrt);
 }
 
 __global__ void k_dot_seq(const double* __restrict__ x, const double* __restrict__ y, int64_t n, double* __restrict__ out,
@@ -117,18 +143,22 @@ unsigned stream_grid(Ctx& c, int64_t n) {
     return std::max(1u, std::min<unsigned>(blocks_for(n, 256), 8u * c.sms));
 }
 
+}  // namespace
+
+unsigned dot_grid(Ctx& c, int64_t n) {
+    return std::max(1u, std::min<unsigned>(blocks_for(n, kDotThreads * kUnroll), 8u * c.sms));
+}
+
+namespace {
+
 void dot_impl(Ctx& c, const double* x, const double* y, int64_t n, double* out, bool take_sqrt) {
     if (c.seq) {
-        launch(c, k_dot_seq, 1, 32, 0, x, y, n, out, take_sqrt);
+        launch_prof(c, c.blas_family, 16.0 * n, k_dot_seq, 1, 32, 0, x, y, n, out, take_sqrt);
         return;
     }
-    const unsigned g = std::max(1u, std::min<unsigned>(blocks_for(n, kDotThreads * 4), 2u * c.sms));
-    if (c.partials.size() < 4096) {
-        c.partials.alloc(4096, c.s);
-        c.tickets.alloc(64, c.s);
-        AMG_CK(cudaMemsetAsync(c.tickets.get(), 0, sizeof(unsigned int) * 64, c.s));
-    }
-    launch(c, k_dot_tree, g, kDotThreads, 0, x, y, n, c.partials.get(), c.tickets.get(), out, take_sqrt);
+    const unsigned g = dot_grid(c, n);
+    ensure_reduction_scratch(c, g);
+    launch_prof(c, c.blas_family, 16.0 * n, k_dot_tree, g, kDotThreads, 0, x, y, n, c.partials.get(), c.tickets.get(), out, take_sqrt);
 }
 
 }  // namespace
@@ -140,13 +170,9 @@ void axpy_dot(Ctx& c, const double* alpha, double sign, const double* x, double*
         dot_impl(c, y, z ? z : y, n, out, take_sqrt);
         return;
     }
-    const unsigned g = std::max(1u, std::min<unsigned>(blocks_for(n, kDotThreads * 4), 2u * c.sms));
-    if (c.partials.size() < 4096) {
-        c.partials.alloc(4096, c.s);
-        c.tickets.alloc(64, c.s);
-        AMG_CK(cudaMemsetAsync(c.tickets.get(), 0, sizeof(unsigned int) * 64, c.s));
-    }
-    launch(c, k_axpy_dot_tree, g, kDotThreads, 0, alpha, sign, x, y, z, n, c.partials.get(), c.tickets.get(), out,
+    const unsigned g = dot_grid(c, n);
+    ensure_reduction_scratch(c, g);
+    launch_prof(c, c.blas_family, (z ? 32.0 : 24.0) * n, k_axpy_dot_tree, g, kDotThreads, 0, alpha, sign, x, y, z, n, c.partials.get(), c.tickets.get(), out,
            take_sqrt);
 }
 
@@ -154,13 +180,13 @@ void dot(Ctx& c, const double* x, const double* y, int64_t n, double* out) { dot
 void nrm2(Ctx& c, const double* x, int64_t n, double* out) { dot_impl(c, x, x, n, out, true); }
 
 void axpy_dev(Ctx& c, const double* alpha, double sign, const double* x, double* y, int64_t n) {
-    launch(c, k_axpy_dev, stream_grid(c, n), 256, 0, alpha, sign, x, y, n);
+    launch_prof(c, c.blas_family, 24.0 * n, k_axpy_dev, stream_grid(c, n), 256, 0, alpha, sign, x, y, n);
 }
 void scale_recip_dev(Ctx& c, const double* denom, double* x, int64_t n) {
-    launch(c, k_scale_recip, stream_grid(c, n), 256, 0, denom, x, n);
+    launch_prof(c, c.blas_family, 16.0 * n, k_scale_recip, stream_grid(c, n), 256, 0, denom, x, n);
 }
 void scale_const(Ctx& c, double alpha, double* x, int64_t n) {
-    launch(c, k_scale_const, stream_grid(c, n), 256, 0, alpha, x, n);
+    launch_prof(c, c.blas_family, 16.0 * n, k_scale_const, stream_grid(c, n), 256, 0, alpha, x, n);
 }
 
 }  // namespace amgcu

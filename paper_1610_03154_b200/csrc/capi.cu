@@ -220,7 +220,9 @@ const char* amgcu_profile_family_name(int32_t family) {
     static const char* names[kProfFamilies] = {"vcycle_relax0_residual", "vcycle_restrict", "vcycle_prolong",
                                                "vcycle_post_relax",      "krylov_spmv",     "emin_masked_product",
                                                "spgemm",                 "evolution_soc",   "gauss_seidel_wavefront",
-                                               "aggregate_lfmis",        "coarse_solve"};
+                                               "aggregate_lfmis",        "coarse_solve",    "blas1",
+                                               "spectral_spmv",          "emin_cg",         "other",
+                                               "arnoldi_blas1",          "emin_blas1"};
     return (family >= 0 && family < kProfFamilies) ? names[family] : "";
 }
 

@@ -471,7 +471,7 @@ SolveResult solve(DHier& h, const double* b, double* x, const amgcu_solve_option
             d.ops += static_cast<double>(L0.A.nnz);
             dot(c, p.get(), q.get(), n, S + 1);
             launch(c, k_pcg_alpha, 1, 1, 0, S, bad.get());
-            launch(c, k_pcg_update, stream_grid(c, n), 256, 0, static_cast<int64_t>(n), static_cast<const double*>(S),
+            launch_prof(c, kProfBlas1, 48.0 * n, k_pcg_update, stream_grid(c, n), 256, 0, static_cast<int64_t>(n), static_cast<const double*>(S),
                    static_cast<const int32_t*>(bad.get()), static_cast<const double*>(p.get()),
                    static_cast<const double*>(q.get()), x, r.get());
             nrm2(c, r.get(), n, S + 5);
@@ -500,7 +500,7 @@ SolveResult solve(DHier& h, const double* b, double* x, const amgcu_solve_option
             d.precond(r.get(), z.get(), o.cycle);
             dot(c, r.get(), z.get(), n, S + 3);
             launch(c, k_pcg_beta, 1, 1, 0, S);
-            launch(c, k_pcg_dir, stream_grid(c, n), 256, 0, static_cast<int64_t>(n), static_cast<const double*>(S),
+            launch_prof(c, kProfBlas1, 24.0 * n, k_pcg_dir, stream_grid(c, n), 256, 0, static_cast<int64_t>(n), static_cast<const double*>(S),
                    static_cast<const double*>(z.get()), p.get());
         }
         return finish();
@@ -567,7 +567,7 @@ SolveResult solve(DHier& h, const double* b, double* x, const amgcu_solve_option
         y[t] = Hij(t, t) != 0.0 ? s / Hij(t, t) : 0.0;
     }
     for (int t = 0; t < built; ++t)
-        launch(c, k_axpy_c, stream_grid(c, n), 256, 0, static_cast<int64_t>(n), y[t],
+        launch_prof(c, kProfBlas1, 24.0 * n, k_axpy_c, stream_grid(c, n), 256, 0, static_cast<int64_t>(n), y[t],
                static_cast<const double*>(Z.get() + static_cast<size_t>(t) * n), x);
     sync(c);
     return finish();

@@ -82,6 +82,12 @@ enum ProfFamily : int {
     kProfGaussSeidel,
     kProfAggregate,
     kProfCoarseSolve,
+    kProfBlas1,         // dots, axpys, fused axpy+dot (Krylov, Arnoldi, energy-min CG)
+    kProfSpectralSpmv,  // Arnoldi D^-1 A v
+    kProfEminCg,        // energy-min CG / GMRES control and column kernels
+    kProfOther,         // every launch not tagged with a family
+    kProfArnoldiBlas1,  // BLAS-1 inside the spectral-radius Arnoldi
+    kProfEminBlas1,     // BLAS-1 inside the energy-minimisation solve
     kProfFamilies
 };
 
@@ -102,6 +108,7 @@ struct Ctx {
     int sms = 148;
     bool seq = false;  // sequential (reference-order) global reductions
     int64_t launches = 0;
+    int blas_family = kProfBlas1;  // family the BLAS-1 launchers record under
     std::string err;
     DBuf<double> scal;         // device scalars for reductions/control
     DBuf<double> partials;     // per-block partial sums
@@ -111,6 +118,23 @@ struct Ctx {
     // (spectral.hpp:32-36); prefixes serve every smaller level.
     DBuf<double> arnoldi_v0;
     size_t arnoldi_v0_n = 0;
+};
+
+// block-partial scratch and wavefront tickets of the tree reductions (>= count partials)
+inline void ensure_reduction_scratch(Ctx& c, size_t count) {
+    if (c.partials.size() < count) c.partials.alloc(std::max<size_t>(4096, count), c.s);
+    if (c.tickets.size() < 64) {
+        c.tickets.alloc(64, c.s);
+        AMG_CK(cudaMemsetAsync(c.tickets.get(), 0, sizeof(unsigned int) * 64, c.s));
+    }
+}
+
+// routes the BLAS-1 launchers' profile records to `family` for a scope
+struct BlasFamilyScope {
+    Ctx& c;
+    int prev;
+    BlasFamilyScope(Ctx& ctx, int family) : c(ctx), prev(ctx.blas_family) { c.blas_family = family; }
+    ~BlasFamilyScope() { c.blas_family = prev; }
 };
 
 struct DCsr {
@@ -142,11 +166,21 @@ struct DSell {
 };
 
 template <typename Kern, typename... Args>
-inline void launch(Ctx& c, Kern k, unsigned grid, unsigned block, size_t smem, Args... args) {
+inline void launch_raw(Ctx& c, Kern k, unsigned grid, unsigned block, size_t smem, Args... args) {
     if (grid == 0) return;
     k<<<grid, block, smem, c.s>>>(args...);
     ++c.launches;
     AMG_CK(cudaGetLastError());
+}
+
+template <typename Kern, typename... Args>
+inline void launch_prof(Ctx& c, int family, double bytes, Kern k, unsigned grid, unsigned block, size_t smem,
+                        Args... args);
+
+// untagged launch: timed under kProfOther when profiling is on
+template <typename Kern, typename... Args>
+inline void launch(Ctx& c, Kern k, unsigned grid, unsigned block, size_t smem, Args... args) {
+    launch_prof(c, kProfOther, 0.0, k, grid, block, smem, args...);
 }
 
 inline cudaEvent_t prof_event(Ctx& c) {
@@ -166,12 +200,12 @@ inline void launch_prof(Ctx& c, int family, double bytes, Kern k, unsigned grid,
                         Args... args) {
     if (grid == 0) return;
     if (!c.profile || !((c.prof_mask >> family) & 1u)) {
-        launch(c, k, grid, block, smem, args...);
+        launch_raw(c, k, grid, block, smem, args...);
         return;
     }
     cudaEvent_t e0 = prof_event(c), e1 = prof_event(c);
     AMG_CK(cudaEventRecord(e0, c.s));
-    launch(c, k, grid, block, smem, args...);
+    launch_raw(c, k, grid, block, smem, args...);
     AMG_CK(cudaEventRecord(e1, c.s));
     ProfRecord& r = c.prof[family];
     r.launches += 1;

@@ -927,6 +927,7 @@ void energy_minimize(Ctx& c, const DCsr& A, const DCsr& T, const double* B, cons
                      const DCsr& N, int iters, int krylov, const int32_t* roots, int32_t n_roots, DCsr& Pout,
                      EnergyMinStats* stats) {
     (void)B;
+    BlasFamilyScope scope(c, kProfEminBlas1);
     if (A.nr != A.nc || A.nr != N.nr) throw InvalidArgument("energy_minimize: dimension mismatch");
     if (k > kKMax) throw InvalidArgument("energy_minimize: at most 8 candidates on the GPU path");
     const int32_t n = N.nr, nc = N.nc;
@@ -972,7 +973,7 @@ void energy_minimize(Ctx& c, const DCsr& A, const DCsr& T, const double* B, cons
                static_cast<const unsigned char*>(is_root.get()), APm.get(), static_cast<double*>(nullptr),
                static_cast<const int32_t*>(nullptr));
         launch(c, k_negate, ew, 256, 0, nz, static_cast<const double*>(APm.get()), R.get());
-        launch(c, k_project, blocks_for(n, 128), 128, 0, n, N.rp.get(), N.ci.get(), k, Bc, nc,
+        launch_prof(c, kProfEminCg, 0.0, k_project, blocks_for(n, 128), 128, 0, n, N.rp.get(), N.ci.get(), k, Bc, nc,
                static_cast<const double*>(gp.get()), static_cast<const unsigned char*>(is_root.get()), R.get());
         DBuf<double> scal(8, c.s);
         DBuf<int32_t> flags(4, c.s);
@@ -984,12 +985,12 @@ void energy_minimize(Ctx& c, const DCsr& A, const DCsr& T, const double* B, cons
         double* S = scal.get();
         int32_t* F = flags.get();
         for (int s = 0; s < iters; ++s) {
-            launch(c, k_cg_z, ew, 256, 0, nz, static_cast<const int32_t*>(prow.get()),
+            launch_prof(c, kProfEminCg, 0.0, k_cg_z, ew, 256, 0, nz, static_cast<const int32_t*>(prow.get()),
                    static_cast<const double*>(dinv.get()), static_cast<const double*>(R.get()), Z.get(),
                    static_cast<const int32_t*>(F));
             dot(c, R.get(), Z.get(), nz, S + 7);
-            launch(c, k_cg_ctl_newsum, 1, 1, 0, S, F);
-            launch(c, k_cg_dir, ew, 256, 0, nz, static_cast<const double*>(Z.get()), D.get(),
+            launch_prof(c, kProfEminCg, 0.0, k_cg_ctl_newsum, 1, 1, 0, S, F);
+            launch_prof(c, kProfEminCg, 0.0, k_cg_dir, ew, 256, 0, nz, static_cast<const double*>(Z.get()), D.get(),
                    static_cast<const double*>(S), static_cast<const int32_t*>(F));
             launch_prof(c, kProfMaskedProduct, mp_bytes(A, 2), k_masked_rows, mp_grid, mp_block, 0, n, A.rp.get(),
                    A.ci.get(), A.va.get(), N.rp.get(),
@@ -997,13 +998,13 @@ void energy_minimize(Ctx& c, const DCsr& A, const DCsr& T, const double* B, cons
                    static_cast<const unsigned char*>(is_root.get()), ADm.get(), ADp.get(),
                    static_cast<const int32_t*>(F));
             dot(c, D.get(), ADm.get(), nz, S + 7);
-            launch(c, k_cg_ctl_denom, 1, 1, 0, S, F, abits.get());
-            launch(c, k_cg_columns, blocks_for(nc, 128), 128, 0, nc, static_cast<const int32_t*>(colptr.get()),
+            launch_prof(c, kProfEminCg, 0.0, k_cg_ctl_denom, 1, 1, 0, S, F, abits.get());
+            launch_prof(c, kProfEminCg, 0.0, k_cg_columns, blocks_for(nc, 128), 128, 0, nc, static_cast<const int32_t*>(colptr.get()),
                    static_cast<const int32_t*>(pos.get()), static_cast<const double*>(P.get()),
                    static_cast<const double*>(APm.get()), static_cast<const double*>(D.get()),
                    static_cast<const double*>(ADm.get()), abits.get(), static_cast<const int32_t*>(F));
-            launch(c, k_cg_ctl_alpha, 1, 1, 0, S, F, static_cast<const unsigned long long*>(abits.get()), s);
-            launch(c, k_cg_update, ew, 256, 0, nz, P.get(), APm.get(), R.get(), static_cast<const double*>(D.get()),
+            launch_prof(c, kProfEminCg, 0.0, k_cg_ctl_alpha, 1, 1, 0, S, F, static_cast<const unsigned long long*>(abits.get()), s);
+            launch_prof(c, kProfEminCg, 0.0, k_cg_update, ew, 256, 0, nz, P.get(), APm.get(), R.get(), static_cast<const double*>(D.get()),
                    static_cast<const double*>(ADm.get()), static_cast<const double*>(ADp.get()),
                    static_cast<const double*>(S), static_cast<const int32_t*>(F), s);
         }
@@ -1026,7 +1027,7 @@ void energy_minimize(Ctx& c, const DCsr& A, const DCsr& T, const double* B, cons
            static_cast<const unsigned char*>(is_root.get()), R0.get(), static_cast<double*>(nullptr),
            static_cast<const int32_t*>(nullptr));
     launch(c, k_negate, ew, 256, 0, nz, static_cast<const double*>(R0.get()), R0.get());
-    launch(c, k_project, blocks_for(n, 128), 128, 0, n, N.rp.get(), N.ci.get(), k, Bc, nc,
+    launch_prof(c, kProfEminCg, 0.0, k_project, blocks_for(n, 128), 128, 0, n, N.rp.get(), N.ci.get(), k, Bc, nc,
            static_cast<const double*>(gp.get()), static_cast<const unsigned char*>(is_root.get()), R0.get());
     DBuf<double> scal(2, c.s);
     nrm2(c, R0.get(), nz, scal.get());
@@ -1090,7 +1091,7 @@ void energy_minimize(Ctx& c, const DCsr& A, const DCsr& T, const double* B, cons
     // V holds built+1 vectors only up to the last normalised one (V[s+1] is filled
     // in place while building); the reference combines V[0..built-1]
     for (int t = 0; t < built; ++t)
-        launch(c, k_axpy_host, ew, 256, 0, nz, y[t], static_cast<const double*>(V.get() + static_cast<size_t>(t) * nz),
+        launch_prof(c, kProfEminCg, 0.0, k_axpy_host, ew, 256, 0, nz, y[t], static_cast<const double*>(V.get() + static_cast<size_t>(t) * nz),
                U.get());
     DCsr Tc, Uc, AT, AU;
     compact_pattern(c, N, P.get(), T.bs, Tc);
@@ -1101,7 +1102,7 @@ void energy_minimize(Ctx& c, const DCsr& A, const DCsr& T, const double* B, cons
     transpose_positions(c, AT, tcp, tpos, nullptr);
     transpose_positions(c, AU, ucp, upos, &urow);
     DBuf<double> e(static_cast<size_t>(nc), c.s), g(static_cast<size_t>(nc), c.s), h(static_cast<size_t>(nc), c.s);
-    launch(c, k_gm_columns, blocks_for(nc, 128), 128, 0, nc, static_cast<const int32_t*>(tcp.get()),
+    launch_prof(c, kProfEminCg, 0.0, k_gm_columns, blocks_for(nc, 128), 128, 0, nc, static_cast<const int32_t*>(tcp.get()),
            static_cast<const int32_t*>(tpos.get()), AT.va.get(), static_cast<const int32_t*>(ucp.get()),
            static_cast<const int32_t*>(upos.get()), static_cast<const int32_t*>(urow.get()), AU.va.get(), AT.rp.get(),
            AT.ci.get(), e.get(), g.get(), h.get());
@@ -1125,7 +1126,7 @@ void energy_minimize(Ctx& c, const DCsr& A, const DCsr& T, const double* B, cons
         Pout = std::move(Tc);
         return;
     }
-    launch(c, k_axpy_host, ew, 256, 0, nz, tau, static_cast<const double*>(U.get()), P.get());
+    launch_prof(c, kProfEminCg, 0.0, k_axpy_host, ew, 256, 0, nz, tau, static_cast<const double*>(U.get()), P.get());
     compact_pattern(c, N, P.get(), T.bs, Pout);
 }
 

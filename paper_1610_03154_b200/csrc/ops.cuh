@@ -49,6 +49,8 @@ void scale_recip_dev(Ctx& c, const double* denom, double* x, int64_t n);
 void axpy_dot(Ctx& c, const double* alpha, double sign, const double* x, double* y, const double* z, int64_t n,
               double* out, bool take_sqrt);
 void scale_const(Ctx& c, double alpha, double* x, int64_t n);
+// grid of the tree reductions for length n (the cooperative Arnoldi reproduces it)
+unsigned dot_grid(Ctx& c, int64_t n);
 
 // ---- strength / aggregation (strength.cu, aggregate.cu) --------------------------------
 void symmetric_strength(Ctx& c, const DCsr& A, double theta, DCsr& S);

@@ -90,6 +90,17 @@ def test_spectral_radius(gpu_seq, gpu, port):
         assert abs(api.spectral_radius_estimate(A, ctx=gpu) - want) <= 1e-12 * want
 
 
+def test_spectral_radius_cooperative_matches_steps(gpu, monkeypatch):
+    """The one-launch cooperative Arnoldi reproduces the launch-per-step path bit for bit
+    (same reduction trees), at sizes that use one and several virtual blocks per block."""
+    for A in (poisson1d(5), aniso2d(30, 0.1), aniso2d(150, 1.0), aniso2d(800, 0.01)):
+        coop = api.spectral_radius_estimate(A, ctx=gpu)
+        monkeypatch.setenv("AMGCU_ARNOLDI_STEPS", "1")
+        steps = api.spectral_radius_estimate(A, ctx=gpu)
+        monkeypatch.delenv("AMGCU_ARNOLDI_STEPS")
+        assert coop == steps, (A.n_rows, coop, steps)
+
+
 @pytest.mark.parametrize("measure,tol", [(StrengthMeasure.symmetric, 0.25), (StrengthMeasure.symmetric, 0.0),
                                          (StrengthMeasure.classical, 0.25), (StrengthMeasure.evolution, 4.0)])
 def test_strength(gpu_seq, port, measure, tol):
