@@ -46,7 +46,6 @@ constexpr int kMaxK = 8;
 // with a smaller ticket, which is already running: the launch cannot deadlock.
 constexpr int kSegMaxE = 32;  // entries per row handled from the prefetch records
 constexpr int kChunk = 8;     // prefetcher: entries loaded per batch
-constexpr int kRegTerms = 16; // solver: terms held in registers
 constexpr unsigned long long kPending = 0x7FF4A11CE5EEDULL;
 
 __device__ __forceinline__ unsigned long long load_relaxed_bits(const double* p) {
@@ -381,74 +380,66 @@ __global__ void __launch_bounds__(3 * gs_segs_per_cta<K>() * 32)
         while (vload(&sh_ready[wl][seq & 1]) != seq) __nanosleep(32);
         __threadfence_block();
         GsBuf<K>& B = buf[seq & 1];
-        const int32_t q = qb + lane;
-        const int32_t i = q < q1 ? (bwd ? n - 1 - q : q) : 0;
-        double acc[K];
-#pragma unroll
-        for (int c = 0; c < K; ++c) acc[c] = B.acc0[c][lane];
-        const double dinv_i = B.dinv[lane];
-        const int32_t nt = B.nterm[lane];
-        // the first kRegTerms terms live in registers for the step (the rest: shared memory)
-        double rta[kRegTerms];
-        int32_t rtoff[kRegTerms];
-#pragma unroll
-        for (int k = 0; k < kRegTerms; ++k) {
-            rta[k] = B.ta[k][lane];
-            rtoff[k] = B.toff[k][lane];
-        }
         if (tr && lane == 0) tr[1] = globaltimer_ns();
+        // ---- phase B, warp-uniform: every lane evaluates row t from broadcast reads of
+        // its records (no divergence, no reconvergence barriers); lane 0 publishes ----
         const int32_t cnt = min(32, q1 - qb);
         for (int32_t t = 0; t < cnt; ++t) {
-            if (lane == t) {
-                if (nt >= 0) {
+            const int32_t q = qb + t;
+            const int32_t i = bwd ? n - 1 - q : q;
+            const int32_t nt = B.nterm[t];
+            double acc[K];
+            if (nt >= 0) {
 #pragma unroll
-                    for (int k = 0; k < kSegMaxE; ++k) {
-                        if (k < nt) {
-                            const double ak = k < kRegTerms ? rta[k] : B.ta[k][lane];
-                            const unsigned char* sp = segmem + (k < kRegTerms ? rtoff[k] : B.toff[k][lane]);
+                for (int c = 0; c < K; ++c) acc[c] = B.acc0[c][t];
+#pragma unroll 4
+                for (int32_t k = 0; k < nt; ++k) {
+                    const double ak = B.ta[k][t];
+                    const unsigned char* sp = segmem + B.toff[k][t];
 #pragma unroll
-                            for (int c = 0; c < K; ++c) {
-                                const unsigned long long* slot = reinterpret_cast<const unsigned long long*>(sp) + 32 * c;
-                                unsigned long long v = vload(slot);
-                                while (v == kPending) v = vload(slot);
-                                acc[c] -= ak * __longlong_as_double(static_cast<long long>(v));
-                            }
-                        }
-                    }
-                } else {
-                    // slow path: the whole row in CSR order, values from xb or global memory
-#pragma unroll
-                    for (int c = 0; c < K; ++c) acc[c] = b ? b[static_cast<size_t>(c) * n + i] : 0.0;
-                    const int32_t lo = rp[i], hi = rp[i + 1];
-                    for (int32_t p = lo; p < hi; ++p) {
-                        const int32_t j = ci[p];
-                        if (j == i) continue;
-                        const int32_t qj = bwd ? n - 1 - j : j;
-                        const bool fresh = qj < q;
-                        const double av = va[p];
-                        if (fresh && qj >= qb) {
-#pragma unroll
-                            for (int c = 0; c < K; ++c)
-                                acc[c] -= av * __longlong_as_double(static_cast<long long>(
-                                                   xb[((seq & 1) * K + c) * 32 + (qj - qb)]));
-                            continue;
-                        }
-                        const double* src = fresh ? xout : xin;
-                        const bool own = fresh && qj >= q0;  // earlier blocks of the own segment: published
-#pragma unroll
-                        for (int c = 0; c < K; ++c) {
-                            const double* addr = &src[static_cast<size_t>(c) * n + j];
-                            const unsigned long long bb =
-                                (own || (!fresh && s == 0))
-                                    ? static_cast<unsigned long long>(__double_as_longlong(__ldcg(addr)))
-                                    : load_relaxed_bits(addr);
-                            acc[c] -= av * wait_bits(addr, bb, max_ns);
-                        }
+                    for (int c = 0; c < K; ++c) {
+                        const unsigned long long* slot = reinterpret_cast<const unsigned long long*>(sp) + 32 * c;
+                        unsigned long long v = vload(slot);
+                        while (v == kPending) v = vload(slot);
+                        acc[c] -= ak * __longlong_as_double(static_cast<long long>(v));
                     }
                 }
+            } else {
+                // slow path: the whole row in CSR order, values from xb or global memory
+#pragma unroll
+                for (int c = 0; c < K; ++c) acc[c] = b ? b[static_cast<size_t>(c) * n + i] : 0.0;
+                const int32_t lo = rp[i], hi = rp[i + 1];
+                for (int32_t p = lo; p < hi; ++p) {
+                    const int32_t j = ci[p];
+                    if (j == i) continue;
+                    const int32_t qj = bwd ? n - 1 - j : j;
+                    const bool fresh = qj < q;
+                    const double av = va[p];
+                    if (fresh && qj >= qb) {
+#pragma unroll
+                        for (int c = 0; c < K; ++c)
+                            acc[c] -= av * __longlong_as_double(static_cast<long long>(
+                                               vload(&xb[((seq & 1) * K + c) * 32 + (qj - qb)])));
+                        continue;
+                    }
+                    const double* src = fresh ? xout : xin;
+                    const bool own = fresh && qj >= q0;  // earlier blocks of the own segment: published
+#pragma unroll
+                    for (int c = 0; c < K; ++c) {
+                        const double* addr = &src[static_cast<size_t>(c) * n + j];
+                        const unsigned long long bb =
+                            (own || (!fresh && s == 0))
+                                ? static_cast<unsigned long long>(__double_as_longlong(__ldcg(addr)))
+                                : load_relaxed_bits(addr);
+                        acc[c] -= av * wait_bits(addr, bb, max_ns);
+                    }
+                }
+            }
+            const double dinv_t = B.dinv[t];
+            if (lane == 0) {
 #pragma unroll
                 for (int c = 0; c < K; ++c) {
-                    const double xi = acc[c] * dinv_i;
+                    const double xi = acc[c] * dinv_t;
                     const unsigned long long xbits = static_cast<unsigned long long>(__double_as_longlong(xi));
                     vstore(&xb[((seq & 1) * K + c) * 32 + t], xbits);
                     cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> out(

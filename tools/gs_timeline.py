@@ -16,6 +16,7 @@ ap.add_argument("--size", type=int, default=1024)
 ap.add_argument("--sweeps", type=int, default=4)
 ap.add_argument("--out", default="gpurun_out/gs_trace.bin")
 ap.add_argument("--level", type=int, default=0, help="relax the hierarchy's level-L matrix (setup first)")
+ap.add_argument("--p1d", type=int, default=0, help="relax a 1D Poisson chain of this length instead")
 a = ap.parse_args()
 if os.path.exists(a.out):
     os.remove(a.out)
@@ -24,6 +25,10 @@ import paper_1610_03154_b200.api as api  # noqa: E402
 
 A, B, Bh, b = api.generate_config(a.config, a.size)
 ctx = api.Context(0)
+if a.p1d:
+    from tests.helpers import poisson1d
+    A = poisson1d(a.p1d)
+    B = api.CandidateSet(A.n_rows, 1, np.ones(A.n_rows))
 if a.level > 0:
     os.environ.pop("AMGCU_GS_TRACE")
     so, _ = api.config_options(a.config)
@@ -78,5 +83,12 @@ for s in range(nsw):
         g = nf // 2
         q0, q1 = segs[g], segs[g + 1]
         rows = tr[s, q0:q1:32] - t0
+    if s == 0:
+        g = nf // 2
+        q0, q1 = segs[g], segs[g + 1]
+        rows = tr[s, q0:q1:32] - t0
+        wa = (rows[:, 1] - rows[:, 0]) / 1e3
+        pb = (rows[:, 2] - rows[:, 1]) / 1e3
+        print(f"  segment {g}: {len(rows)} blocks; wait-for-records med {np.median(wa):.2f} us, serial phase med {np.median(pb):.2f} us")
         print("  mid segment blocks (A start, A dur, B dur) us:",
               [(round(r[0] / 1e3, 1), round((r[1] - r[0]) / 1e3, 2), round((r[2] - r[1]) / 1e3, 2)) for r in rows[:8]])
