@@ -22,6 +22,7 @@ namespace amgcu {
 namespace {
 
 constexpr int kSlice = 32;
+constexpr int kWarpRowThreshold = 32;  // average row length from which warp-per-row kernels are used
 
 __global__ void k_slice_len(int32_t nr, const int32_t* __restrict__ rp, int64_t* __restrict__ slen) {
     const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
@@ -64,7 +65,7 @@ __global__ void k_sell_fill(int32_t nr, const int32_t* __restrict__ rp, const in
 // thread keeps kBatch column/value loads and then kBatch gathers in flight;
 // padding (column -1, always after the row's entries) is skipped by predicate,
 // so the sum is the reference's sequential one.
-constexpr int kBatch = 8;
+constexpr int kBatch = 16;
 
 template <typename Gather>
 __device__ __forceinline__ double sell_row_sum(int64_t base, int32_t w, const int32_t* __restrict__ sci,
@@ -106,9 +107,87 @@ struct SellView {
     const int32_t* slen;
     const int32_t* ci;
     const double* va;
+    const int32_t* crp;  // CSR of the same operator (warp-per-row kernels)
+    const int32_t* cci;
+    const double* cva;
 };
 
-SellView view(const DSell& s) { return {s.nr, s.slice_ptr.get(), s.slice_len.get(), s.ci.get(), s.va.get()}; }
+SellView view(const DSell& s) {
+    return {s.nr, s.slice_ptr.get(), s.slice_len.get(), s.ci.get(), s.va.get(), s.crp, s.cci, s.cva};
+}
+
+// Warp per row for operators with long rows (coarse levels, restriction): the
+// lanes form the row's products a_p * x_{c_p} in parallel into shared memory and
+// lane 0 sums them in CSR order -- the reference's sequential sum, with the
+// loads of a long row in flight together instead of one thread walking it.
+constexpr int kWarpRowsPerBlock = 8;
+constexpr int kWarpCap = 256;  // products staged per pass
+
+template <typename Gather>
+__device__ __forceinline__ double warp_row_sum(const SellView& A, int32_t i, Gather gx, double* buf, int lane) {
+    double acc = 0.0;
+    const int32_t lo = A.crp[i], hi = A.crp[i + 1];
+    for (int32_t base = lo; base < hi; base += kWarpCap) {
+        const int32_t len = min(kWarpCap, hi - base);
+        for (int32_t e = lane; e < len; e += 32) buf[e] = __ldg(&A.cva[base + e]) * gx(__ldg(&A.cci[base + e]));
+        __syncwarp();
+        if (lane == 0) {
+#pragma unroll 8
+            for (int32_t e = 0; e < len; ++e) acc += buf[e];
+        }
+        __syncwarp();
+    }
+    return acc;  // lane 0
+}
+
+#define AMGCU_WARP_ROW_PROLOGUE                                                  \
+    __shared__ double wbuf[kWarpRowsPerBlock][kWarpCap];                          \
+    const int lane = threadIdx.x & 31, wrow = threadIdx.x / 32;                   \
+    const int32_t i = blockIdx.x * kWarpRowsPerBlock + wrow;                      \
+    if (i >= A.nr) return;                                                        \
+    double* buf = wbuf[wrow];
+
+__global__ void __launch_bounds__(kWarpRowsPerBlock * 32)
+    k_wspmv(SellView A, const double* __restrict__ x, double* __restrict__ y) {
+    AMGCU_WARP_ROW_PROLOGUE
+    const double s = warp_row_sum(A, i, [&](int32_t j) { return __ldg(&x[j]); }, buf, lane);
+    if (lane == 0) y[i] = s;
+}
+
+__global__ void __launch_bounds__(kWarpRowsPerBlock * 32)
+    k_wresidual(SellView A, const double* __restrict__ x, const double* __restrict__ b, double* __restrict__ r) {
+    AMGCU_WARP_ROW_PROLOGUE
+    const double s = warp_row_sum(A, i, [&](int32_t j) { return __ldg(&x[j]); }, buf, lane);
+    if (lane == 0) r[i] = b[i] - s;
+}
+
+__global__ void __launch_bounds__(kWarpRowsPerBlock * 32)
+    k_wrelax0_residual(SellView A, const double* __restrict__ wd, const double* __restrict__ b,
+                       double* __restrict__ x, double* __restrict__ r) {
+    AMGCU_WARP_ROW_PROLOGUE
+    const double s =
+        warp_row_sum(A, i, [&](int32_t j) { return 0.0 + __ldg(&wd[j]) * __ldg(&b[j]); }, buf, lane);
+    if (lane == 0) {
+        x[i] = 0.0 + wd[i] * b[i];
+        r[i] = b[i] - s;
+    }
+}
+
+__global__ void __launch_bounds__(kWarpRowsPerBlock * 32)
+    k_wjacobi(SellView A, const double* __restrict__ wd, const double* __restrict__ b,
+              const double* __restrict__ xin, double* __restrict__ xout) {
+    AMGCU_WARP_ROW_PROLOGUE
+    const double s = warp_row_sum(A, i, [&](int32_t j) { return __ldg(&xin[j]); }, buf, lane);
+    if (lane == 0) xout[i] = xin[i] + wd[i] * (b[i] - s);
+}
+
+__global__ void __launch_bounds__(kWarpRowsPerBlock * 32)
+    k_wprolong(SellView A, const double* __restrict__ xc, const double* __restrict__ x, double* __restrict__ t) {
+    AMGCU_WARP_ROW_PROLOGUE
+    const double s = warp_row_sum(A, i, [&](int32_t j) { return __ldg(&xc[j]); }, buf, lane);
+    if (lane == 0) t[i] = x[i] + s;
+}
+#undef AMGCU_WARP_ROW_PROLOGUE
 
 __global__ void k_sell_spmv(SellView A, const double* __restrict__ x, double* __restrict__ y) {
     const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -241,9 +320,15 @@ void build_sell(Ctx& c, const DCsr& A, DSell& S) {
     launch(c, k_sell_fill, blocks_for(static_cast<int64_t>(S.nslices) * kSlice, 256), 256, 0, A.nr, A.rp.get(),
            A.ci.get(), A.va.get(), static_cast<const int64_t*>(S.slice_ptr.get()), S.ci.get(), S.va.get(),
            S.slice_len.get());
+    // long rows on average: the warp-per-row kernels over the CSR
+    S.crp = A.rp.get();
+    S.cci = A.ci.get();
+    S.cva = A.va.get();
+    S.warp_rows = A.nr > 0 && A.nnz >= kWarpRowThreshold * static_cast<int64_t>(A.nr);
 }
 
 unsigned rows_grid(int32_t n) { return blocks_for(n, 128); }
+unsigned warp_rows_grid(int32_t n) { return blocks_for(n, kWarpRowsPerBlock); }
 unsigned stream_grid(Ctx& c, int64_t n) { return std::max(1u, std::min<unsigned>(blocks_for(n, 256), 8u * c.sms)); }
 
 double relax_cost(int scheme, double nnz) { return scheme == 3 ? 2.0 * nnz : nnz; }
@@ -252,6 +337,25 @@ struct Driver {
     DHier& h;
     Ctx& c;
     double ops = 0.0;  // multiply-model count (cycle.hpp cost model)
+
+    // xout = xin + wd (b - A xin); family < 0: untagged
+    void jacobi_sweep(const DSell& S, int family, double bytes, const double* wd, const double* b, const double* xin,
+                      double* xout) {
+        const int fam = family < 0 ? static_cast<int>(kProfOther) : family;
+        if (S.warp_rows)
+            launch_prof(c, fam, bytes, k_wjacobi, warp_rows_grid(S.nr), kWarpRowsPerBlock * 32, 0, view(S), wd, b,
+                        xin, xout);
+        else
+            launch_prof(c, fam, bytes, k_jacobi_sweep, rows_grid(S.nr), 128, 0, view(S), wd, b, xin, xout);
+    }
+
+    // y = S x under a profile family
+    void spmv_fam(const DSell& S, int family, double bytes, const double* x, double* y) {
+        if (S.warp_rows)
+            launch_prof(c, family, bytes, k_wspmv, warp_rows_grid(S.nr), kWarpRowsPerBlock * 32, 0, view(S), x, y);
+        else
+            launch_prof(c, family, bytes, k_sell_spmv, rows_grid(S.nr), 128, 0, view(S), x, y);
+    }
 
     // one cycle at `l`; x_zero: x is known to be all zeros on entry
     void apply(size_t l, double* x, const double* b, int kind, bool x_zero) {
@@ -278,16 +382,21 @@ struct Driver {
             for (int s = 0; s < sweeps; ++s) {
                 if (s == 0 && x_zero) {
                     if (sweeps == 1) {
-                        launch_prof(c, kProfVcycleRelax0Residual, 12.0 * nnz + 4.0 * (n + 1) + 32.0 * n,
-                                    k_relax0_residual, rows_grid(n), 128, 0, A,
-                                    static_cast<const double*>(lev.wd_pre.get()), b, x, lev.r.get());
+                        if (lev.sA.warp_rows)
+                            launch_prof(c, kProfVcycleRelax0Residual, 12.0 * nnz + 4.0 * (n + 1) + 32.0 * n,
+                                        k_wrelax0_residual, warp_rows_grid(n), kWarpRowsPerBlock * 32, 0, A,
+                                        static_cast<const double*>(lev.wd_pre.get()), b, x, lev.r.get());
+                        else
+                            launch_prof(c, kProfVcycleRelax0Residual, 12.0 * nnz + 4.0 * (n + 1) + 32.0 * n,
+                                        k_relax0_residual, rows_grid(n), 128, 0, A,
+                                        static_cast<const double*>(lev.wd_pre.get()), b, x, lev.r.get());
                         residual_done = true;
                     } else {
                         launch(c, k_relax0, rows_grid(n), 128, 0, n, static_cast<const double*>(lev.wd_pre.get()), b, x);
                     }
                 } else {
-                    launch(c, k_jacobi_sweep, rows_grid(n), 128, 0, A, static_cast<const double*>(lev.wd_pre.get()), b,
-                           static_cast<const double*>(x), lev.t.get());
+                    jacobi_sweep(lev.sA, -1, 0.0, static_cast<const double*>(lev.wd_pre.get()), b,
+                                 static_cast<const double*>(x), lev.t.get());
                     copy_d2d(c, x, lev.t.get(), n);
                 }
                 ops += relax_cost(pre, nnz);
@@ -302,21 +411,31 @@ struct Driver {
         }
         if (!residual_done) {
             if (pre == 0 && sweeps == 0 && x_zero) AMG_CK(cudaMemsetAsync(x, 0, sizeof(double) * n, c.s));
-            launch(c, k_sell_residual, rows_grid(n), 128, 0, A, static_cast<const double*>(x), b, lev.r.get());
+            if (lev.sA.warp_rows)
+                launch(c, k_wresidual, warp_rows_grid(n), kWarpRowsPerBlock * 32, 0, A, static_cast<const double*>(x), b,
+                       lev.r.get());
+            else
+                launch(c, k_sell_residual, rows_grid(n), 128, 0, A, static_cast<const double*>(x), b, lev.r.get());
         }
         ops += nnz;
         // restriction
         DLevel& nxt = h.lv[l + 1];
-        launch_prof(c, kProfVcycleRestrict,
-                    12.0 * lev.R.nnz + 4.0 * (lev.R.nr + 1) + 8.0 * n + 8.0 * lev.R.nr, k_sell_spmv,
-                    rows_grid(lev.sR.nr), 128, 0, view(lev.sR), static_cast<const double*>(lev.r.get()), nxt.b.get());
+        spmv_fam(lev.sR, kProfVcycleRestrict, 12.0 * lev.R.nnz + 4.0 * (lev.R.nr + 1) + 8.0 * n + 8.0 * lev.R.nr,
+                 static_cast<const double*>(lev.r.get()), nxt.b.get());
         ops += static_cast<double>(lev.R.nnz);
         apply(l + 1, nxt.x.get(), nxt.b.get(), kind, true);
         if (kind == 1 && l + 1 < L - 1) apply(l + 1, nxt.x.get(), nxt.b.get(), kind, false);
         // interpolate and correct into t, then post-relax back into x
-        launch_prof(c, kProfVcycleProlong, 12.0 * lev.P.nnz + 4.0 * (n + 1) + 8.0 * lev.P.nc + 16.0 * n, k_prolong,
-                    rows_grid(n), 128, 0, view(lev.sP), static_cast<const double*>(nxt.x.get()),
-                    static_cast<const double*>(x), lev.t.get());
+        {
+            const double pb = 12.0 * lev.P.nnz + 4.0 * (n + 1) + 8.0 * lev.P.nc + 16.0 * n;
+            if (lev.sP.warp_rows)
+                launch_prof(c, kProfVcycleProlong, pb, k_wprolong, warp_rows_grid(n), kWarpRowsPerBlock * 32, 0,
+                            view(lev.sP), static_cast<const double*>(nxt.x.get()), static_cast<const double*>(x),
+                            lev.t.get());
+            else
+                launch_prof(c, kProfVcycleProlong, pb, k_prolong, rows_grid(n), 128, 0, view(lev.sP),
+                            static_cast<const double*>(nxt.x.get()), static_cast<const double*>(x), lev.t.get());
+        }
         ops += static_cast<double>(lev.P.nnz);
         const int post = h.o.post_scheme;
         sweeps = h.o.post_sweeps;
@@ -326,13 +445,12 @@ struct Driver {
             } else {
                 for (int s = 0; s < sweeps; ++s) {
                     if (s == 0) {
-                        launch_prof(c, kProfVcyclePostRelax, 12.0 * nnz + 4.0 * (n + 1) + 32.0 * n, k_jacobi_sweep,
-                                    rows_grid(n), 128, 0, A, static_cast<const double*>(lev.wd_post.get()), b,
-                                    static_cast<const double*>(lev.t.get()), x);
+                        jacobi_sweep(lev.sA, kProfVcyclePostRelax, 12.0 * nnz + 4.0 * (n + 1) + 32.0 * n,
+                                     static_cast<const double*>(lev.wd_post.get()), b,
+                                     static_cast<const double*>(lev.t.get()), x);
                     } else {
-                        launch(c, k_jacobi_sweep, rows_grid(n), 128, 0, A,
-                               static_cast<const double*>(lev.wd_post.get()), b, static_cast<const double*>(x),
-                               lev.t.get());
+                        jacobi_sweep(lev.sA, -1, 0.0, static_cast<const double*>(lev.wd_post.get()), b,
+                                     static_cast<const double*>(x), lev.t.get());
                         copy_d2d(c, x, lev.t.get(), n);
                     }
                     ops += relax_cost(post, nnz);
@@ -466,8 +584,8 @@ SolveResult solve(DHier& h, const double* b, double* x, const amgcu_solve_option
         copy_d2d(c, p.get(), z.get(), n);
         dot(c, r.get(), z.get(), n, S + 0);  // rz
         for (int it = 1; it <= o.max_iters; ++it) {
-            launch_prof(c, kProfKrylovSpmv, 12.0 * L0.A.nnz + 4.0 * (n + 1) + 16.0 * n, k_sell_spmv, rows_grid(n), 128,
-                        0, A, static_cast<const double*>(p.get()), q.get());
+            d.spmv_fam(L0.sA, kProfKrylovSpmv, 12.0 * L0.A.nnz + 4.0 * (n + 1) + 16.0 * n,
+                       static_cast<const double*>(p.get()), q.get());
             d.ops += static_cast<double>(L0.A.nnz);
             dot(c, p.get(), q.get(), n, S + 1);
             launch(c, k_pcg_alpha, 1, 1, 0, S, bad.get());
@@ -520,8 +638,8 @@ SolveResult solve(DHier& h, const double* b, double* x, const amgcu_solve_option
         double* zj = Z.get() + static_cast<size_t>(j) * n;
         double* w = V.get() + static_cast<size_t>(j + 1) * n;
         d.precond(V.get() + static_cast<size_t>(j) * n, zj, o.cycle);
-        launch_prof(c, kProfKrylovSpmv, 12.0 * L0.A.nnz + 4.0 * (n + 1) + 16.0 * n, k_sell_spmv, rows_grid(n), 128, 0,
-                    A, static_cast<const double*>(zj), w);
+        d.spmv_fam(L0.sA, kProfKrylovSpmv, 12.0 * L0.A.nnz + 4.0 * (n + 1) + 16.0 * n, static_cast<const double*>(zj),
+                   w);
         d.ops += static_cast<double>(L0.A.nnz);
         // modified Gram-Schmidt (cycle.hpp:228-231); axpy of step t fused with the dot of t + 1
         dot(c, w, V.get(), n, Hcol.get());

@@ -163,6 +163,11 @@ struct DSell {
     DBuf<int32_t> ci;          // -1 marks padding
     DBuf<double> va;
     int64_t stored = 0;
+    // long rows (coarse levels, restriction): the operator's CSR is used by warp-per-row kernels
+    bool warp_rows = false;
+    const int32_t* crp = nullptr;
+    const int32_t* cci = nullptr;
+    const double* cva = nullptr;
 };
 
 template <typename Kern, typename... Args>
