@@ -135,6 +135,8 @@ amgcu_status amgcu_ctx_set_sequential_reductions(amgcu_ctx ctx, int on);
 amgcu_status amgcu_ctx_synchronize(amgcu_ctx ctx);
 /* Kernel launch counter (all kernels this library launched on the context). */
 amgcu_status amgcu_ctx_launch_count(amgcu_ctx ctx, int64_t* launches);
+/* Host synchronisation counter (stream syncs the library performed on the context). */
+amgcu_status amgcu_ctx_sync_count(amgcu_ctx ctx, int64_t* syncs);
 /* Device timer on the context stream: CUDA events recorded at start and stop
  * (the stop call synchronises).  Used by bench.py for device-side timing. */
 amgcu_status amgcu_ctx_timer_start(amgcu_ctx ctx);

@@ -25,7 +25,7 @@ lib = C.CDLL(_LIB_PATH)
 lib.amgcu_last_error.restype = C.c_char_p
 lib.amgcu_last_error.argtypes = [C.c_void_p]
 for _name in ("amgcu_ctx_create", "amgcu_ctx_destroy", "amgcu_ctx_set_sequential_reductions", "amgcu_ctx_synchronize",
-              "amgcu_ctx_launch_count", "amgcu_setup", "amgcu_setup_device", "amgcu_hier_destroy",
+              "amgcu_ctx_launch_count", "amgcu_ctx_sync_count", "amgcu_setup", "amgcu_setup_device", "amgcu_hier_destroy",
               "amgcu_hier_levels", "amgcu_hier_get_matrix", "amgcu_hier_get_candidates", "amgcu_hier_level_symmetric",
               "amgcu_hier_relax_weights", "amgcu_hier_complexity", "amgcu_solve", "amgcu_solve_device", "amgcu_cycle",
               "amgcu_spmv", "amgcu_transpose", "amgcu_matmul", "amgcu_galerkin_product", "amgcu_filter_matrix",
@@ -38,6 +38,7 @@ lib.amgcu_ctx_destroy.argtypes = [C.c_void_p]
 lib.amgcu_ctx_set_sequential_reductions.argtypes = [C.c_void_p, C.c_int]
 lib.amgcu_ctx_synchronize.argtypes = [C.c_void_p]
 lib.amgcu_ctx_launch_count.argtypes = [C.c_void_p, C.POINTER(C.c_int64)]
+lib.amgcu_ctx_sync_count.argtypes = [C.c_void_p, C.POINTER(C.c_int64)]
 lib.amgcu_setup.argtypes = [C.c_void_p, C.POINTER(CsrC), C.c_int32, f64p, f64p, C.POINTER(SetupOptionsC),
                             C.POINTER(C.c_void_p)]
 lib.amgcu_setup_device.argtypes = [C.c_void_p, C.POINTER(CsrC), C.c_int32, C.c_void_p, C.c_void_p,
@@ -107,6 +108,11 @@ class Context:
 
     def synchronize(self):
         self._chk(lib.amgcu_ctx_synchronize(self.handle))
+
+    def sync_count(self) -> int:
+        v = C.c_int64()
+        self._chk(lib.amgcu_ctx_sync_count(self.handle, C.byref(v)))
+        return v.value
 
     def launch_count(self) -> int:
         v = C.c_int64()

@@ -145,6 +145,7 @@ amgcu_status amgcu_ctx_destroy(amgcu_ctx ctx) {
     ctx->c.tickets.release();
     ctx->c.arnoldi_v0.release();
     cudaStreamSynchronize(ctx->c.s);
+    if (ctx->c.pin) cudaFreeHost(ctx->c.pin);
     cudaStreamDestroy(ctx->c.s);
     delete ctx;
     return AMGCU_OK;
@@ -162,6 +163,10 @@ amgcu_status amgcu_ctx_synchronize(amgcu_ctx ctx) {
 
 amgcu_status amgcu_ctx_launch_count(amgcu_ctx ctx, int64_t* launches) {
     return guarded(ctx, [&] { *launches = ctx->c.launches; });
+}
+
+amgcu_status amgcu_ctx_sync_count(amgcu_ctx ctx, int64_t* syncs) {
+    return guarded(ctx, [&] { *syncs = ctx->c.syncs; });
 }
 
 amgcu_status amgcu_ctx_timer_start(amgcu_ctx ctx) {

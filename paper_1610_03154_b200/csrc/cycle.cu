@@ -306,14 +306,22 @@ __global__ void k_axpy_c(int64_t n, double a, const double* __restrict__ x, doub
         y[i] += a * x[i];
 }
 
-void build_sell(Ctx& c, const DCsr& A, DSell& S) {
+// SELL mirror in two halves so that several operators share one synchronisation:
+// begin() sizes the slices and stages the stored-entry total in pinned slot `slot`,
+// finish() (after a sync) allocates and fills.
+void build_sell_begin(Ctx& c, const DCsr& A, DSell& S, int slot) {
     S.nr = A.nr;
     S.nc = A.nc;
     S.nslices = (A.nr + kSlice - 1) / kSlice;
     DBuf<int64_t> slen(static_cast<size_t>(S.nslices) + 1, c.s);
     S.slice_ptr.alloc(static_cast<size_t>(S.nslices) + 1, c.s);
     launch(c, k_slice_len, blocks_for(S.nslices, 256), 256, 0, A.nr, A.rp.get(), slen.get());
-    S.stored = exclusive_scan_i64(c, slen.get(), S.slice_ptr.get(), S.nslices);
+    exclusive_scan_i64(c, slen.get(), S.slice_ptr.get(), S.nslices, false);
+    stage_scalar(c, slot, static_cast<const int64_t*>(S.slice_ptr.get() + S.nslices));
+}
+
+void build_sell_finish(Ctx& c, const DCsr& A, DSell& S, int slot) {
+    S.stored = S.nslices > 0 ? staged<int64_t>(c, slot) : 0;
     S.slice_len.alloc(static_cast<size_t>(S.nslices), c.s);
     S.ci.alloc(static_cast<size_t>(S.stored), c.s);
     S.va.alloc(static_cast<size_t>(S.stored), c.s);
@@ -488,12 +496,21 @@ void prepare_solve(DHier& h) {
             L.b.alloc(static_cast<size_t>(n), c.s);
             L.x.alloc(static_cast<size_t>(n), c.s);
         }
-        build_sell(c, L.A, L.sA);
+    }
+    // all SELL mirrors: sizes first, one synchronisation, then the fills
+    std::vector<std::pair<const DCsr*, DSell*>> ops;
+    for (size_t l = 0; l < h.lv.size(); ++l) {
+        DLevel& L = h.lv[l];
+        ops.emplace_back(&L.A, &L.sA);
         if (l + 1 < h.lv.size()) {
-            build_sell(c, L.P, L.sP);
-            build_sell(c, L.R, L.sR);
+            ops.emplace_back(&L.P, &L.sP);
+            ops.emplace_back(&L.R, &L.sR);
         }
     }
+    if (ops.size() > static_cast<size_t>(Ctx::kPinSlots)) throw std::logic_error("prepare_solve: too many levels");
+    for (size_t k = 0; k < ops.size(); ++k) build_sell_begin(c, *ops[k].first, *ops[k].second, static_cast<int>(k));
+    sync(c);
+    for (size_t k = 0; k < ops.size(); ++k) build_sell_finish(c, *ops[k].first, *ops[k].second, static_cast<int>(k));
     sync(c);
     h.solve_ready = true;
 }

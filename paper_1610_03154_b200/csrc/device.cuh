@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstring>
+#include <stdexcept>
 #include <string>
 #include <utility>
 #include <vector>
@@ -93,6 +95,7 @@ enum ProfFamily : int {
 
 struct ProfRecord {
     int64_t launches = 0;
+    int64_t syncs = 0;  // host synchronisations of the stream
     double bytes = 0.0;
     double ms = 0.0;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending;
@@ -108,12 +111,15 @@ struct Ctx {
     int sms = 148;
     bool seq = false;  // sequential (reference-order) global reductions
     int64_t launches = 0;
+    int64_t syncs = 0;  // host synchronisations of the stream
     int blas_family = kProfBlas1;  // family the BLAS-1 launchers record under
     std::string err;
     DBuf<double> scal;         // device scalars for reductions/control
     DBuf<double> partials;     // per-block partial sums
     DBuf<unsigned int> tickets;  // sync-free wavefront tickets
-    double* hpin = nullptr;    // pinned host staging for scalars
+    // pinned host staging: several device scalars are read back with one synchronisation
+    int64_t* pin = nullptr;
+    static constexpr int kPinSlots = 512;
     // cached Arnoldi start vector 1 + U(-0.5, 0.5) from mt19937(20240911)
     // (spectral.hpp:32-36); prefixes serve every smaller level.
     DBuf<double> arnoldi_v0;
@@ -240,8 +246,10 @@ inline unsigned blocks_for(int64_t n, int per_block) {
 // ---- primitives (primitives.cu) ------------------------------------------
 // out[0..n] = exclusive prefix sum of in[0..n-1], out[n] = total.  Returns
 // the total (synchronising read).  in may alias out only if in == out is false.
-int64_t exclusive_scan_i32(Ctx& c, const int32_t* in, int32_t* out, int64_t n, bool read_total = true);
-int64_t exclusive_scan_i64(Ctx& c, const int64_t* in, int64_t* out, int64_t n, bool read_total = true);
+int64_t exclusive_scan_i32(Ctx& c, const int32_t* in, int32_t* out, int64_t n, bool read_total = true,
+                           const char* file = __builtin_FILE(), int line = __builtin_LINE());
+int64_t exclusive_scan_i64(Ctx& c, const int64_t* in, int64_t* out, int64_t n, bool read_total = true,
+                           const char* file = __builtin_FILE(), int line = __builtin_LINE());
 void fill_f64(Ctx& c, double* p, double v, int64_t n);
 void fill_i32(Ctx& c, int32_t* p, int32_t v, int64_t n);
 template <typename T>
@@ -256,12 +264,38 @@ template <typename T>
 void copy_d2h(Ctx& c, T* dst, const T* src, int64_t n) {
     if (n > 0) AMG_CK(cudaMemcpyAsync(dst, src, sizeof(T) * n, cudaMemcpyDeviceToHost, c.s));
 }
-inline void sync(Ctx& c) { AMG_CK(cudaStreamSynchronize(c.s)); }
+// AMGCU_SYNC_TRACE=1: count the host synchronisations per call site (printed at exit)
+void note_sync_site(const char* file, int line);
+
+inline void sync(Ctx& c, const char* file = __builtin_FILE(), int line = __builtin_LINE()) {
+    ++c.syncs;
+    note_sync_site(file, line);
+    AMG_CK(cudaStreamSynchronize(c.s));
+}
 template <typename T>
-T read_scalar(Ctx& c, const T* dptr) {
+T read_scalar(Ctx& c, const T* dptr, const char* file = __builtin_FILE(), int line = __builtin_LINE()) {
     T v;
     AMG_CK(cudaMemcpyAsync(&v, dptr, sizeof(T), cudaMemcpyDeviceToHost, c.s));
-    sync(c);
+    sync(c, file, line);
+    return v;
+}
+
+// Batched scalar reads: stage(k, dptr) enqueues an async copy into pinned slot k;
+// one flush() synchronises for all of them.
+inline int64_t* pinned_slots(Ctx& c) {
+    if (!c.pin) AMG_CK(cudaMallocHost(&c.pin, sizeof(int64_t) * Ctx::kPinSlots));
+    return c.pin;
+}
+template <typename T>
+inline void stage_scalar(Ctx& c, int slot, const T* dptr) {
+    static_assert(sizeof(T) <= sizeof(int64_t), "scalar too wide");
+    if (slot < 0 || slot >= Ctx::kPinSlots) throw std::logic_error("stage_scalar: slot out of range");
+    AMG_CK(cudaMemcpyAsync(pinned_slots(c) + slot, dptr, sizeof(T), cudaMemcpyDeviceToHost, c.s));
+}
+template <typename T>
+inline T staged(Ctx& c, int slot) {
+    T v;
+    std::memcpy(&v, c.pin + slot, sizeof(T));
     return v;
 }
 

@@ -5,7 +5,39 @@
 
 #include "device.cuh"
 
+#include <cstdio>
+#include <cstring>
+#include <cstdlib>
+#include <map>
+#include <mutex>
+#include <string>
+
 namespace amgcu {
+
+namespace {
+struct SyncSites {
+    std::mutex m;
+    std::map<std::string, long> n;
+    bool on = std::getenv("AMGCU_SYNC_TRACE") != nullptr;
+    ~SyncSites() {
+        if (!on) return;
+        for (auto& kv : n) std::fprintf(stderr, "sync %6ld  %s\n", kv.second, kv.first.c_str());
+    }
+};
+SyncSites& sync_sites() {
+    static SyncSites s;
+    return s;
+}
+}  // namespace
+
+void note_sync_site(const char* file, int line) {
+    SyncSites& s = sync_sites();
+    if (!s.on) return;
+    const char* base = std::strrchr(file, '/');
+    std::lock_guard<std::mutex> g(s.m);
+    s.n[std::string(base ? base + 1 : file) + ":" + std::to_string(line)] += 1;
+}
+
 
 namespace {
 
@@ -81,7 +113,7 @@ __global__ void k_tile_scan(const T* __restrict__ in, T* __restrict__ out, int64
 }
 
 template <typename T>
-int64_t scan_impl(Ctx& c, const T* in, T* out, int64_t n, bool read_total) {
+int64_t scan_impl(Ctx& c, const T* in, T* out, int64_t n, bool read_total, const char* file, int line) {
     if (n == 0) {
         AMG_CK(cudaMemsetAsync(out, 0, sizeof(T), c.s));
         return 0;
@@ -93,7 +125,7 @@ int64_t scan_impl(Ctx& c, const T* in, T* out, int64_t n, bool read_total) {
     launch(c, k_tile_scan<T>, static_cast<unsigned>(ntiles), kScanThreads, 0, in, out, n,
            static_cast<const T*>(sums.get()), ntiles);
     if (!read_total) return -1;
-    return static_cast<int64_t>(read_scalar(c, out + n));
+    return static_cast<int64_t>(read_scalar(c, static_cast<const T*>(out + n), file, line));
 }
 
 template <typename T>
@@ -104,11 +136,13 @@ __global__ void k_fill(T* p, T v, int64_t n) {
 
 }  // namespace
 
-int64_t exclusive_scan_i32(Ctx& c, const int32_t* in, int32_t* out, int64_t n, bool read_total) {
-    return scan_impl<int32_t>(c, in, out, n, read_total);
+int64_t exclusive_scan_i32(Ctx& c, const int32_t* in, int32_t* out, int64_t n, bool read_total, const char* file,
+                           int line) {
+    return scan_impl<int32_t>(c, in, out, n, read_total, file, line);
 }
-int64_t exclusive_scan_i64(Ctx& c, const int64_t* in, int64_t* out, int64_t n, bool read_total) {
-    return scan_impl<int64_t>(c, in, out, n, read_total);
+int64_t exclusive_scan_i64(Ctx& c, const int64_t* in, int64_t* out, int64_t n, bool read_total, const char* file,
+                           int line) {
+    return scan_impl<int64_t>(c, in, out, n, read_total, file, line);
 }
 void fill_f64(Ctx& c, double* p, double v, int64_t n) { launch(c, k_fill<double>, blocks_for(n, 256), 256, 0, p, v, n); }
 void fill_i32(Ctx& c, int32_t* p, int32_t v, int64_t n) {

@@ -552,7 +552,18 @@ void spgemm(Ctx& c, const DCsr& A, const DCsr& B, DCsr& C, double* ops) {
     const int32_t nr = A.nr;
     DBuf<int64_t> np(static_cast<size_t>(nr) + 1, c.s), poff(static_cast<size_t>(nr) + 1, c.s);
     launch(c, k_product_count, blocks_for(nr, 256), 256, 0, nr, A.rp.get(), A.ci.get(), B.rp.get(), np.get());
-    const int64_t total = exclusive_scan_i64(c, np.get(), poff.get(), nr);
+    // rows above the shared-memory capacity are listed now, so the product total and
+    // their count come back with one synchronisation
+    DBuf<int32_t> big_list(static_cast<size_t>(nr), c.s), big_count(1, c.s);
+    AMG_CK(cudaMemsetAsync(big_count.get(), 0, sizeof(int32_t), c.s));
+    launch(c, k_collect_big, blocks_for(nr, 256), 256, 0, nr, static_cast<const int64_t*>(np.get()), big_list.get(),
+           big_count.get());
+    exclusive_scan_i64(c, np.get(), poff.get(), nr, false);
+    stage_scalar(c, 0, static_cast<const int64_t*>(poff.get() + nr));
+    stage_scalar(c, 1, static_cast<const int32_t*>(big_count.get()));
+    sync(c);
+    const int64_t total = nr > 0 ? staged<int64_t>(c, 0) : 0;
+    const int32_t nbig = staged<int32_t>(c, 1);
     if (ops) *ops = static_cast<double>(total);
     DBuf<int32_t> tcol(static_cast<size_t>(total), c.s), cnt(static_cast<size_t>(nr) + 1, c.s);
     DBuf<double> tval(static_cast<size_t>(total), c.s);
@@ -563,11 +574,6 @@ void spgemm(Ctx& c, const DCsr& A, const DCsr& B, DCsr& C, double* ops) {
            A.va.get(), B.rp.get(), B.ci.get(), B.va.get(), static_cast<const int64_t*>(poff.get()), tcol.get(),
            tval.get(), cnt.get());
     // rows above the shared-memory capacity
-    DBuf<int32_t> big_list(static_cast<size_t>(nr), c.s), big_count(1, c.s);
-    AMG_CK(cudaMemsetAsync(big_count.get(), 0, sizeof(int32_t), c.s));
-    launch(c, k_collect_big, blocks_for(nr, 256), 256, 0, nr, static_cast<const int64_t*>(np.get()), big_list.get(),
-           big_count.get());
-    const int32_t nbig = read_scalar(c, big_count.get());
     if (nbig > 0) {
         std::vector<int32_t> hl(nbig);
         copy_d2h(c, hl.data(), big_list.get(), nbig);
