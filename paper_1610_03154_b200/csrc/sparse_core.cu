@@ -101,7 +101,6 @@ __global__ void k_gather_transpose(int64_t nnz, const int32_t* __restrict__ pos,
 // one block over a global scratch region.
 // ---------------------------------------------------------------------------------
 constexpr int kSmallCap = 512;
-constexpr int kGemmWarps = 4;
 
 __global__ void k_product_count(int32_t nr, const int32_t* __restrict__ arp, const int32_t* __restrict__ aci,
                                 const int32_t* __restrict__ brp, int64_t* __restrict__ np) {
@@ -152,6 +151,9 @@ __device__ __forceinline__ void expand_row(int32_t i, const int32_t* __restrict_
     }
 }
 
+constexpr int kGemmWarps = 8;
+constexpr int kSortCap = 64;  // rows up to this many products: the sort kernel
+
 // Warp-cooperative expansion: lanes take A entries (32 at a time), a warp scan
 // of their B-row lengths gives each product's sequence number, and each lane
 // writes its B row's products -- the A-entry loop is no longer a chain of
@@ -189,19 +191,20 @@ __device__ __forceinline__ void expand_row_warp(int32_t i, const int32_t* __rest
     }
 }
 
+// rows with at most kSortCap products: warp bitonic sort of (column, sequence) keys
 __global__ void __launch_bounds__(kGemmWarps * kWarp)
     k_spgemm_small(int32_t nr, const int32_t* __restrict__ arp, const int32_t* __restrict__ aci,
                    const double* __restrict__ ava, const int32_t* __restrict__ brp, const int32_t* __restrict__ bci,
                    const double* __restrict__ bva, const int64_t* __restrict__ poff, int32_t* __restrict__ tcol,
                    double* __restrict__ tval, int32_t* __restrict__ cnt) {
-    __shared__ unsigned long long skeys[kGemmWarps][kSmallCap];
-    __shared__ double svals[kGemmWarps][kSmallCap];
+    __shared__ unsigned long long skeys[kGemmWarps][kSortCap];
+    __shared__ double svals[kGemmWarps][kSortCap];
     const int w = threadIdx.x / kWarp;
     const int lane = threadIdx.x & (kWarp - 1);
     const int32_t i = blockIdx.x * kGemmWarps + w;
     if (i >= nr) return;
     const int64_t np = poff[i + 1] - poff[i];
-    if (np > kSmallCap) return;  // handled by the block kernel
+    if (np > kSortCap) return;  // handled by the hash / block kernels
     if (np == 0) {
         if (lane == 0) cnt[i] = 0;
         return;
@@ -259,6 +262,149 @@ __global__ void __launch_bounds__(kGemmWarps * kWarp)
         written += __popc(ballot);
     }
     if (lane == 0) cnt[i] = written;
+}
+
+// Hash accumulation, sort of the distinct columns only.  Products are staged
+// in sequence order and consumed 32 at a time: each lane finds its column's
+// slot (open addressing, atomicCAS on the key), lanes of one column are grouped
+// with __match_any_sync and the lowest one adds the group's products into the
+// slot in lane order -- chunks in order, lanes in order: every column's sum is
+// the reference's sequential one, starting from 0.0.  The non-zero sums are
+// then compacted and only those D <= np entries are bitonic-sorted by column.
+constexpr int kHashWarps = 4;
+constexpr int kHashSlots = 2 * kSmallCap;  // load factor <= 1/2
+
+struct HashShared {
+    int32_t hkey[kHashSlots];
+    double hval[kHashSlots];
+    int32_t pcol[kSmallCap];                 // staged products: column
+    double pval[kSmallCap];                  // staged products: value; reused as the sort keys
+    double chunk[kWarp];
+};
+
+__device__ __forceinline__ uint32_t col_hash(int32_t col, uint32_t mask) {
+    return (static_cast<uint32_t>(col) * 2654435761u) & mask;
+}
+
+__global__ void __launch_bounds__(kHashWarps * kWarp)
+    k_spgemm_hash(int32_t nr, const int32_t* __restrict__ arp, const int32_t* __restrict__ aci,
+                  const double* __restrict__ ava, const int32_t* __restrict__ brp, const int32_t* __restrict__ bci,
+                  const double* __restrict__ bva, const int64_t* __restrict__ poff, int32_t* __restrict__ tcol,
+                  double* __restrict__ tval, int32_t* __restrict__ cnt) {
+    extern __shared__ unsigned long long hsm[];
+    const int w = threadIdx.x / kWarp;
+    const int lane = threadIdx.x & (kWarp - 1);
+    const int32_t i = blockIdx.x * kHashWarps + w;
+    if (i >= nr) return;
+    const int64_t np = poff[i + 1] - poff[i];
+    if (np > kSmallCap || np <= kSortCap) return;  // handled by the block / sort kernels
+    HashShared& sh = reinterpret_cast<HashShared*>(hsm)[w];
+    // table sized to the row: a power of two >= 2 np (load factor <= 1/2)
+    const int32_t hs = static_cast<int32_t>(max(64u, next_pow2(2u * static_cast<unsigned>(np))));
+    const uint32_t hmask = static_cast<uint32_t>(hs - 1);
+    for (int e = lane; e < hs; e += kWarp) {
+        sh.hkey[e] = -1;
+        sh.hval[e] = 0.0;
+    }
+    // stage the products in sequence order (warp-cooperative expansion)
+    {
+        const int32_t alo = arp[i], ahi = arp[i + 1];
+        int32_t base = 0;
+        for (int32_t p0 = alo; p0 < ahi; p0 += kWarp) {
+            const int32_t p = p0 + lane;
+            int32_t lo = 0, len = 0;
+            double a = 0.0;
+            if (p < ahi) {
+                const int32_t t = aci[p];
+                a = ava[p];
+                lo = brp[t];
+                len = brp[t + 1] - lo;
+            }
+            int32_t incl = len;
+            for (int off = 1; off < kWarp; off <<= 1) {
+                const int32_t v = __shfl_up_sync(0xffffffffu, incl, off);
+                if (lane >= off) incl += v;
+            }
+            const int32_t my = base + incl - len;
+            for (int32_t q = 0; q < len; ++q) {
+                sh.pcol[my + q] = __ldg(&bci[lo + q]);
+                sh.pval[my + q] = a * __ldg(&bva[lo + q]);
+            }
+            base += __shfl_sync(0xffffffffu, incl, kWarp - 1);
+        }
+    }
+    __syncwarp();
+    // ordered accumulation, 32 products at a time
+    const int32_t npi = static_cast<int32_t>(np);
+    for (int32_t c0 = 0; c0 < npi; c0 += kWarp) {
+        const int32_t e = c0 + lane;
+        const bool act = e < npi;
+        const unsigned am = __ballot_sync(0xffffffffu, act);
+        int32_t slot = -1;
+        if (act) {
+            const int32_t col = sh.pcol[e];
+            uint32_t h = col_hash(col, hmask);
+            while (true) {
+                const int32_t k = atomicCAS(&sh.hkey[h], -1, col);
+                if (k == -1 || k == col) break;
+                h = (h + 1) & hmask;
+            }
+            slot = static_cast<int32_t>(h);
+            sh.chunk[lane] = sh.pval[e];
+        }
+        __syncwarp();
+        if (act) {
+            const unsigned grp = __match_any_sync(am, slot);
+            if (lane == __ffs(grp) - 1) {
+                double v = sh.hval[slot];
+                for (unsigned g = grp; g; g &= g - 1) v += sh.chunk[__ffs(g) - 1];
+                sh.hval[slot] = v;
+            }
+        }
+        __syncwarp();
+    }
+    // compact the non-zero sums (key = column << 32 | slot) into the staging area
+    unsigned long long* keys = reinterpret_cast<unsigned long long*>(sh.pval);
+    int32_t d = 0;
+    for (int32_t e0 = 0; e0 < hs; e0 += kWarp) {
+        const int32_t e = e0 + lane;
+        const int32_t col = sh.hkey[e];
+        const bool keep = col >= 0 && sh.hval[e] != 0.0;
+        const unsigned b = __ballot_sync(0xffffffffu, keep);
+        if (keep)
+            keys[d + __popc(b & ((1u << lane) - 1u))] =
+                (static_cast<unsigned long long>(static_cast<uint32_t>(col)) << 32) | static_cast<uint32_t>(e);
+        d += __popc(b);
+    }
+    __syncwarp();
+    if (d > 1) {
+        const unsigned n2 = next_pow2(static_cast<unsigned>(d));
+        for (unsigned e = static_cast<unsigned>(d) + lane; e < n2; e += kWarp) keys[e] = ~0ull;
+        __syncwarp();
+        for (unsigned k = 2; k <= n2; k <<= 1) {
+            for (unsigned j = k >> 1; j > 0; j >>= 1) {
+                for (unsigned e = lane; e < n2 / 2; e += kWarp) {
+                    const unsigned lo = 2 * e - (e & (j - 1));
+                    const unsigned hi = lo + j;
+                    const bool up = ((lo & k) == 0);
+                    const unsigned long long a = keys[lo], b = keys[hi];
+                    if ((a > b) == up) {
+                        keys[lo] = b;
+                        keys[hi] = a;
+                    }
+                }
+                __syncwarp();
+            }
+        }
+    }
+    int32_t* ocol = tcol + poff[i];
+    double* oval = tval + poff[i];
+    for (int32_t e = lane; e < d; e += kWarp) {
+        const unsigned long long k = keys[e];
+        ocol[e] = static_cast<int32_t>(k >> 32);
+        oval[e] = sh.hval[static_cast<uint32_t>(k & 0xffffffffull)];
+    }
+    if (lane == 0) cnt[i] = d;
 }
 
 constexpr int kBigThreads = 512;
@@ -547,6 +693,17 @@ void transpose(Ctx& c, const DCsr& A, DCsr& T) {
            static_cast<const int32_t*>(rows.get()), A.va.get(), T.ci.get(), T.va.get());
 }
 
+namespace {
+size_t hash_smem() {
+    static const size_t bytes = [] {
+        const size_t b = sizeof(HashShared) * kHashWarps;
+        AMG_CK(cudaFuncSetAttribute(k_spgemm_hash, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(b)));
+        return b;
+    }();
+    return bytes;
+}
+}  // namespace
+
 void spgemm(Ctx& c, const DCsr& A, const DCsr& B, DCsr& C, double* ops) {
     if (A.nc != B.nr) throw InvalidArgument("matmul: dimension mismatch");
     const int32_t nr = A.nr;
@@ -570,9 +727,12 @@ void spgemm(Ctx& c, const DCsr& A, const DCsr& B, DCsr& C, double* ops) {
     launch_prof(c, kProfSpgemm,
                 12.0 * A.nnz + 4.0 * (A.nr + 1) + 12.0 * B.nnz + 4.0 * (B.nr + 1) + 12.0 * static_cast<double>(total) +
                     4.0 * nr,
-                k_spgemm_small, blocks_for(nr, kGemmWarps), kGemmWarps * kWarp, 0, nr, A.rp.get(), A.ci.get(),
-           A.va.get(), B.rp.get(), B.ci.get(), B.va.get(), static_cast<const int64_t*>(poff.get()), tcol.get(),
-           tval.get(), cnt.get());
+                k_spgemm_hash, blocks_for(nr, kHashWarps), kHashWarps * kWarp, hash_smem(), nr, A.rp.get(),
+                A.ci.get(), A.va.get(), B.rp.get(), B.ci.get(), B.va.get(), static_cast<const int64_t*>(poff.get()),
+                tcol.get(), tval.get(), cnt.get());
+    launch_prof(c, kProfSpgemm, 0.0, k_spgemm_small, blocks_for(nr, kGemmWarps), kGemmWarps * kWarp, 0, nr, A.rp.get(),
+                A.ci.get(), A.va.get(), B.rp.get(), B.ci.get(), B.va.get(), static_cast<const int64_t*>(poff.get()),
+                tcol.get(), tval.get(), cnt.get());
     // rows above the shared-memory capacity
     if (nbig > 0) {
         std::vector<int32_t> hl(nbig);

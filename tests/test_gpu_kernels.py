@@ -63,6 +63,24 @@ def test_matmul_long_rows_and_cancellation(gpu, port):
     assert C.nnz() == 1
 
 
+def test_matmul_hash_rows_collisions(gpu, port):
+    """65..512 products per row (the hash-accumulation kernel): many products per output
+    column and small-integer values, so exact cancellations to 0.0 are frequent"""
+    rng = np.random.default_rng(11)
+    for n, m, k, da, db in ((50, 40, 20, 0.5, 0.5), (20, 60, 8, 0.9, 0.9), (40, 30, 200, 0.6, 0.4)):
+        ta, tb = [], []
+        for i in range(n):
+            for j in range(m):
+                if rng.random() < da:
+                    ta.append((i, j, float(rng.choice([-2.0, -1.0, 1.0, 2.0]))))
+        for i in range(m):
+            for j in range(k):
+                if rng.random() < db:
+                    tb.append((i, j, float(rng.choice([-1.0, 0.5, 1.0, 3.0]))))
+        A, B = from_triplets(n, m, ta), from_triplets(m, k, tb)
+        assert api.matmul(A, B, ctx=gpu) == port.matmul(A, B), (n, m, k)
+
+
 def test_filter_matrix(gpu, port):
     rng = np.random.default_rng(17)
     for _ in range(20):
