@@ -227,7 +227,7 @@ const char* amgcu_profile_family_name(int32_t family) {
                                                "spgemm",                 "evolution_soc",   "gauss_seidel_wavefront",
                                                "aggregate_lfmis",        "coarse_solve",    "blas1",
                                                "spectral_spmv",          "emin_cg",         "other",
-                                               "arnoldi_blas1",          "emin_blas1"};
+                                               "arnoldi_blas1",          "emin_blas1",      "vcycle_coarse_fused"};
     return (family >= 0 && family < kProfFamilies) ? names[family] : "";
 }
 

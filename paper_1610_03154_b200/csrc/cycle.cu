@@ -13,7 +13,11 @@
 //   * restriction b_c = R r is a gather over R's rows (no atomics).
 // Krylov scalars stay on the device; the host reads one small status record
 // per iteration (the residual norm decides termination, as in the reference).
+#include <cooperative_groups.h>
+
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 
 #include "hier.cuh"
 
@@ -189,6 +193,137 @@ __global__ void __launch_bounds__(kWarpRowsPerBlock * 32)
 }
 #undef AMGCU_WARP_ROW_PROLOGUE
 
+// ---- fused coarse V-cycle -----------------------------------------------------------
+// Levels f .. L-1 of a Jacobi V(1,1) cycle in ONE cooperative launch: every phase
+// (pre-relax+residual, restriction, coarse GEMV, prolongation, post-relax) is the
+// per-row code of the standalone kernels above, distributed grid-stride over the
+// resident grid, with one grid barrier between phases.  Results are therefore
+// bit-identical to the launch-per-kernel cycle; what disappears is ~4 launches per
+// coarse level whose cost there is launch and dependent-load latency.
+struct FusedLevel {
+    SellView A, R, P;     // R, P unused on the coarsest level
+    int wA, wR, wP;       // warp-per-row flags
+    const double* wd_pre;
+    const double* wd_post;
+    double* b;
+    double* x;
+    double* r;
+    double* t;
+    int32_t n;
+};
+
+constexpr int kFusedThreads = 256;
+constexpr int32_t kFusedMaxRows = 65536;  // the fused cycle starts at the first level this small
+constexpr int kFusedWarps = kFusedThreads / 32;
+
+struct FusedCtx {
+    int64_t gtid, gthreads, gwarp, gwarps;
+    int lane;
+    double* buf;  // this warp's product staging (warp-per-row phases)
+};
+
+// y_i = epi(i, sum) over the rows of S, thread-per-row (SELL) or warp-per-row (CSR)
+template <typename Gather, typename Epi>
+__device__ __forceinline__ void fused_rows(const SellView& S, bool warp_rows, const FusedCtx& f, Gather gx, Epi epi) {
+    // fewer rows than warps in the grid: a warp per row spreads them over every SM
+    if (warp_rows || S.nr <= f.gwarps) {
+        for (int64_t i = f.gwarp; i < S.nr; i += f.gwarps) {
+            const double sum = warp_row_sum(S, static_cast<int32_t>(i), gx, f.buf, f.lane);
+            if (f.lane == 0) epi(static_cast<int32_t>(i), sum);
+        }
+    } else {
+        for (int64_t i = f.gtid; i < S.nr; i += f.gthreads) {
+            const int32_t ii = static_cast<int32_t>(i);
+            const int32_t sl = ii / kSlice, ln = ii % kSlice;
+            epi(ii, sell_row_sum(S.sptr[sl] + ln, S.slen[sl], S.ci, S.va, gx));
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kFusedThreads)
+    k_vcycle_fused(const FusedLevel* __restrict__ lv, int nlev, const double* __restrict__ pinv, int32_t coarse_n,
+                   unsigned long long* __restrict__ stamps) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    int ns_ = 0;
+    auto stamp = [&]() {
+        if (stamps && blockIdx.x == 0 && threadIdx.x == 0) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+            stamps[ns_] = t;
+        }
+        ++ns_;
+    };
+    stamp();
+    __shared__ double wbuf[kFusedWarps][kWarpCap];
+    FusedCtx f;
+    f.gtid = static_cast<int64_t>(blockIdx.x) * kFusedThreads + threadIdx.x;
+    f.gthreads = static_cast<int64_t>(gridDim.x) * kFusedThreads;
+    f.gwarp = f.gtid / 32;
+    f.gwarps = f.gthreads / 32;
+    f.lane = threadIdx.x & 31;
+    f.buf = wbuf[threadIdx.x / 32];
+    // down: pre-relax from zero + residual, then restriction
+    for (int l = 0; l + 1 < nlev; ++l) {
+        const FusedLevel& L = lv[l];
+        const double* wd = L.wd_pre;
+        const double* b = L.b;
+        // b (and every level vector) is written inside this launch: coherent loads only
+        fused_rows(L.A, L.wA != 0, f, [&](int32_t j) { return 0.0 + __ldg(&wd[j]) * __ldcg(&b[j]); },
+                   [&](int32_t i, double s) {
+                       L.x[i] = 0.0 + wd[i] * b[i];
+                       L.r[i] = b[i] - s;
+                   });
+        grid.sync();
+        stamp();
+        const double* r = L.r;
+        double* bn = lv[l + 1].b;
+        fused_rows(L.R, L.wR != 0, f, [&](int32_t j) { return __ldcg(&r[j]); },
+                   [&](int32_t i, double s) { bn[i] = s; });
+        grid.sync();
+        stamp();
+    }
+    // coarsest: x = pinv b (k_dense_gemv / k_dense_gemv_warp arithmetic)
+    {
+        const FusedLevel& L = lv[nlev - 1];
+        if (coarse_n <= 256) {
+            for (int64_t i = f.gtid; i < coarse_n; i += f.gthreads) {
+                double s = 0.0;
+                for (int32_t j = 0; j < coarse_n; ++j) s += pinv[i * coarse_n + j] * __ldcg(&L.b[j]);
+                L.x[i] = s;
+            }
+        } else {
+            for (int64_t i = f.gwarp; i < coarse_n; i += f.gwarps) {
+                const double* row = pinv + i * coarse_n;
+                double s = 0.0;
+                for (int32_t j = f.lane; j < coarse_n; j += 32) s += row[j] * __ldcg(&L.b[j]);
+                for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+                if (f.lane == 0) L.x[i] = s;
+            }
+        }
+        grid.sync();
+        stamp();
+    }
+    // up: interpolate and correct into t, post-relax back into x
+    for (int l = nlev - 2; l >= 0; --l) {
+        const FusedLevel& L = lv[l];
+        const double* xc = lv[l + 1].x;
+        const double* x = L.x;
+        double* t = L.t;
+        fused_rows(L.P, L.wP != 0, f, [&](int32_t j) { return __ldcg(&xc[j]); },
+                   [&](int32_t i, double s) { t[i] = x[i] + s; });
+        grid.sync();
+        stamp();
+        const double* wd = L.wd_post;
+        const double* b = L.b;
+        double* xo = L.x;
+        fused_rows(L.A, L.wA != 0, f, [&](int32_t j) { return __ldcg(&t[j]); },
+                   [&](int32_t i, double s) { xo[i] = t[i] + wd[i] * (b[i] - s); });
+        if (l > 0) grid.sync();
+        stamp();
+    }
+}
+
 __global__ void k_sell_spmv(SellView A, const double* __restrict__ x, double* __restrict__ y) {
     const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= A.nr) return;
@@ -341,10 +476,21 @@ unsigned stream_grid(Ctx& c, int64_t n) { return std::max(1u, std::min<unsigned>
 
 double relax_cost(int scheme, double nnz) { return scheme == 3 ? 2.0 * nnz : nnz; }
 
+// AMGCU_FUSED_CYCLE=0 disables the fused coarse cycle (launch-per-kernel reference path)
+bool fused_enabled() {
+    const char* e = std::getenv("AMGCU_FUSED_CYCLE");
+    return !(e && e[0] == '0');
+}
+
 struct Driver {
     DHier& h;
     Ctx& c;
     double ops = 0.0;  // multiply-model count (cycle.hpp cost model)
+    // fused coarse cycle: level descriptors (host copy + device array), built on first use
+    std::vector<FusedLevel> fused_host;
+    DBuf<FusedLevel> fused_desc;
+    DBuf<unsigned long long> fused_stamps;
+    size_t fused_first = 0;
 
     // xout = xin + wd (b - A xin); family < 0: untagged
     void jacobi_sweep(const DSell& S, int family, double bytes, const double* wd, const double* b, const double* xin,
@@ -365,8 +511,108 @@ struct Driver {
             launch_prof(c, family, bytes, k_sell_spmv, rows_grid(S.nr), 128, 0, view(S), x, y);
     }
 
+    // Fused coarse cycle from level `l` (x_zero, V-cycle, Jacobi V(1,1)): one cooperative
+    // launch; returns false when the configuration is not covered.
+    bool apply_fused(size_t l, double* x, const double* b) {
+        const size_t L = h.lv.size();
+        // levels large enough to fill the GPU keep the full-occupancy standalone kernels
+        if (!fused_enabled() || l == 0 || l + 1 >= L || h.lv[l].A.nr > kFusedMaxRows) return false;
+        if (h.o.pre_scheme != 0 || h.o.post_scheme != 0 || h.o.pre_sweeps != 1 || h.o.post_sweeps != 1) return false;
+        const int nlev = static_cast<int>(L - l);
+        // the caller passes level l's own b / x (apply from level l - 1), so the
+        // descriptors are constant and uploaded once
+        if (b != h.lv[l].b.get() || x != h.lv[l].x.get()) return false;
+        if (fused_desc.empty() || fused_first != l) {
+            std::vector<FusedLevel> hd(nlev);
+            for (int q = 0; q < nlev; ++q) {
+                DLevel& lev = h.lv[l + q];
+                FusedLevel& d = hd[q];
+                d = FusedLevel{};
+                d.A = view(lev.sA);
+                d.wA = lev.sA.warp_rows;
+                if (l + q + 1 < L) {
+                    d.R = view(lev.sR);
+                    d.P = view(lev.sP);
+                    d.wR = lev.sR.warp_rows;
+                    d.wP = lev.sP.warp_rows;
+                }
+                d.wd_pre = lev.wd_pre.get();
+                d.wd_post = lev.wd_post.get();
+                d.b = lev.b.get();
+                d.x = lev.x.get();
+                d.r = lev.r.get();
+                d.t = lev.t.get();
+                d.n = lev.A.nr;
+            }
+            fused_host = hd;
+            fused_desc.alloc(hd.size(), c.s);
+            AMG_CK(cudaMemcpyAsync(fused_desc.get(), fused_host.data(), sizeof(FusedLevel) * nlev,
+                                   cudaMemcpyHostToDevice, c.s));
+            sync(c);  // fused_host may be rebuilt while the copy is pending otherwise
+            fused_first = l;
+        }
+        static int per_sm = -1;
+        if (per_sm < 0)
+            AMG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_vcycle_fused, kFusedThreads, 0));
+        int64_t most = 0;
+        double bytes = 0.0;
+        for (int q = 0; q < nlev; ++q) {
+            const DLevel& lev = h.lv[l + q];
+            most = std::max<int64_t>(most, lev.A.nr);
+            if (l + q + 1 < L) {
+                const double nnz = static_cast<double>(lev.A.nnz), n = lev.A.nr;
+                bytes += 2.0 * (12.0 * nnz + 4.0 * (n + 1) + 32.0 * n) + 12.0 * lev.R.nnz + 12.0 * lev.P.nnz + 40.0 * n;
+                ops += relax_cost(0, nnz) + nnz + static_cast<double>(lev.R.nnz) + static_cast<double>(lev.P.nnz) +
+                       relax_cost(0, nnz);
+            }
+        }
+        bytes += 8.0 * h.coarse_n * h.coarse_n;
+        // the whole co-resident grid: small levels run warp-per-row over every SM
+        (void)most;
+        const int g = std::max(1, per_sm * c.sms);
+        const FusedLevel* dp = fused_desc.get();
+        const double* pv = h.coarse_pinv.get();
+        int32_t cn = h.coarse_n;
+        // AMGCU_FUSED_TRACE=1: phase boundary stamps of block 0, printed per call
+        static const bool trace = std::getenv("AMGCU_FUSED_TRACE") != nullptr;
+        unsigned long long* st = nullptr;
+        if (trace) {
+            if (fused_stamps.empty()) fused_stamps.alloc(64, c.s);
+            st = fused_stamps.get();
+        }
+        void* args[] = {&dp, const_cast<int*>(&nlev), &pv, &cn, &st};
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        const bool prof = c.profile && ((c.prof_mask >> kProfVcycleCoarseFused) & 1u);
+        if (prof) {
+            e0 = prof_event(c);
+            e1 = prof_event(c);
+            AMG_CK(cudaEventRecord(e0, c.s));
+        }
+        AMG_CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_vcycle_fused), dim3(g), dim3(kFusedThreads),
+                                           args, 0, c.s));
+        ++c.launches;
+        if (prof) {
+            AMG_CK(cudaEventRecord(e1, c.s));
+            ProfRecord& rec = c.prof[kProfVcycleCoarseFused];
+            rec.launches += 1;
+            rec.bytes += bytes;
+            rec.pending.emplace_back(e0, e1);
+        }
+        if (trace) {
+            unsigned long long hs[64];
+            AMG_CK(cudaMemcpyAsync(hs, st, sizeof(hs), cudaMemcpyDeviceToHost, c.s));
+            sync(c);
+            const int nst = 4 * (nlev - 1) + 2;
+            std::fprintf(stderr, "fused g=%d:", g);
+            for (int q = 1; q < nst; ++q) std::fprintf(stderr, " %.1f", (hs[q] - hs[q - 1]) * 1e-3);
+            std::fprintf(stderr, " us\n");
+        }
+        return true;
+    }
+
     // one cycle at `l`; x_zero: x is known to be all zeros on entry
     void apply(size_t l, double* x, const double* b, int kind, bool x_zero) {
+        if (kind == 0 && x_zero && apply_fused(l, x, b)) return;
         const size_t L = h.lv.size();
         DLevel& lev = h.lv[l];
         if (l == L - 1) {

@@ -90,6 +90,7 @@ enum ProfFamily : int {
     kProfOther,         // every launch not tagged with a family
     kProfArnoldiBlas1,  // BLAS-1 inside the spectral-radius Arnoldi
     kProfEminBlas1,     // BLAS-1 inside the energy-minimisation solve
+    kProfVcycleCoarseFused,  // levels 1.. of the V-cycle in one cooperative launch
     kProfFamilies
 };
 

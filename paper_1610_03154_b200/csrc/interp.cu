@@ -493,6 +493,7 @@ __global__ void k_root_mask(int32_t nroots, const int32_t* __restrict__ roots, u
 // against the sorted row N_t with two pointers.  Rows of N are short (3-8
 // slots on the BASELINE configs), so one thread per row keeps every lane busy.
 constexpr int kMrChunk = 8;
+constexpr int kMrNt = 8;  // rows of N up to this length are merged from registers
 
 __global__ void __launch_bounds__(128)
     k_masked_rows(int32_t n, const int32_t* __restrict__ arp, const int32_t* __restrict__ aci,
@@ -518,15 +519,38 @@ __global__ void __launch_bounds__(128)
             acc[s] = 0.0;
         }
         for (int32_t p = alo; p < ahi; ++p) {
-            const int32_t t = aci[p];
-            const double a = ava[p];
-            int32_t q = nrp[t];
-            const int32_t qe = nrp[t + 1];
+            const int32_t t = __ldg(&aci[p]);
+            const double a = __ldg(&ava[p]);
+            const int32_t q0 = __ldg(&nrp[t]);
+            const int32_t qe = __ldg(&nrp[t + 1]);
+            if (qe - q0 <= kMrNt) {
+                // N_t in registers: one batch of column loads, matches by comparison,
+                // then only the matching x values are gathered (all independent)
+                int32_t nt[kMrNt];
 #pragma unroll
-            for (int s = 0; s < kMrChunk; ++s) {
-                if (s < m) {
-                    while (q < qe && nci[q] < cols[s]) ++q;
-                    if (q < qe && nci[q] == cols[s]) acc[s] += a * x[q];
+                for (int u = 0; u < kMrNt; ++u) nt[u] = q0 + u < qe ? __ldg(&nci[q0 + u]) : -1;
+                int32_t hit[kMrChunk];
+#pragma unroll
+                for (int s2 = 0; s2 < kMrChunk; ++s2) {
+                    hit[s2] = -1;
+#pragma unroll
+                    for (int u = 0; u < kMrNt; ++u)
+                        if (nt[u] == cols[s2]) hit[s2] = q0 + u;
+                }
+                double xv[kMrChunk];
+#pragma unroll
+                for (int s2 = 0; s2 < kMrChunk; ++s2) xv[s2] = (s2 < m && hit[s2] >= 0) ? __ldg(&x[hit[s2]]) : 0.0;
+#pragma unroll
+                for (int s2 = 0; s2 < kMrChunk; ++s2)
+                    if (s2 < m && hit[s2] >= 0) acc[s2] += a * xv[s2];
+            } else {
+                int32_t q = q0;
+#pragma unroll
+                for (int s2 = 0; s2 < kMrChunk; ++s2) {
+                    if (s2 < m) {
+                        while (q < qe && nci[q] < cols[s2]) ++q;
+                        if (q < qe && nci[q] == cols[s2]) acc[s2] += a * x[q];
+                    }
                 }
             }
         }

@@ -155,3 +155,20 @@ def test_errors_map_to_reference_exceptions(gpu):
     Z = from_triplets(2, 2, [(0, 1, 1.0), (1, 1, 1.0)])
     with pytest.raises(RuntimeError, match="zero diagonal at row 0"):
         api.strength(Z, StrengthConfig(StrengthMeasure.symmetric, 0.1), ctx=gpu)
+
+
+@pytest.mark.parametrize("config,size", [(2, 96), (5, 48), (4, 64)])
+def test_fused_coarse_cycle_matches_per_kernel(gpu, monkeypatch, config, size):
+    """The cooperative coarse V-cycle (levels 1.. in one launch) is bit-identical to the
+    launch-per-kernel cycle: same x, same residual history."""
+    A, B, Bh, b = api.generate_config(config, size)
+    so, vo = api.config_options(config)
+    h = api.setup(A, B, so, Bh, ctx=gpu)
+    assert h.n_levels() >= 3
+    x1, r1 = api.solve(h, b, None, vo)
+    monkeypatch.setenv("AMGCU_FUSED_CYCLE", "0")
+    x0, r0 = api.solve(h, b, None, vo)
+    monkeypatch.delenv("AMGCU_FUSED_CYCLE")
+    assert r1.iterations == r0.iterations
+    assert np.asarray(x1).tobytes() == np.asarray(x0).tobytes()
+    assert list(r1.residual_history) == list(r0.residual_history)
