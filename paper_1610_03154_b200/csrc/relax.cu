@@ -105,6 +105,14 @@ __device__ __forceinline__ void vstore(int* p, int v) { *reinterpret_cast<volati
 // prefetcher refills a buffer only when neither the solver nor the poller
 // can still use it).  Arrays are stored [.][lane] (conflict-free).
 constexpr int kMaxPoll = 16;  // pending (entry, column) values tracked per row
+// Sibling segments (earlier segments of the same sweep in the same CTA) hand values
+// over through shared memory: every solver keeps its last kRing published rows in a
+// tagged ring; a consumer reads tag, value, tag (the producer invalidates the tag
+// before rewriting a slot), and falls back to global memory when the row has already
+// left the ring.  K = 1 only.
+constexpr int kRing = 64;
+constexpr int32_t kProductTerm = -1;  // term whose product a * x is precomputed (K = 1)
+constexpr int kSibling = 4;  // entry class: pending value of a sibling segment
 
 template <int K>
 struct GsBuf {
@@ -121,12 +129,46 @@ struct GsBuf {
 
 template <int K>
 constexpr int gs_segs_per_cta() {
-    return K <= 3 ? 2 : 1;
+    return K == 1 ? 4 : (K <= 3 ? 2 : 1);
+}
+
+template <int K>
+constexpr size_t gs_ring_offset() {
+    return (2 * sizeof(GsBuf<K>) + 64 * K * sizeof(double) + 15) / 16 * 16;
 }
 
 template <int K>
 constexpr size_t gs_seg_bytes() {
-    return (2 * sizeof(GsBuf<K>) + 64 * K * sizeof(double) + 15) / 16 * 16;
+    return gs_ring_offset<K>() + (K == 1 ? kRing * (sizeof(double) + sizeof(int32_t)) : 0);
+}
+
+struct GsRing {
+    double* val;
+    int32_t* tag;
+};
+
+template <int K>
+__device__ __forceinline__ GsRing gs_ring(unsigned char* smem_base, int w) {
+    unsigned char* r = smem_base + static_cast<size_t>(w) * gs_seg_bytes<K>() + gs_ring_offset<K>();
+    return {reinterpret_cast<double*>(r), reinterpret_cast<int32_t*>(r + kRing * sizeof(double))};
+}
+
+// value of row qj of a sibling segment: from its ring, or (already overwritten) from global
+__device__ __forceinline__ unsigned long long sibling_value(const GsRing& rg, int32_t qj, const double* gaddr,
+                                                            unsigned max_ns) {
+    const int idx = qj & (kRing - 1);
+    // tag, value, tag (volatile shared loads; the producer fences between its stores)
+    while (true) {
+        const int32_t t1 = vload(&rg.tag[idx]);
+        if (t1 == qj) {
+            const unsigned long long v = vload(reinterpret_cast<const unsigned long long*>(&rg.val[idx]));
+            if (vload(&rg.tag[idx]) == qj) return v;
+        } else if (t1 > qj) {
+            break;
+        }
+        __nanosleep(20);
+    }
+    return static_cast<unsigned long long>(__double_as_longlong(wait_bits(gaddr, load_relaxed_bits(gaddr), max_ns)));
 }
 
 template <int K>
@@ -141,12 +183,30 @@ __global__ void __launch_bounds__(3 * gs_segs_per_cta<K>() * 32)
     extern __shared__ unsigned long long smem[];
     __shared__ unsigned int blk;
     __shared__ int sh_ready[S][2], sh_done[S], sh_step[S], sh_plo[S];
+    __shared__ int32_t sh_sq0[S], sh_sq1[S], sh_ss[S];  // every segment of the CTA: q0, q1, sweep
     if (threadIdx.x == 0) blk = atomicAdd(ticket, 1u);
     if (threadIdx.x < S) {
         sh_ready[threadIdx.x][0] = sh_ready[threadIdx.x][1] = -1;
         sh_done[threadIdx.x] = -1;
         sh_step[threadIdx.x] = 0;
         sh_plo[threadIdx.x] = 0;
+    }
+    if (K == 1)
+        for (int e = threadIdx.x; e < S * kRing; e += blockDim.x)
+            gs_ring<K>(reinterpret_cast<unsigned char*>(smem), e / kRing).tag[e % kRing] = -1;
+    __syncthreads();
+    if (threadIdx.x < S) {
+        const int32_t it2 = static_cast<int32_t>(blk) * S + threadIdx.x;
+        sh_ss[threadIdx.x] = -1;
+        sh_sq0[threadIdx.x] = sh_sq1[threadIdx.x] = 0;
+        if (it2 < item_base[nsweeps]) {
+            int s2 = 0;
+            while (it2 >= item_base[s2 + 1]) ++s2;
+            const int32_t* sg = backward[s2] ? seg_bwd : seg_fwd;
+            sh_ss[threadIdx.x] = s2;
+            sh_sq0[threadIdx.x] = sg[it2 - item_base[s2]];
+            sh_sq1[threadIdx.x] = sg[it2 - item_base[s2] + 1];
+        }
     }
     __syncthreads();
     const int lane = threadIdx.x & 31;
@@ -255,7 +315,18 @@ __global__ void __launch_bounds__(3 * gs_segs_per_cta<K>() * 32)
                         if (cls[u] >= kReady) {
                             const int e = e0 + u;
                             B.bits[e][c][lane] = xv[u];
-                            if (xv[u] == kPending) {
+                            int sw = -1;
+                            if (K == 1 && xv[u] == kPending && cls[u] == kPoll) {
+                                const int32_t qj = bwd ? n - 1 - jj[u] : jj[u];
+                                // an earlier segment of this sweep in this CTA
+                                for (int w2 = 0; w2 < wl; ++w2)
+                                    if (sh_ss[w2] == s && qj >= sh_sq0[w2] && qj < sh_sq1[w2]) sw = w2;
+                                if (sw >= 0) {
+                                    cls[u] = kSibling;
+                                    xslot[u] = ((qj - sh_sq0[sw]) << 2) | sw;
+                                }
+                            }
+                            if (xv[u] == kPending && sw < 0) {
                                 if (np < kMaxPoll) {
                                     const int32_t j = jj[u];
                                     const int32_t qj = bwd ? n - 1 - j : j;
@@ -273,7 +344,7 @@ __global__ void __launch_bounds__(3 * gs_segs_per_cta<K>() * 32)
                 for (int u = 0; u < kChunk; ++u) {
                     if (e0 + u < ne) {
                         B.ta[e0 + u][lane] = aa[u];
-                        B.toff[e0 + u][lane] = cls[u] | (xslot[u] << 2);
+                        B.toff[e0 + u][lane] = cls[u] | (xslot[u] << 3);
                     }
                 }
             }
@@ -283,11 +354,11 @@ __global__ void __launch_bounds__(3 * gs_segs_per_cta<K>() * 32)
             int nt = 0;
             for (int e = 0; e < ne; ++e) {
                 const int code = B.toff[e][lane];
-                const int cl = code & 3;
+                const int cl = code & 7;
                 if (cl == kSelf) continue;
                 const double ae = B.ta[e][lane];
                 if (!stopped) {
-                    bool pending = cl == kInBlock;
+                    bool pending = cl == kInBlock || cl == kSibling;
 #pragma unroll
                     for (int c = 0; c < K; ++c) pending = pending || B.bits[e][c][lane] == kPending;
                     stopped = pending;
@@ -297,9 +368,16 @@ __global__ void __launch_bounds__(3 * gs_segs_per_cta<K>() * 32)
                     for (int c = 0; c < K; ++c)
                         acc[c] -= ae * __longlong_as_double(static_cast<long long>(B.bits[e][c][lane]));
                 } else {
-                    B.ta[nt][lane] = ae;
-                    B.toff[nt][lane] =
-                        cl == kInBlock ? (code >> 2) : buf_off + static_cast<int32_t>(8 * (e * K * 32 + lane));
+                    // slot offset; a sibling term is -2 - ((row - sibling q0) << 2 | sibling);
+                    // K = 1 values known now become product terms (kProductTerm, ta = a * x:
+                    // the reference's acc - (a * x) with the product rounded first)
+                    const bool known = K == 1 && cl != kInBlock && cl != kSibling && B.bits[e][0][lane] != kPending;
+                    B.ta[nt][lane] =
+                        known ? ae * __longlong_as_double(static_cast<long long>(B.bits[e][0][lane])) : ae;
+                    B.toff[nt][lane] = known            ? kProductTerm
+                                       : cl == kInBlock  ? (code >> 3)
+                                       : cl == kSibling ? -2 - (code >> 3)
+                                                        : buf_off + static_cast<int32_t>(8 * (e * K * 32 + lane));
                     ++nt;
                 }
             }
@@ -395,12 +473,30 @@ __global__ void __launch_bounds__(3 * gs_segs_per_cta<K>() * 32)
 #pragma unroll 4
                 for (int32_t k = 0; k < nt; ++k) {
                     const double ak = B.ta[k][t];
-                    const unsigned char* sp = segmem + B.toff[k][t];
+                    const int32_t off = B.toff[k][t];
+                    if (K == 1 && off == kProductTerm) {
+                        acc[0] -= ak;
+                        continue;
+                    }
+                    if (K == 1 && off < 0) {
+                        const int32_t code = -2 - off;
+                        const int sw = code & 3;
+                        const int32_t qj = sh_sq0[sw] + (code >> 2);
+                        const int32_t j = bwd ? n - 1 - qj : qj;
+                        const unsigned long long v =
+                            sibling_value(gs_ring<K>(reinterpret_cast<unsigned char*>(smem), sw), qj, &xout[j], max_ns);
+                        acc[0] -= ak * __longlong_as_double(static_cast<long long>(v));
+                        continue;
+                    }
+                    const unsigned char* sp = segmem + off;
 #pragma unroll
                     for (int c = 0; c < K; ++c) {
                         const unsigned long long* slot = reinterpret_cast<const unsigned long long*>(sp) + 32 * c;
                         unsigned long long v = vload(slot);
-                        while (v == kPending) v = vload(slot);
+                        while (v == kPending) {
+                            __nanosleep(20);
+                            v = vload(slot);
+                        }
                         acc[c] -= ak * __longlong_as_double(static_cast<long long>(v));
                     }
                 }
@@ -442,6 +538,17 @@ __global__ void __launch_bounds__(3 * gs_segs_per_cta<K>() * 32)
                     const double xi = acc[c] * dinv_t;
                     const unsigned long long xbits = static_cast<unsigned long long>(__double_as_longlong(xi));
                     vstore(&xb[((seq & 1) * K + c) * 32 + t], xbits);
+                    if (K == 1) {
+                        // own ring first (its fences then cover shared-memory stores only):
+                        // invalidate the slot, write the value, then the tag
+                        const GsRing rg = gs_ring<K>(reinterpret_cast<unsigned char*>(smem), wl);
+                        const int idx = q & (kRing - 1);
+                        vstore(&rg.tag[idx], -1);
+                        __threadfence_block();
+                        vstore(reinterpret_cast<unsigned long long*>(&rg.val[idx]), xbits);
+                        __threadfence_block();
+                        vstore(&rg.tag[idx], q);
+                    }
                     cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> out(
                         *reinterpret_cast<unsigned long long*>(&xout[static_cast<size_t>(c) * n + i]));
                     out.store(xbits, cuda::memory_order_relaxed);
