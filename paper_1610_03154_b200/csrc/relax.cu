@@ -111,6 +111,8 @@ constexpr int kMaxPoll = 16;  // pending (entry, column) values tracked per row
 // before rewriting a slot), and falls back to global memory when the row has already
 // left the ring.  K = 1 only.
 constexpr int kRing = 64;
+constexpr int kShortSegment = 8;
+constexpr unsigned kWarpRowPollNs = 32;  // poll back-off cap of the warp-per-row kernel  // mean segment length below which the warp-per-row kernel is used
 constexpr int32_t kProductTerm = -1;  // term whose product a * x is precomputed (K = 1)
 constexpr int kSibling = 4;  // entry class: pending value of a sibling segment
 
@@ -568,6 +570,117 @@ __global__ void __launch_bounds__(3 * gs_segs_per_cta<K>() * 32)
     }
 }
 
+// Warp per row for levels whose segments are short (coarse operators: the i-1
+// chains break every row or two, so a segment's three warps have nothing to
+// pipeline).  Items (sweep, position) draw tickets in order, one warp each; the
+// lanes load the row's entries and poll their values in parallel (the previous
+// sweep's for later rows, this sweep's for earlier ones), form the products
+// a * x, and lane 0 subtracts them from b in CSR order -- the reference's row.
+constexpr int kWrWarps = 8;
+
+template <int K>
+__device__ __forceinline__ void gs_warp_row(int32_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                            const double* __restrict__ va, const double* __restrict__ inv_diag,
+                                            const double* __restrict__ b, int s, int32_t q, bool bwd,
+                                            double* __restrict__ X, unsigned max_ns) {
+    const int lane = threadIdx.x & 31;
+    const int32_t i = bwd ? n - 1 - q : q;
+    const size_t stride = static_cast<size_t>(n) * K;
+    const double* xin = X + static_cast<size_t>(s) * stride;
+    double* xout = X + static_cast<size_t>(s + 1) * stride;
+    double acc[K];
+#pragma unroll
+    for (int c = 0; c < K; ++c) acc[c] = b ? b[static_cast<size_t>(c) * n + i] : 0.0;
+    const int32_t lo = rp[i], hi = rp[i + 1];
+    for (int32_t e0 = lo; e0 < hi; e0 += 32) {
+        const int32_t p = e0 + lane;
+        const bool act = p < hi;
+        int32_t j = i;
+        double a = 0.0;
+        if (act) {
+            j = ci[p];
+            a = va[p];
+        }
+        const bool use = act && j != i;
+        double prod[K];
+#pragma unroll
+        for (int c = 0; c < K; ++c) {
+            unsigned long long v = 0ull;
+            const double* addr = nullptr;
+            if (use) {
+                const int32_t qj = bwd ? n - 1 - j : j;
+                addr = &((qj < q) ? xout : xin)[static_cast<size_t>(c) * n + j];
+                v = (qj >= q && s == 0) ? static_cast<unsigned long long>(__double_as_longlong(__ldcg(addr)))
+                                        : load_relaxed_bits(addr);
+            }
+            unsigned ns = 8;
+            while (__any_sync(0xffffffffu, use && v == kPending)) {
+                if (use && v == kPending) {
+                    __nanosleep(ns);
+                    v = load_relaxed_bits(addr);
+                }
+                ns = ns < max_ns ? 2 * ns : max_ns;
+            }
+            prod[c] = use ? a * __longlong_as_double(static_cast<long long>(v)) : 0.0;
+        }
+        // ordered subtraction by lane 0 (CSR order; the diagonal is skipped)
+        const unsigned um = __ballot_sync(0xffffffffu, use);
+#pragma unroll
+        for (int c = 0; c < K; ++c) {
+            for (unsigned m = um; m; m &= m - 1) {
+                const double pr = __shfl_sync(0xffffffffu, prod[c], __ffs(m) - 1);
+                acc[c] -= pr;
+            }
+        }
+    }
+    if (lane == 0) {
+        const double d = inv_diag[i];
+#pragma unroll
+        for (int c = 0; c < K; ++c) {
+            cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> out(
+                *reinterpret_cast<unsigned long long*>(&xout[static_cast<size_t>(c) * n + i]));
+            out.store(static_cast<unsigned long long>(__double_as_longlong(acc[c] * d)), cuda::memory_order_relaxed);
+        }
+    }
+}
+
+// kRowMajor (forward sweeps only): a warp owns one row and relaxes it in every
+// sweep in turn (tickets in row order); sweep s + 1 of row q waits on sweep s of
+// rows at most the bandwidth ahead, so the launcher uses it only when the
+// bandwidth is well below the number of resident warps.  Otherwise items are
+// (sweep, position) in sweep-major order.
+template <int K, bool kRowMajor>
+__global__ void __launch_bounds__(kWrWarps * 32)
+    k_gs_warp_rows(int32_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                   const double* __restrict__ va, const double* __restrict__ inv_diag, const double* __restrict__ b,
+                   int nsweeps, const unsigned char* __restrict__ backward, double* __restrict__ X,
+                   unsigned int* __restrict__ ticket, unsigned max_ns) {
+    __shared__ unsigned int blk;
+    if (threadIdx.x == 0) blk = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const int64_t item = static_cast<int64_t>(blk) * kWrWarps + threadIdx.x / 32;
+    if (kRowMajor) {
+        if (item >= n) return;
+        for (int s = 0; s < nsweeps; ++s) gs_warp_row<K>(n, rp, ci, va, inv_diag, b, s, static_cast<int32_t>(item),
+                                                         false, X, max_ns);
+    } else {
+        if (item >= static_cast<int64_t>(nsweeps) * n) return;
+        const int s = static_cast<int>(item / n);
+        gs_warp_row<K>(n, rp, ci, va, inv_diag, b, s, static_cast<int32_t>(item - static_cast<int64_t>(s) * n),
+                       backward[s] != 0, X, max_ns);
+    }
+}
+
+// max |i - j| over the stored entries
+__global__ void k_bandwidth(int32_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                            int32_t* __restrict__ bw) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int32_t m = 0;
+    for (int32_t p = rp[i]; p < rp[i + 1]; ++p) m = max(m, abs(ci[p] - i));
+    atomicMax(bw, m);
+}
+
 // segment heads in sweep order: position q starts a segment unless row(q)
 // holds column row(q - 1)
 __global__ void k_segment_heads(int32_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci, bool bwd,
@@ -673,6 +786,48 @@ void gauss_seidel(Ctx& c, const DCsr& A, const double* inv_diag, double* x, cons
     copy_h2d(c, dbase.get(), base.data(), nsw + 1);
     DBuf<unsigned int> ticket(1, c.s);
     AMG_CK(cudaMemsetAsync(ticket.get(), 0, sizeof(unsigned int), c.s));
+    // short segments (coarse levels): warp per row
+    const int32_t nseg_max = std::max(nf, nb);
+    // AMGCU_GS_WARPROWS=1 forces the warp-per-row kernel (comparison runs)
+    const char* wr_env = std::getenv("AMGCU_GS_WARPROWS");
+    const bool force_wr = wr_env && wr_env[0] == '1';
+    if ((force_wr || static_cast<int64_t>(nseg_max) * kShortSegment > n) && !std::getenv("AMGCU_GS_TRACE")) {
+        const double bytes = nsw * (12.0 * A.nnz + 4.0 * (n + 1) + 8.0 * n + 16.0 * n * k);
+        // forward sweeps whose stale dependencies stay within the resident window: row-major
+        bool row_major = false;
+        if (!symmetric_sweep && nsw > 1) {
+            DBuf<int32_t> bwd_max(1, c.s);
+            AMG_CK(cudaMemsetAsync(bwd_max.get(), 0, sizeof(int32_t), c.s));
+            launch(c, k_bandwidth, blocks_for(n, 256), 256, 0, n, A.rp.get(), A.ci.get(), bwd_max.get());
+            const int32_t bwidth = read_scalar(c, bwd_max.get());
+            int per_sm = 0;
+            AMG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gs_warp_rows<1, true>, kWrWarps * 32, 0));
+            const int64_t resident_warps = static_cast<int64_t>(per_sm) * c.sms * kWrWarps;
+            row_major = 2 * static_cast<int64_t>(bwidth) + 2 * kWrWarps < resident_warps;
+        }
+        const int64_t items = row_major ? n : static_cast<int64_t>(nsw) * n;
+        const unsigned grid = static_cast<unsigned>((items + kWrWarps - 1) / kWrWarps);
+        auto runw = [&](auto kern) {
+            launch_prof(c, kProfGaussSeidel, bytes, kern, grid, kWrWarps * 32, 0, n, A.rp.get(), A.ci.get(),
+                        A.va.get(), inv_diag, b, nsw, static_cast<const unsigned char*>(bwd.get()), X.get(),
+                        ticket.get(), std::min(gs_max_ns(), kWarpRowPollNs));
+        };
+#define AMGCU_WR(KK) (row_major ? runw(k_gs_warp_rows<KK, true>) : runw(k_gs_warp_rows<KK, false>))
+        switch (k) {
+            case 1: AMGCU_WR(1); break;
+            case 2: AMGCU_WR(2); break;
+            case 3: AMGCU_WR(3); break;
+            case 4: AMGCU_WR(4); break;
+            case 5: AMGCU_WR(5); break;
+            case 6: AMGCU_WR(6); break;
+            case 7: AMGCU_WR(7); break;
+            default: AMGCU_WR(8); break;
+        }
+#undef AMGCU_WR
+        copy_d2d(c, x, X.get() + stride * nsw, static_cast<int64_t>(stride));
+        sync(c);
+        return;
+    }
     // AMGCU_GS_TRACE=<file>: per (sweep, block) globaltimer stamps for the timeline tool
     const char* trace_path = std::getenv("AMGCU_GS_TRACE");
     DBuf<unsigned long long> trace;

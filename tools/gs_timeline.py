@@ -47,6 +47,8 @@ segs = np.frombuffer(raw[12:12 + 4 * (nf + 1)], np.int32)
 tr = np.frombuffer(raw[12 + 4 * (nf + 1):], np.uint64).reshape(nsw, n, 4).astype(np.int64)
 t0 = tr[tr > 0].min()
 print(f"n {n} sweeps {nsw} segments {nf} (mean len {n / nf:.1f})")
+allb = tr[:, :, 2][tr[:, :, 0] > 0]
+print(f"launch span {(allb.max() - t0) / 1e3:.1f} us (first block start to last block end, all sweeps)")
 for s in range(nsw):
     m = tr[s, :, 0] > 0
     blk = tr[s][m] - t0
