@@ -156,16 +156,16 @@ __device__ __forceinline__ GsRing gs_ring(unsigned char* smem_base, int w) {
 }
 
 // value of row qj of a sibling segment: from its ring, or (already overwritten) from global
-__device__ __forceinline__ unsigned long long sibling_value(const GsRing& rg, int32_t qj, const double* gaddr,
-                                                            unsigned max_ns) {
+__device__ __forceinline__ unsigned long long sibling_value(const GsRing& rg, int32_t qj, int32_t tagv,
+                                                            const double* gaddr, unsigned max_ns) {
     const int idx = qj & (kRing - 1);
     // tag, value, tag (volatile shared loads; the producer fences between its stores)
     while (true) {
         const int32_t t1 = vload(&rg.tag[idx]);
-        if (t1 == qj) {
+        if (t1 == tagv) {
             const unsigned long long v = vload(reinterpret_cast<const unsigned long long*>(&rg.val[idx]));
-            if (vload(&rg.tag[idx]) == qj) return v;
-        } else if (t1 > qj) {
+            if (vload(&rg.tag[idx]) == tagv) return v;
+        } else if (t1 > tagv) {
             break;
         }
         __nanosleep(20);
@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(3 * gs_segs_per_cta<K>() * 32)
                   int nsweeps, const unsigned char* __restrict__ backward, const int32_t* __restrict__ item_base,
                   const int32_t* __restrict__ seg_fwd, const int32_t* __restrict__ seg_bwd, double* __restrict__ X,
                   unsigned int* __restrict__ ticket, unsigned max_ns, unsigned long long* __restrict__ trace,
-                  int poll_window) {
+                  int poll_window, int sweep_loop) {
     constexpr int S = gs_segs_per_cta<K>();
     extern __shared__ unsigned long long smem[];
     __shared__ unsigned int blk;
@@ -197,11 +197,18 @@ __global__ void __launch_bounds__(3 * gs_segs_per_cta<K>() * 32)
         for (int e = threadIdx.x; e < S * kRing; e += blockDim.x)
             gs_ring<K>(reinterpret_cast<unsigned char*>(smem), e / kRing).tag[e % kRing] = -1;
     __syncthreads();
+    // sweep_loop (forward sweeps): items are the segments of sweep 0 and every segment
+    // runs all sweeps in turn; otherwise items are (sweep, segment) in sweep-major order
+    const int32_t nitems = sweep_loop ? item_base[1] : item_base[nsweeps];
     if (threadIdx.x < S) {
         const int32_t it2 = static_cast<int32_t>(blk) * S + threadIdx.x;
         sh_ss[threadIdx.x] = -1;
         sh_sq0[threadIdx.x] = sh_sq1[threadIdx.x] = 0;
-        if (it2 < item_base[nsweeps]) {
+        if (sweep_loop && it2 < nitems) {
+            sh_ss[threadIdx.x] = 0;
+            sh_sq0[threadIdx.x] = seg_fwd[it2];
+            sh_sq1[threadIdx.x] = seg_fwd[it2 + 1];
+        } else if (!sweep_loop && it2 < nitems) {
             int s2 = 0;
             while (it2 >= item_base[s2 + 1]) ++s2;
             const int32_t* sg = backward[s2] ? seg_bwd : seg_fwd;
@@ -216,17 +223,19 @@ __global__ void __launch_bounds__(3 * gs_segs_per_cta<K>() * 32)
     const int role = warp / S;  // 0 solver, 1 poller, 2 prefetcher
     const int wl = warp % S;
     const int32_t item = static_cast<int32_t>(blk) * S + wl;
-    if (item >= item_base[nsweeps]) return;
-    int s = 0;
-    while (item >= item_base[s + 1]) ++s;
-    const bool bwd = backward[s] != 0;
+    if (item >= nitems) return;
+    int s_first = 0;
+    if (!sweep_loop)
+        while (item >= item_base[s_first + 1]) ++s_first;
+    const int s_item = sweep_loop ? 0 : s_first;  // sweep tag of the CTA segment table
+    const int nsw_loop = sweep_loop ? nsweeps : 1;
+    const bool bwd = backward[s_first] != 0;
     const int32_t* segs = bwd ? seg_bwd : seg_fwd;
-    const int32_t g = item - item_base[s];
+    const int32_t g = item - (sweep_loop ? 0 : item_base[s_first]);
     const int32_t q0 = segs[g], q1 = segs[g + 1];
     const int nblocks = (q1 - q0 + 31) / 32;
+    const int tblocks = nsw_loop * nblocks;  // hand-shake sequence numbers run over all sweeps
     const size_t stride = static_cast<size_t>(n) * K;
-    const double* xin = X + static_cast<size_t>(s) * stride;
-    double* xout = X + static_cast<size_t>(s + 1) * stride;
     unsigned char* segmem = reinterpret_cast<unsigned char*>(smem) + static_cast<size_t>(wl) * gs_seg_bytes<K>();
     GsBuf<K>* buf = reinterpret_cast<GsBuf<K>*>(segmem);
     // values published by the solver: xb[block & 1][c][lane]
@@ -235,12 +244,15 @@ __global__ void __launch_bounds__(3 * gs_segs_per_cta<K>() * 32)
 
     if (role == 2) {
         // ---------------- prefetcher ----------------
-        for (int seq = 0; seq < nblocks; ++seq) {
-            if (seq >= 2)
-                while (vload(&sh_done[wl]) < seq - 2 || vload(&sh_plo[wl]) < seq - 1) __nanosleep(32);
+        for (int G = 0; G < tblocks; ++G) {
+            const int s = s_first + G / nblocks, seq = G % nblocks;
+            const double* xin = X + static_cast<size_t>(s) * stride;
+            const double* xout = X + static_cast<size_t>(s + 1) * stride;
+            if (G >= 2)
+                while (vload(&sh_done[wl]) < G - 2 || vload(&sh_plo[wl]) < G - 1) __nanosleep(32);
             __threadfence_block();
-            GsBuf<K>& B = buf[seq & 1];
-            const int32_t buf_off = static_cast<int32_t>((seq & 1) * sizeof(GsBuf<K>));
+            GsBuf<K>& B = buf[G & 1];
+            const int32_t buf_off = static_cast<int32_t>((G & 1) * sizeof(GsBuf<K>));
             const int32_t qb = q0 + 32 * seq;
             const int32_t q = qb + lane;
             const bool active = q < q1;
@@ -322,7 +334,7 @@ __global__ void __launch_bounds__(3 * gs_segs_per_cta<K>() * 32)
                                 const int32_t qj = bwd ? n - 1 - jj[u] : jj[u];
                                 // an earlier segment of this sweep in this CTA
                                 for (int w2 = 0; w2 < wl; ++w2)
-                                    if (sh_ss[w2] == s && qj >= sh_sq0[w2] && qj < sh_sq1[w2]) sw = w2;
+                                    if (sh_ss[w2] == s_item && qj >= sh_sq0[w2] && qj < sh_sq1[w2]) sw = w2;
                                 if (sw >= 0) {
                                     cls[u] = kSibling;
                                     xslot[u] = ((qj - sh_sq0[sw]) << 2) | sw;
@@ -390,7 +402,7 @@ __global__ void __launch_bounds__(3 * gs_segs_per_cta<K>() * 32)
             B.npoll[lane] = slow ? 0 : np;
             __syncwarp();
             __threadfence_block();
-            if (lane == 0) vstore(&sh_ready[wl][seq & 1], seq);
+            if (lane == 0) vstore(&sh_ready[wl][G & 1], G);
         }
         return;
     }
@@ -403,7 +415,7 @@ __global__ void __launch_bounds__(3 * gs_segs_per_cta<K>() * 32)
         unsigned long long* bits_base[2] = {&buf[0].bits[0][0][0], &buf[1].bits[0][0][0]};
         while (true) {
             const int cur = vload(&sh_done[wl]) + 1;
-            if (cur >= nblocks) break;
+            if (cur >= tblocks) break;
             vstore(&sh_plo[wl], cur);
             __threadfence_block();
             const int step = vload(&sh_step[wl]);
@@ -412,12 +424,12 @@ __global__ void __launch_bounds__(3 * gs_segs_per_cta<K>() * 32)
             for (int h = 0; h < 2; ++h) {
                 const int bq = cur + h;
                 const int sl = bq & 1;
-                if (bq >= nblocks) continue;
+                if (bq >= tblocks) continue;
                 if (mblk[sl] != bq) {
                     if (vload(&sh_ready[wl][sl]) != bq) continue;
                     __threadfence_block();
                     mblk[sl] = bq;
-                    const int np = q0 + 32 * bq + lane < q1 ? buf[sl].npoll[lane] : 0;
+                    const int np = q0 + 32 * (bq % nblocks) + lane < q1 ? buf[sl].npoll[lane] : 0;
                     mask[sl] = np >= 32 ? 0xffffffffu : ((1u << np) - 1u);
                 }
                 const int rel = h * 32 + lane - step;  // rows ahead of the solver
@@ -450,16 +462,19 @@ __global__ void __launch_bounds__(3 * gs_segs_per_cta<K>() * 32)
     }
 
     // ---------------- solver ----------------
-    for (int seq = 0; seq < nblocks; ++seq) {
+    for (int G = 0; G < tblocks; ++G) {
+        const int s = s_first + G / nblocks, seq = G % nblocks;
+        const double* xin = X + static_cast<size_t>(s) * stride;
+        double* xout = X + static_cast<size_t>(s + 1) * stride;
         const int32_t qb = q0 + 32 * seq;
         unsigned long long* tr = trace ? trace + (static_cast<size_t>(s) * n + qb) * 4 : nullptr;
         if (tr && lane == 0) tr[0] = globaltimer_ns();
         // this block's xb slots become pending (the previous block's stay readable)
 #pragma unroll
         for (int c = 0; c < K; ++c) xb[((seq & 1) * K + c) * 32 + lane] = kPending;
-        while (vload(&sh_ready[wl][seq & 1]) != seq) __nanosleep(32);
+        while (vload(&sh_ready[wl][G & 1]) != G) __nanosleep(32);
         __threadfence_block();
-        GsBuf<K>& B = buf[seq & 1];
+        GsBuf<K>& B = buf[G & 1];
         if (tr && lane == 0) tr[1] = globaltimer_ns();
         // ---- phase B, warp-uniform: every lane evaluates row t from broadcast reads of
         // its records (no divergence, no reconvergence barriers); lane 0 publishes ----
@@ -486,7 +501,8 @@ __global__ void __launch_bounds__(3 * gs_segs_per_cta<K>() * 32)
                         const int32_t qj = sh_sq0[sw] + (code >> 2);
                         const int32_t j = bwd ? n - 1 - qj : qj;
                         const unsigned long long v =
-                            sibling_value(gs_ring<K>(reinterpret_cast<unsigned char*>(smem), sw), qj, &xout[j], max_ns);
+                            sibling_value(gs_ring<K>(reinterpret_cast<unsigned char*>(smem), sw), qj,
+                                          s * n + qj, &xout[j], max_ns);
                         acc[0] -= ak * __longlong_as_double(static_cast<long long>(v));
                         continue;
                     }
@@ -549,7 +565,7 @@ __global__ void __launch_bounds__(3 * gs_segs_per_cta<K>() * 32)
                         __threadfence_block();
                         vstore(reinterpret_cast<unsigned long long*>(&rg.val[idx]), xbits);
                         __threadfence_block();
-                        vstore(&rg.tag[idx], q);
+                        vstore(&rg.tag[idx], s * n + q);
                     }
                     cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> out(
                         *reinterpret_cast<unsigned long long*>(&xout[static_cast<size_t>(c) * n + i]));
@@ -565,7 +581,7 @@ __global__ void __launch_bounds__(3 * gs_segs_per_cta<K>() * 32)
         __threadfence_block();
         if (lane == 0) {
             vstore(&sh_step[wl], 0);
-            vstore(&sh_done[wl], seq);
+            vstore(&sh_done[wl], G);
         }
     }
 }
@@ -845,11 +861,35 @@ void gauss_seidel(Ctx& c, const DCsr& A, const double* inv_diag, double* x, cons
         const size_t smem = std::max(seg_bytes * segs, smem_floor);
         if (smem > 48 * 1024)
             AMG_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        launch_prof(c, kProfGaussSeidel, bytes, kern, blocks_for(base[nsw], segs), 3 * segs * 32, smem, n,
+        // Forward sweeps run segment-major (each segment relaxes all sweeps in turn) when
+        // sweep s + 1 of a segment can only wait on segments that are already resident:
+        // the ones reached within the bandwidth must lie inside the resident window.
+        int sweep_loop = 0;
+        const char* sl_env = std::getenv("AMGCU_GS_SWEEP_LOOP");
+        if (!symmetric_sweep && nsw > 1 && !(sl_env && sl_env[0] == '0')) {
+            DBuf<int32_t> bw_max(1, c.s);
+            AMG_CK(cudaMemsetAsync(bw_max.get(), 0, sizeof(int32_t), c.s));
+            launch(c, k_bandwidth, blocks_for(n, 256), 256, 0, n, A.rp.get(), A.ci.get(), bw_max.get());
+            std::vector<int32_t> hs(static_cast<size_t>(nf) + 1);
+            copy_d2h(c, hs.data(), segf.get(), nf + 1);
+            const int32_t bwidth = read_scalar(c, bw_max.get());
+            int64_t ahead = 0;
+            for (int32_t g2 = 0; g2 < nf; ++g2) {
+                const int64_t reach = static_cast<int64_t>(hs[g2 + 1]) + bwidth;
+                const int64_t last = std::upper_bound(hs.begin(), hs.end(), reach) - hs.begin() - 1;
+                ahead = std::max<int64_t>(ahead, last - g2);
+            }
+            int per_sm = 0;
+            AMG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 3 * segs * 32, smem));
+            const int64_t resident = static_cast<int64_t>(per_sm) * c.sms * segs;
+            sweep_loop = 2 * (ahead + segs) < resident ? 1 : 0;
+        }
+        const int32_t items = sweep_loop ? nf : base[nsw];
+        launch_prof(c, kProfGaussSeidel, bytes, kern, blocks_for(items, segs), 3 * segs * 32, smem, n,
                     A.rp.get(), A.ci.get(), A.va.get(), inv_diag, b, nsw, static_cast<const unsigned char*>(bwd.get()),
                     static_cast<const int32_t*>(dbase.get()), static_cast<const int32_t*>(segf.get()),
                     static_cast<const int32_t*>(symmetric_sweep ? segb.get() : segf.get()), X.get(), ticket.get(),
-                    gs_max_ns(), trace.get(), gs_poll_window());
+                    gs_max_ns(), trace.get(), gs_poll_window(), sweep_loop);
     };
 #define AMGCU_GS_RUN(KK) run(k_gs_segments<KK>, gs_segs_per_cta<KK>(), gs_seg_bytes<KK>())
     switch (k) {
