@@ -14,6 +14,7 @@
 // member is a host mirror filled on demand by Hierarchy::download().
 #pragma once
 
+#include <array>
 #include <cmath>
 #include <cstdint>
 #include <memory>
@@ -215,6 +216,22 @@ inline amgcu_setup_options flatten(const SetupOptions& o) {
 
 }  // namespace b200
 
+// Cumulative cost ledger in work units (work.hpp:27-67): raw op counts / nnz(A_0).
+enum class WorkBucket : int { aggregation = 0, candidates = 1, interp = 2, rap = 3, solve_other = 4 };
+
+struct WorkLedger {
+    double base_nnz = 0.0;
+    std::array<double, 5> wu{};
+    bool active() const { return base_nnz > 0.0; }
+    double operator[](WorkBucket b) const { return wu[static_cast<int>(b)]; }
+    double setup_total() const { return wu[0] + wu[1] + wu[2] + wu[3]; }
+    double total() const {
+        double t = 0.0;
+        for (double v : wu) t += v;
+        return t;
+    }
+};
+
 // Device-resident hierarchy (hierarchy.hpp:80-91).
 struct Hierarchy {
     std::shared_ptr<amgcu_hier_s> handle;
@@ -226,6 +243,19 @@ struct Hierarchy {
         int32_t n = 0, s = 0;
         b200::check(amgcu_hier_levels(handle.get(), &n, &s), b200::default_ctx());
         return n;
+    }
+    // the hierarchy's WorkLedger (the reference's Hierarchy::ledger, charged by setup and
+    // every solve); the evolution-SOC part is counted on the first call
+    WorkLedger ledger() const {
+        WorkLedger w;
+        b200::check(amgcu_hier_ledger(handle.get(), w.wu.data()), b200::default_ctx());
+        int32_t n = 0, s = 0;
+        b200::check(amgcu_hier_levels(handle.get(), &n, &s), b200::default_ctx());
+        amgcu_csr a0{};
+        b200::check(amgcu_hier_get_matrix(handle.get(), 0, 0, &a0), b200::default_ctx());
+        w.base_nnz = static_cast<double>(a0.nnz);
+        amgcu_csr_free(&a0);
+        return w;
     }
     // copy every level's A, P, R, B, Bc to the host mirror (untimed diagnostics)
     void download() {

@@ -172,6 +172,10 @@ amgcu_status amgcu_hier_level_symmetric(amgcu_hier h, int32_t level, int32_t* sy
 amgcu_status amgcu_hier_relax_weights(amgcu_hier h, int32_t level, double* pre, double* post);
 /* chi_OC / chi_CC (complexity.hpp:15-36) */
 amgcu_status amgcu_hier_complexity(amgcu_hier h, double* chi_oc, double* chi_cc);
+/* WorkLedger work units (work.hpp:38-67): wu5 = {aggregation, candidates, interpolation,
+ * RAP, solve (finalize + every solve so far)}, each as op counts / nnz(A_0).  The
+ * evolution-SOC count is taken on the first call (one counting pass per level). */
+amgcu_status amgcu_hier_ledger(amgcu_hier h, double* wu5);
 
 /* amg::solve(h, b, x, opts) — cycle.hpp:114-271.  x is in/out (n doubles;
  * used as the initial guess).  history receives up to history_cap residual

@@ -27,7 +27,7 @@ lib.amgcu_last_error.argtypes = [C.c_void_p]
 for _name in ("amgcu_ctx_create", "amgcu_ctx_destroy", "amgcu_ctx_set_sequential_reductions", "amgcu_ctx_synchronize",
               "amgcu_ctx_launch_count", "amgcu_ctx_sync_count", "amgcu_setup", "amgcu_setup_device", "amgcu_hier_destroy",
               "amgcu_hier_levels", "amgcu_hier_get_matrix", "amgcu_hier_get_candidates", "amgcu_hier_level_symmetric",
-              "amgcu_hier_relax_weights", "amgcu_hier_complexity", "amgcu_solve", "amgcu_solve_device", "amgcu_cycle",
+              "amgcu_hier_relax_weights", "amgcu_hier_complexity", "amgcu_hier_ledger", "amgcu_solve", "amgcu_solve_device", "amgcu_cycle",
               "amgcu_spmv", "amgcu_transpose", "amgcu_matmul", "amgcu_galerkin_product", "amgcu_filter_matrix",
               "amgcu_is_symmetric", "amgcu_spectral_radius", "amgcu_strength", "amgcu_normalize_strength",
               "amgcu_amalgamate", "amgcu_greedy_aggregate", "amgcu_sparsity_pattern", "amgcu_improve_candidates",
@@ -51,6 +51,7 @@ lib.amgcu_hier_get_candidates.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.PO
 lib.amgcu_hier_level_symmetric.argtypes = [C.c_void_p, C.c_int32, C.POINTER(C.c_int32)]
 lib.amgcu_hier_relax_weights.argtypes = [C.c_void_p, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double)]
 lib.amgcu_hier_complexity.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+lib.amgcu_hier_ledger.argtypes = [C.c_void_p, f64p]
 lib.amgcu_solve.argtypes = [C.c_void_p, f64p, f64p, C.POINTER(SolveOptionsC), C.POINTER(SolveReportC), f64p, C.c_int32]
 lib.amgcu_solve_device.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(SolveOptionsC),
                                    C.POINTER(SolveReportC), f64p, C.c_int32]
@@ -215,6 +216,12 @@ class Hierarchy:
         a, b = C.c_double(), C.c_double()
         self.ctx._chk(lib.amgcu_hier_relax_weights(self.handle, level, C.byref(a), C.byref(b)))
         return a.value, b.value
+
+    def ledger(self) -> np.ndarray:
+        """WorkLedger work units {aggregation, candidates, interpolation, RAP, solve}."""
+        out = np.zeros(5)
+        self.ctx._chk(lib.amgcu_hier_ledger(self.handle, ptr_f64(out)))
+        return out
 
     def complexity(self):
         a, b = C.c_double(), C.c_double()

@@ -76,6 +76,12 @@ def build_lib(force=False, jobs=8, verbose=False):
     if tasks or not os.path.exists(LIB) or force:
         _run([NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-lcudart_static", "-L" + os.path.join(CUDA_HOME, "lib64"), "-lcusolver"])
         os.replace(tmp, LIB)
+    # keep only this build's objects (the cache is content-hashed, stale ones pile up)
+    keep = set(objs)
+    for f in os.listdir(OBJDIR):
+        full = os.path.join(OBJDIR, f)
+        if f.endswith(".o") and full not in keep:
+            os.remove(full)
     return LIB
 
 

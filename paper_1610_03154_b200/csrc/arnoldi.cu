@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(kArnThreads)
 
 }  // namespace
 
-double spectral_radius(Ctx& c, const DCsr& A, int steps, const double* dinv) {
+double spectral_radius(Ctx& c, const DCsr& A, int steps, const double* dinv, int* built_out) {
     if (A.nr != A.nc) throw InvalidArgument("spectral_radius_estimate: square matrix required");
     const int32_t n = A.nr;
     if (n == 0) return 0.0;
@@ -244,6 +244,7 @@ double spectral_radius(Ctx& c, const DCsr& A, int steps, const double* dinv) {
         built = j + 1;
         if (H[static_cast<size_t>(j + 1) * m + j] < 1e-14) break;
     }
+    if (built_out) *built_out = built;
     std::vector<double> Hs(static_cast<size_t>(built) * built), wr(built), wi(built);
     for (int i = 0; i < built; ++i)
         for (int j = 0; j < built; ++j) Hs[i * built + j] = H[i * m + j];

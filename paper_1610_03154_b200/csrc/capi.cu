@@ -341,6 +341,30 @@ amgcu_status amgcu_hier_complexity(amgcu_hier h, double* chi_oc, double* chi_cc)
     });
 }
 
+amgcu_status amgcu_hier_ledger(amgcu_hier h, double* wu5) {
+    return guarded(h->owner, [&] {
+        Ctx& c = h->owner->c;
+        AMG_CK(cudaSetDevice(c.device));
+        DHier& H = *h->h;
+        double wu[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+        for (size_t l = 0; l + 1 < H.lv.size(); ++l) {
+            DLevel& L = H.lv[l];
+            if (L.evo_steps > 0 && L.evo_ops < 0.0) {  // evolution SOC's count, on first request
+                DCsr At;
+                transpose(c, L.A, At);
+                L.evo_ops = evolution_ops(c, L.A, At, L.evo_steps);
+            }
+            // charges in level order, as the reference's coarsening loop (hierarchy.hpp:243)
+            wu[0] += (L.ledger[0] + (L.evo_steps > 0 ? L.evo_ops : 0.0)) / H.base_nnz;
+            wu[1] += L.ledger[1] / H.base_nnz;
+            wu[2] += L.ledger[2] / H.base_nnz;
+            wu[3] += L.ledger[3] / H.base_nnz;
+        }
+        wu[4] = H.wu[4];  // finalize + every solve so far
+        for (int b2 = 0; b2 < 5; ++b2) wu5[b2] = wu[b2];
+    });
+}
+
 amgcu_status amgcu_solve(amgcu_hier h, const double* b, double* x, const amgcu_solve_options* opts,
                          amgcu_solve_report* report, double* history, int32_t history_cap) {
     return guarded(h->owner, [&] {

@@ -114,6 +114,7 @@ struct Ctx {
     int64_t launches = 0;
     int64_t syncs = 0;  // host synchronisations of the stream
     int blas_family = kProfBlas1;  // family the BLAS-1 launchers record under
+    double* ops = nullptr;         // WorkLedger sink of the current setup stage (OpCounter, work.hpp:13-22)
     std::string err;
     DBuf<double> scal;         // device scalars for reductions/control
     DBuf<double> partials;     // per-block partial sums
@@ -135,6 +136,19 @@ inline void ensure_reduction_scratch(Ctx& c, size_t count) {
         AMG_CK(cudaMemsetAsync(c.tickets.get(), 0, sizeof(unsigned int) * 64, c.s));
     }
 }
+
+// WorkLedger: add `v` to the current stage's op count (the reference's count(c, v))
+inline void tally(Ctx& c, double v) {
+    if (c.ops) *c.ops += v;
+}
+
+// routes the op counts of a scope to `sink` (nullptr: not counted)
+struct OpsScope {
+    Ctx& c;
+    double* prev;
+    OpsScope(Ctx& ctx, double* sink) : c(ctx), prev(ctx.ops) { c.ops = sink; }
+    ~OpsScope() { c.ops = prev; }
+};
 
 // routes the BLAS-1 launchers' profile records to `family` for a scope
 struct BlasFamilyScope {

@@ -16,6 +16,12 @@ struct DLevel {
     DBuf<double> Bc;  // n_c x k (coarse-side targets of P)
     bool symmetric = true;
     double rho = std::nan("");  // rho(D^-1 A), cached
+    int rho_built = 0;             // its Arnoldi dimension (the reference's SpMV count per estimate)
+    // WorkLedger raw op counts of coarsening this level (work.hpp buckets 0..3); the
+    // evolution-SOC part of bucket 0 is counted on demand (evo_steps > 0)
+    double ledger[4] = {0.0, 0.0, 0.0, 0.0};
+    int evo_steps = 0;
+    double evo_ops = -1.0;
     // solve phase
     DSell sA, sP, sR;
     DBuf<double> inv_diag;  // 1 / a_ii
@@ -43,6 +49,8 @@ std::unique_ptr<DHier> rn_setup(Ctx& c, const DCsr& A, const double* B, int32_t 
 // relaxation helpers shared by setup and solve
 void require_supported_relax(int scheme, const char* who);
 double level_rho(Ctx& c, DLevel& L);
+// level_rho, counted as one reference call of spectral_radius_estimate (WorkLedger)
+double rho_tallied(Ctx& c, DLevel& L);
 
 // solve phase (cycle.cu)
 void prepare_solve(DHier& h);

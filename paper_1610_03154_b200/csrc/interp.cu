@@ -483,6 +483,84 @@ __global__ void k_root_mask(int32_t nroots, const int32_t* __restrict__ roots, u
     if (j < nroots) mask[roots[j]] = 1;
 }
 
+// ---- WorkLedger counts (computed only when a ledger sink is active) ----------------------
+// masked_product's count (interpolation.hpp:200-206): sum_i sum_{t in A row i} |N_i ∩ N_t|
+__global__ void k_masked_count(int32_t n, const int32_t* __restrict__ arp, const int32_t* __restrict__ aci,
+                               const int32_t* __restrict__ nrp, const int32_t* __restrict__ nci,
+                               unsigned long long* __restrict__ out) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long cnt = 0;
+    if (i < n && nrp[i] < nrp[i + 1]) {
+        const int32_t lo = nrp[i], hi = nrp[i + 1];
+        for (int32_t p = arp[i]; p < arp[i + 1]; ++p) {
+            const int32_t t = aci[p];
+            int32_t a = lo, b = nrp[t];
+            const int32_t be = nrp[t + 1];
+            while (a < hi && b < be) {
+                const int32_t x = nci[a], y = nci[b];
+                if (x == y) {
+                    ++cnt;
+                    ++a;
+                    ++b;
+                } else if (x < y) {
+                    ++a;
+                } else {
+                    ++b;
+                }
+            }
+        }
+    }
+    for (int off = 16; off > 0; off >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
+    if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(out, cnt);
+}
+
+// rows (and their lengths) that are not roots / that are not empty
+__global__ void k_row_census(int32_t n, const int32_t* __restrict__ rp, const unsigned char* __restrict__ is_root,
+                             unsigned long long* __restrict__ out) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long nr = 0, len = 0, ne = 0;
+    if (i < n) {
+        const int32_t l = rp[i + 1] - rp[i];
+        if (!is_root || !is_root[i]) {
+            nr = 1;
+            len = static_cast<unsigned long long>(l);
+        }
+        ne = l > 0 ? 1 : 0;
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+        nr += __shfl_xor_sync(0xffffffffu, nr, off);
+        len += __shfl_xor_sync(0xffffffffu, len, off);
+        ne += __shfl_xor_sync(0xffffffffu, ne, off);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(out, nr);
+        atomicAdd(out + 1, len);
+        atomicAdd(out + 2, ne);
+    }
+}
+
+struct RowCensus {
+    double rows = 0.0, len = 0.0, nonempty = 0.0;
+};
+
+RowCensus row_census(Ctx& c, const DCsr& N, const unsigned char* is_root) {
+    DBuf<unsigned long long> o(3, c.s);
+    AMG_CK(cudaMemsetAsync(o.get(), 0, sizeof(unsigned long long) * 3, c.s));
+    launch(c, k_row_census, blocks_for(N.nr, 256), 256, 0, N.nr, N.rp.get(), is_root, o.get());
+    unsigned long long h[3];
+    copy_d2h(c, h, o.get(), 3);
+    sync(c);
+    return {static_cast<double>(h[0]), static_cast<double>(h[1]), static_cast<double>(h[2])};
+}
+
+double masked_count(Ctx& c, const DCsr& A, const DCsr& N) {
+    DBuf<unsigned long long> o(1, c.s);
+    AMG_CK(cudaMemsetAsync(o.get(), 0, sizeof(unsigned long long), c.s));
+    launch(c, k_masked_count, blocks_for(N.nr, 128), 128, 0, N.nr, A.rp.get(), A.ci.get(), N.rp.get(), N.ci.get(),
+           o.get());
+    return static_cast<double>(read_scalar(c, o.get()));
+}
+
 // ---------------------------------------------------------------------------------------
 // Masked product Y = (A X)|_N (interpolation.hpp:186-210) with the constraint
 // projection (150-182) fused.  Y (unprojected) and Yp (projected) are written
@@ -656,6 +734,7 @@ __global__ void k_cg_ctl_newsum(double* __restrict__ st, int32_t* __restrict__ f
     if (st[2] < 0.0) st[2] = newsum;
     if (!(newsum > 1e-28 * sd::dmax(st[2], 1.0))) {
         f[0] = 1;
+        f[4] = 1;
         return;
     }
     if (!f[1]) st[6] = newsum / st[1];
@@ -677,6 +756,7 @@ __global__ void k_cg_ctl_denom(double* __restrict__ st, int32_t* __restrict__ f,
     st[3] = denom;
     if (!(denom > 0.0)) {
         f[0] = 1;
+        f[4] = 2;
         return;
     }
     st[4] = st[0] / denom;
@@ -718,6 +798,7 @@ __global__ void k_cg_ctl_alpha(double* __restrict__ st, int32_t* __restrict__ f,
     if (!(alpha > 1e-14 * alpha_cg)) {
         f[3] = 1;
         f[0] = 1;
+        f[4] = 3;
         return;
     }
     f[1] = alpha < alpha_cg * (1.0 - 1e-12) ? 1 : 0;
@@ -888,6 +969,11 @@ void enforce_constraints(Ctx& c, const DCsr& P, const double* B, const double* B
     const DCsr& N = allowed ? *allowed : P;
     if (P.nr != N.nr || P.nc != N.nc) throw InvalidArgument("enforce_constraints: dimension mismatch");
     if (k > kKMax) throw InvalidArgument("enforce_constraints: at most 8 candidates on the GPU path");
+    if (c.ops) {  // interpolation.hpp:518: 2 len k + k^3 per non-empty row
+        const RowCensus rc = row_census(c, N, nullptr);
+        const double kk = static_cast<double>(k);
+        tally(c, 2.0 * kk * static_cast<double>(N.nnz) + kk * kk * kk * rc.nonempty);
+    }
     DBuf<double> vals(static_cast<size_t>(N.nnz), c.s);
     DBuf<int32_t> err(1, c.s);
     AMG_CK(cudaMemsetAsync(err.get(), 0, sizeof(int32_t), c.s));
@@ -905,6 +991,8 @@ void inject_tentative(Ctx& c, const DAgg& agg, const DCsr& N, const double* B, i
     if (m > 8) throw InvalidArgument("inject_tentative: block size above 8 on the GPU path");
     const int32_t ndof = agg.n_nodes * m, nc = agg.n_agg * m;
     if (N.nr != ndof || N.nc != nc) throw InvalidArgument("inject_tentative: pattern dimensions mismatch");
+    // interpolation.hpp:578: m^3 per aggregate block inverse + m^2 per non-root DOF row
+    tally(c, static_cast<double>(agg.n_nodes) * m * m * m);
     Bc.alloc(static_cast<size_t>(nc) * k, c.s);
     DBuf<double> binv(static_cast<size_t>(agg.n_agg) * m * m, c.s);
     DBuf<int32_t> degenerate(1, c.s);
@@ -966,6 +1054,16 @@ void energy_minimize(Ctx& c, const DCsr& A, const DCsr& T, const double* B, cons
     DBuf<double> gp(static_cast<size_t>(n) * k * k, c.s);
     launch(c, k_gram_pinv, blocks_for(n, 64), 64, 0, n, k, N.rp.get(), N.ci.get(), Bc, nc,
            static_cast<const unsigned char*>(is_root.get()), gp.get());
+    // WorkLedger (only with an active sink): Gram build (interpolation.hpp:140) and the
+    // per-call project count (180)
+    const bool counting = c.ops != nullptr;
+    double proj_ops = 0.0;
+    if (counting) {
+        const RowCensus rc = row_census(c, N, is_root.get());
+        const double kk = static_cast<double>(k);
+        tally(c, kk * kk * rc.len + kk * kk * kk * rc.rows);
+        proj_ops = 2.0 * kk * rc.len + kk * kk * rc.rows;
+    }
     DBuf<double> P(static_cast<size_t>(nz), c.s);
     {
         DBuf<int32_t> err(1, c.s);
@@ -1000,12 +1098,12 @@ void energy_minimize(Ctx& c, const DCsr& A, const DCsr& T, const double* B, cons
         launch_prof(c, kProfEminCg, 0.0, k_project, blocks_for(n, 128), 128, 0, n, N.rp.get(), N.ci.get(), k, Bc, nc,
                static_cast<const double*>(gp.get()), static_cast<const unsigned char*>(is_root.get()), R.get());
         DBuf<double> scal(8, c.s);
-        DBuf<int32_t> flags(4, c.s);
+        DBuf<int32_t> flags(8, c.s);
         DBuf<unsigned long long> abits(1, c.s);
         const double init[8] = {0.0, 0.0, -1.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-        const int32_t finit[4] = {0, 1, 0, 0};
+        const int32_t finit[8] = {0, 1, 0, 0, 0, 0, 0, 0};
         copy_h2d(c, scal.get(), init, 8);
-        copy_h2d(c, flags.get(), finit, 4);
+        copy_h2d(c, flags.get(), finit, 8);
         double* S = scal.get();
         int32_t* F = flags.get();
         for (int s = 0; s < iters; ++s) {
@@ -1032,11 +1130,21 @@ void energy_minimize(Ctx& c, const DCsr& A, const DCsr& T, const double* B, cons
                    static_cast<const double*>(ADm.get()), static_cast<const double*>(ADp.get()),
                    static_cast<const double*>(S), static_cast<const int32_t*>(F), s);
         }
-        int32_t fh[4];
-        copy_d2h(c, fh, F, 4);
+        int32_t fh[8];
+        copy_d2h(c, fh, F, 8);
         sync(c);
         st.iterations = fh[2];
         st.breakdown = fh[3] != 0;
+        if (counting) {
+            // the reference's counts (interpolation.hpp:319,333,355): the initial masked product
+            // and projection, every completed iteration, and the part of the stopping one
+            const double M = masked_count(c, A, N), z = static_cast<double>(nz);
+            const double full = z + (M + proj_ops + 3.0 * z) + 3.0 * z;
+            double ops = M + proj_ops + fh[2] * full;
+            if (fh[4] == 1) ops += z;
+            if (fh[4] == 2 || fh[4] == 3) ops += z + M + proj_ops + 3.0 * z;
+            tally(c, ops);
+        }
         compact_pattern(c, N, P.get(), T.bs, Pout);
         return;
     }
@@ -1056,6 +1164,8 @@ void energy_minimize(Ctx& c, const DCsr& A, const DCsr& T, const double* B, cons
     DBuf<double> scal(2, c.s);
     nrm2(c, R0.get(), nz, scal.get());
     const double beta = read_scalar(c, scal.get());
+    const double Mg = counting ? masked_count(c, AtA, N) : 0.0;
+    tally(c, Mg + proj_ops + static_cast<double>(nz));  // interpolation.hpp:374
     if (beta < 1e-300) {
         compact_pattern(c, N, P.get(), T.bs, Pout);
         return;
@@ -1083,6 +1193,7 @@ void energy_minimize(Ctx& c, const DCsr& A, const DCsr& T, const double* B, cons
         const double hn = read_scalar(c, hn_d);
         built = s + 1;
         st.iterations = s + 1;
+        tally(c, Mg + proj_ops + 2.0 * (s + 1) * static_cast<double>(nz));  // interpolation.hpp:392
         if (hn < 1e-14 * beta) break;
         scale_recip_dev(c, hn_d, W, nz);
     }

@@ -58,6 +58,8 @@ void classical_strength(Ctx& c, const DCsr& A, double theta, DCsr& S);
 // evolution strength (strength.hpp:116-238); winv per row
 void evolution_strength(Ctx& c, const DCsr& A, const DCsr& At, const double* winv, double drop_tol, int steps,
                         DCsr& S);
+// WorkLedger count of evolution_strength on A (exact; computed on demand)
+double evolution_ops(Ctx& c, const DCsr& A, const DCsr& At, int steps);
 void normalize_strength(Ctx& c, const DCsr& S, DCsr& N);
 void amalgamate(Ctx& c, const DCsr& S, int32_t m, DCsr& N);
 struct DAgg {
@@ -69,7 +71,8 @@ void greedy_aggregate(Ctx& c, const DCsr& S, DAgg& agg);
 void aggregate_indicator(Ctx& c, const DAgg& agg, DCsr& Cm);
 
 // ---- spectral radius (arnoldi.cu) ----------------------------------------------------
-double spectral_radius(Ctx& c, const DCsr& A, int steps, const double* dinv);
+// *built_out (optional) receives the Krylov dimension reached (the reference's SpMV count)
+double spectral_radius(Ctx& c, const DCsr& A, int steps, const double* dinv, int* built_out = nullptr);
 
 // ---- relaxation (relax.cu) -----------------------------------------------------------
 // sync-free wavefront Gauss-Seidel sweeps (relaxation.hpp:115-127) over k columns

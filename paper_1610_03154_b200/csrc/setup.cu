@@ -71,7 +71,7 @@ void strength_of(Ctx& c, DLevel& L, const amgcu_setup_options& o, DCsr& S) {
             DBuf<int32_t> bad(1, c.s);
             fill_i32(c, bad.get(), INT32_MAX, 1);
             if (o.weighting == 0) {
-                const double rho = level_rho(c, L);
+                const double rho = rho_tallied(c, L);
                 if (rho <= 0.0) throw RuntimeError("evolution_strength: spectral radius estimate failed");
                 DBuf<double> d(static_cast<size_t>(n), c.s);
                 diagonal(c, A, d.get());
@@ -88,6 +88,7 @@ void strength_of(Ctx& c, DLevel& L, const amgcu_setup_options& o, DCsr& S) {
             DCsr At;
             transpose(c, A, At);
             evolution_strength(c, A, At, winv.get(), o.drop_tol, o.evolution_steps, S);
+            L.evo_steps = o.evolution_steps;  // its ledger count is taken on demand (evolution_ops)
             return;
         }
     }
@@ -101,14 +102,25 @@ bool coarsen(Ctx& c, DHier& H, int level, const double* Bhat, Coarsened& out) {
     const int32_t k = L.k;
     const int32_t m = std::max<int32_t>(1, A.bs);
 
+    // WorkLedger buckets of this level (hierarchy.hpp:243): aggregation, candidates,
+    // interpolation, RAP -- charged only when the level is built
+    double cagg = 0.0, ccand = 0.0, cint = 0.0, crap = 0.0;
     DCsr S0, Sa, S;
-    strength_of(c, L, o, S0);
-    amalgamate(c, S0, m, Sa);
-    normalize_strength(c, Sa, S);
     DAgg agg;
-    greedy_aggregate(c, S, agg);
-    if (agg.n_agg >= agg.n_nodes) return false;
+    {
+        OpsScope scope(c, &cagg);
+        strength_of(c, L, o, S0);
+        amalgamate(c, S0, m, Sa);
+        normalize_strength(c, Sa, S);
+        greedy_aggregate(c, S, agg);
+        tally(c, static_cast<double>(S.nnz));  // hierarchy.hpp:197
+    }
+    if (agg.n_agg >= agg.n_nodes) {
+        L.evo_steps = 0;
+        return false;
+    }
 
+    OpsScope int_scope(c, &cint);
     DCsr N;
     aggregate_indicator(c, agg, N);
     for (int t = 0; t < o.degree; ++t) {
@@ -137,7 +149,10 @@ bool coarsen(Ctx& c, DHier& H, int level, const double* Bhat, Coarsened& out) {
     const int32_t n = A.nr;
     DBuf<double> Bimp(static_cast<size_t>(n) * k, c.s);
     copy_d2d(c, Bimp.get(), L.B.get(), static_cast<int64_t>(n) * k);
-    improve_candidates(c, A, Bimp.get(), k, o.candidate_sweeps, o.cand_scheme, o.cand_weight, &L);
+    {
+        OpsScope scope(c, &ccand);
+        improve_candidates(c, A, Bimp.get(), k, o.candidate_sweeps, o.cand_scheme, o.cand_weight, &L);
+    }
     DCsr T;
     DBuf<double> Bc;
     inject_tentative(c, agg, Nd, Bimp.get(), k, m, T, Bc);
@@ -158,7 +173,10 @@ bool coarsen(Ctx& c, DHier& H, int level, const double* Bhat, Coarsened& out) {
         transpose(c, A, At);
         DBuf<double> Bh(static_cast<size_t>(n) * k, c.s);
         copy_d2d(c, Bh.get(), Bhat, static_cast<int64_t>(n) * k);
-        improve_candidates(c, At, Bh.get(), k, o.candidate_sweeps, o.cand_scheme, o.cand_weight, nullptr);
+        {
+            OpsScope scope(c, &ccand);
+            improve_candidates(c, At, Bh.get(), k, o.candidate_sweeps, o.cand_scheme, o.cand_weight, nullptr);
+        }
         DCsr That, Rt;
         DBuf<double> Bhc;
         inject_tentative(c, agg, Nd, Bh.get(), k, m, That, Bhc);
@@ -167,7 +185,14 @@ bool coarsen(Ctx& c, DHier& H, int level, const double* Bhat, Coarsened& out) {
         transpose(c, Rt, out.R);
         out.Bhc = std::move(Bhc);
     }
-    galerkin(c, out.R, A, out.P, out.Ac);
+    {
+        OpsScope scope(c, &crap);
+        galerkin(c, out.R, A, out.P, out.Ac);
+    }
+    L.ledger[0] = cagg;
+    L.ledger[1] = ccand;
+    L.ledger[2] = cint;
+    L.ledger[3] = crap;
     out.Bf = std::move(Bimp);
     out.Bcoarse = std::move(Bc);
     return true;
@@ -229,8 +254,19 @@ double level_rho(Ctx& c, DLevel& L) {
         L.inv_diag.alloc(static_cast<size_t>(L.A.nr), c.s);
         inverse_diagonal(c, L.A, L.inv_diag.get(), "spectral_radius_estimate: zero diagonal at row ");
     }
-    L.rho = spectral_radius(c, L.A, 15, L.inv_diag.get());
+    {
+        OpsScope none(c, nullptr);  // counted per reference call site (rho_tally)
+        L.rho = spectral_radius(c, L.A, 15, L.inv_diag.get(), &L.rho_built);
+    }
     return L.rho;
+}
+
+// one reference call of spectral_radius_estimate on the level (spectral.hpp:44: one SpMV per
+// Arnoldi step, counted by spmv): the GPU computes rho once per level
+double rho_tallied(Ctx& c, DLevel& L) {
+    const double r = level_rho(c, L);
+    tally(c, static_cast<double>(L.rho_built) * static_cast<double>(L.A.nnz));
+    return r;
 }
 
 void improve_candidates(Ctx& c, const DCsr& A, double* B, int32_t k, int sweeps, int scheme, double weight,
@@ -247,9 +283,14 @@ void improve_candidates(Ctx& c, const DCsr& A, double* B, int32_t k, int sweeps,
             if (w == 0.0) {
                 double rho;
                 if (cache) {
-                    rho = level_rho(c, *cache);
+                    rho = rho_tallied(c, *cache);
                 } else {
-                    rho = spectral_radius(c, A, 15, dinv.get());
+                    int built = 0;
+                    {
+                        OpsScope none(c, nullptr);
+                        rho = spectral_radius(c, A, 15, dinv.get(), &built);
+                    }
+                    tally(c, static_cast<double>(built) * static_cast<double>(A.nnz));
                 }
                 w = 4.0 / (3.0 * rho);
             }
@@ -259,6 +300,8 @@ void improve_candidates(Ctx& c, const DCsr& A, double* B, int32_t k, int sweeps,
         } else {
             gauss_seidel(c, A, dinv.get(), B, nullptr, k, sweeps, scheme == 2);
         }
+        // relaxation.hpp:207: one count of nnz per sweep and candidate column
+        tally(c, static_cast<double>(k) * sweeps * static_cast<double>(A.nnz));
     }
     DBuf<double> nrm(static_cast<size_t>(k), c.s);
     for (int32_t j = 0; j < k; ++j) {
@@ -345,7 +388,9 @@ std::unique_ptr<DHier> rn_setup(Ctx& c, const DCsr& A, const double* B, int32_t 
         H->lv.push_back(std::move(next));
     }
     // finalize_hierarchy (hierarchy.hpp:164-172): relaxation workspaces and the
-    // coarsest-level factorisation
+    // coarsest-level factorisation; its counts open the solve bucket (hierarchy.hpp:171)
+    double cfin = 0.0;
+    OpsScope fin_scope(c, &cfin);
     for (size_t l = 0; l + 1 < H->lv.size(); ++l) {
         DLevel& L = H->lv[l];
         const int32_t n = L.A.nr;
@@ -353,9 +398,9 @@ std::unique_ptr<DHier> rn_setup(Ctx& c, const DCsr& A, const double* B, int32_t 
             L.inv_diag.alloc(static_cast<size_t>(n), c.s);
             inverse_diagonal(c, L.A, L.inv_diag.get(), "relax: zero diagonal at row ");
         }
-        auto weight = [&](int scheme, double w) {
+        auto weight = [&](int scheme, double w) {  // make_ws, relaxation.hpp:52-54
             if (scheme != 0) return 0.0;
-            return w != 0.0 ? w : 4.0 / (3.0 * level_rho(c, L));
+            return w != 0.0 ? w : 4.0 / (3.0 * rho_tallied(c, L));
         };
         L.w_pre = weight(o.pre_scheme, o.pre_weight);
         L.w_post = weight(o.post_scheme, o.post_weight);
@@ -371,6 +416,11 @@ std::unique_ptr<DHier> rn_setup(Ctx& c, const DCsr& A, const double* B, int32_t 
         }
     }
     coarse_factor(c, *H);
+    {
+        const double nL = static_cast<double>(H->lv.back().A.nr);
+        tally(c, nL * nL * nL);  // hierarchy.hpp:68
+    }
+    H->wu[4] = cfin / H->base_nnz;
     prepare_solve(*H);
     return H;
 }

@@ -722,6 +722,7 @@ void spgemm(Ctx& c, const DCsr& A, const DCsr& B, DCsr& C, double* ops) {
     const int64_t total = nr > 0 ? staged<int64_t>(c, 0) : 0;
     const int32_t nbig = staged<int32_t>(c, 1);
     if (ops) *ops = static_cast<double>(total);
+    tally(c, static_cast<double>(total));  // matmul's op count (sparse.hpp:195)
     DBuf<int32_t> tcol(static_cast<size_t>(total), c.s), cnt(static_cast<size_t>(nr) + 1, c.s);
     DBuf<double> tval(static_cast<size_t>(total), c.s);
     launch_prof(c, kProfSpgemm,

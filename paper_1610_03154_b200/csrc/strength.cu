@@ -531,6 +531,57 @@ __global__ void __launch_bounds__(kEv2Warps * kWarp)
     }
 }
 
+// WorkLedger count of evolution_strength (strength.hpp:176-194, count at 236):
+// per row, `steps` times the sum over the distance-`steps` ball of (entries of
+// the node's A row whose column lies in the ball + 1).  Same BFS as the generic
+// kernel; rows whose ball overflows the shared capacity are listed for the host.
+__global__ void __launch_bounds__(kEvWarps * kWarp)
+    k_evolution_count(int32_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                      const int32_t* __restrict__ trp, const int32_t* __restrict__ tci, int steps,
+                      unsigned long long* __restrict__ total, int32_t* __restrict__ overflow_rows,
+                      int32_t* __restrict__ n_overflow) {
+    __shared__ EvShared shm[kEvWarps];
+    const int w = threadIdx.x / kWarp, lane = threadIdx.x & (kWarp - 1);
+    const int32_t i = blockIdx.x * kEvWarps + w;
+    if (i >= n) return;
+    EvShared& sh = shm[w];
+    for (int s = lane; s < kEvHash; s += kWarp) sh.hkey[s] = -1;
+    if (lane == 0) {
+        sh.count = 0;
+        sh.overflow = 0;
+    }
+    __syncwarp();
+    if (lane == 0) h_insert(sh, i);
+    __syncwarp();
+    int32_t lo = 0;
+    for (int st = 0; st < steps; ++st) {
+        const int32_t hi = min(sh.count, kEvCap);
+        for (int32_t f = lo; f < hi; ++f) {
+            const int32_t u = sh.nodes[f];
+            for (int32_t p = rp[u] + lane; p < rp[u + 1]; p += kWarp) h_insert(sh, ci[p]);
+            for (int32_t p = trp[u] + lane; p < trp[u + 1]; p += kWarp) h_insert(sh, tci[p]);
+        }
+        __syncwarp();
+        lo = hi;
+        if (sh.overflow) break;
+    }
+    __syncwarp();
+    if (sh.overflow) {
+        if (lane == 0) overflow_rows[atomicAdd(n_overflow, 1)] = i;
+        return;
+    }
+    unsigned long long cnt = 0;
+    for (int32_t t = lane; t < sh.count; t += kWarp) {
+        const int32_t u = sh.nodes[t];
+        unsigned long long in = 1;
+        for (int32_t p = rp[u]; p < rp[u + 1]; ++p)
+            if (h_lookup(sh, ci[p]) >= 0) ++in;
+        cnt += in;
+    }
+    for (int off = 16; off > 0; off >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
+    if (lane == 0) atomicAdd(total, cnt * static_cast<unsigned long long>(steps));
+}
+
 // Fallback: block per row over a direct-mapped global scratch (local id per node).
 constexpr int kEvBigThreads = 256;
 
@@ -716,6 +767,7 @@ void symmetric_strength(Ctx& c, const DCsr& A, double theta, DCsr& S) {
     inverse_diagonal(c, A, dinv.get(), "symmetric_strength: zero diagonal at row ");
     two_pass(c, A.nr, A.nc, A.bs, S, k_soc<true>, blocks_for(A.nr, 128), 128, A.nr, A.rp.get(), A.ci.get(), A.va.get(),
              static_cast<const double*>(d.get()), theta);
+    tally(c, static_cast<double>(A.nnz) + A.nr);  // strength.hpp:105
 }
 
 void classical_strength(Ctx& c, const DCsr& A, double theta, DCsr& S) {
@@ -723,6 +775,7 @@ void classical_strength(Ctx& c, const DCsr& A, double theta, DCsr& S) {
     if (theta < 0.0 || theta > 1.0) throw InvalidArgument("classical_strength: theta must lie in [0, 1]");
     two_pass(c, A.nr, A.nc, A.bs, S, k_soc<false>, blocks_for(A.nr, 128), 128, A.nr, A.rp.get(), A.ci.get(),
              A.va.get(), static_cast<const double*>(nullptr), theta);
+    tally(c, static_cast<double>(A.nr));  // strength.hpp:64
 }
 
 void normalize_strength(Ctx& c, const DCsr& S, DCsr& N) {
@@ -732,6 +785,7 @@ void normalize_strength(Ctx& c, const DCsr& S, DCsr& N) {
     launch(c, k_negative_check, blocks_for(S.nnz, 256), 256, 0, S.nnz, S.va.get(), bad.get());
     if (read_scalar(c, bad.get())) throw InvalidArgument("normalize_strength: negative strength value");
     two_pass(c, S.nr, S.nc, S.bs, N, k_normalize, blocks_for(S.nr, 128), 128, S.nr, S.rp.get(), S.ci.get(), S.va.get());
+    tally(c, static_cast<double>(S.nnz));  // strength.hpp:286
 }
 
 void amalgamate(Ctx& c, const DCsr& S, int32_t m, DCsr& N) {
@@ -743,6 +797,49 @@ void amalgamate(Ctx& c, const DCsr& S, int32_t m, DCsr& N) {
     if (S.nr % m != 0 || S.nc % m != 0) throw InvalidArgument("amalgamate: dimensions not divisible by block size");
     const int32_t nn = S.nr / m;
     two_pass(c, nn, S.nc / m, 1, N, k_amalgamate, blocks_for(nn, 128), 128, nn, m, S.rp.get(), S.ci.get(), S.va.get());
+}
+
+double evolution_ops(Ctx& c, const DCsr& A, const DCsr& At, int steps) {
+    const int32_t n = A.nr;
+    DBuf<unsigned long long> total(1, c.s);
+    DBuf<int32_t> ovf(static_cast<size_t>(n) + 1, c.s), novf(1, c.s);
+    AMG_CK(cudaMemsetAsync(total.get(), 0, sizeof(unsigned long long), c.s));
+    AMG_CK(cudaMemsetAsync(novf.get(), 0, sizeof(int32_t), c.s));
+    launch(c, k_evolution_count, blocks_for(n, kEvWarps), kEvWarps * kWarp, 0, n, A.rp.get(), A.ci.get(), At.rp.get(),
+           At.ci.get(), steps, total.get(), ovf.get(), novf.get());
+    double ops = static_cast<double>(read_scalar(c, total.get()));
+    const int32_t nbig = read_scalar(c, novf.get());
+    if (nbig > 0) {  // large balls: the reference's BFS on the host
+        const HostCsr ha = download_csr(c, A), ht = download_csr(c, At);
+        std::vector<int32_t> rows(nbig), slot(n, -1), hood;
+        copy_d2h(c, rows.data(), ovf.get(), nbig);
+        sync(c);
+        for (int32_t i : rows) {
+            hood.assign(1, i);
+            slot[i] = 0;
+            size_t lo = 0;
+            for (int st = 0; st < steps; ++st) {
+                const size_t hi = hood.size();
+                for (size_t f = lo; f < hi; ++f)
+                    for (const HostCsr* M : {&ha, &ht})
+                        for (int32_t p = M->row_offsets[hood[f]]; p < M->row_offsets[hood[f] + 1]; ++p)
+                            if (slot[M->col_indices[p]] < 0) {
+                                slot[M->col_indices[p]] = static_cast<int32_t>(hood.size());
+                                hood.push_back(M->col_indices[p]);
+                            }
+                lo = hi;
+            }
+            double cnt = 0.0;
+            for (int32_t u : hood) {
+                cnt += 1.0;
+                for (int32_t p = ha.row_offsets[u]; p < ha.row_offsets[u + 1]; ++p)
+                    if (slot[ha.col_indices[p]] >= 0) cnt += 1.0;
+            }
+            ops += steps * cnt;
+            for (int32_t u : hood) slot[u] = -1;
+        }
+    }
+    return ops;
 }
 
 void evolution_strength(Ctx& c, const DCsr& A, const DCsr& At, const double* winv, double drop_tol, int steps,

@@ -44,8 +44,11 @@ int main(int argc, char** argv) {
     sopts.max_iters = vo.max_iters;
     amg::SolveReport rep = amg::solve(h, b, x, sopts);
     h.download();
-    std::printf("{\"levels\": %d, \"iterations\": %d, \"converged\": %d, \"oc\": %.6f, \"cc\": %.6f, \"nnz_P0\": %d}\n",
+    const amg::WorkLedger led = h.ledger();
+    std::printf("{\"levels\": %d, \"iterations\": %d, \"converged\": %d, \"oc\": %.6f, \"cc\": %.6f, \"nnz_P0\": %d, "
+                "\"sc\": %.17g, \"wu\": [%.17g, %.17g, %.17g, %.17g, %.17g]}\n",
                 h.n_levels(), rep.iterations, rep.converged ? 1 : 0, rep.chi_oc, rep.chi_cc,
-                h.levels.size() > 1 ? h.levels[0].P.nnz() : 0);
+                h.levels.size() > 1 ? h.levels[0].P.nnz() : 0, led.setup_total(), led.wu[0], led.wu[1], led.wu[2],
+                led.wu[3], led.wu[4]);
     return rep.converged ? 0 : 3;
 }

@@ -37,3 +37,5 @@ def test_dropin_runs_like_the_reference_caller(binary, port):
     _, rep = port.solve(h, b, None, vo)
     assert got["levels"] == h.n_levels() and got["iterations"] == rep.iterations
     assert got["nnz_P0"] == h.matrix(0, 1).nnz()
+    # the ledger through the drop-in header (setup buckets; the solve bucket after one solve)
+    assert got["wu"][:4] == list(h.ledger()[:4])

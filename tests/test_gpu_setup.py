@@ -13,7 +13,8 @@ import numpy as np
 import pytest
 
 import paper_1610_03154_b200.api as api
-from paper_1610_03154_b200.types import (FilterRule, KrylovKind, RelaxConfig, RelaxScheme, SetupOptions,
+from paper_1610_03154_b200.types import (EvolutionWeighting, FilterRule, KrylovKind, RelaxConfig, RelaxScheme,
+                                         SetupOptions,
                                          SolveMethod, SolveOptions, StrengthConfig, StrengthMeasure,
                                          constant_candidates)
 from tests.helpers import aniso2d, poisson1d, rel_max_err, same_structure
@@ -90,6 +91,37 @@ def test_setup_bitwise_sequential(gpu_seq, port, name, gen, so, vo):
     assert rel_max_err(rg.residual_history, ro.residual_history) <= 1e-10
     assert rel_max_err(xg, xo) <= 1e-10
     assert rg.chi_oc == ro.chi_oc and rg.chi_cc == ro.chi_cc
+
+
+@pytest.mark.parametrize("name,gen,so,vo", CASES, ids=[c[0] for c in CASES])
+def test_work_ledger_matches_reference(gpu_seq, port, name, gen, so, vo):
+    """WorkLedger (work.hpp:38-67): every bucket's work units equal the reference's, after
+    setup (evolution SOC counted on demand) and after a solve"""
+    A, B, Bh, b = gen()
+    hg = api.setup(A, B, so, Bh, ctx=gpu_seq)
+    ho = port.setup(A, B, so, Bh)
+    assert hg.ledger().tobytes() == ho.ledger().tobytes(), (hg.ledger(), ho.ledger())
+    api.solve(hg, b, None, vo)
+    port.solve(ho, b, None, vo)
+    assert hg.ledger().tobytes() == ho.ledger().tobytes(), (hg.ledger(), ho.ledger())
+
+
+def test_work_ledger_options(gpu_seq, port):
+    """ledger under the other count paths: symmetric SOC, Jacobi candidate improvement
+    (its spectral estimate), l1-weighted evolution, degree 1"""
+    A = aniso2d(30, 0.05)
+    B = constant_candidates(A.n_rows)
+    cases = [SetupOptions(strength=StrengthConfig(StrengthMeasure.symmetric, 0.25), pre_relax=JAC, post_relax=JAC,
+                          max_size=40),
+             SetupOptions(strength=StrengthConfig(StrengthMeasure.evolution, 4.0, 2, EvolutionWeighting.l1jacobi),
+                          pre_relax=JAC, post_relax=JAC, max_size=40),
+             SetupOptions(candidate_relax=RelaxConfig(RelaxScheme.jacobi, 0.0, 1), pre_relax=JAC, post_relax=JAC,
+                          max_size=40)]
+    cases[1].interp.degree = 1
+    for so in cases:
+        hg = api.setup(A, B, so, ctx=gpu_seq)
+        ho = port.setup(A, B, so)
+        assert hg.ledger().tobytes() == ho.ledger().tobytes(), (so, hg.ledger(), ho.ledger())
 
 
 @pytest.mark.parametrize("name,gen,so,vo", CASES, ids=[c[0] for c in CASES])
