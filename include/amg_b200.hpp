@@ -17,6 +17,7 @@
 #include <array>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
 #include <memory>
 #include <optional>
 #include <span>
@@ -337,6 +338,71 @@ inline SolveReport solve(Hierarchy& h, std::span<const double> b, std::vector<do
 
 inline void cycle(Hierarchy& h, std::span<double> x, std::span<const double> b, CycleKind kind = CycleKind::V) {
     b200::check(amgcu_cycle(h.handle.get(), x.data(), b.data(), static_cast<int32_t>(kind)), b200::default_ctx());
+}
+
+// Complexity measures and the setup report (complexity.hpp:15-88).  The report functions
+// read the host mirror, downloading it first if needed.  setup_report_json returns the
+// reference's setup_report() document as text (the reference builds it with nlohmann::json).
+inline double operator_complexity(Hierarchy& h) {
+    double oc = 0.0, cc = 0.0;
+    b200::check(amgcu_hier_complexity(h.handle.get(), &oc, &cc), b200::default_ctx());
+    return oc;
+}
+
+inline double cycle_complexity(Hierarchy& h) {
+    double oc = 0.0, cc = 0.0;
+    b200::check(amgcu_hier_complexity(h.handle.get(), &oc, &cc), b200::default_ctx());
+    return cc;
+}
+
+inline std::string setup_report_json(Hierarchy& h) {
+    if (h.levels.empty()) h.download();
+    const WorkLedger w = h.ledger();
+    const int L = static_cast<int>(h.levels.size());
+    std::string j = "{\"levels\": [";
+    char buf[512];
+    for (int l = 0; l < L; ++l) {
+        const Level& lev = h.levels[l];
+        const double npr = lev.A.n_rows > 0 ? static_cast<double>(lev.A.nnz()) / lev.A.n_rows : 0.0;
+        std::snprintf(buf, sizeof(buf), "%s{\"level\": %d, \"rows\": %d, \"nnz\": %d, \"nnz_per_row\": %.17g, \"symmetric\": %s",
+                      l ? ", " : "", l, lev.A.n_rows, lev.A.nnz(), npr, lev.symmetric ? "true" : "false");
+        j += buf;
+        if (l + 1 < L) {
+            std::snprintf(buf, sizeof(buf), ", \"nnz_P\": %d, \"nnz_R\": %d", lev.P.nnz(), lev.R.nnz());
+            j += buf;
+        }
+        j += "}";
+    }
+    std::snprintf(buf, sizeof(buf),
+                  "], \"operator_complexity\": %.17g, \"cycle_complexity\": %.17g, \"work_units\": {\"aggregation\": "
+                  "%.17g, \"candidates\": %.17g, \"interp\": %.17g, \"rap\": %.17g, \"solve_other\": %.17g, "
+                  "\"setup_total\": %.17g}}",
+                  operator_complexity(h), cycle_complexity(h), w.wu[0], w.wu[1], w.wu[2], w.wu[3], w.wu[4],
+                  w.setup_total());
+    return j + buf;
+}
+
+inline std::string setup_report_csv(Hierarchy& h) {
+    if (h.levels.empty()) h.download();
+    std::string os = "level,rows,nnz,nnz_per_row,nnz_P,nnz_R\n";
+    const int L = static_cast<int>(h.levels.size());
+    char buf[256];
+    for (int l = 0; l < L; ++l) {
+        const Level& lev = h.levels[l];
+        const double npr = lev.A.n_rows > 0 ? static_cast<double>(lev.A.nnz()) / lev.A.n_rows : 0.0;
+        std::snprintf(buf, sizeof(buf), "%d,%d,%d,%g", l, lev.A.n_rows, lev.A.nnz(), npr);
+        os += buf;
+        if (l + 1 < L) {
+            std::snprintf(buf, sizeof(buf), ",%d,%d", lev.P.nnz(), lev.R.nnz());
+            os += buf;
+        } else {
+            os += ",,";
+        }
+        os += "\n";
+    }
+    std::snprintf(buf, sizeof(buf), "operator_complexity,%g,,,,\ncycle_complexity,%g,,,,\nsetup_work_units,%g,,,,\n",
+                  operator_complexity(h), cycle_complexity(h), h.ledger().setup_total());
+    return os + buf;
 }
 
 }  // namespace amg

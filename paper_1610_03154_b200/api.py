@@ -223,6 +223,24 @@ class Hierarchy:
         self.ctx._chk(lib.amgcu_hier_ledger(self.handle, ptr_f64(out)))
         return out
 
+    def setup_report(self) -> dict:
+        """The reference's setup_report (complexity.hpp:39-66) as a dict."""
+        L = self.n_levels()
+        levels = []
+        for l in range(L):
+            A = self.matrix(l, 0)
+            row = {"level": l, "rows": A.n_rows, "nnz": A.nnz(),
+                   "nnz_per_row": A.nnz() / A.n_rows if A.n_rows else 0.0, "symmetric": self.symmetric(l)}
+            if l + 1 < L:
+                row["nnz_P"] = self.matrix(l, 1).nnz()
+                row["nnz_R"] = self.matrix(l, 2).nnz()
+            levels.append(row)
+        oc, cc = self.complexity()
+        w = self.ledger()
+        return {"levels": levels, "operator_complexity": oc, "cycle_complexity": cc,
+                "work_units": {"aggregation": w[0], "candidates": w[1], "interp": w[2], "rap": w[3],
+                               "solve_other": w[4], "setup_total": w[0] + w[1] + w[2] + w[3]}}
+
     def complexity(self):
         a, b = C.c_double(), C.c_double()
         self.ctx._chk(lib.amgcu_hier_complexity(self.handle, C.byref(a), C.byref(b)))

@@ -50,5 +50,6 @@ int main(int argc, char** argv) {
                 h.n_levels(), rep.iterations, rep.converged ? 1 : 0, rep.chi_oc, rep.chi_cc,
                 h.levels.size() > 1 ? h.levels[0].P.nnz() : 0, led.setup_total(), led.wu[0], led.wu[1], led.wu[2],
                 led.wu[3], led.wu[4]);
+    if (argc > 3) std::fprintf(stderr, "%s\n%s", amg::setup_report_json(h).c_str(), amg::setup_report_csv(h).c_str());
     return rep.converged ? 0 : 3;
 }

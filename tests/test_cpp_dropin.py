@@ -28,7 +28,7 @@ def test_dropin_compiles_and_links(binary):
 @pytest.mark.gpu
 def test_dropin_runs_like_the_reference_caller(binary, port):
     import paper_1610_03154_b200.api as api
-    r = subprocess.run([binary, "2", "65"], capture_output=True, text=True, timeout=300)
+    r = subprocess.run([binary, "2", "65", "report"], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stderr
     got = json.loads(r.stdout)
     A, B, Bh, b = api.generate_config(2, 65)
@@ -39,3 +39,9 @@ def test_dropin_runs_like_the_reference_caller(binary, port):
     assert got["nnz_P0"] == h.matrix(0, 1).nnz()
     # the ledger through the drop-in header (setup buckets; the solve bucket after one solve)
     assert got["wu"][:4] == list(h.ledger()[:4])
+    # setup_report (complexity.hpp:39-66) through the header: per-level sizes, complexities, work units
+    rep_json = json.loads(r.stderr.splitlines()[0])
+    oc, cc = h.complexity()
+    assert [lv["rows"] for lv in rep_json["levels"]] == [h.matrix(l, 0).n_rows for l in range(h.n_levels())]
+    assert rep_json["operator_complexity"] == oc and rep_json["cycle_complexity"] == cc
+    assert rep_json["work_units"]["setup_total"] == sum(h.ledger()[:4])
