@@ -127,6 +127,7 @@ amgcu_status amgcu_ctx_create(int device, amgcu_ctx* out) {
         auto* ctx = new amgcu_ctx_s;
         ctx->c.device = device;
         AMG_CK(cudaStreamCreateWithFlags(&ctx->c.s, cudaStreamNonBlocking));
+        AMG_CK(cudaStreamCreateWithFlags(&ctx->c.side, cudaStreamNonBlocking));
         AMG_CK(cudaDeviceGetAttribute(&ctx->c.sms, cudaDevAttrMultiProcessorCount, device));
         cudaMemPool_t pool;
         AMG_CK(cudaDeviceGetDefaultMemPool(&pool, device));
@@ -146,6 +147,8 @@ amgcu_status amgcu_ctx_destroy(amgcu_ctx ctx) {
     ctx->c.arnoldi_v0.release();
     cudaStreamSynchronize(ctx->c.s);
     if (ctx->c.pin) cudaFreeHost(ctx->c.pin);
+    cudaStreamSynchronize(ctx->c.side);
+    cudaStreamDestroy(ctx->c.side);
     cudaStreamDestroy(ctx->c.s);
     delete ctx;
     return AMGCU_OK;
@@ -345,22 +348,8 @@ amgcu_status amgcu_hier_ledger(amgcu_hier h, double* wu5) {
     return guarded(h->owner, [&] {
         Ctx& c = h->owner->c;
         AMG_CK(cudaSetDevice(c.device));
-        DHier& H = *h->h;
-        double wu[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-        for (size_t l = 0; l + 1 < H.lv.size(); ++l) {
-            DLevel& L = H.lv[l];
-            if (L.evo_steps > 0 && L.evo_ops < 0.0) {  // evolution SOC's count, on first request
-                DCsr At;
-                transpose(c, L.A, At);
-                L.evo_ops = evolution_ops(c, L.A, At, L.evo_steps);
-            }
-            // charges in level order, as the reference's coarsening loop (hierarchy.hpp:243)
-            wu[0] += (L.ledger[0] + (L.evo_steps > 0 ? L.evo_ops : 0.0)) / H.base_nnz;
-            wu[1] += L.ledger[1] / H.base_nnz;
-            wu[2] += L.ledger[2] / H.base_nnz;
-            wu[3] += L.ledger[3] / H.base_nnz;
-        }
-        wu[4] = H.wu[4];  // finalize + every solve so far
+        double wu[5];
+        hier_ledger(*h->h, wu);
         for (int b2 = 0; b2 < 5; ++b2) wu5[b2] = wu[b2];
     });
 }

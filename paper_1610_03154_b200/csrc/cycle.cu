@@ -793,7 +793,11 @@ SolveResult solve(DHier& h, const double* b, double* x, const amgcu_solve_option
     SolveResult rep;
     rep.chi_oc = operator_complexity(h);
     rep.chi_cc = cycle_complexity(h);
-    rep.wu_setup = h.wu[0] + h.wu[1] + h.wu[2] + h.wu[3];
+    {
+        double wu[5];  // work.hpp:59 setup_total, cycle.hpp:126
+        hier_ledger(h, wu);
+        rep.wu_setup = wu[0] + wu[1] + wu[2] + wu[3];
+    }
     Driver d{h, c};
     auto finish = [&]() {
         rep.rho = conv_factor(rep.history);

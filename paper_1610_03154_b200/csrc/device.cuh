@@ -109,6 +109,7 @@ struct Ctx {
     std::vector<cudaEvent_t> event_pool;
     int device = 0;
     cudaStream_t s = nullptr;
+    cudaStream_t side = nullptr;  // independent side work (the evolution-SOC ledger count)
     int sms = 148;
     bool seq = false;  // sequential (reference-order) global reductions
     int64_t launches = 0;
@@ -191,12 +192,18 @@ struct DSell {
     const double* cva = nullptr;
 };
 
+// AMGCU_LAUNCH_CHECK=1 (debugging): synchronise after every launch and name the kernel
+// that faulted
+bool launch_check_enabled();
+void launch_check(Ctx& c, const void* kernel);
+
 template <typename Kern, typename... Args>
 inline void launch_raw(Ctx& c, Kern k, unsigned grid, unsigned block, size_t smem, Args... args) {
     if (grid == 0) return;
     k<<<grid, block, smem, c.s>>>(args...);
     ++c.launches;
     AMG_CK(cudaGetLastError());
+    if (launch_check_enabled()) launch_check(c, reinterpret_cast<const void*>(k));
 }
 
 template <typename Kern, typename... Args>

@@ -22,6 +22,7 @@ struct DLevel {
     double ledger[4] = {0.0, 0.0, 0.0, 0.0};
     int evo_steps = 0;
     double evo_ops = -1.0;
+    std::unique_ptr<EvoCount> evo_count;  // in flight on the side stream during setup
     // solve phase
     DSell sA, sP, sR;
     DBuf<double> inv_diag;  // 1 / a_ii
@@ -45,6 +46,10 @@ struct DHier {
 // amg::rn_setup on the GPU.  A, B, left are device arrays (left may be null).
 std::unique_ptr<DHier> rn_setup(Ctx& c, const DCsr& A, const double* B, int32_t k, const double* left,
                                 const amgcu_setup_options& o);
+
+// WorkLedger (work.hpp:38-67) in work units: per-level buckets 0-3 summed in level order,
+// bucket 4 = finalize + solves.  Takes the evolution-SOC count on first request.
+void hier_ledger(DHier& h, double wu[5]);
 
 // relaxation helpers shared by setup and solve
 void require_supported_relax(int scheme, const char* who);

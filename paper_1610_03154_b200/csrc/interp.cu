@@ -10,6 +10,7 @@
 
 #include "interp.cuh"
 #include "small_dense.h"
+#include "stl_sort.cuh"
 
 namespace amgcu {
 
@@ -68,63 +69,6 @@ __global__ void k_any_missing(int32_t n, const int32_t* __restrict__ rp, const i
     if (!(pos < rp[i + 1] && ci[pos] == own[i])) atomicExch(flag, 1);
 }
 
-// ---------------------------------------------------------------------------------------
-// ensure_min_support (no Bc): re-add the largest dropped magnitudes (descending,
-// ties by position) until the row holds min(min_cols, |full row|) entries.
-// ---------------------------------------------------------------------------------------
-__global__ void k_min_support(int32_t n, const int32_t* __restrict__ frp, const int32_t* __restrict__ fci,
-                              const double* __restrict__ fva, const int32_t* __restrict__ grp,
-                              const int32_t* __restrict__ gci, const double* __restrict__ gva, int32_t min_cols,
-                              const int32_t* __restrict__ orp, int32_t* __restrict__ cnt, int32_t* __restrict__ oci,
-                              double* __restrict__ ova) {
-    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const int32_t flo = frp[i], fhi = frp[i + 1], glo = grp[i], ghi = grp[i + 1];
-    const int32_t have = fhi - flo;
-    const int32_t target = min(min_cols, ghi - glo);
-    // candidate q (in full row) is chosen if its descending rank among candidates < need
-    const int32_t need = have >= target ? 0 : target - have;
-    auto is_candidate = [&](int32_t q) {
-        const int32_t pos = lower_bound_i32(fci, flo, fhi, gci[q]);
-        return !(pos < fhi && fci[pos] == gci[q]) && gva[q] != 0.0;
-    };
-    auto chosen = [&](int32_t q) {
-        if (need == 0 || !is_candidate(q)) return false;
-        const double m = fabs(gva[q]);
-        int32_t rank = 0;
-        for (int32_t r = glo; r < ghi; ++r) {
-            if (r == q || !is_candidate(r)) continue;
-            const double o = fabs(gva[r]);
-            rank += (o > m || (o == m && r < q)) ? 1 : 0;
-        }
-        return rank < need;
-    };
-    if (!orp) {
-        int32_t add = 0;
-        for (int32_t q = glo; q < ghi; ++q) add += chosen(q) ? 1 : 0;
-        cnt[i] = have + add;
-        return;
-    }
-    // merge filtered row with chosen entries, ascending column
-    int32_t o = orp[i], p = flo;
-    for (int32_t q = glo; q < ghi; ++q) {
-        if (!chosen(q)) continue;
-        while (p < fhi && fci[p] < gci[q]) {
-            oci[o] = fci[p];
-            ova[o] = fva[p];
-            ++o;
-            ++p;
-        }
-        oci[o] = gci[q];
-        ova[o] = gva[q];
-        ++o;
-    }
-    for (; p < fhi; ++p) {
-        oci[o] = fci[p];
-        ova[o] = fva[p];
-        ++o;
-    }
-}
 
 // ---------------------------------------------------------------------------------------
 // widen_deficient_rows: block per deficient row, whole-level BFS over S and S^T
@@ -854,6 +798,89 @@ __global__ void k_axpy_host(int64_t n, double a, const double* __restrict__ x, d
     if (p < n) y[p] += a * x[p];
 }
 
+// ensure_min_support (interpolation.hpp:607-643), thread per row with the row in
+// local arrays: the filtered row, then the full row's other non-zero entries sorted
+// by magnitude with libstdc++'s std::sort (stl_sort.cuh: the reference's tie order),
+// appended until the row holds min(min_cols, |full row|) entries and -- with Bc --
+// until the coarse-candidate rows it spans reach rank min_cols (span_rank: QR with
+// column pivoting, threshold 1e-3, small_dense.h qr_rank).  Output in column order.
+constexpr int kEmsMax = 64;  // entries per row handled (longer rows: error flag)
+
+struct EmsCand {
+    double mag;
+    int32_t col;
+    double val;
+};
+
+__global__ void k_min_support_rows(int32_t n, const int32_t* __restrict__ frp, const int32_t* __restrict__ fci,
+                                   const double* __restrict__ fva, const int32_t* __restrict__ grp,
+                                   const int32_t* __restrict__ gci, const double* __restrict__ gva, int32_t min_cols,
+                                   const double* __restrict__ Bc, int32_t k, int32_t nc, int32_t* __restrict__ err,
+                                   const int32_t* __restrict__ orp, int32_t* __restrict__ cnt, int32_t* __restrict__ oci,
+                                   double* __restrict__ ova) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int32_t flo = frp[i], fhi = frp[i + 1], glo = grp[i], ghi = grp[i + 1];
+    if (fhi - flo > kEmsMax || ghi - glo > kEmsMax) {
+        atomicExch(err, 1);
+        if (!orp) cnt[i] = 0;
+        return;
+    }
+    int32_t oc[kEmsMax];
+    double ov[kEmsMax];
+    int no = 0;
+    for (int32_t p = flo; p < fhi; ++p, ++no) {
+        oc[no] = fci[p];
+        ov[no] = fva[p];
+    }
+    auto span_rank = [&]() {
+        double M[kEmsMax * kKMax];
+        for (int r = 0; r < no; ++r)
+            for (int a = 0; a < k; ++a) M[r * k + a] = Bc[static_cast<size_t>(a) * nc + oc[r]];
+        return sd::qr_rank<kKMax>(no, k, M, 1e-3);
+    };
+    const int32_t have = no, full_len = ghi - glo;
+    const int32_t target = min(min_cols, full_len);
+    const bool short_rank = Bc && have >= target && full_len > have && span_rank() < min_cols;
+    if (!(have >= target && !short_rank)) {
+        EmsCand cand[kEmsMax];
+        int ncand = 0;
+        for (int32_t p = glo; p < ghi; ++p) {
+            const int32_t j = gci[p];
+            bool present = false;
+            for (int e = 0; e < have; ++e) present = present || oc[e] == j;
+            if (!present && gva[p] != 0.0) cand[ncand++] = {fabs(gva[p]), j, gva[p]};
+        }
+        stlsort::sort(cand, cand + ncand, [](const EmsCand& a, const EmsCand& b) { return a.mag > b.mag; });
+        int t = 0;
+        for (; t < ncand && no < target; ++t, ++no) {
+            oc[no] = cand[t].col;
+            ov[no] = cand[t].val;
+        }
+        if (Bc)
+            for (; t < ncand && span_rank() < min_cols; ++t, ++no) {
+                oc[no] = cand[t].col;
+                ov[no] = cand[t].val;
+            }
+    }
+    if (!orp) {
+        cnt[i] = no;
+        return;
+    }
+    // from_rows: ascending column (the columns are distinct; values pass through 0.0 + v)
+    int32_t o = orp[i];
+    int32_t last = -1;
+    for (int w = 0; w < no; ++w) {
+        int best = -1;
+        for (int e = 0; e < no; ++e)
+            if (oc[e] > last && (best < 0 || oc[e] < oc[best])) best = e;
+        oci[o] = oc[best];
+        ova[o] = 0.0 + ov[best];
+        ++o;
+        last = oc[best];
+    }
+}
+
 // two-pass helper for row kernels with (..., orp, cnt, oci, ova) tails
 template <typename K, typename... Args>
 void build_rows(Ctx& c, int32_t nr, int32_t nc, int32_t bs, DCsr& out, K k, unsigned grid, unsigned block,
@@ -886,11 +913,17 @@ void add_aggregate_entries(Ctx& c, const DCsr& N, const DAgg& agg, DCsr& out) {
                static_cast<const int32_t*>(agg.owner.get()));
 }
 
-void ensure_min_support(Ctx& c, const DCsr& filtered, const DCsr& full, int32_t min_cols, DCsr& out) {
+void ensure_min_support(Ctx& c, const DCsr& filtered, const DCsr& full, int32_t min_cols, DCsr& out, const double* Bc,
+                        int32_t k) {
     if (filtered.nr != full.nr || filtered.nc != full.nc) throw InvalidArgument("ensure_min_support: shape mismatch");
-    build_rows(c, filtered.nr, filtered.nc, filtered.bs, out, k_min_support, blocks_for(filtered.nr, 128), 128,
+    if (Bc && k > kKMax) throw InvalidArgument("ensure_min_support: at most 8 candidates on the GPU path");
+    DBuf<int32_t> err(1, c.s);
+    AMG_CK(cudaMemsetAsync(err.get(), 0, sizeof(int32_t), c.s));
+    build_rows(c, filtered.nr, filtered.nc, filtered.bs, out, k_min_support_rows, blocks_for(filtered.nr, 64), 64,
                filtered.nr, filtered.rp.get(), filtered.ci.get(), filtered.va.get(), full.rp.get(), full.ci.get(),
-               full.va.get(), min_cols);
+               full.va.get(), min_cols, Bc, k, filtered.nc, err.get());
+    if (read_scalar(c, err.get()))
+        throw InvalidArgument("ensure_min_support: rows above 64 entries are not on the GPU path");
 }
 
 void widen_deficient_rows(Ctx& c, const DCsr& N, const DCsr& S, const DAgg& agg, int32_t min_aggs, DCsr& out) {

@@ -8,7 +8,10 @@ namespace amgcu {
 // add_aggregate_entries (hierarchy.hpp:98-110)
 void add_aggregate_entries(Ctx& c, const DCsr& N, const DAgg& agg, DCsr& out);
 // ensure_min_support without Bc (interpolation.hpp:607-643; the prefilter path)
-void ensure_min_support(Ctx& c, const DCsr& filtered, const DCsr& full, int32_t min_cols, DCsr& out);
+// ensure_min_support (interpolation.hpp:607-643); with Bc (n_c x k, column-major) the
+// span-rank floor of the post-filter
+void ensure_min_support(Ctx& c, const DCsr& filtered, const DCsr& full, int32_t min_cols, DCsr& out,
+                        const double* Bc = nullptr, int32_t k = 0);
 // widen_deficient_rows (hierarchy.hpp:118-154)
 void widen_deficient_rows(Ctx& c, const DCsr& N, const DCsr& S, const DAgg& agg, int32_t min_aggs, DCsr& out);
 // unamalgamate (aggregation.hpp:103-127) + root_node_pattern (interpolation.hpp:53-77)

@@ -5,6 +5,8 @@
 // given bit-identical inputs (SURVEY.md §7 hard part 1).
 #pragma once
 
+#include <memory>
+
 #include "device.cuh"
 
 namespace amgcu {
@@ -58,8 +60,24 @@ void classical_strength(Ctx& c, const DCsr& A, double theta, DCsr& S);
 // evolution strength (strength.hpp:116-238); winv per row
 void evolution_strength(Ctx& c, const DCsr& A, const DCsr& At, const double* winv, double drop_tol, int steps,
                         DCsr& S);
-// WorkLedger count of evolution_strength on A (exact; computed on demand)
-double evolution_ops(Ctx& c, const DCsr& A, const DCsr& At, int steps);
+// WorkLedger count of evolution_strength on A (exact).  Started on the context's side
+// stream right after the SOC (it reuses the SOC's transpose, kept here for the host
+// fallback of large balls) so it overlaps the rest of the setup; collected by
+// evolution_ops_finish.
+struct EvoCount {
+    DCsr At;
+    DBuf<unsigned long long> total;
+    DBuf<int32_t> ovf, novf;
+    int steps = 0;
+    cudaStream_t s = nullptr;     // stream the buffers are released on
+    cudaEvent_t done = nullptr;   // recorded on the side stream after the count
+    EvoCount() = default;
+    EvoCount(const EvoCount&) = delete;
+    EvoCount& operator=(const EvoCount&) = delete;
+    ~EvoCount();
+};
+std::unique_ptr<EvoCount> evolution_ops_start(Ctx& c, const DCsr& A, DCsr&& At, int steps);
+double evolution_ops_finish(Ctx& c, const DCsr& A, EvoCount& e);
 void normalize_strength(Ctx& c, const DCsr& S, DCsr& N);
 void amalgamate(Ctx& c, const DCsr& S, int32_t m, DCsr& N);
 struct DAgg {

@@ -38,6 +38,18 @@ void note_sync_site(const char* file, int line) {
     s.n[std::string(base ? base + 1 : file) + ":" + std::to_string(line)] += 1;
 }
 
+bool launch_check_enabled() {
+    static const bool on = std::getenv("AMGCU_LAUNCH_CHECK") != nullptr;
+    return on;
+}
+
+void launch_check(Ctx& c, const void* kernel) {
+    const cudaError_t e = cudaStreamSynchronize(c.s);
+    if (e == cudaSuccess) return;
+    const char* name = nullptr;
+    if (cudaFuncGetName(&name, kernel) != cudaSuccess || !name) name = "?";
+    throw CudaFailure(std::string("kernel ") + name + " failed: " + cudaGetErrorString(e));
+}
 
 namespace {
 

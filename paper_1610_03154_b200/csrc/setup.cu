@@ -88,11 +88,27 @@ void strength_of(Ctx& c, DLevel& L, const amgcu_setup_options& o, DCsr& S) {
             DCsr At;
             transpose(c, A, At);
             evolution_strength(c, A, At, winv.get(), o.drop_tol, o.evolution_steps, S);
-            L.evo_steps = o.evolution_steps;  // its ledger count is taken on demand (evolution_ops)
+            // its ledger count overlaps the rest of the setup (collected in rn_setup)
+            L.evo_steps = o.evolution_steps;
+            L.evo_count = evolution_ops_start(c, A, std::move(At), o.evolution_steps);
             return;
         }
     }
     throw InvalidArgument("strength: unknown measure");
+}
+
+// postfilter_pipeline (interpolation.hpp:648-659): drop small entries of P, restore
+// the support (rank floor over the coarse candidates), re-impose the constraints,
+// then one energy-minimisation iteration on the reduced pattern
+void postfilter(Ctx& c, const amgcu_setup_options& o, const DCsr& A, const DCsr& P, const double* B, const double* Bc,
+                int32_t k, int krylov, const int32_t* roots, int32_t n_roots, DCsr& out) {
+    DCsr Pf, Pm, Pe;
+    filter_matrix(c, P, o.postfilter_theta_set != 0, o.postfilter_theta, o.postfilter_k, Pf);
+    ensure_min_support(c, Pf, P, k, Pm, Bc, k);
+    enforce_constraints(c, Pm, B, Bc, k, nullptr, Pe);
+    Pe.bs = P.bs;
+    energy_minimize(c, A, Pe, B, Bc, k, Pe, 1, krylov, roots, n_roots, out, nullptr);
+    out.bs = P.bs;
 }
 
 bool coarsen(Ctx& c, DHier& H, int level, const double* Bhat, Coarsened& out) {
@@ -160,9 +176,13 @@ bool coarsen(Ctx& c, DHier& H, int level, const double* Bhat, Coarsened& out) {
     int kry = o.krylov;
     if (!L.symmetric && kry == 0) kry = 1;
     const int iters = energy_iterations(o);
-    if (o.postfilter_set) throw InvalidArgument("rn_setup: post-filtering is not on the GPU path yet");
     energy_minimize(c, A, T, Bimp.get(), Bc.get(), k, Nd, iters, kry, droots.get(), agg.n_agg * m, out.P, nullptr);
     out.P.bs = T.bs;
+    if (o.postfilter_set) {
+        DCsr Pp;
+        postfilter(c, o, A, out.P, Bimp.get(), Bc.get(), k, kry, droots.get(), agg.n_agg * m, Pp);
+        out.P = std::move(Pp);
+    }
 
     if (L.symmetric) {
         transpose(c, out.P, out.R);
@@ -182,6 +202,11 @@ bool coarsen(Ctx& c, DHier& H, int level, const double* Bhat, Coarsened& out) {
         inject_tentative(c, agg, Nd, Bh.get(), k, m, That, Bhc);
         energy_minimize(c, At, That, Bh.get(), Bhc.get(), k, Nd, iters, 1, droots.get(), agg.n_agg * m, Rt, nullptr);
         Rt.bs = That.bs;
+        if (o.postfilter_set) {
+            DCsr Rp;
+            postfilter(c, o, At, Rt, Bh.get(), Bhc.get(), k, 1, droots.get(), agg.n_agg * m, Rp);
+            Rt = std::move(Rp);
+        }
         transpose(c, Rt, out.R);
         out.Bhc = std::move(Bhc);
     }
@@ -416,6 +441,11 @@ std::unique_ptr<DHier> rn_setup(Ctx& c, const DCsr& A, const double* B, int32_t 
         }
     }
     coarse_factor(c, *H);
+    for (DLevel& L : H->lv)
+        if (L.evo_count) {
+            L.evo_ops = evolution_ops_finish(c, L.A, *L.evo_count);
+            L.evo_count.reset();
+        }
     {
         const double nL = static_cast<double>(H->lv.back().A.nr);
         tally(c, nL * nL * nL);  // hierarchy.hpp:68
@@ -423,6 +453,28 @@ std::unique_ptr<DHier> rn_setup(Ctx& c, const DCsr& A, const double* B, int32_t 
     H->wu[4] = cfin / H->base_nnz;
     prepare_solve(*H);
     return H;
+}
+
+void hier_ledger(DHier& H, double wu[5]) {
+    Ctx& c = *H.ctx;
+    for (int b = 0; b < 5; ++b) wu[b] = 0.0;
+    for (size_t l = 0; l + 1 < H.lv.size(); ++l) {
+        DLevel& L = H.lv[l];
+        if (L.evo_steps > 0 && L.evo_ops < 0.0) {  // not collected by the setup
+            OpsScope none(c, nullptr);
+            DCsr At;
+            transpose(c, L.A, At);
+            L.evo_count = evolution_ops_start(c, L.A, std::move(At), L.evo_steps);
+            L.evo_ops = evolution_ops_finish(c, L.A, *L.evo_count);
+            L.evo_count.reset();
+        }
+        // charges in level order, as the reference's coarsening loop (hierarchy.hpp:243)
+        wu[0] += (L.ledger[0] + (L.evo_steps > 0 ? L.evo_ops : 0.0)) / H.base_nnz;
+        wu[1] += L.ledger[1] / H.base_nnz;
+        wu[2] += L.ledger[2] / H.base_nnz;
+        wu[3] += L.ledger[3] / H.base_nnz;
+    }
+    wu[4] = H.wu[4];  // finalize + every solve so far
 }
 
 }  // namespace amgcu

@@ -275,7 +275,7 @@ struct COD {
     std::vector<int> perm;  // column j of A P is column perm[j] of A
     std::vector<double> src;
 
-    static double make_householder(double* x, int len, int stride, double* tau) {
+    SD_HD static double make_householder(double* x, int len, int stride, double* tau) {
         double tail = 0.0;
         for (int i = 1; i < len; ++i) tail += x[i * stride] * x[i * stride];
         const double c0 = x[0];
@@ -429,6 +429,53 @@ struct COD {
         }
     }
 };
+
+// Rank of a row-major r x c matrix by Householder QR with column pivoting, as
+// COD::qr_only followed by rank_for(thr) (ColPivHouseholderQR + setThreshold:
+// the span_rank of ensure_min_support, interpolation.hpp:585-595), with the same
+// operation order; usable on the device.  `qr` is overwritten.  c <= CMAX.
+template <int CMAX>
+SD_HD int qr_rank(int r, int c, double* qr, double thr) {
+    const int size = r < c ? r : c;
+    double rdiag[CMAX];
+    double maxpivot = 0.0;
+    int nonzero = size;
+    for (int k = 0; k < size; ++k) {
+        int best = k;
+        double bn = -1.0;
+        for (int j = k; j < c; ++j) {
+            double s2 = 0.0;
+            for (int i = k; i < r; ++i) s2 += qr[i * c + j] * qr[i * c + j];
+            if (s2 > bn) {
+                bn = s2;
+                best = j;
+            }
+        }
+        if (bn == 0.0 && nonzero == size) nonzero = k;
+        if (best != k) {
+            for (int i = 0; i < r; ++i) {
+                const double t = qr[i * c + k];
+                qr[i * c + k] = qr[i * c + best];
+                qr[i * c + best] = t;
+            }
+        }
+        double tau;
+        const double beta = COD::make_householder(&qr[k * c + k], r - k, c, &tau);
+        qr[k * c + k] = beta;
+        rdiag[k] = beta;
+        if (dabs(beta) > maxpivot) maxpivot = dabs(beta);
+        for (int j = k + 1; j < c; ++j) {
+            double s2 = qr[k * c + j];
+            for (int i = k + 1; i < r; ++i) s2 += qr[i * c + k] * qr[i * c + j];
+            s2 = tau * s2;
+            qr[k * c + j] -= s2;
+            for (int i = k + 1; i < r; ++i) qr[i * c + j] -= qr[i * c + k] * s2;
+        }
+    }
+    int rk = 0;
+    for (int i = 0; i < nonzero; ++i) rk += (dabs(rdiag[i]) > thr * maxpivot) ? 1 : 0;
+    return rk;
+}
 
 // ---------------------------------------------------------------------------
 // Eigenvalues of a real upper-Hessenberg matrix by the Francis double-shift

@@ -799,20 +799,55 @@ void amalgamate(Ctx& c, const DCsr& S, int32_t m, DCsr& N) {
     two_pass(c, nn, S.nc / m, 1, N, k_amalgamate, blocks_for(nn, 128), 128, nn, m, S.rp.get(), S.ci.get(), S.va.get());
 }
 
-double evolution_ops(Ctx& c, const DCsr& A, const DCsr& At, int steps) {
+EvoCount::~EvoCount() {
+    if (done) {
+        // the buffers are freed stream-ordered on s: after the count has read them
+        cudaStreamWaitEvent(s, done, 0);
+        cudaEventDestroy(done);
+    }
+}
+
+std::unique_ptr<EvoCount> evolution_ops_start(Ctx& c, const DCsr& A, DCsr&& At, int steps) {
     const int32_t n = A.nr;
-    DBuf<unsigned long long> total(1, c.s);
-    DBuf<int32_t> ovf(static_cast<size_t>(n) + 1, c.s), novf(1, c.s);
-    AMG_CK(cudaMemsetAsync(total.get(), 0, sizeof(unsigned long long), c.s));
-    AMG_CK(cudaMemsetAsync(novf.get(), 0, sizeof(int32_t), c.s));
-    launch(c, k_evolution_count, blocks_for(n, kEvWarps), kEvWarps * kWarp, 0, n, A.rp.get(), A.ci.get(), At.rp.get(),
-           At.ci.get(), steps, total.get(), ovf.get(), novf.get());
-    double ops = static_cast<double>(read_scalar(c, total.get()));
-    const int32_t nbig = read_scalar(c, novf.get());
+    auto e = std::make_unique<EvoCount>();
+    e->steps = steps;
+    e->s = c.s;
+    e->At = std::move(At);
+    e->total.alloc(1, c.s);
+    e->ovf.alloc(static_cast<size_t>(n) + 1, c.s);
+    e->novf.alloc(1, c.s);
+    AMG_CK(cudaMemsetAsync(e->total.get(), 0, sizeof(unsigned long long), c.s));
+    AMG_CK(cudaMemsetAsync(e->novf.get(), 0, sizeof(int32_t), c.s));
+    cudaEvent_t ready;
+    AMG_CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    AMG_CK(cudaEventRecord(ready, c.s));
+    AMG_CK(cudaStreamWaitEvent(c.side, ready, 0));
+    cudaEventDestroy(ready);
+    if (n > 0) {
+        k_evolution_count<<<blocks_for(n, kEvWarps), kEvWarps * kWarp, 0, c.side>>>(
+            n, A.rp.get(), A.ci.get(), e->At.rp.get(), e->At.ci.get(), steps, e->total.get(), e->ovf.get(),
+            e->novf.get());
+        ++c.launches;
+        AMG_CK(cudaGetLastError());
+    }
+    AMG_CK(cudaEventCreateWithFlags(&e->done, cudaEventDisableTiming));
+    AMG_CK(cudaEventRecord(e->done, c.side));
+    return e;
+}
+
+double evolution_ops_finish(Ctx& c, const DCsr& A, EvoCount& e) {
+    const int32_t n = A.nr;
+    const int steps = e.steps;
+    AMG_CK(cudaStreamWaitEvent(c.s, e.done, 0));
+    stage_scalar(c, 0, e.total.get());
+    stage_scalar(c, 1, e.novf.get());
+    sync(c);
+    double ops = static_cast<double>(staged<unsigned long long>(c, 0));
+    const int32_t nbig = staged<int32_t>(c, 1);
     if (nbig > 0) {  // large balls: the reference's BFS on the host
-        const HostCsr ha = download_csr(c, A), ht = download_csr(c, At);
+        const HostCsr ha = download_csr(c, A), ht = download_csr(c, e.At);
         std::vector<int32_t> rows(nbig), slot(n, -1), hood;
-        copy_d2h(c, rows.data(), ovf.get(), nbig);
+        copy_d2h(c, rows.data(), e.ovf.get(), nbig);
         sync(c);
         for (int32_t i : rows) {
             hood.assign(1, i);

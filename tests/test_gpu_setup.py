@@ -106,6 +106,42 @@ def test_work_ledger_matches_reference(gpu_seq, port, name, gen, so, vo):
     assert hg.ledger().tobytes() == ho.ledger().tobytes(), (hg.ledger(), ho.ledger())
 
 
+def _postfilter_cases():
+    cases = []
+    so = SetupOptions(pre_relax=JAC, post_relax=JAC, max_size=40)
+    so.interp.prefilter = FilterRule(0.1, None)
+    so.interp.postfilter = FilterRule(0.1, None)
+    so.interp.energy_iters = 6
+    cases.append(("rotated-post", lambda: api.generate_config(2, 33), so, SolveOptions(SolveMethod.pcg)))
+    so = SetupOptions(strength=StrengthConfig(StrengthMeasure.symmetric, 0.1), pre_relax=JAC, post_relax=JAC,
+                      max_size=40)
+    so.interp.postfilter = FilterRule(0.2, None)
+    so.interp.energy_iters = 4
+    cases.append(("elasticity-post", lambda: api.generate_config(5, 12), so, SolveOptions(SolveMethod.pcg)))
+    so = SetupOptions(pre_relax=JAC, post_relax=JAC, max_size=40)
+    so.interp.krylov = KrylovKind.gmres
+    so.interp.energy_iters = 4
+    so.interp.postfilter = FilterRule(None, 3)
+    cases.append(("recirc-post-k3", lambda: api.generate_config(3, 24), so,
+                  SolveOptions(SolveMethod.fgmres, max_iters=30)))
+    return cases
+
+
+@pytest.mark.parametrize("name,gen,so,vo", _postfilter_cases(), ids=[c[0] for c in _postfilter_cases()])
+def test_postfilter_bitwise(gpu_seq, port, name, gen, so, vo):
+    """post-filter pipeline (interpolation.hpp:648-659): filter, support floor with the
+    span-rank test and the reference's std::sort tie order, constraints, one energy-min
+    iteration -- every level bitwise, ledger equal"""
+    A, B, Bh, b = gen()
+    hg = api.setup(A, B, so, Bh, ctx=gpu_seq)
+    ho = port.setup(A, B, so, Bh)
+    compare(hg, ho, bitwise=True)
+    assert hg.ledger().tobytes() == ho.ledger().tobytes()
+    xg, rg = api.solve(hg, b, None, vo)
+    xo, ro = port.solve(ho, b, None, vo)
+    assert rg.iterations == ro.iterations
+
+
 def test_work_ledger_options(gpu_seq, port):
     """ledger under the other count paths: symmetric SOC, Jacobi candidate improvement
     (its spectral estimate), l1-weighted evolution, degree 1"""

@@ -30,7 +30,8 @@ def load_golden(name):
     return z, A, B, Bh, z["b"]
 
 
-def check_against_golden(z, h, x, rep, values_bitwise=True, tol=1e-10):
+def check_against_golden(z, h, x, rep, values_bitwise=True, tol=1e-10, solve_bitwise=None):
+    solve_bitwise = values_bitwise if solve_bitwise is None else solve_bitwise
     assert h.n_levels() == int(z["levels"][0])
     assert int(h.stagnated) == int(z["stagnated"][0])
     for l in range(h.n_levels()):
@@ -53,7 +54,7 @@ def check_against_golden(z, h, x, rep, values_bitwise=True, tol=1e-10):
     hist = np.array(rep.residual_history)
     assert rep.iterations == int(z["its"][0])
     assert int(rep.converged) == int(z["its"][1])
-    if values_bitwise:
+    if solve_bitwise:
         assert hist.tobytes() == z["hist"].tobytes()
         assert x.tobytes() == z["x"].tobytes()
     else:
