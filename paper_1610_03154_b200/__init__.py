@@ -17,6 +17,10 @@ def __getattr__(name):
     if name.startswith("__"):
         raise AttributeError(name)
     import importlib
+    if name in ("build", "api", "types", "replicas", "_abi"):
+        # submodules: `from paper_1610_03154_b200 import build` must work before
+        # libamgcu.so exists (a fresh checkout builds through it)
+        return importlib.import_module(__name__ + "." + name)
     api = importlib.import_module(__name__ + ".api")
     if hasattr(api, name):
         return getattr(api, name)
