@@ -31,7 +31,8 @@ CXX_FLAGS = ["-O3", "-std=gnu++20", "-fPIC", "-ffp-contract=off", "-I" + os.path
 CU_SOURCES = ["primitives.cu", "sparse_core.cu", "blas.cu", "strength.cu", "aggregate.cu", "relax.cu", "arnoldi.cu",
               "interp.cu", "setup.cu", "cycle.cu", "capi.cu"]
 CXX_SOURCES = ["problems.cpp"]
-HEADERS = ["device.cuh", "ops.cuh", "interp.cuh", "hier.cuh", "host_common.h", "small_dense.h"]
+# every header in csrc (a header edit must rebuild its includers)
+HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith((".cuh", ".h")))
 
 
 def _digest(paths):

@@ -100,7 +100,13 @@ struct ProfRecord {
     double bytes = 0.0;
     double ms = 0.0;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending;
+    std::vector<const void*> kernels;  // kProfOther with AMGCU_PROF_OTHER: symbol per pending pair
 };
+
+// AMGCU_PROF_OTHER=1: untagged launches are also timed per kernel symbol and the
+// breakdown is printed to stderr when the profile is read (tools/family_times.py)
+bool prof_other_enabled();
+void prof_other_add(const void* kernel, double ms);
 
 struct Ctx {
     bool profile = false;
@@ -244,20 +250,24 @@ inline void launch_prof(Ctx& c, int family, double bytes, Kern k, unsigned grid,
     r.launches += 1;
     r.bytes += bytes;
     r.pending.emplace_back(e0, e1);
+    if (family == kProfOther && prof_other_enabled()) r.kernels.push_back(reinterpret_cast<const void*>(k));
 }
 
 // resolve pending event pairs into milliseconds (synchronises)
 inline void prof_collect(Ctx& c) {
     AMG_CK(cudaStreamSynchronize(c.s));
     for (auto& r : c.prof) {
-        for (auto& pr : r.pending) {
+        for (size_t q = 0; q < r.pending.size(); ++q) {
+            auto& pr = r.pending[q];
             float ms = 0.f;
             AMG_CK(cudaEventElapsedTime(&ms, pr.first, pr.second));
             r.ms += ms;
+            if (q < r.kernels.size()) prof_other_add(r.kernels[q], ms);
             c.event_pool.push_back(pr.first);
             c.event_pool.push_back(pr.second);
         }
         r.pending.clear();
+        r.kernels.clear();
     }
 }
 

@@ -881,6 +881,13 @@ __global__ void k_min_support_rows(int32_t n, const int32_t* __restrict__ frp, c
     }
 }
 
+// rows below min(min_cols, |full row|) entries (the count floor; no rank floor)
+__global__ void k_support_short(int32_t n, const int32_t* __restrict__ frp, const int32_t* __restrict__ grp,
+                                int32_t min_cols, int32_t* __restrict__ flag) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n && frp[i + 1] - frp[i] < min(min_cols, grp[i + 1] - grp[i])) atomicExch(flag, 1);
+}
+
 // two-pass helper for row kernels with (..., orp, cnt, oci, ova) tails
 template <typename K, typename... Args>
 void build_rows(Ctx& c, int32_t nr, int32_t nc, int32_t bs, DCsr& out, K k, unsigned grid, unsigned block,
@@ -919,6 +926,17 @@ void ensure_min_support(Ctx& c, const DCsr& filtered, const DCsr& full, int32_t 
     if (Bc && k > kKMax) throw InvalidArgument("ensure_min_support: at most 8 candidates on the GPU path");
     DBuf<int32_t> err(1, c.s);
     AMG_CK(cudaMemsetAsync(err.get(), 0, sizeof(int32_t), c.s));
+    if (!Bc) {
+        // count floor only: rows already at the floor keep their entries (interpolation.hpp:623),
+        // so when none is below it the result is the filtered matrix itself
+        launch(c, k_support_short, blocks_for(filtered.nr, 256), 256, 0, filtered.nr, filtered.rp.get(),
+               full.rp.get(), min_cols, err.get());
+        if (!read_scalar(c, err.get())) {
+            clone_csr(c, filtered, out);
+            return;
+        }
+        AMG_CK(cudaMemsetAsync(err.get(), 0, sizeof(int32_t), c.s));
+    }
     build_rows(c, filtered.nr, filtered.nc, filtered.bs, out, k_min_support_rows, blocks_for(filtered.nr, 64), 64,
                filtered.nr, filtered.rp.get(), filtered.ci.get(), filtered.va.get(), full.rp.get(), full.ci.get(),
                full.va.get(), min_cols, Bc, k, filtered.nc, err.get());

@@ -5,7 +5,9 @@
 
 #include "device.cuh"
 
+#include <algorithm>
 #include <cstdio>
+#include <vector>
 #include <cstring>
 #include <cstdlib>
 #include <map>
@@ -36,6 +38,39 @@ void note_sync_site(const char* file, int line) {
     const char* base = std::strrchr(file, '/');
     std::lock_guard<std::mutex> g(s.m);
     s.n[std::string(base ? base + 1 : file) + ":" + std::to_string(line)] += 1;
+}
+
+namespace {
+struct OtherKernels {
+    std::mutex m;
+    std::map<std::string, std::pair<long, double>> t;  // symbol -> (launches, ms)
+    ~OtherKernels() {
+        std::vector<std::pair<double, std::string>> v;
+        for (auto& kv : t) v.emplace_back(kv.second.second, kv.first);
+        std::sort(v.rbegin(), v.rend());
+        for (auto& e : v)
+            std::fprintf(stderr, "other %9.3f ms %6ld x  %s\n", e.first, t[e.second].first, e.second.c_str());
+    }
+};
+OtherKernels& other_kernels() {
+    static OtherKernels o;
+    return o;
+}
+}  // namespace
+
+bool prof_other_enabled() {
+    static const bool on = std::getenv("AMGCU_PROF_OTHER") != nullptr;
+    return on;
+}
+
+void prof_other_add(const void* kernel, double ms) {
+    const char* name = nullptr;
+    if (cudaFuncGetName(&name, kernel) != cudaSuccess || !name) name = "?";
+    OtherKernels& o = other_kernels();
+    std::lock_guard<std::mutex> g(o.m);
+    auto& e = o.t[name];
+    e.first += 1;
+    e.second += ms;
 }
 
 bool launch_check_enabled() {

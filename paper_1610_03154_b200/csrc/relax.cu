@@ -44,7 +44,6 @@ constexpr int kMaxK = 8;
 // Items (sweep, segment) draw tickets in (sweep, position) order; segments are
 // contiguous, so any unfinished row that an item waits on belongs to an item
 // with a smaller ticket, which is already running: the launch cannot deadlock.
-constexpr int kSegMaxE = 32;  // entries per row handled from the prefetch records
 constexpr int kChunk = 8;     // prefetcher: entries loaded per batch
 constexpr unsigned long long kPending = 0x7FF4A11CE5EEDULL;
 
@@ -96,7 +95,7 @@ __device__ __forceinline__ void vstore(int* p, int v) { *reinterpret_cast<volati
 //     wait until the slot is no longer kPending, then acc -= a * x.  The step
 //     is a short branch-free loop over registers (the i-cache matters here:
 //     the three roles run side by side on the SM).
-// Rows whose entries do not fit the records (more than kSegMaxE, or more
+// Rows whose entries do not fit the records (more than E, or more
 // pending values than the poll list) take a rolled slow path that polls
 // global memory directly.
 // Hand-shakes (shared memory, volatile): ready[b] = block sequence number the
@@ -104,7 +103,11 @@ __device__ __forceinline__ void vstore(int* p, int v) { *reinterpret_cast<volati
 // done + 1 finished; plo = lowest block the poller may still touch (the
 // prefetcher refills a buffer only when neither the solver nor the poller
 // can still use it).  Arrays are stored [.][lane] (conflict-free).
-constexpr int kMaxPoll = 16;  // pending (entry, column) values tracked per row
+// pending (entry, column) values tracked per row
+template <int E>
+constexpr int gs_max_poll() {
+    return E <= 16 ? 8 : 16;
+}
 // Sibling segments (earlier segments of the same sweep in the same CTA) hand values
 // over through shared memory: every solver keeps its last kRing published rows in a
 // tagged ring; a consumer reads tag, value, tag (the producer invalidates the tag
@@ -116,32 +119,36 @@ constexpr unsigned kWarpRowPollNs = 32;  // poll back-off cap of the warp-per-ro
 constexpr int32_t kProductTerm = -1;  // term whose product a * x is precomputed (K = 1)
 constexpr int kSibling = 4;  // entry class: pending value of a sibling segment
 
-template <int K>
+// E: entries per row handled from the records (longer rows take the slow path)
+template <int K, int E>
 struct GsBuf {
-    unsigned long long bits[kSegMaxE][K][32];  // value slots (c stride = 32 words)
-    double ta[kSegMaxE][32];                   // term: matrix value
-    int32_t toff[kSegMaxE][32];                // term: slot offset (bytes from the segment base)
-    const double* paddr[kMaxPoll][32];         // poll list: address
-    int32_t pslot[kMaxPoll][32];               // poll list: word offset of the slot in bits
+    unsigned long long bits[E][K][32];        // value slots (c stride = 32 words)
+    double ta[E][32];                         // term: matrix value
+    int32_t toff[E][32];                      // term: slot offset (bytes from the segment base)
+    uint32_t paddr[gs_max_poll<E>()][32];     // poll list: element offset of the value in X
+    int16_t pslot[gs_max_poll<E>()][32];      // poll list: word offset of the slot in bits
     double acc0[K][32];
     double dinv[32];
     int32_t nterm[32];  // -1: slow path
     int32_t npoll[32];
 };
 
-template <int K>
+// segments per CTA: 8 short-row (E = 16) single-column segments fit one SM (24 warps,
+// ~205 KB), so a 1024-row-grid level is resident at once
+template <int K, int E>
 constexpr int gs_segs_per_cta() {
-    return K == 1 ? 4 : (K <= 3 ? 2 : 1);
+    return K == 1 ? (E <= 16 ? 8 : 4) : (K <= 3 ? 2 : 1);
 }
+constexpr int kSwBits = 3;  // sibling index bits in a sibling term code (<= 8 segments per CTA)
 
-template <int K>
+template <int K, int E>
 constexpr size_t gs_ring_offset() {
-    return (2 * sizeof(GsBuf<K>) + 64 * K * sizeof(double) + 15) / 16 * 16;
+    return (2 * sizeof(GsBuf<K, E>) + 64 * K * sizeof(double) + 15) / 16 * 16;
 }
 
-template <int K>
+template <int K, int E>
 constexpr size_t gs_seg_bytes() {
-    return gs_ring_offset<K>() + (K == 1 ? kRing * (sizeof(double) + sizeof(int32_t)) : 0);
+    return gs_ring_offset<K, E>() + (K == 1 ? kRing * (sizeof(double) + sizeof(int32_t)) : 0);
 }
 
 struct GsRing {
@@ -149,15 +156,15 @@ struct GsRing {
     int32_t* tag;
 };
 
-template <int K>
+template <int K, int E>
 __device__ __forceinline__ GsRing gs_ring(unsigned char* smem_base, int w) {
-    unsigned char* r = smem_base + static_cast<size_t>(w) * gs_seg_bytes<K>() + gs_ring_offset<K>();
+    unsigned char* r = smem_base + static_cast<size_t>(w) * gs_seg_bytes<K, E>() + gs_ring_offset<K, E>();
     return {reinterpret_cast<double*>(r), reinterpret_cast<int32_t*>(r + kRing * sizeof(double))};
 }
 
 // value of row qj of a sibling segment: from its ring, or (already overwritten) from global
 __device__ __forceinline__ unsigned long long sibling_value(const GsRing& rg, int32_t qj, int32_t tagv,
-                                                            const double* gaddr, unsigned max_ns) {
+                                                            const double* gaddr, unsigned max_ns, unsigned spin_ns) {
     const int idx = qj & (kRing - 1);
     // tag, value, tag (volatile shared loads; the producer fences between its stores)
     while (true) {
@@ -168,20 +175,21 @@ __device__ __forceinline__ unsigned long long sibling_value(const GsRing& rg, in
         } else if (t1 > tagv) {
             break;
         }
-        __nanosleep(20);
+        if (spin_ns) __nanosleep(spin_ns);
     }
     return static_cast<unsigned long long>(__double_as_longlong(wait_bits(gaddr, load_relaxed_bits(gaddr), max_ns)));
 }
 
-template <int K>
-__global__ void __launch_bounds__(3 * gs_segs_per_cta<K>() * 32)
+template <int K, int E>
+__global__ void __launch_bounds__(3 * gs_segs_per_cta<K, E>() * 32)
     k_gs_segments(int32_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
                   const double* __restrict__ va, const double* __restrict__ inv_diag, const double* __restrict__ b,
                   int nsweeps, const unsigned char* __restrict__ backward, const int32_t* __restrict__ item_base,
                   const int32_t* __restrict__ seg_fwd, const int32_t* __restrict__ seg_bwd, double* __restrict__ X,
                   unsigned int* __restrict__ ticket, unsigned max_ns, unsigned long long* __restrict__ trace,
-                  int poll_window, int sweep_loop) {
-    constexpr int S = gs_segs_per_cta<K>();
+                  int poll_window, int sweep_loop, unsigned spin_ns) {
+    constexpr int S = gs_segs_per_cta<K, E>();
+    constexpr int kMaxPoll = gs_max_poll<E>();
     extern __shared__ unsigned long long smem[];
     __shared__ unsigned int blk;
     __shared__ int sh_ready[S][2], sh_done[S], sh_step[S], sh_plo[S];
@@ -195,7 +203,7 @@ __global__ void __launch_bounds__(3 * gs_segs_per_cta<K>() * 32)
     }
     if (K == 1)
         for (int e = threadIdx.x; e < S * kRing; e += blockDim.x)
-            gs_ring<K>(reinterpret_cast<unsigned char*>(smem), e / kRing).tag[e % kRing] = -1;
+            gs_ring<K, E>(reinterpret_cast<unsigned char*>(smem), e / kRing).tag[e % kRing] = -1;
     __syncthreads();
     // sweep_loop (forward sweeps): items are the segments of sweep 0 and every segment
     // runs all sweeps in turn; otherwise items are (sweep, segment) in sweep-major order
@@ -236,11 +244,11 @@ __global__ void __launch_bounds__(3 * gs_segs_per_cta<K>() * 32)
     const int nblocks = (q1 - q0 + 31) / 32;
     const int tblocks = nsw_loop * nblocks;  // hand-shake sequence numbers run over all sweeps
     const size_t stride = static_cast<size_t>(n) * K;
-    unsigned char* segmem = reinterpret_cast<unsigned char*>(smem) + static_cast<size_t>(wl) * gs_seg_bytes<K>();
-    GsBuf<K>* buf = reinterpret_cast<GsBuf<K>*>(segmem);
+    unsigned char* segmem = reinterpret_cast<unsigned char*>(smem) + static_cast<size_t>(wl) * gs_seg_bytes<K, E>();
+    GsBuf<K, E>* buf = reinterpret_cast<GsBuf<K, E>*>(segmem);
     // values published by the solver: xb[block & 1][c][lane]
-    unsigned long long* xb = reinterpret_cast<unsigned long long*>(segmem + 2 * sizeof(GsBuf<K>));
-    const int32_t xb_off = static_cast<int32_t>(2 * sizeof(GsBuf<K>));
+    unsigned long long* xb = reinterpret_cast<unsigned long long*>(segmem + 2 * sizeof(GsBuf<K, E>));
+    const int32_t xb_off = static_cast<int32_t>(2 * sizeof(GsBuf<K, E>));
 
     if (role == 2) {
         // ---------------- prefetcher ----------------
@@ -251,8 +259,8 @@ __global__ void __launch_bounds__(3 * gs_segs_per_cta<K>() * 32)
             if (G >= 2)
                 while (vload(&sh_done[wl]) < G - 2 || vload(&sh_plo[wl]) < G - 1) __nanosleep(32);
             __threadfence_block();
-            GsBuf<K>& B = buf[G & 1];
-            const int32_t buf_off = static_cast<int32_t>((G & 1) * sizeof(GsBuf<K>));
+            GsBuf<K, E>& B = buf[G & 1];
+            const int32_t buf_off = static_cast<int32_t>((G & 1) * sizeof(GsBuf<K, E>));
             const int32_t qb = q0 + 32 * seq;
             const int32_t q = qb + lane;
             const bool active = q < q1;
@@ -271,9 +279,9 @@ __global__ void __launch_bounds__(3 * gs_segs_per_cta<K>() * 32)
                     for (int c = 0; c < K; ++c) acc[c] = b[static_cast<size_t>(c) * n + i];
                 }
             }
-            const int32_t ne = min(hi - lo, kSegMaxE);
+            const int32_t ne = min(hi - lo, E);
             int np = 0;
-            bool slow = active && hi - lo > kSegMaxE;
+            bool slow = active && hi - lo > E;
             // pass 1, kChunk entries at a time: class, slot and every independent value.
             // Staging: ta[e] = a, toff[e] = class | xb offset << 2.
             for (int e0 = 0; e0 < ne; e0 += kChunk) {
@@ -337,15 +345,16 @@ __global__ void __launch_bounds__(3 * gs_segs_per_cta<K>() * 32)
                                     if (sh_ss[w2] == s_item && qj >= sh_sq0[w2] && qj < sh_sq1[w2]) sw = w2;
                                 if (sw >= 0) {
                                     cls[u] = kSibling;
-                                    xslot[u] = ((qj - sh_sq0[sw]) << 2) | sw;
+                                    xslot[u] = ((qj - sh_sq0[sw]) << kSwBits) | sw;
                                 }
                             }
                             if (xv[u] == kPending && sw < 0) {
                                 if (np < kMaxPoll) {
                                     const int32_t j = jj[u];
                                     const int32_t qj = bwd ? n - 1 - j : j;
-                                    B.paddr[np][lane] = &((qj < q) ? xout : xin)[static_cast<size_t>(c) * n + j];
-                                    B.pslot[np][lane] = (e * K + c) * 32 + lane;
+                                    B.paddr[np][lane] = static_cast<uint32_t>(
+                                        static_cast<size_t>((qj < q) ? s + 1 : s) * stride + static_cast<size_t>(c) * n + j);
+                                    B.pslot[np][lane] = static_cast<int16_t>((e * K + c) * 32 + lane);
                                     ++np;
                                 } else {
                                     slow = true;
@@ -435,10 +444,10 @@ __global__ void __launch_bounds__(3 * gs_segs_per_cta<K>() * 32)
                 const int rel = h * 32 + lane - step;  // rows ahead of the solver
                 const unsigned m = (rel < 0 || rel >= poll_window) ? 0u : mask[sl];
                 if (!m) continue;
-                GsBuf<K>& B = buf[sl];
+                GsBuf<K, E>& B = buf[sl];
                 unsigned long long got[kMaxPoll];
 #pragma unroll
-                for (int u = 0; u < kMaxPoll; ++u) got[u] = (m >> u) & 1u ? load_relaxed_bits(B.paddr[u][lane]) : kPending;
+                for (int u = 0; u < kMaxPoll; ++u) got[u] = (m >> u) & 1u ? load_relaxed_bits(X + B.paddr[u][lane]) : kPending;
 #pragma unroll
                 for (int u = 0; u < kMaxPoll; ++u) {
                     if (((m >> u) & 1u) && got[u] != kPending) {
@@ -454,8 +463,12 @@ __global__ void __launch_bounds__(3 * gs_segs_per_cta<K>() * 32)
             } else {
                 // nothing resolved: back off (longer when nothing is pending at all)
                 const bool any_more = __any_sync(0xffffffffu, more);
-                ns = ns ? min(2 * ns, any_more ? 64u : 512u) : 16u;
-                __nanosleep(ns);
+                if (any_more && !spin_ns) {
+                    ns = 0;  // values pending: keep polling
+                } else {
+                    ns = ns ? min(2 * ns, any_more ? 64u : 512u) : 16u;
+                    __nanosleep(ns);
+                }
             }
         }
         return;
@@ -474,7 +487,7 @@ __global__ void __launch_bounds__(3 * gs_segs_per_cta<K>() * 32)
         for (int c = 0; c < K; ++c) xb[((seq & 1) * K + c) * 32 + lane] = kPending;
         while (vload(&sh_ready[wl][G & 1]) != G) __nanosleep(32);
         __threadfence_block();
-        GsBuf<K>& B = buf[G & 1];
+        GsBuf<K, E>& B = buf[G & 1];
         if (tr && lane == 0) tr[1] = globaltimer_ns();
         // ---- phase B, warp-uniform: every lane evaluates row t from broadcast reads of
         // its records (no divergence, no reconvergence barriers); lane 0 publishes ----
@@ -484,7 +497,46 @@ __global__ void __launch_bounds__(3 * gs_segs_per_cta<K>() * 32)
             const int32_t i = bwd ? n - 1 - q : q;
             const int32_t nt = B.nterm[t];
             double acc[K];
-            if (nt >= 0) {
+            if (K == 1 && nt >= 0) {
+                // lane k resolves term k (its product a * x rounded, as the reference's
+                // acc - a * x rounds it); the warp then subtracts the products in term order
+                // from shuffles, so the serial part is the chain of subtractions alone
+                double p = 0.0;
+                if (lane < nt) {
+                    const double ak = B.ta[lane][t];
+                    const int32_t off = B.toff[lane][t];
+                    if (off == kProductTerm) {
+                        p = ak;
+                    } else if (off < 0) {
+                        const int32_t code = -2 - off;
+                        const int sw = code & ((1 << kSwBits) - 1);
+                        const int32_t qj = sh_sq0[sw] + (code >> kSwBits);
+                        const int32_t j = bwd ? n - 1 - qj : qj;
+                        const unsigned long long v =
+                            sibling_value(gs_ring<K, E>(reinterpret_cast<unsigned char*>(smem), sw), qj, s * n + qj,
+                                          &xout[j], max_ns, spin_ns);
+                        p = ak * __longlong_as_double(static_cast<long long>(v));
+                    } else {
+                        const unsigned long long* slot = reinterpret_cast<const unsigned long long*>(segmem + off);
+                        unsigned long long v = vload(slot);
+                        while (v == kPending) {
+                            if (spin_ns) __nanosleep(spin_ns);
+                            v = vload(slot);
+                        }
+                        p = ak * __longlong_as_double(static_cast<long long>(v));
+                    }
+                }
+                double a0 = B.acc0[0][t];
+                for (int32_t k0 = 0; k0 < nt; k0 += 8) {
+                    double pk[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) pk[u] = __shfl_sync(0xffffffffu, p, k0 + u);
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+                        if (k0 + u < nt) a0 -= pk[u];
+                }
+                acc[0] = a0;
+            } else if (nt >= 0) {
 #pragma unroll
                 for (int c = 0; c < K; ++c) acc[c] = B.acc0[c][t];
 #pragma unroll 4
@@ -497,12 +549,12 @@ __global__ void __launch_bounds__(3 * gs_segs_per_cta<K>() * 32)
                     }
                     if (K == 1 && off < 0) {
                         const int32_t code = -2 - off;
-                        const int sw = code & 3;
-                        const int32_t qj = sh_sq0[sw] + (code >> 2);
+                        const int sw = code & ((1 << kSwBits) - 1);
+                        const int32_t qj = sh_sq0[sw] + (code >> kSwBits);
                         const int32_t j = bwd ? n - 1 - qj : qj;
                         const unsigned long long v =
-                            sibling_value(gs_ring<K>(reinterpret_cast<unsigned char*>(smem), sw), qj,
-                                          s * n + qj, &xout[j], max_ns);
+                            sibling_value(gs_ring<K, E>(reinterpret_cast<unsigned char*>(smem), sw), qj,
+                                          s * n + qj, &xout[j], max_ns, spin_ns);
                         acc[0] -= ak * __longlong_as_double(static_cast<long long>(v));
                         continue;
                     }
@@ -512,7 +564,7 @@ __global__ void __launch_bounds__(3 * gs_segs_per_cta<K>() * 32)
                         const unsigned long long* slot = reinterpret_cast<const unsigned long long*>(sp) + 32 * c;
                         unsigned long long v = vload(slot);
                         while (v == kPending) {
-                            __nanosleep(20);
+                            if (spin_ns) __nanosleep(spin_ns);
                             v = vload(slot);
                         }
                         acc[c] -= ak * __longlong_as_double(static_cast<long long>(v));
@@ -559,7 +611,7 @@ __global__ void __launch_bounds__(3 * gs_segs_per_cta<K>() * 32)
                     if (K == 1) {
                         // own ring first (its fences then cover shared-memory stores only):
                         // invalidate the slot, write the value, then the tag
-                        const GsRing rg = gs_ring<K>(reinterpret_cast<unsigned char*>(smem), wl);
+                        const GsRing rg = gs_ring<K, E>(reinterpret_cast<unsigned char*>(smem), wl);
                         const int idx = q & (kRing - 1);
                         vstore(&rg.tag[idx], -1);
                         __threadfence_block();
@@ -687,7 +739,7 @@ __global__ void __launch_bounds__(kWrWarps * 32)
     }
 }
 
-// max |i - j| over the stored entries
+// bw[0] = max |i - j| over the stored entries, bw[1] = longest row
 __global__ void k_bandwidth(int32_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
                             int32_t* __restrict__ bw) {
     const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -695,6 +747,7 @@ __global__ void k_bandwidth(int32_t n, const int32_t* __restrict__ rp, const int
     int32_t m = 0;
     for (int32_t p = rp[i]; p < rp[i + 1]; ++p) m = max(m, abs(ci[p] - i));
     atomicMax(bw, m);
+    atomicMax(bw + 1, rp[i + 1] - rp[i]);
 }
 
 // segment heads in sweep order: position q starts a segment unless row(q)
@@ -739,6 +792,21 @@ unsigned gs_max_ns() {
     return v;
 }
 
+unsigned gs_env_u(const char* name, unsigned dflt) {
+    const char* e = std::getenv(name);
+    return e ? static_cast<unsigned>(std::atoi(e)) : dflt;
+}
+
+// back-off of the shared-memory spins and of the poller while values are pending
+// (AMGCU_GS_SPIN; 0 = spin without sleeping)
+unsigned gs_spin_ns() {
+    static const unsigned v = [] {
+        const char* e = std::getenv("AMGCU_GS_SPIN");
+        return e ? static_cast<unsigned>(std::atoi(e)) : 0u;
+    }();
+    return v;
+}
+
 // rows ahead of the solver whose pending values the poller keeps loading (AMGCU_GS_PW)
 int gs_poll_window() {
     static const int v = [] {
@@ -774,6 +842,8 @@ __global__ void k_jacobi(int32_t n, const int32_t* __restrict__ rp, const int32_
     }
 }
 
+#include "gs_lanes.cuh"
+
 }  // namespace
 
 void gauss_seidel(Ctx& c, const DCsr& A, const double* inv_diag, double* x, const double* b, int k, int sweeps,
@@ -807,13 +877,15 @@ void gauss_seidel(Ctx& c, const DCsr& A, const double* inv_diag, double* x, cons
     // AMGCU_GS_WARPROWS=1 forces the warp-per-row kernel (comparison runs)
     const char* wr_env = std::getenv("AMGCU_GS_WARPROWS");
     const bool force_wr = wr_env && wr_env[0] == '1';
-    if ((force_wr || static_cast<int64_t>(nseg_max) * kShortSegment > n) && !std::getenv("AMGCU_GS_TRACE")) {
+    // the segment kernel's poll lists hold 32-bit offsets into the sweep buffers
+    const bool huge = stride * (nsw + 1) >= (size_t(1) << 32);
+    if ((force_wr || huge || static_cast<int64_t>(nseg_max) * kShortSegment > n) && !std::getenv("AMGCU_GS_TRACE")) {
         const double bytes = nsw * (12.0 * A.nnz + 4.0 * (n + 1) + 8.0 * n + 16.0 * n * k);
         // forward sweeps whose stale dependencies stay within the resident window: row-major
         bool row_major = false;
         if (!symmetric_sweep && nsw > 1) {
-            DBuf<int32_t> bwd_max(1, c.s);
-            AMG_CK(cudaMemsetAsync(bwd_max.get(), 0, sizeof(int32_t), c.s));
+            DBuf<int32_t> bwd_max(2, c.s);
+            AMG_CK(cudaMemsetAsync(bwd_max.get(), 0, 2 * sizeof(int32_t), c.s));
             launch(c, k_bandwidth, blocks_for(n, 256), 256, 0, n, A.rp.get(), A.ci.get(), bwd_max.get());
             const int32_t bwidth = read_scalar(c, bwd_max.get());
             int per_sm = 0;
@@ -852,6 +924,56 @@ void gauss_seidel(Ctx& c, const DCsr& A, const double* inv_diag, double* x, cons
         AMG_CK(cudaMemsetAsync(trace.get(), 0, sizeof(unsigned long long) * nsw * n * 4, c.s));
     }
     const double bytes = nsw * (12.0 * A.nnz + 4.0 * (n + 1) + 8.0 * n + 16.0 * n * k);
+    // bandwidth and longest row: the record width E and the segment-major test
+    int32_t bwidth = 0, longest_row = 0;
+    {
+        DBuf<int32_t> st(2, c.s);
+        AMG_CK(cudaMemsetAsync(st.get(), 0, 2 * sizeof(int32_t), c.s));
+        launch(c, k_bandwidth, blocks_for(n, 256), 256, 0, n, A.rp.get(), A.ci.get(), st.get());
+        stage_scalar(c, 0, st.get());
+        stage_scalar(c, 1, st.get() + 1);
+        sync(c);
+        bwidth = staged<int32_t>(c, 0);
+        longest_row = staged<int32_t>(c, 1);
+    }
+    // lane per segment (gs_lanes.cuh): single column, forward sweeps, rows of at most 9
+    // entries, every segment resident at once (one CTA of 32 segments per SM)
+    {
+        const char* ln_env = std::getenv("AMGCU_GS_LANES");
+        const bool ln_off = ln_env && ln_env[0] == '0';
+        const int32_t nctas = (nf + kLnLanes - 1) / kLnLanes;
+        if (!ln_off && !trace_path && k == 1 && !symmetric_sweep && longest_row <= 9 && nctas <= c.sms &&
+            static_cast<int64_t>(nsw) * n < (int64_t(1) << 31) && n < (1 << 24) && static_cast<int64_t>(nf) * 16 <= n) {
+            constexpr size_t smem = ln_smem_bytes<8>();
+            AMG_CK(cudaFuncSetAttribute(k_gs_lanes<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(smem)));
+            // AMGCU_GS_STATS=1: solver iteration / stall counters on stderr
+            static const bool want_stats = std::getenv("AMGCU_GS_STATS") != nullptr;
+            DBuf<unsigned long long> st;
+            if (want_stats) {
+                st.alloc(32, c.s);
+                AMG_CK(cudaMemsetAsync(st.get(), 0, 32 * sizeof(unsigned long long), c.s));
+            }
+            launch_prof(c, kProfGaussSeidel, bytes, k_gs_lanes<8>, static_cast<unsigned>(nctas), kLnThreads, smem, n,
+                        A.rp.get(), A.ci.get(), A.va.get(), inv_diag, b, nsw, static_cast<const int32_t*>(segf.get()),
+                        nf, X.get(), ticket.get(), st.get(), gs_env_u("AMGCU_GS_POLL_NS", 128u),
+                        gs_env_u("AMGCU_GS_PF_NS", 128u));
+            copy_d2d(c, x, X.get() + stride * nsw, static_cast<int64_t>(stride));
+            sync(c);
+            if (want_stats) {
+                unsigned long long h[32];
+                copy_d2h(c, h, st.get(), 32);
+                sync(c);
+                std::fprintf(stderr, "[gs lanes] n=%d segs=%d ctas=%d iterations(all ctas)=%llu rows=%llu lane-iters=%llu "
+                             "record-stalls=%llu value-stalls=%llu\n", n, nf, nctas, h[0], h[1], h[2], h[3],
+                             h[2] - h[1] - h[3]);
+                const double it = static_cast<double>(h[0]);
+                std::fprintf(stderr, "[gs lanes] cycles/iteration: rows %.0f sync %.0f publish %.0f total %.0f\n",
+                             h[16] / it, h[17] / it, h[18] / it, h[19] / it);
+            }
+            return;
+        }
+    }
     auto run = [&](auto kern, int segs, size_t seg_bytes) {
         // AMGCU_GS_SMEM: request at least this much shared memory per CTA (caps CTAs per SM)
         static const size_t smem_floor = [] {
@@ -867,12 +989,9 @@ void gauss_seidel(Ctx& c, const DCsr& A, const double* inv_diag, double* x, cons
         int sweep_loop = 0;
         const char* sl_env = std::getenv("AMGCU_GS_SWEEP_LOOP");
         if (!symmetric_sweep && nsw > 1 && !(sl_env && sl_env[0] == '0')) {
-            DBuf<int32_t> bw_max(1, c.s);
-            AMG_CK(cudaMemsetAsync(bw_max.get(), 0, sizeof(int32_t), c.s));
-            launch(c, k_bandwidth, blocks_for(n, 256), 256, 0, n, A.rp.get(), A.ci.get(), bw_max.get());
             std::vector<int32_t> hs(static_cast<size_t>(nf) + 1);
             copy_d2h(c, hs.data(), segf.get(), nf + 1);
-            const int32_t bwidth = read_scalar(c, bw_max.get());
+            sync(c);
             int64_t ahead = 0;
             for (int32_t g2 = 0; g2 < nf; ++g2) {
                 const int64_t reach = static_cast<int64_t>(hs[g2 + 1]) + bwidth;
@@ -889,11 +1008,16 @@ void gauss_seidel(Ctx& c, const DCsr& A, const double* inv_diag, double* x, cons
                     A.rp.get(), A.ci.get(), A.va.get(), inv_diag, b, nsw, static_cast<const unsigned char*>(bwd.get()),
                     static_cast<const int32_t*>(dbase.get()), static_cast<const int32_t*>(segf.get()),
                     static_cast<const int32_t*>(symmetric_sweep ? segb.get() : segf.get()), X.get(), ticket.get(),
-                    gs_max_ns(), trace.get(), gs_poll_window(), sweep_loop);
+                    gs_max_ns(), trace.get(), gs_poll_window(), sweep_loop, gs_spin_ns());
     };
-#define AMGCU_GS_RUN(KK) run(k_gs_segments<KK>, gs_segs_per_cta<KK>(), gs_seg_bytes<KK>())
+#define AMGCU_GS_RUN(KK) run(k_gs_segments<KK, 32>, gs_segs_per_cta<KK, 32>(), gs_seg_bytes<KK, 32>())
+    // short rows: 16-entry records, 8 segments per CTA; poll offsets are 32-bit
+    const bool narrow = longest_row <= 16;
     switch (k) {
-        case 1: AMGCU_GS_RUN(1); break;
+        case 1:
+            if (narrow) run(k_gs_segments<1, 16>, gs_segs_per_cta<1, 16>(), gs_seg_bytes<1, 16>());
+            else AMGCU_GS_RUN(1);
+            break;
         case 2: AMGCU_GS_RUN(2); break;
         case 3: AMGCU_GS_RUN(3); break;
         case 4: AMGCU_GS_RUN(4); break;

@@ -66,3 +66,27 @@ def rel_max_err(got, want):
 def same_structure(a: SparseMatrix, b: SparseMatrix):
     return (a.n_rows == b.n_rows and a.n_cols == b.n_cols and np.array_equal(a.row_offsets, b.row_offsets)
             and np.array_equal(a.col_indices, b.col_indices))
+
+
+def stencil9(nx, ny, rng, extra=0.0, reach=None):
+    """nx x ny grid, 9-point coupling with seeded random off-diagonal values and a
+    dominant diagonal; `extra` = fraction of rows given one more coupling to a random
+    row within `reach` (long-range hand-offs for the Gauss-Seidel kernels)."""
+    t = []
+    n = nx * ny
+    for j in range(ny):
+        for i in range(nx):
+            r = j * nx + i
+            t.append((r, r, 9.0 + rng.uniform()))
+            for dj in (-1, 0, 1):
+                for di in (-1, 0, 1):
+                    if (di or dj) and 0 <= i + di < nx and 0 <= j + dj < ny:
+                        t.append((r, r + dj * nx + di, -rng.uniform(0.1, 1.0)))
+    if extra:
+        reach = reach or n
+        for r in range(n):
+            if rng.uniform() < extra:
+                c = int(np.clip(r + rng.integers(-reach, reach + 1), 0, n - 1))
+                if abs(c - r) > nx + 1:
+                    t.append((r, c, -rng.uniform(0.01, 0.1)))
+    return from_triplets(n, n, t)

@@ -10,7 +10,7 @@ import paper_1610_03154_b200.api as api
 from paper_1610_03154_b200.types import (CandidateSet, EvolutionWeighting, StrengthConfig, StrengthMeasure,
                                          constant_candidates,
                                          from_triplets, identity)
-from tests.helpers import aniso2d, poisson1d, random_sparse, random_spd_sparse, rel_max_err, tridiag
+from tests.helpers import aniso2d, poisson1d, random_sparse, random_spd_sparse, rel_max_err, stencil9, tridiag
 
 pytestmark = pytest.mark.gpu
 
@@ -233,6 +233,30 @@ def test_gauss_seidel_long_segments(gpu_seq, port):
                 got = api.improve_candidates(A_, B, 3, scheme, 0.0, ctx=gpu_seq)
                 want = port.improve_candidates(A_, B, 3, scheme, 0.0)
                 assert got.data.tobytes() == want.data.tobytes(), (A_.n_rows, k, scheme)
+
+
+@pytest.mark.parametrize("lanes", ["1", "0"])
+def test_gauss_seidel_lane_segments(gpu_seq, port, monkeypatch, lanes):
+    """Lane-per-segment kernel (gs_lanes.cuh) against the reference sweep: 9-point
+    grids over several CTAs (cross-CTA poll slots), long-range couplings (sibling
+    rings, evicted ring slots, rows past the record), 1..4 sweeps, zero and non-zero
+    right-hand sides; lanes=0 runs the same cases through the 3-warp segment kernel."""
+    monkeypatch.setenv("AMGCU_GS_LANES", lanes)
+    rng = np.random.default_rng(41)
+    cases = [stencil9(64, 100, rng), stencil9(200, 40, rng), stencil9(48, 70, rng, extra=0.05),
+             stencil9(40, 90, rng, extra=0.03, reach=300)]
+    for A_ in cases:
+        n = A_.n_rows
+        for sweeps in (1, 4):
+            B = CandidateSet(n, 1, rng.uniform(0.5, 1.5, n))
+            got = api.improve_candidates(A_, B, sweeps, 1, 0.0, ctx=gpu_seq)
+            want = port.improve_candidates(A_, B, sweeps, 1, 0.0)
+            assert got.data.tobytes() == want.data.tobytes(), (n, sweeps)
+        b = rng.uniform(-1, 1, n)
+        x0 = rng.uniform(-1, 1, n)
+        got = api.relax(A_, 1, 0.0, 3, x0, b, ctx=gpu_seq)
+        want = port.relax(A_, 1, 0.0, 3, x0, b)
+        assert got.tobytes() == want.tobytes(), n
 
 
 def test_relax(gpu_seq, port):
