@@ -33,11 +33,11 @@
 
 constexpr int kLnLanes = 32;  // segments per CTA
 constexpr int kLnRb = 8;      // rows per record block
-constexpr int kLnBlk = 3;     // record blocks per lane
-constexpr int kLnRows = kLnRb * kLnBlk;
 constexpr int kLnPf = 8;      // prefetch warps (each serves 4 lanes)
-constexpr int kLnSlots = 4;   // poll slots per row
-constexpr int kLnRing = 64;   // published rows kept per lane
+// Per-configuration sizes (template parameters): T terms per row record, BLK record
+// blocks per lane (kLnRb * BLK rows of look-ahead), SLOTS poll slots per row, RING
+// published rows kept per lane.  The launcher instantiates T = 8 (rows of up to 9
+// entries): 3 blocks, 4 slots, 64-row rings, ~208 KB of shared memory.
 constexpr int kLnThreads = (2 + kLnPf) * 32;
 
 struct LnCell {
@@ -46,8 +46,12 @@ struct LnCell {
     int32_t pad;
 };
 
-template <int T>
+template <int T, int BLK, int SLOTS, int RING>
 struct LnRec {
+    static constexpr int kLnBlk = BLK;
+    static constexpr int kLnRows = kLnRb * BLK;
+    static constexpr int kLnSlots = SLOTS;
+    static constexpr int kLnRing = RING;
     double ta[kLnRows][T][kLnLanes];              // a, or the folded product
     unsigned long long tw[kLnRows][T][kLnLanes];  // source cell smem address | expected tag << 32
     LnCell sv[kLnRows][kLnSlots][kLnLanes];       // poll slots
@@ -63,9 +67,9 @@ struct LnRec {
     int32_t live;                // the solver is running
 };
 
-template <int T>
+template <int T, int BLK, int SLOTS, int RING>
 constexpr size_t ln_smem_bytes() {
-    return sizeof(LnRec<T>);
+    return sizeof(LnRec<T, BLK, SLOTS, RING>);
 }
 
 // acquire / release on shared-memory flags.  In the shared state space the acquire
@@ -97,7 +101,7 @@ __device__ __forceinline__ unsigned smem_addr(const void* p) {
     return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
 
-template <int T>
+template <int T, int BLK, int SLOTS, int RING>
 __global__ void __launch_bounds__(kLnThreads, 1)
     k_gs_lanes(int32_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
                const double* __restrict__ va, const double* __restrict__ inv_diag, const double* __restrict__ b,
@@ -105,7 +109,12 @@ __global__ void __launch_bounds__(kLnThreads, 1)
                unsigned int* __restrict__ ticket, unsigned long long* __restrict__ stats, unsigned poll_ns,
                unsigned pf_ns) {
     extern __shared__ unsigned long long ln_smem[];
-    LnRec<T>& R = *reinterpret_cast<LnRec<T>*>(ln_smem);
+    using Rec = LnRec<T, BLK, SLOTS, RING>;
+    Rec& R = *reinterpret_cast<Rec*>(ln_smem);
+    constexpr int kLnBlk = Rec::kLnBlk;
+    constexpr int kLnRows = Rec::kLnRows;
+    constexpr int kLnSlots = Rec::kLnSlots;
+    constexpr int kLnRing = Rec::kLnRing;
     __shared__ unsigned int blk;
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -285,15 +294,20 @@ __global__ void __launch_bounds__(kLnThreads, 1)
         const int32_t q0 = R.sq0[l], len = R.sq0[l + 1] - q0;
         const int32_t total = len * nsw;
         const int32_t nblocks = (total + kLnRb - 1) / kLnRb;
-        const int32_t wblocks = __reduce_max_sync(0xffffffffu, nblocks);  // warp-uniform trip count
         const unsigned one_addr = smem_addr(&R.one);
-        for (int32_t bi = 0; bi < wblocks; ++bi) {
-            // the slot's previous block (bi - kLnBlk) must be consumed
-            if (bi >= kLnBlk && bi < nblocks)
-                while (ld_acquire_cta(&R.consumed[l]) < (bi - kLnBlk + 1) * kLnRb) __nanosleep(pf_ns);
+        // Each pass serves, together, the lanes whose next block has a free slot (the
+        // slot's previous block consumed); a lane never waits on another lane's
+        // consumption (it may need values of a row that lane reaches only with new records).
+        int32_t bi = 0;  // next block of this thread's lane
+        while (__any_sync(0xffffffffu, bi < nblocks)) {
+            const bool go = bi < nblocks && (bi < kLnBlk || ld_acquire_cta(&R.consumed[l]) >= (bi - kLnBlk + 1) * kLnRb);
+            if (!__any_sync(0xffffffffu, go)) {
+                __nanosleep(pf_ns);
+                continue;
+            }
             const int32_t u = bi * kLnRb + r;
             const int slot = u % kLnRows;
-            if (u < total) {
+            if (go && u < total) {
                 const int32_t s = u / len;
                 const int32_t q = q0 + (u - s * len);
                 const double* xin = X + static_cast<size_t>(s) * stride;
@@ -385,7 +399,10 @@ __global__ void __launch_bounds__(kLnThreads, 1)
                 R.meta[slot][l] = slow ? (1 << 16) : (nt | (nslot << 8));
             }
             __syncwarp();
-            if (r == 0 && bi < nblocks) st_release_cta(&R.ready[l], bi + 1);
+            if (go) {
+                if (r == 0) st_release_cta(&R.ready[l], bi + 1);
+                ++bi;
+            }
         }
         return;
     }

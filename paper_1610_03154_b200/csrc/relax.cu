@@ -937,16 +937,14 @@ void gauss_seidel(Ctx& c, const DCsr& A, const double* inv_diag, double* x, cons
         longest_row = staged<int32_t>(c, 1);
     }
     // lane per segment (gs_lanes.cuh): single column, forward sweeps, rows of at most 9
-    // entries, every segment resident at once (one CTA of 32 segments per SM)
+    // entries (wider rows -- 19-point coarse operators -- measured slower than the 3-warp
+    // kernel), every segment resident at once (one CTA of 32 segments per SM)
     {
         const char* ln_env = std::getenv("AMGCU_GS_LANES");
         const bool ln_off = ln_env && ln_env[0] == '0';
         const int32_t nctas = (nf + kLnLanes - 1) / kLnLanes;
         if (!ln_off && !trace_path && k == 1 && !symmetric_sweep && longest_row <= 9 && nctas <= c.sms &&
             static_cast<int64_t>(nsw) * n < (int64_t(1) << 31) && n < (1 << 24) && static_cast<int64_t>(nf) * 16 <= n) {
-            constexpr size_t smem = ln_smem_bytes<8>();
-            AMG_CK(cudaFuncSetAttribute(k_gs_lanes<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(smem)));
             // AMGCU_GS_STATS=1: solver iteration / stall counters on stderr
             static const bool want_stats = std::getenv("AMGCU_GS_STATS") != nullptr;
             DBuf<unsigned long long> st;
@@ -954,10 +952,14 @@ void gauss_seidel(Ctx& c, const DCsr& A, const double* inv_diag, double* x, cons
                 st.alloc(32, c.s);
                 AMG_CK(cudaMemsetAsync(st.get(), 0, 32 * sizeof(unsigned long long), c.s));
             }
-            launch_prof(c, kProfGaussSeidel, bytes, k_gs_lanes<8>, static_cast<unsigned>(nctas), kLnThreads, smem, n,
-                        A.rp.get(), A.ci.get(), A.va.get(), inv_diag, b, nsw, static_cast<const int32_t*>(segf.get()),
-                        nf, X.get(), ticket.get(), st.get(), gs_env_u("AMGCU_GS_POLL_NS", 128u),
-                        gs_env_u("AMGCU_GS_PF_NS", 128u));
+            auto runl = [&](auto kern, size_t smem) {
+                AMG_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+                launch_prof(c, kProfGaussSeidel, bytes, kern, static_cast<unsigned>(nctas), kLnThreads, smem, n,
+                            A.rp.get(), A.ci.get(), A.va.get(), inv_diag, b, nsw,
+                            static_cast<const int32_t*>(segf.get()), nf, X.get(), ticket.get(), st.get(),
+                            gs_env_u("AMGCU_GS_POLL_NS", 128u), gs_env_u("AMGCU_GS_PF_NS", 128u));
+            };
+            runl(k_gs_lanes<8, 3, 4, 64>, ln_smem_bytes<8, 3, 4, 64>());
             copy_d2d(c, x, X.get() + stride * nsw, static_cast<int64_t>(stride));
             sync(c);
             if (want_stats) {

@@ -68,18 +68,21 @@ def same_structure(a: SparseMatrix, b: SparseMatrix):
             and np.array_equal(a.col_indices, b.col_indices))
 
 
-def stencil9(nx, ny, rng, extra=0.0, reach=None):
-    """nx x ny grid, 9-point coupling with seeded random off-diagonal values and a
-    dominant diagonal; `extra` = fraction of rows given one more coupling to a random
-    row within `reach` (long-range hand-offs for the Gauss-Seidel kernels)."""
+def stencil9(nx, ny, rng, extra=0.0, reach=None, rx=1, ry=1, cross=False):
+    """nx x ny grid, (2 rx + 1) x (2 ry + 1)-point coupling (9-point by default) with
+    seeded random off-diagonal values and a dominant diagonal; `extra` = fraction of
+    rows given one more coupling to a random row within `reach` (long-range hand-offs
+    for the Gauss-Seidel kernels); cross=True keeps only the axis neighbours (5-point)."""
     t = []
     n = nx * ny
     for j in range(ny):
         for i in range(nx):
             r = j * nx + i
-            t.append((r, r, 9.0 + rng.uniform()))
-            for dj in (-1, 0, 1):
-                for di in (-1, 0, 1):
+            t.append((r, r, 4.0 * (2 * rx + 1) * (2 * ry + 1) + rng.uniform()))
+            for dj in range(-ry, ry + 1):
+                for di in range(-rx, rx + 1):
+                    if cross and di and dj:
+                        continue
                     if (di or dj) and 0 <= i + di < nx and 0 <= j + dj < ny:
                         t.append((r, r + dj * nx + di, -rng.uniform(0.1, 1.0)))
     if extra:

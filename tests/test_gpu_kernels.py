@@ -243,8 +243,10 @@ def test_gauss_seidel_lane_segments(gpu_seq, port, monkeypatch, lanes):
     right-hand sides; lanes=0 runs the same cases through the 3-warp segment kernel."""
     monkeypatch.setenv("AMGCU_GS_LANES", lanes)
     rng = np.random.default_rng(41)
-    cases = [stencil9(64, 100, rng), stencil9(200, 40, rng), stencil9(48, 70, rng, extra=0.05),
-             stencil9(40, 90, rng, extra=0.03, reach=300)]
+    cases = [stencil9(64, 100, rng), stencil9(200, 40, rng), stencil9(48, 70, rng, cross=True, extra=0.3),
+             stencil9(40, 90, rng, cross=True, extra=0.2, reach=300),
+             stencil9(40, 90, rng, cross=True, extra=0.5, reach=2000), stencil9(50, 80, rng, ry=2, cross=True),
+             stencil9(36, 75, rng, ry=2, cross=True, extra=0.3, reach=200)]
     for A_ in cases:
         n = A_.n_rows
         for sweeps in (1, 4):
