@@ -145,36 +145,43 @@ __global__ void __launch_bounds__(kLnThreads, 1)
         const int32_t total = len * nsw;
         int32_t u = 0, kres = 0;
         int32_t s = 0, q = q0;  // sweep and row of row u
+        int slot = 0;           // u % kLnRows
         double acc = 0.0;
-        bool fresh = true;  // the next row starts from its record's acc0
-        int32_t rdy = 0;    // record rows known to be prepared (acquired)
+        int32_t rdy = 0;  // record rows known to be prepared (acquired)
+        // the current row's record in registers (loaded one iteration ahead when possible,
+        // so the record round trip is off the critical path)
+        bool have = false;
+        int32_t meta = 0;
+        double dq = 0.0;
+        double ta[T];
+        unsigned long long tw[T];
         long long ck[4] = {0, 0, 0, 0};
+        if (stats && lane == 0) atomicMin(stats + 24, globaltimer_ns());
+        long long iters = 0;
         while (true) {
+            ++iters;
             const long long c0 = stats ? clock64() : 0;
             const bool act = u < total;
             if (!__any_sync(0xffffffffu, act)) break;
             bool fin = false;
             double xnew = 0.0;
             if (act) {
-                const int slot = u % kLnRows;
-                if (rdy <= u) rdy = ld_acquire_cta(&R.ready[lane]) * kLnRb;
-                if (rdy > u) {
-                    // the whole record in one round trip (issued before any of it is used)
-                    const int32_t meta = R.meta[slot][lane];
-                    const double acc0 = R.acc0[slot][lane];
-                    const double dq = R.dinv[slot][lane];
-                    double ta[T];
-                    unsigned long long tw[T];
+                if (!have) {
+                    if (rdy <= u) rdy = ld_acquire_cta(&R.ready[lane]) * kLnRb;
+                    if (rdy > u) {
+                        meta = R.meta[slot][lane];
+                        acc = R.acc0[slot][lane];
+                        dq = R.dinv[slot][lane];
 #pragma unroll
-                    for (int k = 0; k < T; ++k) {
-                        ta[k] = R.ta[slot][k][lane];
-                        tw[k] = R.tw[slot][k][lane];
-                    }
-                    if (fresh) {
-                        acc = acc0;
+                        for (int k = 0; k < T; ++k) {
+                            ta[k] = R.ta[slot][k][lane];
+                            tw[k] = R.tw[slot][k][lane];
+                        }
                         kres = 0;
-                        fresh = false;
+                        have = true;
                     }
+                }
+                if (have) {
                     const int nt = meta & 0xff;
                     if (!(meta >> 16)) {
                         unsigned long long vv[T];
@@ -245,7 +252,7 @@ __global__ void __launch_bounds__(kLnThreads, 1)
             if (stats) {
                 const unsigned mfin = __ballot_sync(0xffffffffu, fin);
                 const unsigned mact = __ballot_sync(0xffffffffu, act);
-                const unsigned mrec = __ballot_sync(0xffffffffu, act && rdy <= u);
+                const unsigned mrec = __ballot_sync(0xffffffffu, act && !have);
                 if (lane == 0) {
                     atomicAdd(stats + 0, 1ull);
                     atomicAdd(stats + 1, static_cast<unsigned long long>(__popc(mfin)));
@@ -264,12 +271,30 @@ __global__ void __launch_bounds__(kLnThreads, 1)
                     *reinterpret_cast<unsigned long long*>(X + static_cast<size_t>(s + 1) * stride + q));
                 out.store(xb, cuda::memory_order_relaxed);
                 ++u;
+                if (++slot == kLnRows) slot = 0;
                 if (++q == q0 + len) {
                     q = q0;
                     ++s;
                 }
-                fresh = true;
                 vstore(&R.consumed[lane], u);
+                // the next row's record, if prepared: its loads overlap the barrier and the
+                // loop head
+                have = false;
+                if (u < total) {
+                    if (rdy <= u) rdy = ld_acquire_cta(&R.ready[lane]) * kLnRb;
+                    if (rdy > u) {
+                        meta = R.meta[slot][lane];
+                        acc = R.acc0[slot][lane];
+                        dq = R.dinv[slot][lane];
+#pragma unroll
+                        for (int k = 0; k < T; ++k) {
+                            ta[k] = R.ta[slot][k][lane];
+                            tw[k] = R.tw[slot][k][lane];
+                        }
+                        kres = 0;
+                        have = true;
+                    }
+                }
             }
             __syncwarp();
             if (stats) {
@@ -280,8 +305,12 @@ __global__ void __launch_bounds__(kLnThreads, 1)
                 ck[3] += c3 - c0;
             }
         }
-        if (stats && lane == 0)
+        if (stats && lane == 0) {
             for (int e = 0; e < 4; ++e) atomicAdd(stats + 16 + e, static_cast<unsigned long long>(ck[e]));
+            atomicMax(stats + 25, globaltimer_ns());
+            atomicMax(stats + 26, static_cast<unsigned long long>(iters));
+            atomicMax(stats + 27, static_cast<unsigned long long>(ck[3]));
+        }
         if (lane == 0) vstore(&R.live, 0);
         return;
     }

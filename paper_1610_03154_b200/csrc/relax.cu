@@ -951,6 +951,7 @@ void gauss_seidel(Ctx& c, const DCsr& A, const double* inv_diag, double* x, cons
             if (want_stats) {
                 st.alloc(32, c.s);
                 AMG_CK(cudaMemsetAsync(st.get(), 0, 32 * sizeof(unsigned long long), c.s));
+                AMG_CK(cudaMemsetAsync(st.get() + 24, 0xff, sizeof(unsigned long long), c.s));
             }
             auto runl = [&](auto kern, size_t smem) {
                 AMG_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
@@ -972,6 +973,8 @@ void gauss_seidel(Ctx& c, const DCsr& A, const double* inv_diag, double* x, cons
                 const double it = static_cast<double>(h[0]);
                 std::fprintf(stderr, "[gs lanes] cycles/iteration: rows %.0f sync %.0f publish %.0f total %.0f\n",
                              h[16] / it, h[17] / it, h[18] / it, h[19] / it);
+                std::fprintf(stderr, "[gs lanes] solver span %.1f us, max iterations per CTA %llu, max cycles per CTA %llu\n",
+                             (h[25] - h[24]) * 1e-3, h[26], h[27]);
             }
             return;
         }
