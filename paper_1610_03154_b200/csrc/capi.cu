@@ -126,8 +126,13 @@ amgcu_status amgcu_ctx_create(int device, amgcu_ctx* out) {
         AMG_CK(cudaSetDevice(device));
         auto* ctx = new amgcu_ctx_s;
         ctx->c.device = device;
-        AMG_CK(cudaStreamCreateWithFlags(&ctx->c.s, cudaStreamNonBlocking));
-        AMG_CK(cudaStreamCreateWithFlags(&ctx->c.side, cudaStreamNonBlocking));
+        // the main stream gets the highest priority and the side stream (background work:
+        // the evolution-SOC ledger count) the lowest, so the block scheduler fills idle SMs
+        // with side work without delaying the main stream's kernels
+        int prio_lo = 0, prio_hi = 0;
+        AMG_CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+        AMG_CK(cudaStreamCreateWithPriority(&ctx->c.s, cudaStreamNonBlocking, prio_hi));
+        AMG_CK(cudaStreamCreateWithPriority(&ctx->c.side, cudaStreamNonBlocking, prio_lo));
         AMG_CK(cudaDeviceGetAttribute(&ctx->c.sms, cudaDevAttrMultiProcessorCount, device));
         cudaMemPool_t pool;
         AMG_CK(cudaDeviceGetDefaultMemPool(&pool, device));

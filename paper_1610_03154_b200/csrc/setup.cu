@@ -9,6 +9,8 @@
 #include <cusolverDn.h>
 
 #include "hier.cuh"
+
+#include <cstdlib>
 #include "small_dense.h"
 
 namespace amgcu {
@@ -90,6 +92,12 @@ void strength_of(Ctx& c, DLevel& L, const amgcu_setup_options& o, DCsr& S) {
             evolution_strength(c, A, At, winv.get(), o.drop_tol, o.evolution_steps, S);
             // its ledger count overlaps the rest of the setup (collected in rn_setup)
             L.evo_steps = o.evolution_steps;
+            // AMGCU_NO_EVO_COUNT=1 (timing experiments only): skip the ledger's evolution count
+            static const bool no_count = std::getenv("AMGCU_NO_EVO_COUNT") != nullptr;
+            if (no_count) {
+                L.evo_ops = 0.0;
+                return;
+            }
             L.evo_count = evolution_ops_start(c, A, std::move(At), o.evolution_steps);
             return;
         }
