@@ -37,7 +37,8 @@ constexpr int kLnPf = 8;      // prefetch warps (each serves 4 lanes)
 // Per-configuration sizes (template parameters): T terms per row record, BLK record
 // blocks per lane (kLnRb * BLK rows of look-ahead), SLOTS poll slots per row, RING
 // published rows kept per lane.  The launcher instantiates T = 8 (rows of up to 9
-// entries): 3 blocks, 4 slots, 64-row rings, ~208 KB of shared memory.
+// entries: 3 blocks, 4 slots, 64-row rings) and T = 20 (up to 21 entries, e.g. the
+// 19-point coarse operators: 2 blocks, 2 slots, 32-row rings), both ~210 KB.
 constexpr int kLnThreads = (2 + kLnPf) * 32;
 
 struct LnCell {
@@ -59,9 +60,12 @@ struct LnRec {
     double acc0[kLnRows][kLnLanes];
     double dinv[kLnRows][kLnLanes];
     int32_t meta[kLnRows][kLnLanes];  // nterm | nslot << 8 | slow << 16
-    LnCell ring[kLnLanes][kLnRing];
+    // rings: [0, 1] halo (the previous CTA's last two segments, streamed in by the
+    // poller), [2 + l] lane l's published rows
+    LnCell ring[kLnLanes + 2][kLnRing];
     LnCell one;  // (1.0, tag 0): source of folded products
     int32_t sq0[kLnLanes + 1];
+    int32_t hq0[3];  // halo segments: [hq0[0], hq0[1]), [hq0[1], hq0[2] = sq0[0])
     int32_t ready[kLnLanes];     // record blocks prepared
     int32_t consumed[kLnLanes];  // rows finished
     int32_t live;                // the solver is running
@@ -115,17 +119,20 @@ __global__ void __launch_bounds__(kLnThreads, 1)
     constexpr int kLnRows = Rec::kLnRows;
     constexpr int kLnSlots = Rec::kLnSlots;
     constexpr int kLnRing = Rec::kLnRing;
+    // prefetch: a row's entries (and then their published values) loaded in batches of
+    constexpr int kPfChunk = 8;
     __shared__ unsigned int blk;
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) blk = atomicAdd(ticket, 1u);
     __syncthreads();
     const int32_t g0 = static_cast<int32_t>(blk) * kLnLanes;
-    for (int e = threadIdx.x; e < kLnLanes * kLnRing; e += blockDim.x) {
+    for (int e = threadIdx.x; e < (kLnLanes + 2) * kLnRing; e += blockDim.x) {
         R.ring[e / kLnRing][e % kLnRing].v = kPending;
         R.ring[e / kLnRing][e % kLnRing].tag = -1;
     }
     if (threadIdx.x <= kLnLanes) R.sq0[threadIdx.x] = segs[min(g0 + static_cast<int32_t>(threadIdx.x), nseg)];
+    if (threadIdx.x < 3) R.hq0[threadIdx.x] = segs[max(g0 - 2 + static_cast<int32_t>(threadIdx.x), 0)];
     if (threadIdx.x < kLnLanes) {
         R.ready[threadIdx.x] = 0;
         R.consumed[threadIdx.x] = 0;
@@ -138,6 +145,7 @@ __global__ void __launch_bounds__(kLnThreads, 1)
     __syncthreads();
     const size_t stride = static_cast<size_t>(n);
     const int32_t qc0 = R.sq0[0];  // first row of this CTA's segments
+    const int32_t hq0 = R.hq0[0];  // first row served by a ring (halo included)
 
     if (warp == 0) {
         // ---------------- solver ----------------
@@ -184,44 +192,61 @@ __global__ void __launch_bounds__(kLnThreads, 1)
                 if (have) {
                     const int nt = meta & 0xff;
                     if (!(meta >> 16)) {
-                        unsigned long long vv[T];
-                        int32_t tg[T];
-#pragma unroll
-                        for (int k = 0; k < T; ++k) ld_cell(static_cast<unsigned>(tw[k]), vv[k], tg[k]);
-                        double pk[T];
-                        unsigned okm = 0u, evm = 0u;
-#pragma unroll
-                        for (int k = 0; k < T; ++k) {
-                            const int32_t want = static_cast<int32_t>(tw[k] >> 32);
-                            okm |= ((tg[k] == want && vv[k] != kPending) ? 1u : 0u) << k;
-                            evm |= (tg[k] > want ? 1u : 0u) << k;
-                            pk[k] = ta[k] * __longlong_as_double(static_cast<long long>(vv[k]));
-                        }
+                        // chunks of 8 terms (register pressure for wide rows): resolve the
+                        // chunk's cells, subtract in term order up to the first value that is
+                        // not there yet
                         const unsigned live_m = ((1u << nt) - 1u) & ~((1u << kres) - 1u);
-                        if (evm & live_m) {
-                            // a ring value was overwritten before this lane read it (it was
-                            // published long ago; rare): read it from the sweep buffer
+                        bool stopped = false;
+                        int kstop = nt;
 #pragma unroll
-                            for (int k = 0; k < T; ++k) {
-                                if ((evm >> k) & 1u) {
-                                    const int32_t want = static_cast<int32_t>(tw[k] >> 32);
-                                    const unsigned long long bits =
-                                        load_relaxed_bits(X + stride + static_cast<size_t>(want));
-                                    if (bits != kPending) {
-                                        okm |= 1u << k;
-                                        pk[k] = ta[k] * __longlong_as_double(static_cast<long long>(bits));
+                        for (int cb = 0; cb < T; cb += 8) {
+                            if (!stopped && cb < nt) {
+                                unsigned long long vv[8];
+                                int32_t tg[8];
+#pragma unroll
+                                for (int w = 0; w < 8; ++w)
+                                    if (cb + w < T) ld_cell(static_cast<unsigned>(tw[cb + w]), vv[w], tg[w]);
+                                double pk[8];
+                                unsigned okc = 0u, evc = 0u;
+#pragma unroll
+                                for (int w = 0; w < 8; ++w) {
+                                    if (cb + w < T) {
+                                        const int32_t want = static_cast<int32_t>(tw[cb + w] >> 32);
+                                        okc |= ((tg[w] == want && vv[w] != kPending) ? 1u : 0u) << w;
+                                        evc |= (tg[w] > want ? 1u : 0u) << w;
+                                        pk[w] = ta[cb + w] * __longlong_as_double(static_cast<long long>(vv[w]));
                                     }
+                                }
+                                const unsigned livec = (live_m >> cb) & 0xffu;
+                                if (evc & livec) {
+                                    // a ring value was overwritten before this lane read it (it
+                                    // was published long ago; rare): read it from the sweep buffer
+#pragma unroll
+                                    for (int w = 0; w < 8; ++w) {
+                                        if (cb + w < T && ((evc >> w) & 1u)) {
+                                            const int32_t want = static_cast<int32_t>(tw[cb + w] >> 32);
+                                            const unsigned long long bits =
+                                                load_relaxed_bits(X + stride + static_cast<size_t>(want));
+                                            if (bits != kPending) {
+                                                okc |= 1u << w;
+                                                pk[w] = ta[cb + w] * __longlong_as_double(static_cast<long long>(bits));
+                                            }
+                                        }
+                                    }
+                                }
+                                const unsigned badc = ~okc & livec;
+                                const int ks = badc ? cb + __ffs(badc) - 1 : min(nt, cb + 8);
+#pragma unroll
+                                for (int w = 0; w < 8; ++w)
+                                    if (cb + w < T && cb + w >= kres && cb + w < ks) acc -= pk[w];
+                                if (badc) {
+                                    stopped = true;
+                                    kstop = ks;
                                 }
                             }
                         }
-                        // subtract in term order up to the first value that is not there yet
-                        const unsigned bad = ~okm & live_m;
-                        const int kstop = bad ? __ffs(bad) - 1 : nt;
-#pragma unroll
-                        for (int k = 0; k < T; ++k)
-                            if (k >= kres && k < kstop) acc -= pk[k];
                         kres = kstop;
-                        fin = bad == 0u;
+                        fin = !stopped;
                     } else {
                         // slow row (more terms or pending values than the record holds): the
                         // CSR row from global memory, resumable at entry kres
@@ -264,7 +289,7 @@ __global__ void __launch_bounds__(kLnThreads, 1)
             const long long c2 = stats ? clock64() : 0;
             if (fin) {
                 const unsigned long long xb = static_cast<unsigned long long>(__double_as_longlong(xnew));
-                LnCell& cell = R.ring[lane][q & (kLnRing - 1)];
+                LnCell& cell = R.ring[lane + 2][q & (kLnRing - 1)];
                 cell.v = xb;
                 cell.tag = s * n + q;
                 cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> out(
@@ -346,12 +371,12 @@ __global__ void __launch_bounds__(kLnThreads, 1)
                 const double dq = inv_diag[q];
                 int nt = 0, nslot = 0;
                 bool slow = false, prefix = true;
-                for (int32_t e0 = lo; e0 < hi; e0 += 8) {
-                    int32_t jj[8];
-                    double aa[8];
-                    unsigned long long xv[8];
+                for (int32_t e0 = lo; e0 < hi; e0 += kPfChunk) {
+                    int32_t jj[kPfChunk];
+                    double aa[kPfChunk];
+                    unsigned long long xv[kPfChunk];
 #pragma unroll
-                    for (int w = 0; w < 8; ++w) {
+                    for (int w = 0; w < kPfChunk; ++w) {
                         jj[w] = q;
                         aa[w] = 0.0;
                         if (e0 + w < hi) {
@@ -362,17 +387,17 @@ __global__ void __launch_bounds__(kLnThreads, 1)
                     // values that are published now: every old value (previous sweep; sweep 0
                     // reads the input x) and new values of rows outside this CTA's segments
 #pragma unroll
-                    for (int w = 0; w < 8; ++w) {
+                    for (int w = 0; w < kPfChunk; ++w) {
                         const int32_t j = jj[w];
                         xv[w] = kPending;
                         if (j > q)
                             xv[w] = s == 0 ? static_cast<unsigned long long>(__double_as_longlong(__ldcg(xin + j)))
                                            : load_relaxed_bits(xin + j);
-                        else if (j < qc0)
+                        else if (j < hq0)
                             xv[w] = load_relaxed_bits(xo + j);
                     }
 #pragma unroll
-                    for (int w = 0; w < 8; ++w) {
+                    for (int w = 0; w < kPfChunk; ++w) {
                         const int32_t j = jj[w];
                         if (j == q) continue;  // diagonal or padding
                         if (xv[w] != kPending) {
@@ -393,11 +418,20 @@ __global__ void __launch_bounds__(kLnThreads, 1)
                         prefix = false;
                         unsigned addr;
                         int32_t want;
-                        if (j < q && j >= qc0) {
-                            // earlier row of a segment of this CTA (own included): its ring cell
-                            int l2 = 0;
-                            while (l2 + 1 < kLnLanes && R.sq0[l2 + 1] <= j) ++l2;
-                            addr = smem_addr(&R.ring[l2][j & (kLnRing - 1)]);
+                        if (j < q && j >= hq0) {
+                            // earlier row of a segment of this CTA (own included) or of the
+                            // previous CTA's last two: its ring cell
+                            int rg;
+                            if (j >= qc0) {
+                                // the producing lane: walk back from the own one (stencil
+                                // couplings reach a segment or two)
+                                int l2 = l;
+                                while (R.sq0[l2] > j) --l2;
+                                rg = l2 + 2;
+                            } else {
+                                rg = j >= R.hq0[1] ? 1 : 0;
+                            }
+                            addr = smem_addr(&R.ring[rg][j & (kLnRing - 1)]);
                             want = s * n + j;
                         } else {
                             if (nslot >= kLnSlots) {
@@ -440,10 +474,42 @@ __global__ void __launch_bounds__(kLnThreads, 1)
     // A pass finds the solver lanes whose next kLnRb rows hold a pending poll slot (thread
     // = solver lane); each such lane's (row, slot) pairs are then loaded by the whole warp
     // at once (thread = row * 4 + slot), so one global round trip serves a lane's window.
+    // It also streams the halo: lanes 0-15 / 16-31 follow the previous CTA's last two
+    // segments in (sweep, row) order, 16 rows per round trip, and copy every published
+    // value, in order, into the halo ring with one 16-byte store (value and tag together).
     {
         const int32_t total_l = (R.sq0[lane + 1] - R.sq0[lane]) * nsw;
+        const int hh = lane >> 4;
+        const int32_t hbase = R.hq0[hh], hlen = R.hq0[hh + 1] - hbase;
+        const int32_t htotal = hlen * nsw;
+        int32_t hcur = 0;  // halo rows copied so far (uniform within a 16-lane group)
         unsigned ns = 0;
         while (__shfl_sync(0xffffffffu, vload(&R.live), 0)) {
+            bool hprog = false;
+            {
+                const int32_t hu = hcur + (lane & 15);
+                bool ok = false;
+                unsigned long long bits = kPending;
+                int32_t hs = 0, hq = 0;
+                if (hu < htotal) {
+                    hs = hu / hlen;
+                    hq = hbase + (hu - hs * hlen);
+                    bits = load_relaxed_bits(X + static_cast<size_t>(hs + 1) * stride + hq);
+                    ok = bits != kPending;
+                }
+                const unsigned okm = __ballot_sync(0xffffffffu, ok);
+                const unsigned gm = (okm >> (hh * 16)) & 0xffffu;
+                const int pre = __ffs(~gm) - 1;  // ready rows from the group's cursor on
+                if ((lane & 15) < pre) {
+                    const unsigned a = smem_addr(&R.ring[hh][hq & (kLnRing - 1)]);
+                    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a),
+                                 "r"(static_cast<unsigned>(bits)), "r"(static_cast<unsigned>(bits >> 32)),
+                                 "r"(static_cast<unsigned>(hs * n + hq)), "r"(0u)
+                                 : "memory");
+                }
+                hcur += pre;
+                hprog = pre > 0;
+            }
             const int32_t u0 = vload(&R.consumed[lane]);
             const int32_t uready = min(ld_acquire_cta(&R.ready[lane]) * kLnRb, total_l);
             bool pend = false;
@@ -477,7 +543,7 @@ __global__ void __launch_bounds__(kLnThreads, 1)
                 }
             }
             // back off between passes (the shared-memory pipe is the solver's critical path)
-            if (__any_sync(0xffffffffu, progress) || any) {
+            if (__any_sync(0xffffffffu, progress || hprog) || any) {
                 ns = poll_ns;
             } else {
                 ns = ns ? min(2 * ns, 1024u) : poll_ns;

@@ -936,14 +936,13 @@ void gauss_seidel(Ctx& c, const DCsr& A, const double* inv_diag, double* x, cons
         bwidth = staged<int32_t>(c, 0);
         longest_row = staged<int32_t>(c, 1);
     }
-    // lane per segment (gs_lanes.cuh): single column, forward sweeps, rows of at most 9
-    // entries (wider rows -- 19-point coarse operators -- measured slower than the 3-warp
-    // kernel), every segment resident at once (one CTA of 32 segments per SM)
+    // lane per segment (gs_lanes.cuh): single column, forward sweeps, rows of at most 21
+    // entries, every segment resident at once (one CTA of 32 segments per SM)
     {
         const char* ln_env = std::getenv("AMGCU_GS_LANES");
         const bool ln_off = ln_env && ln_env[0] == '0';
         const int32_t nctas = (nf + kLnLanes - 1) / kLnLanes;
-        if (!ln_off && !trace_path && k == 1 && !symmetric_sweep && longest_row <= 9 && nctas <= c.sms &&
+        if (!ln_off && !trace_path && k == 1 && !symmetric_sweep && longest_row <= 21 && nctas <= c.sms &&
             static_cast<int64_t>(nsw) * n < (int64_t(1) << 31) && n < (1 << 24) && static_cast<int64_t>(nf) * 16 <= n) {
             // AMGCU_GS_STATS=1: solver iteration / stall counters on stderr
             static const bool want_stats = std::getenv("AMGCU_GS_STATS") != nullptr;
@@ -960,7 +959,8 @@ void gauss_seidel(Ctx& c, const DCsr& A, const double* inv_diag, double* x, cons
                             static_cast<const int32_t*>(segf.get()), nf, X.get(), ticket.get(), st.get(),
                             gs_env_u("AMGCU_GS_POLL_NS", 128u), gs_env_u("AMGCU_GS_PF_NS", 128u));
             };
-            runl(k_gs_lanes<8, 3, 4, 64>, ln_smem_bytes<8, 3, 4, 64>());
+            if (longest_row <= 9) runl(k_gs_lanes<8, 3, 4, 64>, ln_smem_bytes<8, 3, 4, 64>());
+            else runl(k_gs_lanes<20, 2, 2, 32>, ln_smem_bytes<20, 2, 2, 32>());
             copy_d2d(c, x, X.get() + stride * nsw, static_cast<int64_t>(stride));
             sync(c);
             if (want_stats) {

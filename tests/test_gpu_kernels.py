@@ -246,7 +246,10 @@ def test_gauss_seidel_lane_segments(gpu_seq, port, monkeypatch, lanes):
     cases = [stencil9(64, 100, rng), stencil9(200, 40, rng), stencil9(48, 70, rng, cross=True, extra=0.3),
              stencil9(40, 90, rng, cross=True, extra=0.2, reach=300),
              stencil9(40, 90, rng, cross=True, extra=0.5, reach=2000), stencil9(50, 80, rng, ry=2, cross=True),
-             stencil9(36, 75, rng, ry=2, cross=True, extra=0.3, reach=200)]
+             stencil9(36, 75, rng, ry=2, cross=True, extra=0.3, reach=200),
+             # wide rows (10..21 entries: the T = 20 records, halo of two segments)
+             stencil9(50, 80, rng, ry=2), stencil9(36, 110, rng, ry=2, extra=0.2, reach=300),
+             stencil9(64, 70, rng, rx=3, ry=1, extra=0.1)]
     for A_ in cases:
         n = A_.n_rows
         for sweeps in (1, 4):
