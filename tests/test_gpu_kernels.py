@@ -200,6 +200,20 @@ def test_aggregation_known_answers(gpu):
     assert n == 1 and list(roots) == [0] and list(own) == [0, 0, 0]
 
 
+def test_aggregation_grids(gpu, port):
+    """Pass 1 (the sync-free wavefront) on grids of 20k-36k nodes, with long-range
+    couplings and with two-row reach, against the sequential pass."""
+    rng = np.random.default_rng(47)
+    for A_ in (stencil9(200, 150, rng), stencil9(300, 120, rng, cross=True, extra=0.02, reach=20000),
+               stencil9(130, 260, rng, ry=2, cross=True)):
+        R = A_.copy() if hasattr(A_, "copy") else A_
+        R.values = np.abs(R.values)
+        S = port.normalize_strength(R)
+        a = api.greedy_aggregate(S, ctx=gpu)
+        b = port.greedy_aggregate(S)
+        assert a[0] == b[0] and np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2]), A_.n_rows
+
+
 def test_aggregation_random(gpu, port):
     rng = np.random.default_rng(31)
     for _ in range(10):

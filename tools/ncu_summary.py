@@ -8,13 +8,13 @@ import json
 import subprocess
 import sys
 
-tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
+tag = sys.argv[1] if len(sys.argv) > 1 else "r02"
 want = {"Duration": "dur", "DRAM Throughput": "dram_pct", "Memory Throughput": "mem",
         "Compute (SM) Throughput": "sm_pct", "Achieved Occupancy": "occ", "Registers Per Thread": "regs",
         "Grid Size": "grid", "L2 Hit Rate": "l2hit", "L1/TEX Hit Rate": "l1hit"}
 rows = []
-CAPTURES = ("gs", "lfmis", "evolution", "spgemm_hash", "spgemm_sort", "arnoldi", "masked", "relax0", "jacobi",
-            "prolong", "sell_spmv")
+CAPTURES = ("gs", "gs_seg", "lfmis", "evolution", "spgemm_hash", "spgemm_sort", "arnoldi", "masked", "relax0",
+            "jacobi", "prolong", "sell_spmv", "vcycle_fused", "count")
 SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1.0, "nsecond": 1.0, "us": 1e3,
          "usecond": 1e3, "ms": 1e6, "msecond": 1e6}
 for rep in [f"gpurun_out/{tag}_{c}.ncu-rep" for c in CAPTURES if glob.glob(f"gpurun_out/{tag}_{c}.ncu-rep")]:
