@@ -57,6 +57,8 @@ void ensure_start_vector(Ctx& c, size_t n) {
 // w -= h_t v_t fused with the next dot (the last one with (w, w)); then
 // v_{j+1} = w * (1 / h).  H is written by block 0.
 constexpr int kArnThreads = 256;  // == blas.cu kDotThreads
+constexpr int kArnRegElems = 4;   // == blas.cu kUnroll: dot_grid gives <= 4 elements per thread
+constexpr int kArnRegVb = 3;      // virtual blocks per physical block with w in registers
 using ArnBR = cub::BlockReduce<double, kArnThreads>;
 
 struct ArnShared {
@@ -65,8 +67,18 @@ struct ArnShared {
 };
 
 // finish one reduction: partials of the gv virtual blocks -> every block
+// grid barrier; a one-block launch (the smallest levels) needs only the block barrier
+__device__ __forceinline__ void arn_sync(cooperative_groups::grid_group& grid) {
+    if (gridDim.x == 1) {
+        __threadfence_block();
+        __syncthreads();
+    } else {
+        grid.sync();
+    }
+}
+
 __device__ double arn_finish(double* partials, int gv, cooperative_groups::grid_group& grid, ArnShared& sh) {
-    grid.sync();
+    arn_sync(grid);
     double t = 0.0;
     for (int k = threadIdx.x; k < gv; k += kArnThreads) t += __ldcg(&partials[k]);
     t = ArnBR(sh.tmp).Sum(t);
@@ -83,7 +95,7 @@ __device__ __forceinline__ void arn_partial(double s, int vb, double* partials, 
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(kArnThreads)
+__global__ void __launch_bounds__(kArnThreads, 3)  // >= 3 blocks per SM: 444 blocks serve level 0's 1022 virtual ones
     k_arnoldi_coop(int32_t n, int m, int gv, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
                    const double* __restrict__ va, const double* __restrict__ dinv, const double* __restrict__ v0,
                    double* __restrict__ V, double* __restrict__ H, double* __restrict__ partials_base) {
@@ -111,7 +123,78 @@ __global__ void __launch_bounds__(kArnThreads)
     const double inv0 = 1.0 / sqrt(arn_finish(P, gv, grid, sh));
     for (int vb = blockIdx.x; vb < gv; vb += gridDim.x)
         for (int64_t i = static_cast<int64_t>(vb) * kArnThreads + threadIdx.x; i < n; i += vstride) V[i] *= inv0;
-    grid.sync();
+    arn_sync(grid);
+    if (gridDim.x * kArnRegVb >= gv && static_cast<int64_t>(kArnRegElems) * vstride >= n) {
+        // every physical block serves at most kArnRegVb virtual blocks of at most
+        // kArnRegElems elements per thread: w stays in registers through the whole
+        // Gram-Schmidt loop (a sub-step reads v_t and v_{t+1} only); same element order,
+        // same per-virtual-block partials, same trees
+        for (int j = 0; j < m; ++j) {
+            const double* vj = V + static_cast<size_t>(j) * n;
+            double wr[kArnRegVb][kArnRegElems];
+            P = next_partials();
+#pragma unroll
+            for (int b = 0; b < kArnRegVb; ++b) {
+                const int vb = blockIdx.x + b * gridDim.x;
+                if (vb >= gv) break;
+                double s = 0.0;
+#pragma unroll
+                for (int e = 0; e < kArnRegElems; ++e) {
+                    const int64_t i = static_cast<int64_t>(vb) * kArnThreads + threadIdx.x + e * vstride;
+                    wr[b][e] = 0.0;
+                    if (i < n) {
+                        double a = 0.0;
+                        for (int32_t p = rp[i]; p < rp[i + 1]; ++p) a += va[p] * vj[ci[p]];
+                        a *= dinv[i];
+                        wr[b][e] = a;
+                        s += a * V[i];
+                    }
+                }
+                arn_partial(s, vb, P, sh);
+            }
+            double h = arn_finish(P, gv, grid, sh);
+            for (int t = 0; t <= j; ++t) {
+                if (blockIdx.x == 0 && threadIdx.x == 0) H[static_cast<size_t>(t) * m + j] = h;
+                const double* vt = V + static_cast<size_t>(t) * n;
+                const double* vn = t < j ? V + static_cast<size_t>(t + 1) * n : nullptr;
+                const double a = -1.0 * h;
+                P = next_partials();
+#pragma unroll
+                for (int b = 0; b < kArnRegVb; ++b) {
+                    const int vb = blockIdx.x + b * gridDim.x;
+                    if (vb >= gv) break;
+                    double s = 0.0;
+#pragma unroll
+                    for (int e = 0; e < kArnRegElems; ++e) {
+                        const int64_t i = static_cast<int64_t>(vb) * kArnThreads + threadIdx.x + e * vstride;
+                        if (i < n) {
+                            const double wi = wr[b][e] + a * vt[i];
+                            wr[b][e] = wi;
+                            s += wi * (vn ? vn[i] : wi);
+                        }
+                    }
+                    arn_partial(s, vb, P, sh);
+                }
+                h = arn_finish(P, gv, grid, sh);
+            }
+            const double hn = sqrt(h);
+            if (blockIdx.x == 0 && threadIdx.x == 0) H[static_cast<size_t>(j + 1) * m + j] = hn;
+            const double inv = 1.0 / hn;
+            double* w = V + static_cast<size_t>(j + 1) * n;
+#pragma unroll
+            for (int b = 0; b < kArnRegVb; ++b) {
+                const int vb = blockIdx.x + b * gridDim.x;
+                if (vb >= gv) break;
+#pragma unroll
+                for (int e = 0; e < kArnRegElems; ++e) {
+                    const int64_t i = static_cast<int64_t>(vb) * kArnThreads + threadIdx.x + e * vstride;
+                    if (i < n) w[i] = wr[b][e] * inv;
+                }
+            }
+            arn_sync(grid);
+        }
+        return;
+    }
     for (int j = 0; j < m; ++j) {
         const double* vj = V + static_cast<size_t>(j) * n;
         double* w = V + static_cast<size_t>(j + 1) * n;
@@ -152,7 +235,7 @@ __global__ void __launch_bounds__(kArnThreads)
         const double inv = 1.0 / hn;
         for (int vb = blockIdx.x; vb < gv; vb += gridDim.x)
             for (int64_t i = static_cast<int64_t>(vb) * kArnThreads + threadIdx.x; i < n; i += vstride) w[i] *= inv;
-        grid.sync();
+        arn_sync(grid);
     }
 }
 
@@ -179,7 +262,8 @@ double spectral_radius(Ctx& c, const DCsr& A, int steps, const double* dinv, int
             AMG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_arnoldi_coop, kArnThreads, 0));
         // virtual grid = the launch-per-step path's dot grid (blas.cu), physical grid co-resident
         const int gv = static_cast<int>(dot_grid(c, n));
-        const int g = std::max(1, std::min(per_sm * c.sms, gv));
+        // register path when g * kArnRegVb >= gv; the smallest levels run as one block
+        const int g = gv <= kArnRegVb ? 1 : std::max(1, std::min(per_sm * c.sms, gv));
         ensure_reduction_scratch(c, 2 * static_cast<size_t>(gv));
         int32_t nn = n;
         int mm = m;

@@ -105,6 +105,49 @@ __global__ void __launch_bounds__(kDotThreads)
     finish_tree(b, partials, done, out, take_sqrt);
 }
 
+// PCG step (cycle.hpp:190-194): x += alpha p, r -= alpha q (alpha = st[2]), then
+// *out = ||r|| -- the norm summed exactly as k_dot_tree sums (r, r) on the same grid, so
+// the fused pass gives the same bits as the update followed by nrm2.  Skipped (no
+// update, no norm) when *bad is set.
+__global__ void __launch_bounds__(kDotThreads)
+    k_pcg_update_nrm(const double* __restrict__ st, const int32_t* __restrict__ bad, const double* __restrict__ p,
+                     const double* __restrict__ q, double* __restrict__ x, double* __restrict__ r, int64_t n,
+                     double* __restrict__ partials, unsigned int* __restrict__ done, double* __restrict__ out) {
+    using BR = cub::BlockReduce<double, kDotThreads>;
+    __shared__ typename BR::TempStorage tmp;
+    if (*bad) return;
+    const double a = st[2];
+    const double na = -a;
+    double s = 0.0;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * kDotThreads;
+    int64_t i = static_cast<int64_t>(blockIdx.x) * kDotThreads + threadIdx.x;
+    for (; i + (kUnroll - 1) * stride < n; i += kUnroll * stride) {
+        double rv[kUnroll], qv[kUnroll], xv[kUnroll], pv[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            rv[u] = r[i + u * stride];
+            qv[u] = __ldg(&q[i + u * stride]);
+            xv[u] = x[i + u * stride];
+            pv[u] = __ldg(&p[i + u * stride]);
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            x[i + u * stride] = xv[u] + a * pv[u];
+            const double ri = rv[u] + na * qv[u];
+            r[i + u * stride] = ri;
+            s += ri * ri;
+        }
+    }
+    for (; i < n; i += stride) {
+        x[i] += a * p[i];
+        const double ri = r[i] + na * q[i];
+        r[i] = ri;
+        s += ri * ri;
+    }
+    const double b = BR(tmp).Sum(s);
+    finish_tree(b, partials, done, out, true);
+}
+
 __global__ void k_dot_seq(const double* __restrict__ x, const double* __restrict__ y, int64_t n, double* __restrict__ out,
                           bool take_sqrt) {
     const int lane = threadIdx.x;
@@ -178,6 +221,16 @@ void axpy_dot(Ctx& c, const double* alpha, double sign, const double* x, double*
 
 void dot(Ctx& c, const double* x, const double* y, int64_t n, double* out) { dot_impl(c, x, y, n, out, false); }
 void nrm2(Ctx& c, const double* x, int64_t n, double* out) { dot_impl(c, x, x, n, out, true); }
+
+bool pcg_update_nrm(Ctx& c, const double* st, const int32_t* bad, const double* p, const double* q, double* x,
+                    double* r, int64_t n, double* out) {
+    if (c.seq) return false;  // parity mode: the update kernel and the sequential norm
+    const unsigned g = dot_grid(c, n);
+    ensure_reduction_scratch(c, g);
+    launch_prof(c, kProfBlas1, 56.0 * n, k_pcg_update_nrm, g, kDotThreads, 0, st, bad, p, q, x, r, n,
+                c.partials.get(), c.tickets.get(), out);
+    return true;
+}
 
 void axpy_dev(Ctx& c, const double* alpha, double sign, const double* x, double* y, int64_t n) {
     launch_prof(c, c.blas_family, 24.0 * n, k_axpy_dev, stream_grid(c, n), 256, 0, alpha, sign, x, y, n);

@@ -856,10 +856,12 @@ SolveResult solve(DHier& h, const double* b, double* x, const amgcu_solve_option
             d.ops += static_cast<double>(L0.A.nnz);
             dot(c, p.get(), q.get(), n, S + 1);
             launch(c, k_pcg_alpha, 1, 1, 0, S, bad.get());
-            launch_prof(c, kProfBlas1, 48.0 * n, k_pcg_update, stream_grid(c, n), 256, 0, static_cast<int64_t>(n), static_cast<const double*>(S),
-                   static_cast<const int32_t*>(bad.get()), static_cast<const double*>(p.get()),
-                   static_cast<const double*>(q.get()), x, r.get());
-            nrm2(c, r.get(), n, S + 5);
+            if (!pcg_update_nrm(c, S, bad.get(), p.get(), q.get(), x, r.get(), n, S + 5)) {
+                launch_prof(c, kProfBlas1, 48.0 * n, k_pcg_update, stream_grid(c, n), 256, 0, static_cast<int64_t>(n),
+                            static_cast<const double*>(S), static_cast<const int32_t*>(bad.get()),
+                            static_cast<const double*>(p.get()), static_cast<const double*>(q.get()), x, r.get());
+                nrm2(c, r.get(), n, S + 5);
+            }
             struct {
                 double rn;
                 int32_t bad;

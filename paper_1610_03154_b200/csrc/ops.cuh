@@ -43,6 +43,9 @@ void entry_rows(Ctx& c, const DCsr& A, int32_t* rows);
 void dot(Ctx& c, const double* x, const double* y, int64_t n, double* out);
 // *out = sqrt(dot(x, x))
 void nrm2(Ctx& c, const double* x, int64_t n, double* out);
+// x += st[2] p, r -= st[2] q, *out = ||r|| in one pass (false in parity mode: not launched)
+bool pcg_update_nrm(Ctx& c, const double* st, const int32_t* bad, const double* p, const double* q, double* x,
+                    double* r, int64_t n, double* out);
 // y += s * x with s = sign * (*alpha)   (axpy, sparse.hpp:317-319)
 void axpy_dev(Ctx& c, const double* alpha, double sign, const double* x, double* y, int64_t n);
 // x *= 1 / (*denom)                      (scale(1.0 / h, v))
