@@ -1,6 +1,8 @@
 // extern "C" boundary of libamgcu (include/amgcu.h).  Exceptions of the
 // reference's types are mapped to status codes here; messages go to
 // amgcu_last_error().
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -286,7 +288,15 @@ amgcu_status amgcu_setup_device(amgcu_ctx ctx, const amgcu_csr* A, int32_t k, co
         copy_d2d(c, view.rp.get(), A->row_offsets, A->n_rows + 1);
         copy_d2d(c, view.ci.get(), A->col_indices, A->nnz);
         copy_d2d(c, view.va.get(), A->values, A->nnz);
-        *out = make_hier(ctx, rn_setup(c, view, B, k, left, *opts));
+        static const bool ht = std::getenv("AMGCU_HOST_TRACE") != nullptr;
+        const auto t0 = std::chrono::steady_clock::now();
+        auto hh = rn_setup(c, view, B, k, left, *opts);
+        const auto t1 = std::chrono::steady_clock::now();
+        *out = make_hier(ctx, std::move(hh));
+        if (ht)
+            std::fprintf(stderr, "[host] rn_setup %.3f ms, returned after %.3f ms\n",
+                         std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t1).count());
     });
 }
 

@@ -15,6 +15,7 @@
 // per iteration (the residual norm decides termination, as in the reference).
 #include <cooperative_groups.h>
 
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -805,8 +806,13 @@ SolveResult solve(DHier& h, const double* b, double* x, const amgcu_solve_option
         h.wu[4] += d.ops / h.base_nnz;
         return rep;
     };
+    static const bool ht = std::getenv("AMGCU_HOST_TRACE") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
     DBuf<double> r(static_cast<size_t>(n), c.s), st(16, c.s);
     DBuf<int32_t> bad(1, c.s);
+    if (ht)
+        std::fprintf(stderr, "[host] solve preamble (complexities, ledger, buffers) %.3f ms\n",
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
     launch(c, k_sell_residual, rows_grid(n), 128, 0, A, static_cast<const double*>(x), b, r.get());
     d.ops += static_cast<double>(L0.A.nnz);
     double* S = st.get();

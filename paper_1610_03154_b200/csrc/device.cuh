@@ -105,6 +105,13 @@ struct ProfRecord {
 
 // AMGCU_PROF_OTHER=1: untagged launches are also timed per kernel symbol and the
 // breakdown is printed to stderr when the profile is read (tools/family_times.py)
+// AMGCU_SYNC_TRACE=1 also measures the GPU idle time each synchronisation causes: an
+// event before the wait and one right before the next launch on the stream
+void gap_before_sync(cudaStream_t s, const char* file, int line);
+void gap_before_launch(cudaStream_t s);
+void gap_after_sync();
+bool sync_trace_on();
+
 bool prof_other_enabled();
 void prof_other_add(const void* kernel, double ms);
 
@@ -206,6 +213,7 @@ void launch_check(Ctx& c, const void* kernel);
 template <typename Kern, typename... Args>
 inline void launch_raw(Ctx& c, Kern k, unsigned grid, unsigned block, size_t smem, Args... args) {
     if (grid == 0) return;
+    if (sync_trace_on()) gap_before_launch(c.s);
     k<<<grid, block, smem, c.s>>>(args...);
     ++c.launches;
     AMG_CK(cudaGetLastError());
@@ -302,7 +310,9 @@ void note_sync_site(const char* file, int line);
 inline void sync(Ctx& c, const char* file = __builtin_FILE(), int line = __builtin_LINE()) {
     ++c.syncs;
     note_sync_site(file, line);
+    if (sync_trace_on()) gap_before_sync(c.s, file, line);
     AMG_CK(cudaStreamSynchronize(c.s));
+    if (sync_trace_on()) gap_after_sync();
 }
 template <typename T>
 T read_scalar(Ctx& c, const T* dptr, const char* file = __builtin_FILE(), int line = __builtin_LINE()) {

@@ -6,6 +6,7 @@
 #include "device.cuh"
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <vector>
 #include <cstring>
@@ -20,10 +21,34 @@ namespace {
 struct SyncSites {
     std::mutex m;
     std::map<std::string, long> n;
+    std::map<std::string, double> idle_ms;  // GPU idle after the synchronisations of a site
+    std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
+    std::string open_site;
+    cudaEvent_t open_ev = nullptr;
+    std::chrono::steady_clock::time_point open_t;  // host time the synchronisation returned
+    std::map<std::string, double> host_ms;          // host time from the return to the next launch
     bool on = std::getenv("AMGCU_SYNC_TRACE") != nullptr;
+    void resolve() {
+        for (auto& p : pending) {
+            float ms = 0.f;
+            if (cudaEventSynchronize(p.second.second) == cudaSuccess &&
+                cudaEventElapsedTime(&ms, p.second.first, p.second.second) == cudaSuccess)
+                idle_ms[p.first] += ms;
+            cudaEventDestroy(p.second.first);
+            cudaEventDestroy(p.second.second);
+        }
+        pending.clear();
+    }
     ~SyncSites() {
         if (!on) return;
-        for (auto& kv : n) std::fprintf(stderr, "sync %6ld  %s\n", kv.second, kv.first.c_str());
+        resolve();
+        double tot = 0.0;
+        for (auto& kv : n) {
+            std::fprintf(stderr, "sync %6ld  idle %8.3f ms  host %8.3f ms  %s\n", kv.second, idle_ms[kv.first],
+                         host_ms[kv.first], kv.first.c_str());
+            tot += idle_ms[kv.first];
+        }
+        std::fprintf(stderr, "sync total GPU idle after synchronisations: %.3f ms\n", tot);
     }
 };
 SyncSites& sync_sites() {
@@ -31,6 +56,38 @@ SyncSites& sync_sites() {
     return s;
 }
 }  // namespace
+
+bool sync_trace_on() { return sync_sites().on; }
+
+void gap_before_sync(cudaStream_t s, const char* file, int line) {
+    SyncSites& ss = sync_sites();
+    std::lock_guard<std::mutex> g(ss.m);
+    const char* base = std::strrchr(file, '/');
+    if (ss.open_ev) cudaEventDestroy(ss.open_ev);  // two syncs without a launch between them
+    cudaEventCreate(&ss.open_ev);
+    cudaEventRecord(ss.open_ev, s);
+    ss.open_site = std::string(base ? base + 1 : file) + ":" + std::to_string(line);
+    if (ss.pending.size() > 4096) ss.resolve();
+}
+
+void gap_after_sync() {
+    SyncSites& ss = sync_sites();
+    std::lock_guard<std::mutex> g(ss.m);
+    ss.open_t = std::chrono::steady_clock::now();
+}
+
+void gap_before_launch(cudaStream_t s) {
+    SyncSites& ss = sync_sites();
+    std::lock_guard<std::mutex> g(ss.m);
+    if (!ss.open_ev) return;
+    ss.host_ms[ss.open_site] +=
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - ss.open_t).count();
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, s);
+    ss.pending.push_back({ss.open_site, {ss.open_ev, e}});
+    ss.open_ev = nullptr;
+}
 
 void note_sync_site(const char* file, int line) {
     SyncSites& s = sync_sites();

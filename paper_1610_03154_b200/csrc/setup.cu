@@ -3,7 +3,9 @@
 // interp.cuh, level data resident in HBM.  Sizes cross to the host only where
 // an allocation depends on them (scan totals) and for the scalar decisions the
 // reference takes on the host (stagnation, symmetry, rho).
+#include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <string>
 
 #include <cusolverDn.h>
@@ -459,7 +461,14 @@ std::unique_ptr<DHier> rn_setup(Ctx& c, const DCsr& A, const double* B, int32_t 
         tally(c, nL * nL * nL);  // hierarchy.hpp:68
     }
     H->wu[4] = cfin / H->base_nnz;
-    prepare_solve(*H);
+    {
+        static const bool ht = std::getenv("AMGCU_HOST_TRACE") != nullptr;
+        const auto t0 = std::chrono::steady_clock::now();
+        prepare_solve(*H);
+        if (ht)
+            std::fprintf(stderr, "[host] prepare_solve %.3f ms\n",
+                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    }
     return H;
 }
 
