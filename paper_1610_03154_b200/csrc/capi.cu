@@ -619,6 +619,20 @@ amgcu_status amgcu_relax(amgcu_ctx ctx, const amgcu_csr* A, int32_t scheme, doub
         if (L.A.nr != L.A.nc) throw InvalidArgument("relax: square matrix required");
         const int32_t n = L.A.nr;
         DBuf<double> dx = up_vec(c, x, n), db = up_vec(c, b, n);
+        if (scheme == 3 || scheme == 4) {
+            // relaxation.hpp:67-97, 128-167
+            if (scheme == 3) {
+                GsneWs ws;
+                gsne_workspace(c, L.A, ws);
+                gsne(c, L.A, ws, dx.get(), db.get(), sweeps);
+            } else {
+                DBuf<double> inv;
+                block_workspace(c, L.A, inv);
+                block_sym_gs(c, L.A, inv.get(), dx.get(), db.get(), sweeps);
+            }
+            down_vec(c, x, dx.get(), n);
+            return;
+        }
         L.inv_diag.alloc(static_cast<size_t>(n), c.s);
         inverse_diagonal(c, L.A, L.inv_diag.get(), "relax: zero diagonal at row ");
         if (scheme == 0) {

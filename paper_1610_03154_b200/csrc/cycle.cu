@@ -658,7 +658,7 @@ struct Driver {
             }
         } else {
             if (x_zero) AMG_CK(cudaMemsetAsync(x, 0, sizeof(double) * n, c.s));
-            if (sweeps > 0) gauss_seidel(c, lev.A, lev.inv_diag.get(), x, b, 1, sweeps, pre == 2);
+            if (sweeps > 0) relax_other(lev, pre, x, b, sweeps);
             ops += sweeps * relax_cost(pre, nnz);
         }
         if (pre != 0 && x_zero && sweeps == 0) {
@@ -713,12 +713,19 @@ struct Driver {
             }
         } else {
             copy_d2d(c, x, lev.t.get(), n);
-            if (sweeps > 0) gauss_seidel(c, lev.A, lev.inv_diag.get(), x, b, 1, sweeps, post == 2);
+            if (sweeps > 0) relax_other(lev, post, x, b, sweeps);
             ops += sweeps * relax_cost(post, nnz);
         }
     }
 
     void precond(const double* rhs, double* out, int kind) { apply(0, out, rhs, kind, true); }
+
+    // the sequential schemes: (symmetric) Gauss-Seidel, gsne, block symmetric GS
+    void relax_other(DLevel& lev, int scheme, double* x, const double* b, int sweeps) {
+        if (scheme == 3) gsne(c, lev.A, lev.gsne_ws, x, b, sweeps);
+        else if (scheme == 4) block_sym_gs(c, lev.A, lev.block_inv.get(), x, b, sweeps);
+        else gauss_seidel(c, lev.A, lev.inv_diag.get(), x, b, 1, sweeps, scheme == 2);
+    }
 };
 
 double conv_factor(const std::vector<double>& hist, int window = 5) {  // cycle.hpp:39-46

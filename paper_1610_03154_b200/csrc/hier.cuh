@@ -29,6 +29,8 @@ struct DLevel {
     DBuf<double> wd_pre, wd_post;  // jacobi weight * inv_diag
     double w_pre = 0.0, w_post = 0.0;
     DBuf<double> r, t, b, x;  // cycle scratch (b, x used on levels > 0)
+    GsneWs gsne_ws;           // gsne workspace (pre or post scheme 3)
+    DBuf<double> block_inv;   // block symmetric GS workspace (scheme 4)
 };
 
 struct DHier {

@@ -103,4 +103,16 @@ void gauss_seidel(Ctx& c, const DCsr& A, const double* inv_diag, double* x, cons
 // weighted Jacobi sweeps x += (w dinv) (b - A x) (relaxation.hpp:107-113); b may be nullptr (0)
 void jacobi(Ctx& c, const DCsr& A, const double* wdinv, double* x, const double* b, int k, int sweeps);
 
+// relax_more.cu: gsne (relaxation.hpp:128-142) and block symmetric Gauss-Seidel
+// (relaxation.hpp:143-167), one column of x; workspaces as make_relax_workspace
+// (relaxation.hpp:67-97): A^T and the squared column norms / the diagonal block inverses
+struct GsneWs {
+    DCsr At;
+    DBuf<double> cn2;
+};
+void gsne_workspace(Ctx& c, const DCsr& A, GsneWs& ws);
+void gsne(Ctx& c, const DCsr& A, const GsneWs& ws, double* x, const double* b, int sweeps);
+void block_workspace(Ctx& c, const DCsr& A, DBuf<double>& inv);
+void block_sym_gs(Ctx& c, const DCsr& A, const double* inv, double* x, const double* b, int sweeps);
+
 }  // namespace amgcu

@@ -278,9 +278,9 @@ bool dense_inverse_gpu(Ctx& c, double* D, int32_t n, double* inv) {
 }  // namespace
 
 void require_supported_relax(int scheme, const char* who) {
-    if (scheme == 0 || scheme == 1 || scheme == 2) return;
+    if (scheme >= 0 && scheme <= 4) return;
     throw InvalidArgument(std::string(who) +
-                          ": relaxation scheme not available on the GPU path (jacobi, gauss_seidel, sym_gauss_seidel)");
+                          ": unknown relaxation scheme");
 }
 
 double level_rho(Ctx& c, DLevel& L) {
@@ -311,9 +311,24 @@ void improve_candidates(Ctx& c, const DCsr& A, double* B, int32_t k, int sweeps,
     const int32_t n = A.nr;
     if (sweeps > 0) {
         require_supported_relax(scheme, "improve_candidates");
-        DBuf<double> dinv(static_cast<size_t>(n), c.s);
-        inverse_diagonal(c, A, dinv.get(), "relax: zero diagonal at row ");
-        if (scheme == 0) {
+        DBuf<double> dinv;
+        if (scheme <= 2) {
+            dinv.alloc(static_cast<size_t>(n), c.s);
+            inverse_diagonal(c, A, dinv.get(), "relax: zero diagonal at row ");
+        }
+        if (scheme == 3 || scheme == 4) {
+            // make_relax_workspace then relax per candidate column with b = 0
+            // (interpolation.hpp:88-92)
+            GsneWs gw;
+            DBuf<double> binv;
+            if (scheme == 3) gsne_workspace(c, A, gw);
+            else block_workspace(c, A, binv);
+            for (int32_t j = 0; j < k; ++j) {
+                double* col = B + static_cast<size_t>(j) * n;
+                if (scheme == 3) gsne(c, A, gw, col, nullptr, sweeps);
+                else block_sym_gs(c, A, binv.get(), col, nullptr, sweeps);
+            }
+        } else if (scheme == 0) {
             double w = weight;
             if (w == 0.0) {
                 double rho;
@@ -335,8 +350,8 @@ void improve_candidates(Ctx& c, const DCsr& A, double* B, int32_t k, int sweeps,
         } else {
             gauss_seidel(c, A, dinv.get(), B, nullptr, k, sweeps, scheme == 2);
         }
-        // relaxation.hpp:207: one count of nnz per sweep and candidate column
-        tally(c, static_cast<double>(k) * sweeps * static_cast<double>(A.nnz));
+        // relaxation.hpp:207: relax_sweep_cost per sweep and candidate column (2 |A| for gsne)
+        tally(c, static_cast<double>(k) * sweeps * (scheme == 3 ? 2.0 : 1.0) * static_cast<double>(A.nnz));
     }
     DBuf<double> nrm(static_cast<size_t>(k), c.s);
     for (int32_t j = 0; j < k; ++j) {
@@ -429,10 +444,13 @@ std::unique_ptr<DHier> rn_setup(Ctx& c, const DCsr& A, const double* B, int32_t 
     for (size_t l = 0; l + 1 < H->lv.size(); ++l) {
         DLevel& L = H->lv[l];
         const int32_t n = L.A.nr;
-        if (L.inv_diag.empty()) {
+        if (L.inv_diag.empty() && (o.pre_scheme <= 2 || o.post_scheme <= 2)) {
             L.inv_diag.alloc(static_cast<size_t>(n), c.s);
             inverse_diagonal(c, L.A, L.inv_diag.get(), "relax: zero diagonal at row ");
         }
+        // make_relax_workspace (relaxation.hpp:67-97) for the remaining schemes
+        if (o.pre_scheme == 3 || o.post_scheme == 3) gsne_workspace(c, L.A, L.gsne_ws);
+        if (o.pre_scheme == 4 || o.post_scheme == 4) block_workspace(c, L.A, L.block_inv);
         auto weight = [&](int scheme, double w) {  // make_ws, relaxation.hpp:52-54
             if (scheme != 0) return 0.0;
             return w != 0.0 ? w : 4.0 / (3.0 * rho_tallied(c, L));

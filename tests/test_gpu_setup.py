@@ -240,3 +240,50 @@ def test_fused_coarse_cycle_matches_per_kernel(gpu, monkeypatch, config, size):
     assert r1.iterations == r0.iterations
     assert np.asarray(x1).tobytes() == np.asarray(x0).tobytes()
     assert list(r1.residual_history) == list(r0.residual_history)
+
+
+GSNE = RelaxConfig(RelaxScheme.gsne, 0.0, 1)
+BSGS = RelaxConfig(RelaxScheme.block_sym_gauss_seidel, 0.0, 1)
+
+
+@pytest.mark.parametrize("scheme", [RelaxScheme.gsne, RelaxScheme.block_sym_gauss_seidel],
+                         ids=["gsne", "block_sgs"])
+def test_relax_remaining_schemes(gpu, port, scheme):
+    """gsne (relaxation.hpp:128-142) and block symmetric Gauss-Seidel (143-167) against
+    the reference sweeps, bit for bit: several sweeps, block sizes 1 and 2 (elasticity),
+    non-symmetric rows, long rows"""
+    rng = np.random.default_rng(53)
+    mats = [aniso2d(20, 0.1), api.generate_config(5, 6)[0], api.generate_config(3, 16)[0]]
+    for A in mats:
+        n = A.n_rows
+        b = rng.uniform(-1, 1, n)
+        x0 = rng.uniform(-1, 1, n)
+        for sweeps in (1, 3):
+            got = api.relax(A, int(scheme), 0.0, sweeps, x0, b, ctx=gpu)
+            want = port.relax(A, int(scheme), 0.0, sweeps, x0, b)
+            assert got.tobytes() == want.tobytes(), (n, A.block_size, sweeps)
+        B = api.CandidateSet(n, 2, rng.uniform(0.5, 1.5, 2 * n))
+        got = api.improve_candidates(A, B, 2, int(scheme), 0.0, ctx=gpu)
+        want = port.improve_candidates(A, B, 2, int(scheme), 0.0)
+        assert got.data.tobytes() == want.data.tobytes(), n
+
+
+@pytest.mark.parametrize("relax", [GSNE, BSGS], ids=["gsne", "block_sgs"])
+def test_setup_solve_remaining_schemes(gpu_seq, port, relax):
+    """rn_setup + solve with gsne / block symmetric GS as pre-, post- and candidate
+    relaxation: hierarchy bitwise (parity mode), ledger equal, solves equal"""
+    for gen, vo in ((lambda: api.generate_config(2, 17), SolveOptions(SolveMethod.stationary, max_iters=10)),
+                    (lambda: api.generate_config(5, 6), SolveOptions(SolveMethod.fgmres, max_iters=8))):
+        A, B, Bh, b = gen()
+        so = SetupOptions(pre_relax=relax, post_relax=relax, candidate_relax=RelaxConfig(relax.scheme, 0.0, 1),
+                          max_size=30)
+        hg = api.setup(A, B, so, Bh, ctx=gpu_seq)
+        ho = port.setup(A, B, so, Bh)
+        compare(hg, ho, bitwise=True)
+        assert hg.ledger().tobytes() == ho.ledger().tobytes()
+        xg, rg = api.solve(hg, b, None, vo)
+        xo, ro = port.solve(ho, b, None, vo)
+        assert rg.iterations == ro.iterations and rg.converged == ro.converged
+        assert rel_max_err(rg.residual_history, ro.residual_history) <= 1e-10
+        assert rel_max_err(xg, xo) <= 1e-10
+        assert hg.ledger().tobytes() == ho.ledger().tobytes()
