@@ -248,7 +248,7 @@ BSGS = RelaxConfig(RelaxScheme.block_sym_gauss_seidel, 0.0, 1)
 
 @pytest.mark.parametrize("scheme", [RelaxScheme.gsne, RelaxScheme.block_sym_gauss_seidel],
                          ids=["gsne", "block_sgs"])
-def test_relax_remaining_schemes(gpu, port, scheme):
+def test_relax_remaining_schemes(gpu_seq, port, scheme):
     """gsne (relaxation.hpp:128-142) and block symmetric Gauss-Seidel (143-167) against
     the reference sweeps, bit for bit: several sweeps, block sizes 1 and 2 (elasticity),
     non-symmetric rows, long rows"""
@@ -259,11 +259,11 @@ def test_relax_remaining_schemes(gpu, port, scheme):
         b = rng.uniform(-1, 1, n)
         x0 = rng.uniform(-1, 1, n)
         for sweeps in (1, 3):
-            got = api.relax(A, int(scheme), 0.0, sweeps, x0, b, ctx=gpu)
+            got = api.relax(A, int(scheme), 0.0, sweeps, x0, b, ctx=gpu_seq)
             want = port.relax(A, int(scheme), 0.0, sweeps, x0, b)
             assert got.tobytes() == want.tobytes(), (n, A.block_size, sweeps)
         B = api.CandidateSet(n, 2, rng.uniform(0.5, 1.5, 2 * n))
-        got = api.improve_candidates(A, B, 2, int(scheme), 0.0, ctx=gpu)
+        got = api.improve_candidates(A, B, 2, int(scheme), 0.0, ctx=gpu_seq)
         want = port.improve_candidates(A, B, 2, int(scheme), 0.0)
         assert got.data.tobytes() == want.data.tobytes(), n
 
