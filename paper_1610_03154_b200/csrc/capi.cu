@@ -152,6 +152,7 @@ amgcu_status amgcu_ctx_destroy(amgcu_ctx ctx) {
     ctx->c.partials.release();
     ctx->c.tickets.release();
     ctx->c.arnoldi_v0.release();
+    ctx->c.scan_tmp.release();  // every stream-ordered buffer before its stream goes
     cudaStreamSynchronize(ctx->c.s);
     if (ctx->c.pin) cudaFreeHost(ctx->c.pin);
     cudaStreamSynchronize(ctx->c.side);

@@ -133,6 +133,7 @@ struct Ctx {
     DBuf<double> scal;         // device scalars for reductions/control
     DBuf<double> partials;     // per-block partial sums
     DBuf<unsigned int> tickets;  // sync-free wavefront tickets
+    DBuf<unsigned char> scan_tmp;  // cub::DeviceScan temporary storage
     // pinned host staging: several device scalars are read back with one synchronisation
     int64_t* pin = nullptr;
     static constexpr int kPinSlots = 512;

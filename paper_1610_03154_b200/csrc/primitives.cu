@@ -2,6 +2,9 @@
 // fills, CSR upload/download.
 #include <cub/block/block_reduce.cuh>
 #include <cub/block/block_scan.cuh>
+#include <cub/device/device_scan.cuh>
+#include <thrust/iterator/counting_iterator.h>
+#include <thrust/iterator/transform_iterator.h>
 
 #include "device.cuh"
 
@@ -206,15 +209,23 @@ __global__ void k_tile_scan(const T* __restrict__ in, T* __restrict__ out, int64
         const int64_t i = base + threadIdx.x * kScanItems + k;
         v[k] = i < n ? in[i] : T(0);
     }
-    BS(tmp).ExclusiveSum(v, v);
-    const T off = offs[blockIdx.x];
+    T agg;
+    BS(tmp).ExclusiveSum(v, v, agg);
+    const T off = offs ? offs[blockIdx.x] : T(0);
 #pragma unroll
     for (int k = 0; k < kScanItems; ++k) {
         const int64_t i = base + threadIdx.x * kScanItems + k;
         if (i < n) out[i] = v[k] + off;
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) out[n] = offs[ntiles];
+    if (blockIdx.x == 0 && threadIdx.x == 0) out[n] = offs ? offs[ntiles] : agg;
 }
+
+template <typename T>
+struct PadZero {  // in[i] for i < n, 0 at i == n
+    const T* in;
+    int64_t n;
+    __host__ __device__ T operator()(int64_t i) const { return i < n ? in[i] : T(0); }
+};
 
 template <typename T>
 int64_t scan_impl(Ctx& c, const T* in, T* out, int64_t n, bool read_total, const char* file, int line) {
@@ -222,12 +233,21 @@ int64_t scan_impl(Ctx& c, const T* in, T* out, int64_t n, bool read_total, const
         AMG_CK(cudaMemsetAsync(out, 0, sizeof(T), c.s));
         return 0;
     }
-    const int64_t ntiles = (n + kTile - 1) / kTile;
-    DBuf<T> sums(static_cast<size_t>(ntiles) + 1, c.s);
-    launch(c, k_tile_reduce<T>, static_cast<unsigned>(ntiles), kScanThreads, 0, in, n, sums.get());
-    launch(c, k_scan_tile_sums<T>, 1, kScanThreads, 0, sums.get(), ntiles);
-    launch(c, k_tile_scan<T>, static_cast<unsigned>(ntiles), kScanThreads, 0, in, out, n,
-           static_cast<const T*>(sums.get()), ntiles);
+    if (n <= kTile) {
+        // one tile: one block scans it and writes the total
+        const T zero = 0;
+        launch(c, k_tile_scan<T>, 1u, kScanThreads, 0, in, out, n, static_cast<const T*>(nullptr), int64_t(0));
+        (void)zero;
+    } else {
+        // single-pass decoupled look-back scan (cub::DeviceScan) over n + 1 items, the last
+        // one zero, so out[n] is the total
+        auto it = thrust::make_transform_iterator(thrust::counting_iterator<int64_t>(0), PadZero<T>{in, n});
+        size_t bytes = 0;
+        AMG_CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, it, out, n + 1, c.s));
+        if (c.scan_tmp.size() < bytes) c.scan_tmp.alloc(std::max<size_t>(bytes, size_t(1) << 20), c.s);
+        AMG_CK(cub::DeviceScan::ExclusiveSum(c.scan_tmp.get(), bytes, it, out, n + 1, c.s));
+        c.launches += 2;
+    }
     if (!read_total) return -1;
     return static_cast<int64_t>(read_scalar(c, static_cast<const T*>(out + n), file, line));
 }
