@@ -570,7 +570,9 @@ struct Driver {
         bytes += 8.0 * h.coarse_n * h.coarse_n;
         // the whole co-resident grid: small levels run warp-per-row over every SM
         (void)most;
-        const int g = std::max(1, per_sm * c.sms);
+        // AMGCU_FUSED_GRID overrides the grid (barrier cost grows with the block count)
+        static const int g_env = std::getenv("AMGCU_FUSED_GRID") ? std::atoi(std::getenv("AMGCU_FUSED_GRID")) : 0;
+        const int g = g_env > 0 ? std::min(g_env, std::max(1, per_sm * c.sms)) : std::max(1, per_sm * c.sms);
         const FusedLevel* dp = fused_desc.get();
         const double* pv = h.coarse_pinv.get();
         int32_t cn = h.coarse_n;
