@@ -752,8 +752,11 @@ __global__ void k_bandwidth(int32_t n, const int32_t* __restrict__ rp, const int
 
 // segment heads in sweep order: position q starts a segment unless row(q)
 // holds column row(q - 1)
+// window w: position q continues a segment if row(q) holds a column among the w rows
+// before it in sweep order (w = 1: the predecessor; w = block size: interleaved vector
+// unknowns, whose chains run with stride w)
 __global__ void k_segment_heads(int32_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci, bool bwd,
-                                int32_t* __restrict__ head) {
+                                int32_t* __restrict__ head, int32_t w) {
     const int32_t q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= n) return;
     if (q == 0) {
@@ -761,14 +764,15 @@ __global__ void k_segment_heads(int32_t n, const int32_t* __restrict__ rp, const
         return;
     }
     const int32_t i = bwd ? n - 1 - q : q;
-    const int32_t prev = bwd ? i + 1 : i - 1;
+    // columns in [a, b] (row indices of the w previous positions)
+    const int32_t a = bwd ? i + 1 : max(i - w, 0), bcol = bwd ? min(i + w, n - 1) : i - 1;
     int32_t lo = rp[i], hi = rp[i + 1];
     while (lo < hi) {
         const int32_t mid = (lo + hi) >> 1;
-        if (ci[mid] < prev) lo = mid + 1;
+        if (ci[mid] < a) lo = mid + 1;
         else hi = mid;
     }
-    head[q] = (lo < rp[i + 1] && ci[lo] == prev) ? 0 : 1;
+    head[q] = (lo < rp[i + 1] && ci[lo] <= bcol) ? 0 : 1;
 }
 
 __global__ void k_segment_starts(int32_t n, const int32_t* __restrict__ head, const int32_t* __restrict__ rank,
@@ -816,10 +820,10 @@ int gs_poll_window() {
     return v;
 }
 
-int32_t build_segments(Ctx& c, const DCsr& A, bool bwd, DBuf<int32_t>& starts) {
+int32_t build_segments(Ctx& c, const DCsr& A, bool bwd, DBuf<int32_t>& starts, int32_t window = 1) {
     const int32_t n = A.nr;
     DBuf<int32_t> head(static_cast<size_t>(n) + 1, c.s), rank(static_cast<size_t>(n) + 1, c.s);
-    launch(c, k_segment_heads, blocks_for(n, 256), 256, 0, n, A.rp.get(), A.ci.get(), bwd, head.get());
+    launch(c, k_segment_heads, blocks_for(n, 256), 256, 0, n, A.rp.get(), A.ci.get(), bwd, head.get(), window);
     const int32_t nseg = static_cast<int32_t>(exclusive_scan_i32(c, head.get(), rank.get(), n));
     starts.alloc(static_cast<size_t>(nseg) + 1, c.s);
     launch(c, k_segment_starts, blocks_for(n, 256), 256, 0, n, static_cast<const int32_t*>(head.get()),
@@ -846,12 +850,101 @@ __global__ void k_jacobi(int32_t n, const int32_t* __restrict__ rp, const int32_
 
 }  // namespace
 
+// the lane-per-segment kernel's conditions (single column, forward sweeps assumed by the
+// caller): rows of at most 21 entries, segments of at least 16 rows on average, every CTA
+// of 32 segments resident, 32-bit tags
+bool lanes_eligible(Ctx& c, const DCsr& A) {
+    const char* ln_env = std::getenv("AMGCU_GS_LANES");
+    if ((ln_env && ln_env[0] == '0') || std::getenv("AMGCU_GS_TRACE")) return false;
+    const int32_t n = A.nr;
+    if (n == 0 || n >= (1 << 24)) return false;
+    DBuf<int32_t> st(2, c.s);
+    AMG_CK(cudaMemsetAsync(st.get(), 0, 2 * sizeof(int32_t), c.s));
+    launch(c, k_bandwidth, blocks_for(n, 256), 256, 0, n, A.rp.get(), A.ci.get(), st.get());
+    DBuf<int32_t> segf;
+    const int32_t nf = build_segments(c, A, false, segf, std::max(A.bs, 1));
+    stage_scalar(c, 1, st.get() + 1);
+    sync(c);
+    const int32_t longest_row = staged<int32_t>(c, 1);
+    return longest_row <= 21 && (nf + kLnLanes - 1) / kLnLanes <= c.sms && static_cast<int64_t>(nf) * 16 <= n;
+}
+
+// Forward sweeps of one column by the lane-per-segment kernel (gs_lanes.cuh) when the
+// matrix suits it: rows of at most 21 entries; segments (window = block size, so the
+// stride-m chains of interleaved vector unknowns count) of at least 16 rows on average;
+// every CTA of 32 segments resident at once; 32-bit tags.  Returns false otherwise.
+bool gs_lanes_run(Ctx& c, const DCsr& A, const double* inv_diag, double* x, const double* b, int nsw) {
+    const char* ln_env = std::getenv("AMGCU_GS_LANES");
+    if ((ln_env && ln_env[0] == '0') || std::getenv("AMGCU_GS_TRACE")) return false;
+    const int32_t n = A.nr;
+    if (n == 0 || n >= (1 << 24) || static_cast<int64_t>(nsw) * n >= (int64_t(1) << 31)) return false;
+    DBuf<int32_t> st2(2, c.s);
+    AMG_CK(cudaMemsetAsync(st2.get(), 0, 2 * sizeof(int32_t), c.s));
+    launch(c, k_bandwidth, blocks_for(n, 256), 256, 0, n, A.rp.get(), A.ci.get(), st2.get());
+    DBuf<int32_t> segf;
+    const int32_t nf = build_segments(c, A, false, segf, std::max(A.bs, 1));
+    stage_scalar(c, 1, st2.get() + 1);
+    sync(c);
+    const int32_t longest_row = staged<int32_t>(c, 1);
+    const int32_t nctas = (nf + kLnLanes - 1) / kLnLanes;
+    if (!(longest_row <= 21 && nctas <= c.sms && static_cast<int64_t>(nf) * 16 <= n)) return false;
+    const size_t stride = static_cast<size_t>(n);
+    DBuf<double> X(stride * (nsw + 1), c.s);
+    copy_d2d(c, X.get(), x, static_cast<int64_t>(stride));
+    launch(c, k_fill_pending, blocks_for(static_cast<int64_t>(stride) * nsw, 256), 256, 0,
+           static_cast<int64_t>(stride) * nsw, X.get() + stride);
+    DBuf<unsigned int> ticket(1, c.s);
+    AMG_CK(cudaMemsetAsync(ticket.get(), 0, sizeof(unsigned int), c.s));
+    const double bytes = nsw * (12.0 * A.nnz + 4.0 * (n + 1) + 8.0 * n + 16.0 * n);
+    // AMGCU_GS_STATS=1: solver iteration / stall counters on stderr
+    static const bool want_stats = std::getenv("AMGCU_GS_STATS") != nullptr;
+    DBuf<unsigned long long> st;
+    if (want_stats) {
+        st.alloc(32, c.s);
+        AMG_CK(cudaMemsetAsync(st.get(), 0, 32 * sizeof(unsigned long long), c.s));
+        AMG_CK(cudaMemsetAsync(st.get() + 24, 0xff, sizeof(unsigned long long), c.s));
+    }
+    auto runl = [&](auto kern, size_t smem) {
+        AMG_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        launch_prof(c, kProfGaussSeidel, bytes, kern, static_cast<unsigned>(nctas), kLnThreads, smem, n, A.rp.get(),
+                    A.ci.get(), A.va.get(), inv_diag, b, nsw, static_cast<const int32_t*>(segf.get()), nf, X.get(),
+                    ticket.get(), st.get(), gs_env_u("AMGCU_GS_POLL_NS", 128u), gs_env_u("AMGCU_GS_PF_NS", 128u));
+    };
+    if (longest_row <= 9) runl(k_gs_lanes<8, 3, 4, 64>, ln_smem_bytes<8, 3, 4, 64>());
+    else runl(k_gs_lanes<20, 2, 2, 32>, ln_smem_bytes<20, 2, 2, 32>());
+    copy_d2d(c, x, X.get() + stride * nsw, static_cast<int64_t>(stride));
+    sync(c);
+    if (want_stats) {
+        unsigned long long h[32];
+        copy_d2h(c, h, st.get(), 32);
+        sync(c);
+        std::fprintf(stderr, "[gs lanes] n=%d segs=%d ctas=%d iterations(all ctas)=%llu rows=%llu lane-iters=%llu "
+                     "record-stalls=%llu value-stalls=%llu\n", n, nf, nctas, h[0], h[1], h[2], h[3],
+                     h[2] - h[1] - h[3]);
+        const double it = static_cast<double>(h[0]);
+        std::fprintf(stderr, "[gs lanes] cycles/iteration: rows %.0f sync %.0f publish %.0f total %.0f\n",
+                     h[16] / it, h[17] / it, h[18] / it, h[19] / it);
+        std::fprintf(stderr, "[gs lanes] solver span %.1f us, max iterations per CTA %llu, max cycles per CTA %llu\n",
+                     (h[25] - h[24]) * 1e-3, h[26], h[27]);
+    }
+    return true;
+}
+
 void gauss_seidel(Ctx& c, const DCsr& A, const double* inv_diag, double* x, const double* b, int k, int sweeps,
                   bool symmetric_sweep) {
     if (k > kMaxK) throw InvalidArgument("relax: at most 8 candidate columns on the GPU path");
     const int32_t n = A.nr;
     const int nsw = symmetric_sweep ? 2 * sweeps : sweeps;
     if (nsw == 0 || n == 0) return;
+    if (k == 1 && !symmetric_sweep && gs_lanes_run(c, A, inv_diag, x, b, nsw)) return;
+    if (k > 1 && !symmetric_sweep && lanes_eligible(c, A)) {
+        // the columns are independent sweeps (the reference relaxes each candidate column
+        // in turn, interpolation.hpp:91): one lane-per-segment launch per column
+        for (int col = 0; col < k; ++col)
+            gauss_seidel(c, A, inv_diag, x + static_cast<size_t>(col) * n, b ? b + static_cast<size_t>(col) * n : nullptr,
+                         1, sweeps, false);
+        return;
+    }
     const size_t stride = static_cast<size_t>(n) * k;
     DBuf<double> X(stride * (nsw + 1), c.s);
     copy_d2d(c, X.get(), x, static_cast<int64_t>(stride));
@@ -879,7 +972,17 @@ void gauss_seidel(Ctx& c, const DCsr& A, const double* inv_diag, double* x, cons
     const bool force_wr = wr_env && wr_env[0] == '1';
     // the segment kernel's poll lists hold 32-bit offsets into the sweep buffers
     const bool huge = stride * (nsw + 1) >= (size_t(1) << 32);
-    if ((force_wr || huge || static_cast<int64_t>(nseg_max) * kShortSegment > n) && !std::getenv("AMGCU_GS_TRACE")) {
+    // rows longer than the segment kernel's 32-entry records (dense coarse operators of
+    // vector problems) would all take its rolled slow path: warp per row instead
+    int32_t longest_row0 = 0;
+    {
+        DBuf<int32_t> st(2, c.s);
+        AMG_CK(cudaMemsetAsync(st.get(), 0, 2 * sizeof(int32_t), c.s));
+        launch(c, k_bandwidth, blocks_for(n, 256), 256, 0, n, A.rp.get(), A.ci.get(), st.get());
+        longest_row0 = read_scalar(c, st.get() + 1);
+    }
+    if ((force_wr || huge || longest_row0 > 32 || static_cast<int64_t>(nseg_max) * kShortSegment > n) &&
+        !std::getenv("AMGCU_GS_TRACE")) {
         const double bytes = nsw * (12.0 * A.nnz + 4.0 * (n + 1) + 8.0 * n + 16.0 * n * k);
         // forward sweeps whose stale dependencies stay within the resident window: row-major
         bool row_major = false;
@@ -935,49 +1038,6 @@ void gauss_seidel(Ctx& c, const DCsr& A, const double* inv_diag, double* x, cons
         sync(c);
         bwidth = staged<int32_t>(c, 0);
         longest_row = staged<int32_t>(c, 1);
-    }
-    // lane per segment (gs_lanes.cuh): single column, forward sweeps, rows of at most 21
-    // entries, every segment resident at once (one CTA of 32 segments per SM)
-    {
-        const char* ln_env = std::getenv("AMGCU_GS_LANES");
-        const bool ln_off = ln_env && ln_env[0] == '0';
-        const int32_t nctas = (nf + kLnLanes - 1) / kLnLanes;
-        if (!ln_off && !trace_path && k == 1 && !symmetric_sweep && longest_row <= 21 && nctas <= c.sms &&
-            static_cast<int64_t>(nsw) * n < (int64_t(1) << 31) && n < (1 << 24) && static_cast<int64_t>(nf) * 16 <= n) {
-            // AMGCU_GS_STATS=1: solver iteration / stall counters on stderr
-            static const bool want_stats = std::getenv("AMGCU_GS_STATS") != nullptr;
-            DBuf<unsigned long long> st;
-            if (want_stats) {
-                st.alloc(32, c.s);
-                AMG_CK(cudaMemsetAsync(st.get(), 0, 32 * sizeof(unsigned long long), c.s));
-                AMG_CK(cudaMemsetAsync(st.get() + 24, 0xff, sizeof(unsigned long long), c.s));
-            }
-            auto runl = [&](auto kern, size_t smem) {
-                AMG_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-                launch_prof(c, kProfGaussSeidel, bytes, kern, static_cast<unsigned>(nctas), kLnThreads, smem, n,
-                            A.rp.get(), A.ci.get(), A.va.get(), inv_diag, b, nsw,
-                            static_cast<const int32_t*>(segf.get()), nf, X.get(), ticket.get(), st.get(),
-                            gs_env_u("AMGCU_GS_POLL_NS", 128u), gs_env_u("AMGCU_GS_PF_NS", 128u));
-            };
-            if (longest_row <= 9) runl(k_gs_lanes<8, 3, 4, 64>, ln_smem_bytes<8, 3, 4, 64>());
-            else runl(k_gs_lanes<20, 2, 2, 32>, ln_smem_bytes<20, 2, 2, 32>());
-            copy_d2d(c, x, X.get() + stride * nsw, static_cast<int64_t>(stride));
-            sync(c);
-            if (want_stats) {
-                unsigned long long h[32];
-                copy_d2h(c, h, st.get(), 32);
-                sync(c);
-                std::fprintf(stderr, "[gs lanes] n=%d segs=%d ctas=%d iterations(all ctas)=%llu rows=%llu lane-iters=%llu "
-                             "record-stalls=%llu value-stalls=%llu\n", n, nf, nctas, h[0], h[1], h[2], h[3],
-                             h[2] - h[1] - h[3]);
-                const double it = static_cast<double>(h[0]);
-                std::fprintf(stderr, "[gs lanes] cycles/iteration: rows %.0f sync %.0f publish %.0f total %.0f\n",
-                             h[16] / it, h[17] / it, h[18] / it, h[19] / it);
-                std::fprintf(stderr, "[gs lanes] solver span %.1f us, max iterations per CTA %llu, max cycles per CTA %llu\n",
-                             (h[25] - h[24]) * 1e-3, h[26], h[27]);
-            }
-            return;
-        }
     }
     auto run = [&](auto kern, int segs, size_t seg_bytes) {
         // AMGCU_GS_SMEM: request at least this much shared memory per CTA (caps CTAs per SM)

@@ -276,6 +276,12 @@ def test_gauss_seidel_lane_segments(gpu_seq, port, monkeypatch, lanes):
         got = api.relax(A_, 1, 0.0, 3, x0, b, ctx=gpu_seq)
         want = port.relax(A_, 1, 0.0, 3, x0, b)
         assert got.tobytes() == want.tobytes(), n
+    # interleaved vector unknowns (block size 2, chains of stride 2), three candidate
+    # columns relaxed one launch each
+    A_, B_, _, _ = api.generate_config(5, 24)
+    got = api.improve_candidates(A_, B_, 4, 1, 0.0, ctx=gpu_seq)
+    want = port.improve_candidates(A_, B_, 4, 1, 0.0)
+    assert got.data.tobytes() == want.data.tobytes()
 
 
 def test_relax(gpu_seq, port):
