@@ -237,8 +237,12 @@ __global__ void __launch_bounds__(kLnThreads, 1)
                                 const unsigned badc = ~okc & livec;
                                 const int ks = badc ? cb + __ffs(badc) - 1 : min(nt, cb + 8);
 #pragma unroll
-                                for (int w = 0; w < 8; ++w)
-                                    if (cb + w < T && cb + w >= kres && cb + w < ks) acc -= pk[w];
+                                for (int w = 0; w < 8; ++w) {
+                                    // predicated, not branched: the subtraction chain is the
+                                    // iteration's critical path
+                                    const double d = acc - pk[w];
+                                    acc = (cb + w < T && cb + w >= kres && cb + w < ks) ? d : acc;
+                                }
                                 if (badc) {
                                     stopped = true;
                                     kstop = ks;
@@ -289,9 +293,12 @@ __global__ void __launch_bounds__(kLnThreads, 1)
             const long long c2 = stats ? clock64() : 0;
             if (fin) {
                 const unsigned long long xb = static_cast<unsigned long long>(__double_as_longlong(xnew));
-                LnCell& cell = R.ring[lane + 2][q & (kLnRing - 1)];
-                cell.v = xb;
-                cell.tag = s * n + q;
+                // value and tag in one 16-byte store: a sibling lane's 16-byte read of the
+                // cell never sees one without the other
+                const unsigned ca = smem_addr(&R.ring[lane + 2][q & (kLnRing - 1)]);
+                asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(ca), "r"(static_cast<unsigned>(xb)),
+                             "r"(static_cast<unsigned>(xb >> 32)), "r"(static_cast<unsigned>(s * n + q)), "r"(0u)
+                             : "memory");
                 cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> out(
                     *reinterpret_cast<unsigned long long*>(X + static_cast<size_t>(s + 1) * stride + q));
                 out.store(xb, cuda::memory_order_relaxed);
@@ -321,7 +328,7 @@ __global__ void __launch_bounds__(kLnThreads, 1)
                     }
                 }
             }
-            __syncwarp();
+            // (no barrier here: the loop head's vote reconverges the warp)
             if (stats) {
                 const long long c3 = clock64();
                 ck[0] += c1 - c0;
