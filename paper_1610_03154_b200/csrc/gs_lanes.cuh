@@ -328,7 +328,7 @@ __global__ void __launch_bounds__(kLnThreads, 1)
                     }
                 }
             }
-            // (no barrier here: the loop head's vote reconverges the warp)
+            __syncwarp();  // lanes stay in step (skew between sibling segments is in iterations)
             if (stats) {
                 const long long c3 = clock64();
                 ck[0] += c1 - c0;

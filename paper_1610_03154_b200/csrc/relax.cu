@@ -850,44 +850,41 @@ __global__ void k_jacobi(int32_t n, const int32_t* __restrict__ rp, const int32_
 
 }  // namespace
 
-// the lane-per-segment kernel's conditions (single column, forward sweeps assumed by the
-// caller): rows of at most 21 entries, segments of at least 16 rows on average, every CTA
-// of 32 segments resident, 32-bit tags
-bool lanes_eligible(Ctx& c, const DCsr& A) {
+// The lane-per-segment kernel's plan for a matrix (forward sweeps): segments with a
+// block-size window (so the stride-m chains of interleaved vector unknowns count) and
+// the longest row.  It applies to rows of at most 21 entries, segments of at least 16
+// rows on average, every CTA of 32 segments resident at once, and 32-bit tags.
+struct LanePlan {
+    bool ok = false;
+    int32_t nf = 0, longest_row = 0;
+    DBuf<int32_t> segf;
+};
+
+LanePlan lane_plan(Ctx& c, const DCsr& A, int nsw) {
+    LanePlan pl;
     const char* ln_env = std::getenv("AMGCU_GS_LANES");
-    if ((ln_env && ln_env[0] == '0') || std::getenv("AMGCU_GS_TRACE")) return false;
+    if ((ln_env && ln_env[0] == '0') || std::getenv("AMGCU_GS_TRACE")) return pl;
     const int32_t n = A.nr;
-    if (n == 0 || n >= (1 << 24)) return false;
+    if (n == 0 || n >= (1 << 24) || static_cast<int64_t>(nsw) * n >= (int64_t(1) << 31)) return pl;
     DBuf<int32_t> st(2, c.s);
     AMG_CK(cudaMemsetAsync(st.get(), 0, 2 * sizeof(int32_t), c.s));
     launch(c, k_bandwidth, blocks_for(n, 256), 256, 0, n, A.rp.get(), A.ci.get(), st.get());
-    DBuf<int32_t> segf;
-    const int32_t nf = build_segments(c, A, false, segf, std::max(A.bs, 1));
+    pl.nf = build_segments(c, A, false, pl.segf, std::max(A.bs, 1));
     stage_scalar(c, 1, st.get() + 1);
     sync(c);
-    const int32_t longest_row = staged<int32_t>(c, 1);
-    return longest_row <= 21 && (nf + kLnLanes - 1) / kLnLanes <= c.sms && static_cast<int64_t>(nf) * 16 <= n;
+    pl.longest_row = staged<int32_t>(c, 1);
+    pl.ok = pl.longest_row <= 21 && (pl.nf + kLnLanes - 1) / kLnLanes <= c.sms &&
+            static_cast<int64_t>(pl.nf) * 16 <= n;
+    return pl;
 }
 
-// Forward sweeps of one column by the lane-per-segment kernel (gs_lanes.cuh) when the
-// matrix suits it: rows of at most 21 entries; segments (window = block size, so the
-// stride-m chains of interleaved vector unknowns count) of at least 16 rows on average;
-// every CTA of 32 segments resident at once; 32-bit tags.  Returns false otherwise.
-bool gs_lanes_run(Ctx& c, const DCsr& A, const double* inv_diag, double* x, const double* b, int nsw) {
-    const char* ln_env = std::getenv("AMGCU_GS_LANES");
-    if ((ln_env && ln_env[0] == '0') || std::getenv("AMGCU_GS_TRACE")) return false;
+// Forward sweeps of one column by the lane-per-segment kernel (gs_lanes.cuh).
+void gs_lanes_run(Ctx& c, const DCsr& A, const LanePlan& pl, const double* inv_diag, double* x, const double* b,
+                  int nsw) {
     const int32_t n = A.nr;
-    if (n == 0 || n >= (1 << 24) || static_cast<int64_t>(nsw) * n >= (int64_t(1) << 31)) return false;
-    DBuf<int32_t> st2(2, c.s);
-    AMG_CK(cudaMemsetAsync(st2.get(), 0, 2 * sizeof(int32_t), c.s));
-    launch(c, k_bandwidth, blocks_for(n, 256), 256, 0, n, A.rp.get(), A.ci.get(), st2.get());
-    DBuf<int32_t> segf;
-    const int32_t nf = build_segments(c, A, false, segf, std::max(A.bs, 1));
-    stage_scalar(c, 1, st2.get() + 1);
-    sync(c);
-    const int32_t longest_row = staged<int32_t>(c, 1);
+    const int32_t nf = pl.nf, longest_row = pl.longest_row;
     const int32_t nctas = (nf + kLnLanes - 1) / kLnLanes;
-    if (!(longest_row <= 21 && nctas <= c.sms && static_cast<int64_t>(nf) * 16 <= n)) return false;
+    const DBuf<int32_t>& segf = pl.segf;
     const size_t stride = static_cast<size_t>(n);
     DBuf<double> X(stride * (nsw + 1), c.s);
     copy_d2d(c, X.get(), x, static_cast<int64_t>(stride));
@@ -927,7 +924,6 @@ bool gs_lanes_run(Ctx& c, const DCsr& A, const double* inv_diag, double* x, cons
         std::fprintf(stderr, "[gs lanes] solver span %.1f us, max iterations per CTA %llu, max cycles per CTA %llu\n",
                      (h[25] - h[24]) * 1e-3, h[26], h[27]);
     }
-    return true;
 }
 
 void gauss_seidel(Ctx& c, const DCsr& A, const double* inv_diag, double* x, const double* b, int k, int sweeps,
@@ -936,14 +932,16 @@ void gauss_seidel(Ctx& c, const DCsr& A, const double* inv_diag, double* x, cons
     const int32_t n = A.nr;
     const int nsw = symmetric_sweep ? 2 * sweeps : sweeps;
     if (nsw == 0 || n == 0) return;
-    if (k == 1 && !symmetric_sweep && gs_lanes_run(c, A, inv_diag, x, b, nsw)) return;
-    if (k > 1 && !symmetric_sweep && lanes_eligible(c, A)) {
-        // the columns are independent sweeps (the reference relaxes each candidate column
-        // in turn, interpolation.hpp:91): one lane-per-segment launch per column
-        for (int col = 0; col < k; ++col)
-            gauss_seidel(c, A, inv_diag, x + static_cast<size_t>(col) * n, b ? b + static_cast<size_t>(col) * n : nullptr,
-                         1, sweeps, false);
-        return;
+    if (!symmetric_sweep) {
+        const LanePlan pl = lane_plan(c, A, nsw);
+        if (pl.ok) {
+            // the columns are independent sweeps (the reference relaxes each candidate
+            // column in turn, interpolation.hpp:91): one lane-per-segment launch per column
+            for (int col = 0; col < k; ++col)
+                gs_lanes_run(c, A, pl, inv_diag, x + static_cast<size_t>(col) * n,
+                             b ? b + static_cast<size_t>(col) * n : nullptr, nsw);
+            return;
+        }
     }
     const size_t stride = static_cast<size_t>(n) * k;
     DBuf<double> X(stride * (nsw + 1), c.s);
