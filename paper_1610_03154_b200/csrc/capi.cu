@@ -135,6 +135,7 @@ amgcu_status amgcu_ctx_create(int device, amgcu_ctx* out) {
         AMG_CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
         AMG_CK(cudaStreamCreateWithPriority(&ctx->c.s, cudaStreamNonBlocking, prio_hi));
         AMG_CK(cudaStreamCreateWithPriority(&ctx->c.side, cudaStreamNonBlocking, prio_lo));
+        AMG_CK(cudaStreamCreateWithPriority(&ctx->c.side2, cudaStreamNonBlocking, prio_hi));
         AMG_CK(cudaDeviceGetAttribute(&ctx->c.sms, cudaDevAttrMultiProcessorCount, device));
         cudaMemPool_t pool;
         AMG_CK(cudaDeviceGetDefaultMemPool(&pool, device));
@@ -156,7 +157,9 @@ amgcu_status amgcu_ctx_destroy(amgcu_ctx ctx) {
     cudaStreamSynchronize(ctx->c.s);
     if (ctx->c.pin) cudaFreeHost(ctx->c.pin);
     cudaStreamSynchronize(ctx->c.side);
+    cudaStreamSynchronize(ctx->c.side2);
     cudaStreamDestroy(ctx->c.side);
+    cudaStreamDestroy(ctx->c.side2);
     cudaStreamDestroy(ctx->c.s);
     delete ctx;
     return AMGCU_OK;

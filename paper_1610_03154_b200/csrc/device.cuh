@@ -123,6 +123,7 @@ struct Ctx {
     int device = 0;
     cudaStream_t s = nullptr;
     cudaStream_t side = nullptr;  // independent side work (the evolution-SOC ledger count)
+    cudaStream_t side2 = nullptr;  // candidate Gauss-Seidel, overlapping the aggregation
     int sms = 148;
     bool seq = false;  // sequential (reference-order) global reductions
     int64_t launches = 0;
@@ -163,6 +164,14 @@ struct OpsScope {
     double* prev;
     OpsScope(Ctx& ctx, double* sink) : c(ctx), prev(ctx.ops) { c.ops = sink; }
     ~OpsScope() { c.ops = prev; }
+};
+
+// launches of a scope go to another stream (the context's stream member is swapped)
+struct StreamScope {
+    Ctx& c;
+    cudaStream_t prev;
+    StreamScope(Ctx& ctx, cudaStream_t s) : c(ctx), prev(ctx.s) { c.s = s; }
+    ~StreamScope() { c.s = prev; }
 };
 
 // routes the BLAS-1 launchers' profile records to `family` for a scope
@@ -265,6 +274,7 @@ inline void launch_prof(Ctx& c, int family, double bytes, Kern k, unsigned grid,
 // resolve pending event pairs into milliseconds (synchronises)
 inline void prof_collect(Ctx& c) {
     AMG_CK(cudaStreamSynchronize(c.s));
+    if (c.side2) AMG_CK(cudaStreamSynchronize(c.side2));
     for (auto& r : c.prof) {
         for (size_t q = 0; q < r.pending.size(); ++q) {
             auto& pr = r.pending[q];

@@ -98,6 +98,18 @@ double spectral_radius(Ctx& c, const DCsr& A, int steps, const double* dinv, int
 // ---- relaxation (relax.cu) -----------------------------------------------------------
 // sync-free wavefront Gauss-Seidel sweeps (relaxation.hpp:115-127) over k columns
 // (column-major x of size n*k; b n*k or nullptr for b = 0)
+// The lane-per-segment Gauss-Seidel kernel (gs_lanes.cuh) for forward sweeps: its plan
+// for a matrix (segments, longest row; host synchronisations) and one column's sweeps
+// (no host synchronisation: may run on another stream than the plan's)
+struct LanePlan {
+    bool ok = false;
+    int32_t nf = 0, longest_row = 0;
+    DBuf<int32_t> segf;
+};
+LanePlan lane_plan(Ctx& c, const DCsr& A, int nsw);
+void gs_lanes_run(Ctx& c, const DCsr& A, const LanePlan& pl, const double* inv_diag, double* x, const double* b,
+                  int nsw);
+
 void gauss_seidel(Ctx& c, const DCsr& A, const double* inv_diag, double* x, const double* b, int k, int sweeps,
                   bool symmetric_sweep);
 // weighted Jacobi sweeps x += (w dinv) (b - A x) (relaxation.hpp:107-113); b may be nullptr (0)

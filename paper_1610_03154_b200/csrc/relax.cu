@@ -854,12 +854,6 @@ __global__ void k_jacobi(int32_t n, const int32_t* __restrict__ rp, const int32_
 // block-size window (so the stride-m chains of interleaved vector unknowns count) and
 // the longest row.  It applies to rows of at most 21 entries, segments of at least 16
 // rows on average, every CTA of 32 segments resident at once, and 32-bit tags.
-struct LanePlan {
-    bool ok = false;
-    int32_t nf = 0, longest_row = 0;
-    DBuf<int32_t> segf;
-};
-
 LanePlan lane_plan(Ctx& c, const DCsr& A, int nsw) {
     LanePlan pl;
     const char* ln_env = std::getenv("AMGCU_GS_LANES");
@@ -910,7 +904,6 @@ void gs_lanes_run(Ctx& c, const DCsr& A, const LanePlan& pl, const double* inv_d
     if (longest_row <= 9) runl(k_gs_lanes<8, 3, 4, 64>, ln_smem_bytes<8, 3, 4, 64>());
     else runl(k_gs_lanes<20, 2, 2, 32>, ln_smem_bytes<20, 2, 2, 32>());
     copy_d2d(c, x, X.get() + stride * nsw, static_cast<int64_t>(stride));
-    sync(c);
     if (want_stats) {
         unsigned long long h[32];
         copy_d2h(c, h, st.get(), 32);

@@ -17,6 +17,9 @@
 
 namespace amgcu {
 
+// normalize_columns on the device (defined below)
+void normalize_candidates(Ctx& c, double* B, int32_t n, int32_t k);
+
 namespace {
 
 __global__ void k_evolution_weights(int32_t n, const double* __restrict__ d, double omega, double* __restrict__ winv,
@@ -121,6 +124,56 @@ void postfilter(Ctx& c, const amgcu_setup_options& o, const DCsr& A, const DCsr&
     out.bs = P.bs;
 }
 
+// Candidate improvement with forward Gauss-Seidel, started early on the context's second
+// stream: it depends on A and B only, so its sweeps (lane kernel, latency-bound, 32 SMs
+// per 1024 segments) overlap the strength / aggregation / pattern work of the level.
+// start: host synchronisations (zero-diagonal check, lane plan) on the main stream, then
+// the sweeps on side2; join: the main stream waits for them, then normalizes.
+struct CandidateSweeps {
+    bool active = false;
+    DBuf<double> dinv;
+    LanePlan plan;
+    cudaEvent_t done = nullptr;
+    ~CandidateSweeps() {
+        if (done) cudaEventDestroy(done);
+    }
+};
+
+bool candidate_sweeps_start(Ctx& c, const DCsr& A, double* B, int32_t k, int sweeps, int scheme, CandidateSweeps& cs) {
+    if (scheme != 1 || sweeps <= 0 || !c.side2 || c.seq || A.nr != A.nc) return false;
+    static const bool off = [] {
+        const char* e = std::getenv("AMGCU_CAND_OVERLAP");
+        return e && e[0] == '0';
+    }();
+    if (off) return false;
+    const int32_t n = A.nr;
+    cs.dinv.alloc(static_cast<size_t>(n), c.s);
+    inverse_diagonal(c, A, cs.dinv.get(), "relax: zero diagonal at row ");
+    cs.plan = lane_plan(c, A, sweeps);
+    if (!cs.plan.ok) return false;
+    cudaEvent_t ready;
+    AMG_CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    AMG_CK(cudaEventRecord(ready, c.s));
+    AMG_CK(cudaStreamWaitEvent(c.side2, ready, 0));
+    cudaEventDestroy(ready);
+    {
+        StreamScope on_side(c, c.side2);
+        for (int32_t j = 0; j < k; ++j)
+            gs_lanes_run(c, A, cs.plan, cs.dinv.get(), B + static_cast<size_t>(j) * n, nullptr, sweeps);
+    }
+    AMG_CK(cudaEventCreateWithFlags(&cs.done, cudaEventDisableTiming));
+    AMG_CK(cudaEventRecord(cs.done, c.side2));
+    cs.active = true;
+    return true;
+}
+
+void candidate_sweeps_join(Ctx& c, const DCsr& A, double* B, int32_t k, int sweeps, CandidateSweeps& cs) {
+    AMG_CK(cudaStreamWaitEvent(c.s, cs.done, 0));
+    // relaxation.hpp:207: |A| per sweep and candidate column
+    tally(c, static_cast<double>(k) * sweeps * static_cast<double>(A.nnz));
+    normalize_candidates(c, B, A.nr, k);
+}
+
 bool coarsen(Ctx& c, DHier& H, int level, const double* Bhat, Coarsened& out) {
     const amgcu_setup_options& o = H.o;
     DLevel& L = H.lv[level];
@@ -131,11 +184,21 @@ bool coarsen(Ctx& c, DHier& H, int level, const double* Bhat, Coarsened& out) {
     // WorkLedger buckets of this level (hierarchy.hpp:243): aggregation, candidates,
     // interpolation, RAP -- charged only when the level is built
     double cagg = 0.0, ccand = 0.0, cint = 0.0, crap = 0.0;
+    DBuf<double> Bimp;
+    CandidateSweeps cand;
     DCsr S0, Sa, S;
     DAgg agg;
     {
         OpsScope scope(c, &cagg);
         strength_of(c, L, o, S0);
+        // the candidates' sweeps depend on A and B only: start them now, beside the
+        // aggregation and pattern work (joined before the injection)
+        Bimp.alloc(static_cast<size_t>(A.nr) * k, c.s);
+        copy_d2d(c, Bimp.get(), L.B.get(), static_cast<int64_t>(A.nr) * k);
+        {
+            OpsScope none(c, nullptr);
+            candidate_sweeps_start(c, A, Bimp.get(), k, o.candidate_sweeps, o.cand_scheme, cand);
+        }
         amalgamate(c, S0, m, Sa);
         normalize_strength(c, Sa, S);
         greedy_aggregate(c, S, agg);
@@ -173,11 +236,12 @@ bool coarsen(Ctx& c, DHier& H, int level, const double* Bhat, Coarsened& out) {
     root_node_pattern(c, Nd0, droots.get(), agg.n_agg * m, Nd);
 
     const int32_t n = A.nr;
-    DBuf<double> Bimp(static_cast<size_t>(n) * k, c.s);
-    copy_d2d(c, Bimp.get(), L.B.get(), static_cast<int64_t>(n) * k);
     {
         OpsScope scope(c, &ccand);
-        improve_candidates(c, A, Bimp.get(), k, o.candidate_sweeps, o.cand_scheme, o.cand_weight, &L);
+        if (cand.active)
+            candidate_sweeps_join(c, A, Bimp.get(), k, o.candidate_sweeps, cand);
+        else
+            improve_candidates(c, A, Bimp.get(), k, o.candidate_sweeps, o.cand_scheme, o.cand_weight, &L);
     }
     DCsr T;
     DBuf<double> Bc;
@@ -304,6 +368,8 @@ double rho_tallied(Ctx& c, DLevel& L) {
     return r;
 }
 
+void normalize_candidates(Ctx& c, double* B, int32_t n, int32_t k);
+
 void improve_candidates(Ctx& c, const DCsr& A, double* B, int32_t k, int sweeps, int scheme, double weight,
                         DLevel* cache) {
     if (A.nr != A.nc) throw InvalidArgument("improve_candidates: dimension mismatch");
@@ -353,6 +419,11 @@ void improve_candidates(Ctx& c, const DCsr& A, double* B, int32_t k, int sweeps,
         // relaxation.hpp:207: relax_sweep_cost per sweep and candidate column (2 |A| for gsne)
         tally(c, static_cast<double>(k) * sweeps * (scheme == 3 ? 2.0 : 1.0) * static_cast<double>(A.nnz));
     }
+    normalize_candidates(c, B, n, k);
+}
+
+// normalize_columns (dense.hpp:41-46): every column to unit 2-norm (zero columns kept)
+void normalize_candidates(Ctx& c, double* B, int32_t n, int32_t k) {
     DBuf<double> nrm(static_cast<size_t>(k), c.s);
     for (int32_t j = 0; j < k; ++j) {
         double* col = B + static_cast<size_t>(j) * n;
@@ -361,6 +432,7 @@ void improve_candidates(Ctx& c, const DCsr& A, double* B, int32_t k, int sweeps,
                static_cast<int64_t>(n), static_cast<const double*>(nrm.get() + j), col);
     }
 }
+
 
 // CoarseSolver::factor (hierarchy.hpp:59-68).  The coarsest operator is
 // inverted once; each cycle then applies the inverse with one dense GEMV.
