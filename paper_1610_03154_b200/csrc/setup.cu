@@ -131,11 +131,17 @@ void postfilter(Ctx& c, const amgcu_setup_options& o, const DCsr& A, const DCsr&
 // the sweeps on side2; join: the main stream waits for them, then normalizes.
 struct CandidateSweeps {
     bool active = false;
+    cudaStream_t main = nullptr;
     DBuf<double> dinv;
     LanePlan plan;
     cudaEvent_t done = nullptr;
     ~CandidateSweeps() {
-        if (done) cudaEventDestroy(done);
+        // left without a join (an exception, or the level stagnated): the main stream must
+        // not free or reuse the buffers the sweeps still write before they finish
+        if (done) {
+            if (main) cudaStreamWaitEvent(main, done, 0);
+            cudaEventDestroy(done);
+        }
     }
 };
 
@@ -163,6 +169,7 @@ bool candidate_sweeps_start(Ctx& c, const DCsr& A, double* B, int32_t k, int swe
     }
     AMG_CK(cudaEventCreateWithFlags(&cs.done, cudaEventDisableTiming));
     AMG_CK(cudaEventRecord(cs.done, c.side2));
+    cs.main = c.s;
     cs.active = true;
     return true;
 }
