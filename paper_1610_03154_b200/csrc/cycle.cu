@@ -517,7 +517,11 @@ struct Driver {
     bool apply_fused(size_t l, double* x, const double* b) {
         const size_t L = h.lv.size();
         // levels large enough to fill the GPU keep the full-occupancy standalone kernels
-        if (!fused_enabled() || l == 0 || l + 1 >= L || h.lv[l].A.nr > kFusedMaxRows) return false;
+        // AMGCU_FUSED_MAX_ROWS overrides the size below which the fused cycle takes over
+        static const int32_t max_rows = std::getenv("AMGCU_FUSED_MAX_ROWS")
+                                            ? std::atoi(std::getenv("AMGCU_FUSED_MAX_ROWS"))
+                                            : kFusedMaxRows;
+        if (!fused_enabled() || l == 0 || l + 1 >= L || h.lv[l].A.nr > max_rows) return false;
         if (h.o.pre_scheme != 0 || h.o.post_scheme != 0 || h.o.pre_sweeps != 1 || h.o.post_sweeps != 1) return false;
         const int nlev = static_cast<int>(L - l);
         // the caller passes level l's own b / x (apply from level l - 1), so the
