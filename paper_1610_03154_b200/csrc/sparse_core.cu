@@ -274,31 +274,38 @@ __global__ void __launch_bounds__(kGemmWarps * kWarp)
 constexpr int kHashWarps = 4;
 constexpr int kHashSlots = 2 * kSmallCap;  // load factor <= 1/2
 
-struct HashShared {
-    int32_t hkey[kHashSlots];
-    double hval[kHashSlots];
-    int32_t pcol[kSmallCap];                 // staged products: column
-    double pval[kSmallCap];                  // staged products: value; reused as the sort keys
+template <int CAP>
+struct HashSharedT {
+    int32_t hkey[2 * CAP];
+    double hval[2 * CAP];
+    int32_t pcol[CAP];  // staged products: column
+    double pval[CAP];   // staged products: value; reused as the sort keys
     double chunk[kWarp];
 };
+using HashShared = HashSharedT<kSmallCap>;
+constexpr int kMidCap = 2048;  // rows of 512..2048 products: one warp per block, 72 KB of shared memory
 
 __device__ __forceinline__ uint32_t col_hash(int32_t col, uint32_t mask) {
     return (static_cast<uint32_t>(col) * 2654435761u) & mask;
 }
 
-__global__ void __launch_bounds__(kHashWarps * kWarp)
+// CAP products per row at most, W warps (rows) per block, rows of more than MINNP
+// products; `list` (optional) names the rows (block b, warp w: list[b * W + w])
+template <int CAP, int W, int MINNP>
+__global__ void __launch_bounds__(W * kWarp)
     k_spgemm_hash(int32_t nr, const int32_t* __restrict__ arp, const int32_t* __restrict__ aci,
                   const double* __restrict__ ava, const int32_t* __restrict__ brp, const int32_t* __restrict__ bci,
                   const double* __restrict__ bva, const int64_t* __restrict__ poff, int32_t* __restrict__ tcol,
-                  double* __restrict__ tval, int32_t* __restrict__ cnt) {
+                  double* __restrict__ tval, int32_t* __restrict__ cnt, const int32_t* __restrict__ list) {
     extern __shared__ unsigned long long hsm[];
     const int w = threadIdx.x / kWarp;
     const int lane = threadIdx.x & (kWarp - 1);
-    const int32_t i = blockIdx.x * kHashWarps + w;
-    if (i >= nr) return;
+    const int32_t slot_id = blockIdx.x * W + w;
+    if (slot_id >= nr) return;
+    const int32_t i = list ? list[slot_id] : slot_id;
     const int64_t np = poff[i + 1] - poff[i];
-    if (np > kSmallCap || np <= kSortCap) return;  // handled by the block / sort kernels
-    HashShared& sh = reinterpret_cast<HashShared*>(hsm)[w];
+    if (np > CAP || np <= MINNP) return;  // handled by the block / sort kernels
+    HashSharedT<CAP>& sh = reinterpret_cast<HashSharedT<CAP>*>(hsm)[w];
     // table sized to the row: a power of two >= 2 np (load factor <= 1/2)
     const int32_t hs = static_cast<int32_t>(max(64u, next_pow2(2u * static_cast<unsigned>(np))));
     const uint32_t hmask = static_cast<uint32_t>(hs - 1);
@@ -415,7 +422,8 @@ __global__ void __launch_bounds__(kBigThreads)
                  const double* __restrict__ bva, const int64_t* __restrict__ poff,
                  const int64_t* __restrict__ scratch_off, unsigned long long* __restrict__ gkeys,
                  double* __restrict__ gvals, int32_t* __restrict__ tcol, double* __restrict__ tval,
-                 int32_t* __restrict__ cnt) {
+                 int32_t* __restrict__ cnt, const int32_t* __restrict__ handled) {
+    if (handled[blockIdx.x]) return;  // k_spgemm_big_hash wrote the row
     const int32_t i = list[blockIdx.x];
     const int64_t np = poff[i + 1] - poff[i];
     unsigned long long* keys = gkeys + scratch_off[blockIdx.x];
@@ -484,6 +492,145 @@ __global__ void __launch_bounds__(kBigThreads)
         __syncthreads();
     }
     if (threadIdx.x == 0) cnt[i] = s_written;
+}
+
+// Rows beyond the warp kernels whose DISTINCT columns fit a shared-memory table: the
+// columns are hashed first, then the A entries are taken one at a time (a block
+// barrier between them) and the B row's products are added to their columns' sums.
+// A B row holds each column once, so every column's sum is built in expansion order
+// -- the (column, position) order the bitonic kernel sums in -- and the result is
+// bitwise the same. The table's columns are then sorted and the nonzero sums written.
+// Rows with more distinct columns than kBigHashMax are left to the bitonic kernel.
+constexpr int kBigHashSlots = 8192;
+constexpr int kBigHashMax = 6144;
+constexpr size_t kBigHashSmem = kBigHashSlots * (sizeof(int32_t) + sizeof(double)) +
+                                kBigHashSlots * sizeof(unsigned long long);
+
+__device__ __forceinline__ uint32_t big_slot(int32_t col) {
+    return (static_cast<uint32_t>(col) * 2654435761u) >> (32 - 13);
+}
+
+__global__ void __launch_bounds__(kBigThreads)
+    k_spgemm_big_hash(const int32_t* __restrict__ list, const int32_t* __restrict__ arp,
+                      const int32_t* __restrict__ aci, const double* __restrict__ ava,
+                      const int32_t* __restrict__ brp, const int32_t* __restrict__ bci,
+                      const double* __restrict__ bva, const int64_t* __restrict__ poff, int32_t* __restrict__ tcol,
+                      double* __restrict__ tval, int32_t* __restrict__ cnt, int32_t* __restrict__ handled) {
+    static_assert(kBigHashSlots == 1 << 13, "big_slot shift");
+    extern __shared__ __align__(16) unsigned char big_smem[];
+    double* hv = reinterpret_cast<double*>(big_smem);
+    unsigned long long* sk = reinterpret_cast<unsigned long long*>(hv + kBigHashSlots);
+    int32_t* hk = reinterpret_cast<int32_t*>(sk + kBigHashSlots);
+    __shared__ int32_t s_n;
+    __shared__ int32_t s_warp[kBigThreads / kWarp];
+    const int32_t i = list[blockIdx.x];
+    const int tid = threadIdx.x;
+    for (int e = tid; e < kBigHashSlots; e += kBigThreads) {
+        hk[e] = -1;
+        hv[e] = 0.0;
+    }
+    if (tid == 0) s_n = 0;
+    __syncthreads();
+    const int32_t alo = arp[i], ahi = arp[i + 1];
+    // distinct columns
+    for (int32_t p = alo; p < ahi; ++p) {
+        const int32_t t = aci[p];
+        bool over = false;
+        for (int32_t q = brp[t] + tid; q < brp[t + 1] && !over; q += kBigThreads) {
+            const int32_t col = bci[q];
+            uint32_t h = big_slot(col);
+            for (int probe = 0;; ) {
+                const int32_t k = hk[h];
+                if (k == col) break;
+                if (k == -1) {
+                    const int32_t old = atomicCAS(&hk[h], -1, col);
+                    if (old == -1) {
+                        over = atomicAdd(&s_n, 1) >= kBigHashMax;
+                        break;
+                    }
+                    if (old == col) break;
+                }
+                h = (h + 1) & (kBigHashSlots - 1);
+                if (++probe == kBigHashSlots) {
+                    over = true;
+                    break;
+                }
+            }
+        }
+        if (__syncthreads_or(over)) {
+            if (tid == 0) handled[blockIdx.x] = 0;
+            return;
+        }
+    }
+    // sums in expansion order, one A entry at a time
+    for (int32_t p = alo; p < ahi; ++p) {
+        const int32_t t = aci[p];
+        const double a = ava[p];
+        for (int32_t q = brp[t] + tid; q < brp[t + 1]; q += kBigThreads) {
+            const int32_t col = bci[q];
+            uint32_t h = big_slot(col);
+            while (hk[h] != col) h = (h + 1) & (kBigHashSlots - 1);
+            hv[h] = __dadd_rn(hv[h], __dmul_rn(a, bva[q]));
+        }
+        __syncthreads();
+    }
+    // compact the occupied slots as (column, slot) keys and sort them
+    const int32_t d = s_n;
+    int32_t n2 = 1;
+    while (n2 < d) n2 <<= 1;
+    if (tid == 0) s_n = 0;
+    __syncthreads();
+    for (int e = tid; e < kBigHashSlots; e += kBigThreads)
+        if (hk[e] != -1) {
+            const int32_t at = atomicAdd(&s_n, 1);
+            sk[at] = (static_cast<unsigned long long>(static_cast<uint32_t>(hk[e])) << 32) | static_cast<uint32_t>(e);
+        }
+    for (int e = d + tid; e < n2; e += kBigThreads) sk[e] = ~0ull;
+    __syncthreads();
+    for (int32_t k = 2; k <= n2; k <<= 1)
+        for (int32_t j = k >> 1; j > 0; j >>= 1) {
+            for (int32_t e = tid; e < n2 / 2; e += kBigThreads) {
+                const int32_t lo = 2 * e - (e & (j - 1));
+                const int32_t hi = lo + j;
+                const bool up = ((lo & k) == 0);
+                const unsigned long long x = sk[lo], y = sk[hi];
+                if ((x > y) == up) {
+                    sk[lo] = y;
+                    sk[hi] = x;
+                }
+            }
+            __syncthreads();
+        }
+    // nonzero sums in column order
+    const int lane = tid & (kWarp - 1), wid = tid / kWarp;
+    int32_t* ocol = tcol + poff[i];
+    double* oval = tval + poff[i];
+    int32_t written = 0;
+    for (int32_t e0 = 0; e0 < d; e0 += kBigThreads) {
+        const int32_t e = e0 + tid;
+        double acc = 0.0;
+        bool emit = false;
+        if (e < d) {
+            acc = hv[static_cast<uint32_t>(sk[e] & 0xffffffffull)];
+            emit = acc != 0.0;
+        }
+        const unsigned ballot = __ballot_sync(0xffffffffu, emit);
+        if (lane == 0) s_warp[wid] = __popc(ballot);
+        __syncthreads();
+        int32_t before = written;
+        for (int w = 0; w < wid; ++w) before += s_warp[w];
+        if (emit) {
+            const int32_t at = before + __popc(ballot & ((1u << lane) - 1u));
+            ocol[at] = static_cast<int32_t>(sk[e] >> 32);
+            oval[at] = acc;
+        }
+        for (int w = 0; w < kBigThreads / kWarp; ++w) written += s_warp[w];
+        __syncthreads();
+    }
+    if (tid == 0) {
+        cnt[i] = written;
+        handled[blockIdx.x] = 1;
+    }
 }
 
 __global__ void k_copy_rows(int32_t nr, const int64_t* __restrict__ poff, const int32_t* __restrict__ tcol,
@@ -697,7 +844,25 @@ namespace {
 size_t hash_smem() {
     static const size_t bytes = [] {
         const size_t b = sizeof(HashShared) * kHashWarps;
-        AMG_CK(cudaFuncSetAttribute(k_spgemm_hash, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(b)));
+        AMG_CK(cudaFuncSetAttribute(k_spgemm_hash<kSmallCap, kHashWarps, kSortCap>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(b)));
+        return b;
+    }();
+    return bytes;
+}
+size_t big_hash_smem() {
+    static const size_t bytes = [] {
+        AMG_CK(cudaFuncSetAttribute(k_spgemm_big_hash, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(kBigHashSmem)));
+        return kBigHashSmem;
+    }();
+    return bytes;
+}
+size_t mid_smem() {
+    static const size_t bytes = [] {
+        const size_t b = sizeof(HashSharedT<kMidCap>);
+        AMG_CK(cudaFuncSetAttribute(k_spgemm_hash<kMidCap, 1, kSmallCap>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(b)));
         return b;
     }();
     return bytes;
@@ -728,39 +893,59 @@ void spgemm(Ctx& c, const DCsr& A, const DCsr& B, DCsr& C, double* ops) {
     launch_prof(c, kProfSpgemm,
                 12.0 * A.nnz + 4.0 * (A.nr + 1) + 12.0 * B.nnz + 4.0 * (B.nr + 1) + 12.0 * static_cast<double>(total) +
                     4.0 * nr,
-                k_spgemm_hash, blocks_for(nr, kHashWarps), kHashWarps * kWarp, hash_smem(), nr, A.rp.get(),
-                A.ci.get(), A.va.get(), B.rp.get(), B.ci.get(), B.va.get(), static_cast<const int64_t*>(poff.get()),
-                tcol.get(), tval.get(), cnt.get());
+                k_spgemm_hash<kSmallCap, kHashWarps, kSortCap>, blocks_for(nr, kHashWarps), kHashWarps * kWarp,
+                hash_smem(), nr, A.rp.get(), A.ci.get(), A.va.get(), B.rp.get(), B.ci.get(), B.va.get(),
+                static_cast<const int64_t*>(poff.get()), tcol.get(), tval.get(), cnt.get(),
+                static_cast<const int32_t*>(nullptr));
     launch_prof(c, kProfSpgemm, 0.0, k_spgemm_small, blocks_for(nr, kGemmWarps), kGemmWarps * kWarp, 0, nr, A.rp.get(),
                 A.ci.get(), A.va.get(), B.rp.get(), B.ci.get(), B.va.get(), static_cast<const int64_t*>(poff.get()),
                 tcol.get(), tval.get(), cnt.get());
-    // rows above the shared-memory capacity
+    // rows above the warp kernels' capacity: up to kMidCap products one warp per block
+    // over the list, the rest block per row
+    static const bool mid_on = std::getenv("AMGCU_SPGEMM_NO_MID") == nullptr;
+    const int64_t mid_cap = mid_on ? kMidCap : kSmallCap;
+    if (nbig > 0 && mid_on)
+        launch_prof(c, kProfSpgemm, 0.0, k_spgemm_hash<kMidCap, 1, kSmallCap>, static_cast<unsigned>(nbig), kWarp,
+                    mid_smem(), nbig, A.rp.get(), A.ci.get(), A.va.get(), B.rp.get(), B.ci.get(), B.va.get(),
+                    static_cast<const int64_t*>(poff.get()), tcol.get(), tval.get(), cnt.get(),
+                    static_cast<const int32_t*>(big_list.get()));
     if (nbig > 0) {
         std::vector<int32_t> hl(nbig);
         copy_d2h(c, hl.data(), big_list.get(), nbig);
         std::vector<int64_t> hpoff(static_cast<size_t>(nr) + 1);
         copy_d2h(c, hpoff.data(), poff.get(), nr + 1);
         sync(c);
-        std::sort(hl.begin(), hl.end());
-        std::vector<int64_t> soff(nbig);
-        int64_t acc = 0;
-        for (int32_t b = 0; b < nbig; ++b) {
-            soff[b] = acc;
-            int64_t np2 = 1;
-            while (np2 < hpoff[hl[b] + 1] - hpoff[hl[b]]) np2 <<= 1;
-            acc += np2;
+        // the rows left for the block kernel, ascending
+        hl.erase(std::remove_if(hl.begin(), hl.end(), [&](int32_t r) { return hpoff[r + 1] - hpoff[r] <= mid_cap; }),
+                 hl.end());
+        const int32_t nb2 = static_cast<int32_t>(hl.size());
+        if (nb2 > 0) {
+            std::sort(hl.begin(), hl.end());
+            std::vector<int64_t> soff(nb2);
+            int64_t acc = 0;
+            for (int32_t b = 0; b < nb2; ++b) {
+                soff[b] = acc;
+                int64_t np2 = 1;
+                while (np2 < hpoff[hl[b] + 1] - hpoff[hl[b]]) np2 <<= 1;
+                acc += np2;
+            }
+            DBuf<int32_t> dl(static_cast<size_t>(nb2), c.s);
+            DBuf<int64_t> doff(static_cast<size_t>(nb2), c.s);
+            DBuf<unsigned long long> gkeys(static_cast<size_t>(acc), c.s);
+            DBuf<double> gvals(static_cast<size_t>(total), c.s);
+            copy_h2d(c, dl.get(), hl.data(), nb2);
+            copy_h2d(c, doff.get(), soff.data(), nb2);
+            DBuf<int32_t> handled(static_cast<size_t>(nb2), c.s);
+            launch(c, k_spgemm_big_hash, static_cast<unsigned>(nb2), kBigThreads, big_hash_smem(),
+                   static_cast<const int32_t*>(dl.get()), A.rp.get(), A.ci.get(), A.va.get(), B.rp.get(), B.ci.get(),
+                   B.va.get(), static_cast<const int64_t*>(poff.get()), tcol.get(), tval.get(), cnt.get(),
+                   handled.get());
+            launch(c, k_spgemm_big, static_cast<unsigned>(nb2), kBigThreads, 0, static_cast<const int32_t*>(dl.get()),
+                   A.rp.get(), A.ci.get(), A.va.get(), B.rp.get(), B.ci.get(), B.va.get(),
+                   static_cast<const int64_t*>(poff.get()), static_cast<const int64_t*>(doff.get()), gkeys.get(),
+                   gvals.get(), tcol.get(), tval.get(), cnt.get(), static_cast<const int32_t*>(handled.get()));
+            sync(c);
         }
-        DBuf<int32_t> dl(static_cast<size_t>(nbig), c.s);
-        DBuf<int64_t> doff(static_cast<size_t>(nbig), c.s);
-        DBuf<unsigned long long> gkeys(static_cast<size_t>(acc), c.s);
-        DBuf<double> gvals(static_cast<size_t>(total), c.s);
-        copy_h2d(c, dl.get(), hl.data(), nbig);
-        copy_h2d(c, doff.get(), soff.data(), nbig);
-        launch(c, k_spgemm_big, static_cast<unsigned>(nbig), kBigThreads, 0, static_cast<const int32_t*>(dl.get()),
-               A.rp.get(), A.ci.get(), A.va.get(), B.rp.get(), B.ci.get(), B.va.get(),
-               static_cast<const int64_t*>(poff.get()), static_cast<const int64_t*>(doff.get()), gkeys.get(),
-               gvals.get(), tcol.get(), tval.get(), cnt.get());
-        sync(c);
     }
     C.nr = nr;
     C.nc = B.nc;

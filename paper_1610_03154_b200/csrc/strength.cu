@@ -131,11 +131,9 @@ __global__ void k_negative_check(int64_t nnz, const double* __restrict__ va, int
 }
 
 // ---- amalgamate (strength.hpp:292-324): node row = max |s| per block column ----------------
-__global__ void k_amalgamate(int32_t nn, int32_t m, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+__device__ void amalgamate_row_serial(int32_t bi, int32_t m, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
                              const double* __restrict__ va, const int32_t* __restrict__ orp, int32_t* __restrict__ cnt,
                              int32_t* __restrict__ oci, double* __restrict__ ova) {
-    const int32_t bi = blockIdx.x * blockDim.x + threadIdx.x;
-    if (bi >= nn) return;
     const int32_t lo = rp[bi * m], hi = rp[bi * m + m];
     int32_t o = 0;
     for (int32_t p = lo; p < hi; ++p) {
@@ -174,6 +172,143 @@ __global__ void k_amalgamate(int32_t nn, int32_t m, const int32_t* __restrict__ 
         ++o;
     }
     if (!orp) cnt[bi] = o;
+}
+
+// One warp per node row: the row's block columns are rank-sorted in shared memory
+// (ties by position), each distinct block column's max |s| is read off its group and
+// the nonzero ones are numbered in ascending order -- the same entries and values as
+// the serial restatement above. Longer node rows are listed for k_amalgamate_long.
+constexpr int kAmWarps = 4;
+constexpr int kAmCap = 640;
+
+__global__ void __launch_bounds__(kAmWarps * 32) k_amalgamate(int32_t nn, int32_t m, const int32_t* __restrict__ rp,
+                                                              const int32_t* __restrict__ ci,
+                                                              const double* __restrict__ va,
+                                                              const int32_t* __restrict__ orp, int32_t* __restrict__ cnt,
+                                                              int32_t* __restrict__ oci, double* __restrict__ ova,
+                                                              int32_t* __restrict__ long_rows,
+                                                              int32_t* __restrict__ n_long) {
+    __shared__ int32_t s_in[kAmWarps][kAmCap];
+    __shared__ int32_t s_bc[kAmWarps][kAmCap];
+    __shared__ double s_v[kAmWarps][kAmCap];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int32_t bi = blockIdx.x * kAmWarps + warp;
+    if (bi >= nn) return;
+    const int32_t lo = rp[bi * m], hi = rp[bi * m + m], L = hi - lo;
+    if (L > kAmCap) {
+        if (lane == 0) long_rows[atomicAdd(n_long, 1)] = bi;  // k_amalgamate_long
+        return;
+    }
+    int32_t* in = s_in[warp];
+    int32_t* bc = s_bc[warp];
+    double* v = s_v[warp];
+    for (int32_t j = lane; j < L; j += 32) in[j] = ci[lo + j] / m;
+    __syncwarp();
+    for (int32_t j = lane; j < L; j += 32) {
+        const int32_t k = in[j];
+        int32_t r = 0;
+        for (int32_t q = 0; q < L; ++q) {
+            const int32_t kq = in[q];
+            r += (kq < k) || (kq == k && q < j);
+        }
+        bc[r] = k;
+        v[r] = fabs(va[lo + j]);
+    }
+    __syncwarp();
+    int32_t o = 0;
+    for (int32_t base = 0; base < L; base += 32) {
+        const int32_t j = base + lane;
+        bool keep = false;
+        int32_t k = 0;
+        double mx = 0.0;
+        if (j < L && (j == 0 || bc[j - 1] != bc[j])) {
+            k = bc[j];
+            for (int32_t q = j; q < L && bc[q] == k; ++q) mx = fmax(mx, v[q]);
+            keep = mx != 0.0;
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, keep);
+        if (keep && orp) {
+            const int32_t pos = orp[bi] + o + __popc(bal & ((1u << lane) - 1u));
+            oci[pos] = k;
+            ova[pos] = mx;
+        }
+        o += __popc(bal);
+    }
+    if (!orp && lane == 0) cnt[bi] = o;
+}
+
+// Node rows above kAmCap entries, a block each (grid-stride over the list): the
+// (block column, position) keys are bitonic-sorted in shared memory, then each
+// distinct block column's max |s| is read in position order. Rows above
+// kAmLongCap entries fall back to the serial restatement.
+constexpr int kAmLongThreads = 512;
+constexpr int kAmLongCap = 16384;
+
+__global__ void __launch_bounds__(kAmLongThreads)
+    k_amalgamate_long(const int32_t* __restrict__ long_rows, const int32_t* __restrict__ n_long, int32_t m,
+                      const int32_t* __restrict__ rp, const int32_t* __restrict__ ci, const double* __restrict__ va,
+                      const int32_t* __restrict__ orp, int32_t* __restrict__ cnt, int32_t* __restrict__ oci,
+                      double* __restrict__ ova) {
+    extern __shared__ __align__(16) unsigned long long am_keys[];
+    __shared__ int32_t s_warp[kAmLongThreads / 32];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int32_t nl = *n_long;
+    for (int32_t b = blockIdx.x; b < nl; b += gridDim.x) {
+        const int32_t bi = long_rows[b];
+        const int32_t lo = rp[bi * m], hi = rp[bi * m + m], L = hi - lo;
+        if (L > kAmLongCap) {
+            if (tid == 0) amalgamate_row_serial(bi, m, rp, ci, va, orp, cnt, oci, ova);
+            continue;
+        }
+        int32_t n2 = 1;
+        while (n2 < L) n2 <<= 1;
+        for (int32_t j = tid; j < n2; j += kAmLongThreads)
+            am_keys[j] = j < L ? (static_cast<unsigned long long>(static_cast<uint32_t>(ci[lo + j] / m)) << 32) |
+                                     static_cast<uint32_t>(j)
+                               : ~0ull;
+        __syncthreads();
+        for (int32_t k = 2; k <= n2; k <<= 1)
+            for (int32_t j = k >> 1; j > 0; j >>= 1) {
+                for (int32_t e = tid; e < n2 / 2; e += kAmLongThreads) {
+                    const int32_t x = 2 * e - (e & (j - 1)), y = x + j;
+                    const bool up = (x & k) == 0;
+                    const unsigned long long a = am_keys[x], c = am_keys[y];
+                    if ((a > c) == up) {
+                        am_keys[x] = c;
+                        am_keys[y] = a;
+                    }
+                }
+                __syncthreads();
+            }
+        int32_t o = 0;
+        for (int32_t base = 0; base < L; base += kAmLongThreads) {
+            const int32_t j = base + tid;
+            bool keep = false;
+            uint32_t bc = 0;
+            double mx = 0.0;
+            if (j < L) {
+                bc = static_cast<uint32_t>(am_keys[j] >> 32);
+                if (j == 0 || static_cast<uint32_t>(am_keys[j - 1] >> 32) != bc) {
+                    for (int32_t q = j; q < L && static_cast<uint32_t>(am_keys[q] >> 32) == bc; ++q)
+                        mx = fmax(mx, fabs(va[lo + static_cast<uint32_t>(am_keys[q] & 0xffffffffu)]));
+                    keep = mx != 0.0;
+                }
+            }
+            const unsigned bal = __ballot_sync(0xffffffffu, keep);
+            if (lane == 0) s_warp[wid] = __popc(bal);
+            __syncthreads();
+            int32_t before = o;
+            for (int w = 0; w < wid; ++w) before += s_warp[w];
+            if (keep && orp) {
+                const int32_t pos = orp[bi] + before + __popc(bal & ((1u << lane) - 1u));
+                oci[pos] = static_cast<int32_t>(bc);
+                ova[pos] = mx;
+            }
+            for (int w = 0; w < kAmLongThreads / 32; ++w) o += s_warp[w];
+            __syncthreads();
+        }
+        if (!orp && tid == 0) cnt[bi] = o;
+    }
 }
 
 // ---- evolution (strength.hpp:116-238) -------------------------------------------------------
@@ -796,7 +931,31 @@ void amalgamate(Ctx& c, const DCsr& S, int32_t m, DCsr& N) {
     }
     if (S.nr % m != 0 || S.nc % m != 0) throw InvalidArgument("amalgamate: dimensions not divisible by block size");
     const int32_t nn = S.nr / m;
-    two_pass(c, nn, S.nc / m, 1, N, k_amalgamate, blocks_for(nn, 128), 128, nn, m, S.rp.get(), S.ci.get(), S.va.get());
+    static const size_t long_smem = [] {
+        const size_t b = kAmLongCap * sizeof(unsigned long long);
+        AMG_CK(cudaFuncSetAttribute(k_amalgamate_long, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(b)));
+        return b;
+    }();
+    DBuf<int32_t> cnt(static_cast<size_t>(nn) + 1, c.s), long_rows(static_cast<size_t>(nn), c.s), n_long(1, c.s);
+    const unsigned long_grid = static_cast<unsigned>(c.sms * 2);
+    auto pass = [&](const int32_t* orp, int32_t* oci, double* ova) {
+        AMG_CK(cudaMemsetAsync(n_long.get(), 0, sizeof(int32_t), c.s));
+        launch(c, k_amalgamate, blocks_for(nn, kAmWarps), kAmWarps * 32, 0, nn, m, S.rp.get(), S.ci.get(), S.va.get(),
+               orp, cnt.get(), oci, ova, long_rows.get(), n_long.get());
+        launch(c, k_amalgamate_long, long_grid, kAmLongThreads, long_smem, static_cast<const int32_t*>(long_rows.get()),
+               static_cast<const int32_t*>(n_long.get()), m, S.rp.get(), S.ci.get(), S.va.get(), orp, cnt.get(), oci,
+               ova);
+    };
+    pass(nullptr, nullptr, nullptr);
+    N.nr = nn;
+    N.nc = S.nc / m;
+    N.bs = 1;
+    N.rp.alloc(static_cast<size_t>(nn) + 1, c.s);
+    N.nnz = exclusive_scan_i32(c, cnt.get(), N.rp.get(), nn);
+    N.ci.alloc(static_cast<size_t>(N.nnz), c.s);
+    N.va.alloc(static_cast<size_t>(N.nnz), c.s);
+    pass(N.rp.get(), N.ci.get(), N.va.get());
 }
 
 EvoCount::~EvoCount() {

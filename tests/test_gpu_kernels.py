@@ -10,7 +10,7 @@ import paper_1610_03154_b200.api as api
 from paper_1610_03154_b200.types import (CandidateSet, EvolutionWeighting, StrengthConfig, StrengthMeasure,
                                          constant_candidates,
                                          from_triplets, identity)
-from tests.helpers import aniso2d, poisson1d, random_sparse, random_spd_sparse, rel_max_err, stencil9, tridiag
+from tests.helpers import aniso2d, from_triplets, poisson1d, random_sparse, random_spd_sparse, rel_max_err, stencil9, tridiag
 
 pytestmark = pytest.mark.gpu
 
@@ -54,6 +54,18 @@ def test_matmul_long_rows_and_cancellation(gpu, port):
     rng = np.random.default_rng(3)
     A = random_sparse(30, 400, 0.9, rng)
     B = random_sparse(400, 300, 0.5, rng)
+    assert api.matmul(A, B, ctx=gpu) == port.matmul(A, B)
+    # 512..2048 products per row (one warp per block, shared-memory hash), mixed with
+    # shorter and longer rows
+    for da, db in ((0.1, 0.2), (0.05, 0.5), (0.3, 0.1)):
+        A = random_sparse(60, 200, da, rng)
+        B = random_sparse(200, 300, db, rng)
+        assert api.matmul(A, B, ctx=gpu) == port.matmul(A, B), (da, db)
+    # more distinct columns than the shared-memory table of the block kernel holds:
+    # those rows take the global bitonic sort
+    A = random_sparse(3, 1500, 0.9, rng)
+    ii, jj = np.nonzero(rng.random((1500, 8000)) < 0.02)
+    B = from_triplets(1500, 8000, list(zip(ii.tolist(), jj.tolist(), rng.uniform(0.5, 1.0, ii.size).tolist())))
     assert api.matmul(A, B, ctx=gpu) == port.matmul(A, B)
     # exact cancellation: (1, -1) . (x, x) = 0 is dropped
     A2 = from_triplets(2, 2, [(0, 0, 1.0), (0, 1, -1.0), (1, 1, 2.0)])
@@ -183,6 +195,14 @@ def test_amalgamate(gpu, port):
     R = random_sparse(12, 12, 0.3, rng)
     for m in (1, 2, 3):
         assert api.amalgamate(R, m, ctx=gpu) == port.amalgamate(R, m)
+    # node rows on both sides of the warp kernel's shared-memory capacity (640 entries),
+    # with explicit zeros (blocks whose max |s| is 0 are dropped)
+    t = [(i, j, 0.0 if rng.uniform() < 0.2 else rng.uniform(-1.0, 1.0))
+         for i in range(240) for j in range(480) if rng.uniform() < (0.75 if i < 40 else 0.08)]
+    t.append((239, 479, 0.0))
+    Z = from_triplets(240, 480, t)
+    for m in (2, 3, 4):
+        assert api.amalgamate(Z, m, ctx=gpu) == port.amalgamate(Z, m), m
 
 
 def test_aggregation_known_answers(gpu):
