@@ -936,7 +936,9 @@ void spgemm(Ctx& c, const DCsr& A, const DCsr& B, DCsr& C, double* ops) {
             copy_h2d(c, dl.get(), hl.data(), nb2);
             copy_h2d(c, doff.get(), soff.data(), nb2);
             DBuf<int32_t> handled(static_cast<size_t>(nb2), c.s);
-            launch(c, k_spgemm_big_hash, static_cast<unsigned>(nb2), kBigThreads, big_hash_smem(),
+            static const bool no_hash = std::getenv("AMGCU_SPGEMM_NO_BIGHASH") != nullptr;
+            if (no_hash) AMG_CK(cudaMemsetAsync(handled.get(), 0, sizeof(int32_t) * nb2, c.s));
+            else launch(c, k_spgemm_big_hash, static_cast<unsigned>(nb2), kBigThreads, big_hash_smem(),
                    static_cast<const int32_t*>(dl.get()), A.rp.get(), A.ci.get(), A.va.get(), B.rp.get(), B.ci.get(),
                    B.va.get(), static_cast<const int64_t*>(poff.get()), tcol.get(), tval.get(), cnt.get(),
                    handled.get());

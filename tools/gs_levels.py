@@ -19,4 +19,6 @@ for l in range(h.n_levels() - 1):
     api.improve_candidates(M, Bl, so.candidate_sweeps, 1, 0.0, ctx=ctx)
     ms = ctx.profile()["gauss_seidel_wavefront"][1]
     ctx.set_profiling(False)
-    print(f"L{l} n {M.n_rows}: {ms:.3f} ms", flush=True)
+    rl = np.diff(M.row_offsets)
+    bw = int(np.max(np.abs(M.col_indices - np.repeat(np.arange(M.n_rows), rl)))) if M.nnz() else 0
+    print(f"L{l} n {M.n_rows} bs {M.block_size} longest row {int(rl.max())} bandwidth {bw}: {ms:.3f} ms", flush=True)
