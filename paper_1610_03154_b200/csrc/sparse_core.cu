@@ -503,33 +503,76 @@ __global__ void __launch_bounds__(kBigThreads)
 // Rows with more distinct columns than kBigHashMax are left to the bitonic kernel.
 constexpr int kBigHashSlots = 8192;
 constexpr int kBigHashMax = 6144;
+constexpr int kBigHashMinB = 128;
 constexpr size_t kBigHashSmem = kBigHashSlots * (sizeof(int32_t) + sizeof(double)) +
                                 kBigHashSlots * sizeof(unsigned long long);
 
-__device__ __forceinline__ uint32_t big_slot(int32_t col) {
-    return (static_cast<uint32_t>(col) * 2654435761u) >> (32 - 13);
+template <bool G, class T>
+__device__ __forceinline__ T bh_ld(const T* p) {
+    if constexpr (G) return __ldcg(p);  // global tables: other threads' writes, past L1
+    else return *p;
 }
 
+// G = false: the table is in shared memory (kBigHashSlots slots, rows of at most
+// kBigHashMax distinct columns). G = true: rows the shared table refused, with a
+// table in global scratch of the next power of two above the row's product count.
+template <bool G>
 __global__ void __launch_bounds__(kBigThreads)
     k_spgemm_big_hash(const int32_t* __restrict__ list, const int32_t* __restrict__ arp,
                       const int32_t* __restrict__ aci, const double* __restrict__ ava,
                       const int32_t* __restrict__ brp, const int32_t* __restrict__ bci,
                       const double* __restrict__ bva, const int64_t* __restrict__ poff, int32_t* __restrict__ tcol,
-                      double* __restrict__ tval, int32_t* __restrict__ cnt, int32_t* __restrict__ handled) {
-    static_assert(kBigHashSlots == 1 << 13, "big_slot shift");
+                      double* __restrict__ tval, int32_t* __restrict__ cnt, int32_t* __restrict__ handled,
+                      const int64_t* __restrict__ scratch_off, int32_t* gk, double* gv, unsigned long long* gs) {
     extern __shared__ __align__(16) unsigned char big_smem[];
-    double* hv = reinterpret_cast<double*>(big_smem);
-    unsigned long long* sk = reinterpret_cast<unsigned long long*>(hv + kBigHashSlots);
-    int32_t* hk = reinterpret_cast<int32_t*>(sk + kBigHashSlots);
-    __shared__ int32_t s_n;
+    __shared__ int32_t s_n, s_over;
     __shared__ int32_t s_warp[kBigThreads / kWarp];
+    if (G && handled[blockIdx.x]) return;
     const int32_t i = list[blockIdx.x];
     const int tid = threadIdx.x;
-    for (int e = tid; e < kBigHashSlots; e += kBigThreads) {
+    // one block barrier per A entry: rows whose B rows average under kBigHashMinB
+    // products would leave most threads idle, so the bitonic kernel takes them
+    if (poff[i + 1] - poff[i] < static_cast<int64_t>(kBigHashMinB) * (arp[i + 1] - arp[i])) {
+        if (tid == 0) handled[blockIdx.x] = 0;
+        return;
+    }
+    int32_t* hk;
+    double* hv;
+    unsigned long long* sk;
+    int32_t size, maxd, lg;
+    if constexpr (G) {
+        const int64_t np = poff[i + 1] - poff[i];
+        size = 1;
+        lg = 0;
+        while (size < np) {
+            size <<= 1;
+            ++lg;
+        }
+        maxd = size;
+        hk = gk + scratch_off[blockIdx.x];
+        hv = gv + scratch_off[blockIdx.x];
+        sk = gs + scratch_off[blockIdx.x];
+    } else {
+        size = kBigHashSlots;
+        lg = 13;
+        maxd = kBigHashMax;
+        hv = reinterpret_cast<double*>(big_smem);
+        sk = reinterpret_cast<unsigned long long*>(hv + kBigHashSlots);
+        hk = reinterpret_cast<int32_t*>(sk + kBigHashSlots);
+    }
+    const uint32_t mask = static_cast<uint32_t>(size) - 1u;
+    // the shared table refuses a row early (long probe chains or too many columns);
+    // the global one is sized to the row and probes to the end
+    const int32_t probe_cap = G ? size : 128;
+    auto slot = [&](int32_t col) { return (static_cast<uint32_t>(col) * 2654435761u) >> (32 - lg); };
+    for (int e = tid; e < size; e += kBigThreads) {
         hk[e] = -1;
         hv[e] = 0.0;
     }
-    if (tid == 0) s_n = 0;
+    if (tid == 0) {
+        s_n = 0;
+        s_over = 0;
+    }
     __syncthreads();
     const int32_t alo = arp[i], ahi = arp[i + 1];
     // distinct columns
@@ -537,25 +580,27 @@ __global__ void __launch_bounds__(kBigThreads)
         const int32_t t = aci[p];
         bool over = false;
         for (int32_t q = brp[t] + tid; q < brp[t + 1] && !over; q += kBigThreads) {
+            if (*reinterpret_cast<volatile int32_t*>(&s_over)) break;  // another thread refused the row
             const int32_t col = bci[q];
-            uint32_t h = big_slot(col);
-            for (int probe = 0;; ) {
-                const int32_t k = hk[h];
+            uint32_t h = slot(col);
+            for (int32_t probe = 0;;) {
+                const int32_t k = bh_ld<G>(hk + h);
                 if (k == col) break;
                 if (k == -1) {
                     const int32_t old = atomicCAS(&hk[h], -1, col);
                     if (old == -1) {
-                        over = atomicAdd(&s_n, 1) >= kBigHashMax;
+                        over = atomicAdd(&s_n, 1) >= maxd;
                         break;
                     }
                     if (old == col) break;
                 }
-                h = (h + 1) & (kBigHashSlots - 1);
-                if (++probe == kBigHashSlots) {
+                h = (h + 1) & mask;
+                if (++probe == probe_cap) {
                     over = true;
                     break;
                 }
             }
+            if (over) s_over = 1;
         }
         if (__syncthreads_or(over)) {
             if (tid == 0) handled[blockIdx.x] = 0;
@@ -568,9 +613,9 @@ __global__ void __launch_bounds__(kBigThreads)
         const double a = ava[p];
         for (int32_t q = brp[t] + tid; q < brp[t + 1]; q += kBigThreads) {
             const int32_t col = bci[q];
-            uint32_t h = big_slot(col);
-            while (hk[h] != col) h = (h + 1) & (kBigHashSlots - 1);
-            hv[h] = __dadd_rn(hv[h], __dmul_rn(a, bva[q]));
+            uint32_t h = slot(col);
+            while (bh_ld<G>(hk + h) != col) h = (h + 1) & mask;
+            hv[h] = __dadd_rn(bh_ld<G>(hv + h), __dmul_rn(a, bva[q]));
         }
         __syncthreads();
     }
@@ -578,13 +623,16 @@ __global__ void __launch_bounds__(kBigThreads)
     const int32_t d = s_n;
     int32_t n2 = 1;
     while (n2 < d) n2 <<= 1;
+    __syncthreads();
     if (tid == 0) s_n = 0;
     __syncthreads();
-    for (int e = tid; e < kBigHashSlots; e += kBigThreads)
-        if (hk[e] != -1) {
+    for (int e = tid; e < size; e += kBigThreads) {
+        const int32_t k = bh_ld<G>(hk + e);
+        if (k != -1) {
             const int32_t at = atomicAdd(&s_n, 1);
-            sk[at] = (static_cast<unsigned long long>(static_cast<uint32_t>(hk[e])) << 32) | static_cast<uint32_t>(e);
+            sk[at] = (static_cast<unsigned long long>(static_cast<uint32_t>(k)) << 32) | static_cast<uint32_t>(e);
         }
+    }
     for (int e = d + tid; e < n2; e += kBigThreads) sk[e] = ~0ull;
     __syncthreads();
     for (int32_t k = 2; k <= n2; k <<= 1)
@@ -593,7 +641,7 @@ __global__ void __launch_bounds__(kBigThreads)
                 const int32_t lo = 2 * e - (e & (j - 1));
                 const int32_t hi = lo + j;
                 const bool up = ((lo & k) == 0);
-                const unsigned long long x = sk[lo], y = sk[hi];
+                const unsigned long long x = bh_ld<G>(sk + lo), y = bh_ld<G>(sk + hi);
                 if ((x > y) == up) {
                     sk[lo] = y;
                     sk[hi] = x;
@@ -611,7 +659,7 @@ __global__ void __launch_bounds__(kBigThreads)
         double acc = 0.0;
         bool emit = false;
         if (e < d) {
-            acc = hv[static_cast<uint32_t>(sk[e] & 0xffffffffull)];
+            acc = bh_ld<G>(hv + static_cast<uint32_t>(bh_ld<G>(sk + e) & 0xffffffffull));
             emit = acc != 0.0;
         }
         const unsigned ballot = __ballot_sync(0xffffffffu, emit);
@@ -621,7 +669,7 @@ __global__ void __launch_bounds__(kBigThreads)
         for (int w = 0; w < wid; ++w) before += s_warp[w];
         if (emit) {
             const int32_t at = before + __popc(ballot & ((1u << lane) - 1u));
-            ocol[at] = static_cast<int32_t>(sk[e] >> 32);
+            ocol[at] = static_cast<int32_t>(bh_ld<G>(sk + e) >> 32);
             oval[at] = acc;
         }
         for (int w = 0; w < kBigThreads / kWarp; ++w) written += s_warp[w];
@@ -852,7 +900,7 @@ size_t hash_smem() {
 }
 size_t big_hash_smem() {
     static const size_t bytes = [] {
-        AMG_CK(cudaFuncSetAttribute(k_spgemm_big_hash, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        AMG_CK(cudaFuncSetAttribute(k_spgemm_big_hash<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(kBigHashSmem)));
         return kBigHashSmem;
     }();
@@ -938,10 +986,22 @@ void spgemm(Ctx& c, const DCsr& A, const DCsr& B, DCsr& C, double* ops) {
             DBuf<int32_t> handled(static_cast<size_t>(nb2), c.s);
             static const bool no_hash = std::getenv("AMGCU_SPGEMM_NO_BIGHASH") != nullptr;
             if (no_hash) AMG_CK(cudaMemsetAsync(handled.get(), 0, sizeof(int32_t) * nb2, c.s));
-            else launch(c, k_spgemm_big_hash, static_cast<unsigned>(nb2), kBigThreads, big_hash_smem(),
-                   static_cast<const int32_t*>(dl.get()), A.rp.get(), A.ci.get(), A.va.get(), B.rp.get(), B.ci.get(),
-                   B.va.get(), static_cast<const int64_t*>(poff.get()), tcol.get(), tval.get(), cnt.get(),
-                   handled.get());
+            else launch(c, k_spgemm_big_hash<false>, static_cast<unsigned>(nb2), kBigThreads, big_hash_smem(),
+                        static_cast<const int32_t*>(dl.get()), A.rp.get(), A.ci.get(), A.va.get(), B.rp.get(),
+                        B.ci.get(), B.va.get(), static_cast<const int64_t*>(poff.get()), tcol.get(), tval.get(),
+                        cnt.get(), handled.get(), static_cast<const int64_t*>(nullptr),
+                        static_cast<int32_t*>(nullptr), static_cast<double*>(nullptr),
+                        static_cast<unsigned long long*>(nullptr));
+            if (!no_hash) {
+                // rows the shared table refused: the same with the table in global scratch
+                DBuf<int32_t> gk(static_cast<size_t>(acc), c.s);
+                DBuf<double> gv(static_cast<size_t>(acc), c.s);
+                launch(c, k_spgemm_big_hash<true>, static_cast<unsigned>(nb2), kBigThreads, 0,
+                       static_cast<const int32_t*>(dl.get()), A.rp.get(), A.ci.get(), A.va.get(), B.rp.get(),
+                       B.ci.get(), B.va.get(), static_cast<const int64_t*>(poff.get()), tcol.get(), tval.get(),
+                       cnt.get(), handled.get(), static_cast<const int64_t*>(doff.get()), gk.get(), gv.get(),
+                       gkeys.get());
+            }
             launch(c, k_spgemm_big, static_cast<unsigned>(nb2), kBigThreads, 0, static_cast<const int32_t*>(dl.get()),
                    A.rp.get(), A.ci.get(), A.va.get(), B.rp.get(), B.ci.get(), B.va.get(),
                    static_cast<const int64_t*>(poff.get()), static_cast<const int64_t*>(doff.get()), gkeys.get(),

@@ -62,7 +62,7 @@ def test_matmul_long_rows_and_cancellation(gpu, port):
         B = random_sparse(200, 300, db, rng)
         assert api.matmul(A, B, ctx=gpu) == port.matmul(A, B), (da, db)
     # more distinct columns than the shared-memory table of the block kernel holds:
-    # those rows take the global bitonic sort
+    # those rows take the table in global scratch
     A = random_sparse(3, 1500, 0.9, rng)
     ii, jj = np.nonzero(rng.random((1500, 8000)) < 0.02)
     B = from_triplets(1500, 8000, list(zip(ii.tolist(), jj.tolist(), rng.uniform(0.5, 1.0, ii.size).tolist())))
