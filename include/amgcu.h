@@ -190,6 +190,15 @@ amgcu_status amgcu_cycle(amgcu_hier h, double* x, const double* b, int32_t kind)
 
 /* ---- kernel-level entry points (each one reference function; host in/out) */
 amgcu_status amgcu_spmv(amgcu_ctx ctx, const amgcu_csr* A, const double* x, double* y);      /* sparse.hpp:141 */
+/* dot(x, y) (take_sqrt = 0) or norm2(x) = sqrt(dot(x, x)) (take_sqrt = 1, y ignored):
+   sparse.hpp:309-315.  In the default context mode the sum is the reference's
+   left-to-right chain bit for bit (csrc/seqsum.cu); with sequential reductions off it
+   is a deterministic tree. */
+amgcu_status amgcu_dot(amgcu_ctx ctx, const double* x, const double* y, int64_t n, int32_t take_sqrt, double* out);
+/* the same on device-resident x, y (y may equal x), result written to device *out_dev;
+   enqueued on the context stream, no synchronisation */
+amgcu_status amgcu_dot_device(amgcu_ctx ctx, const double* x_dev, const double* y_dev, int64_t n, int32_t take_sqrt,
+                              double* out_dev);
 amgcu_status amgcu_transpose(amgcu_ctx ctx, const amgcu_csr* A, amgcu_csr* out);             /* sparse.hpp:161 */
 amgcu_status amgcu_matmul(amgcu_ctx ctx, const amgcu_csr* A, const amgcu_csr* B, amgcu_csr* out); /* :183 */
 amgcu_status amgcu_galerkin_product(amgcu_ctx ctx, const amgcu_csr* R, const amgcu_csr* A, const amgcu_csr* P,

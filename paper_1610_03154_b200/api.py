@@ -31,7 +31,7 @@ for _name in ("amgcu_ctx_create", "amgcu_ctx_destroy", "amgcu_ctx_set_sequential
               "amgcu_spmv", "amgcu_transpose", "amgcu_matmul", "amgcu_galerkin_product", "amgcu_filter_matrix",
               "amgcu_is_symmetric", "amgcu_spectral_radius", "amgcu_strength", "amgcu_normalize_strength",
               "amgcu_amalgamate", "amgcu_greedy_aggregate", "amgcu_sparsity_pattern", "amgcu_improve_candidates",
-              "amgcu_relax", "amgcu_generate", "amgcu_config_options"):
+              "amgcu_relax", "amgcu_generate", "amgcu_config_options", "amgcu_dot", "amgcu_dot_device"):
     getattr(lib, _name).restype = C.c_int
 lib.amgcu_ctx_create.argtypes = [C.c_int, C.POINTER(C.c_void_p)]
 lib.amgcu_ctx_destroy.argtypes = [C.c_void_p]
@@ -57,6 +57,8 @@ lib.amgcu_solve_device.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER
                                    C.POINTER(SolveReportC), f64p, C.c_int32]
 lib.amgcu_cycle.argtypes = [C.c_void_p, f64p, f64p, C.c_int32]
 lib.amgcu_spmv.argtypes = [C.c_void_p, C.POINTER(CsrC), f64p, f64p]
+lib.amgcu_dot.argtypes = [C.c_void_p, f64p, f64p, C.c_int64, C.c_int32, C.POINTER(C.c_double)]
+lib.amgcu_dot_device.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p]
 lib.amgcu_transpose.argtypes = [C.c_void_p, C.POINTER(CsrC), C.POINTER(CsrC)]
 lib.amgcu_matmul.argtypes = [C.c_void_p, C.POINTER(CsrC), C.POINTER(CsrC), C.POINTER(CsrC)]
 lib.amgcu_galerkin_product.argtypes = [C.c_void_p, C.POINTER(CsrC), C.POINTER(CsrC), C.POINTER(CsrC), C.POINTER(CsrC)]
@@ -81,17 +83,17 @@ lib.amgcu_csr_free.argtypes = [C.POINTER(CsrC)]
 
 
 class Context:
-    """One CUDA device + stream.  sequential_reductions=True selects the
-    parity-debug mode (global sums in the reference's index order)."""
+    """One CUDA device + stream.  sequential_reductions=True (the default) takes every
+    global sum in the reference's left-to-right order, bit for bit (csrc/seqsum.cu);
+    False selects deterministic tree reductions (reproducible, not the reference's bits)."""
 
-    def __init__(self, device: int = 0, sequential_reductions: bool = False):
+    def __init__(self, device: int = 0, sequential_reductions: bool = True):
         h = C.c_void_p()
         code = lib.amgcu_ctx_create(device, C.byref(h))
         if code != 0:
             raise_for(code if code in (1, 2, 3) else 2, lib.amgcu_last_error(None).decode())
         self.handle = h.value
-        if sequential_reductions:
-            self.set_sequential_reductions(True)
+        self.set_sequential_reductions(sequential_reductions)
 
     def close(self):
         if getattr(self, "handle", None):
@@ -315,6 +317,26 @@ def spmv(A: SparseMatrix, x, ctx=None):
     y = np.zeros(A.n_rows)
     ctx._chk(lib.amgcu_spmv(ctx.handle, C.byref(A.to_c()), ptr_f64(x), ptr_f64(y)))
     return y
+
+
+def dot(x, y, ctx=None):
+    """sparse.hpp:309-313: sum of x[i] * y[i] from 0.0, left to right"""
+    ctx = _ctx(ctx)
+    x, y = as_f64(x), as_f64(y)
+    if x.shape != y.shape:
+        raise ValueError("dot: size mismatch")
+    out = C.c_double()
+    ctx._chk(lib.amgcu_dot(ctx.handle, ptr_f64(x), ptr_f64(y), x.size, 0, C.byref(out)))
+    return out.value
+
+
+def norm2(x, ctx=None):
+    """sparse.hpp:315: sqrt(dot(x, x))"""
+    ctx = _ctx(ctx)
+    x = as_f64(x)
+    out = C.c_double()
+    ctx._chk(lib.amgcu_dot(ctx.handle, ptr_f64(x), ptr_f64(x), x.size, 1, C.byref(out)))
+    return out.value
 
 
 def transpose(A: SparseMatrix, ctx=None):

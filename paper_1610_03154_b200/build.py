@@ -28,7 +28,7 @@ NVCC_FLAGS = ARCH + ["-lineinfo", "-O3", "--fmad=false", "-std=c++20", "--expt-r
                      "-Xcompiler", "-fPIC,-ffp-contract=off,-O3", "-I" + os.path.join(ROOT, "include")]
 CXX_FLAGS = ["-O3", "-std=gnu++20", "-fPIC", "-ffp-contract=off", "-I" + os.path.join(ROOT, "include")]
 
-CU_SOURCES = ["primitives.cu", "sparse_core.cu", "blas.cu", "strength.cu", "aggregate.cu", "relax.cu", "relax_more.cu", "arnoldi.cu",
+CU_SOURCES = ["primitives.cu", "sparse_core.cu", "blas.cu", "seqsum.cu", "strength.cu", "aggregate.cu", "relax.cu", "relax_more.cu", "arnoldi.cu",
               "interp.cu", "setup.cu", "cycle.cu", "capi.cu"]
 CXX_SOURCES = ["problems.cpp"]
 # every header in csrc (a header edit must rebuild its includers)

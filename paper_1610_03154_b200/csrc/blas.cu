@@ -1,13 +1,14 @@
 // BLAS-1 on device-resident scalars (sparse.hpp:309-323).
 //
-// dot: default = deterministic two-stage tree (fixed grid, fixed per-thread
-// order, last-block final sum in index order of the block partials), so the
-// same inputs always give the same bits.  With Ctx::seq the sum is taken in
-// the reference's order s = ((0 + x0 y0) + x1 y1) + ... by one warp
-// (parity-debug mode): bit-identical to the CPU, slower.
+// Ctx::seq (the default): every sum is the reference's s = ((0 + x0 y0) + x1 y1) + ...
+// bit for bit, evaluated in parallel by seqsum.cu (AMGCU_SEQ_NAIVE=1: by one warp, the
+// slow original, kept to A/B the fast one).  Ctx::seq off: a deterministic two-stage
+// tree (fixed grid, fixed per-thread order, last-block final sum in index order of the
+// block partials) -- reproducible, but not the reference's bits.
 #include <cub/block/block_reduce.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "ops.cuh"
 
@@ -194,9 +195,20 @@ unsigned dot_grid(Ctx& c, int64_t n) {
 
 namespace {
 
+bool seq_naive() {
+    static const bool on = [] {
+        const char* e = std::getenv("AMGCU_SEQ_NAIVE");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+
 void dot_impl(Ctx& c, const double* x, const double* y, int64_t n, double* out, bool take_sqrt) {
     if (c.seq) {
-        launch_prof(c, c.blas_family, 16.0 * n, k_dot_seq, 1, 32, 0, x, y, n, out, take_sqrt);
+        if (seq_naive())
+            launch_prof(c, c.blas_family, 16.0 * n, k_dot_seq, 1, 32, 0, x, y, n, out, take_sqrt);
+        else
+            seqsum_dot(c, x, y, n, out, take_sqrt);
         return;
     }
     const unsigned g = dot_grid(c, n);
@@ -209,8 +221,12 @@ void dot_impl(Ctx& c, const double* x, const double* y, int64_t n, double* out, 
 void axpy_dot(Ctx& c, const double* alpha, double sign, const double* x, double* y, const double* z, int64_t n,
               double* out, bool take_sqrt) {
     if (c.seq) {
-        axpy_dev(c, alpha, sign, x, y, n);
-        dot_impl(c, y, z ? z : y, n, out, take_sqrt);
+        if (seq_naive()) {
+            axpy_dev(c, alpha, sign, x, y, n);
+            dot_impl(c, y, z ? z : y, n, out, take_sqrt);
+        } else {
+            seqsum_axpy_dot(c, alpha, sign, x, y, z, n, out, take_sqrt);
+        }
         return;
     }
     const unsigned g = dot_grid(c, n);
@@ -224,7 +240,11 @@ void nrm2(Ctx& c, const double* x, int64_t n, double* out) { dot_impl(c, x, x, n
 
 bool pcg_update_nrm(Ctx& c, const double* st, const int32_t* bad, const double* p, const double* q, double* x,
                     double* r, int64_t n, double* out) {
-    if (c.seq) return false;  // parity mode: the update kernel and the sequential norm
+    if (c.seq) {
+        if (seq_naive()) return false;  // the update kernel and the one-warp norm
+        seqsum_pcg_update_nrm(c, st, bad, p, q, x, r, n, out);
+        return true;
+    }
     const unsigned g = dot_grid(c, n);
     ensure_reduction_scratch(c, g);
     launch_prof(c, kProfBlas1, 56.0 * n, k_pcg_update_nrm, g, kDotThreads, 0, st, bad, p, q, x, r, n,

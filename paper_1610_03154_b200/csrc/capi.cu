@@ -136,6 +136,7 @@ amgcu_status amgcu_ctx_create(int device, amgcu_ctx* out) {
         AMG_CK(cudaStreamCreateWithPriority(&ctx->c.s, cudaStreamNonBlocking, prio_hi));
         AMG_CK(cudaStreamCreateWithPriority(&ctx->c.side, cudaStreamNonBlocking, prio_lo));
         AMG_CK(cudaStreamCreateWithPriority(&ctx->c.side2, cudaStreamNonBlocking, prio_hi));
+        ctx->c.main_s = ctx->c.s;
         AMG_CK(cudaDeviceGetAttribute(&ctx->c.sms, cudaDevAttrMultiProcessorCount, device));
         cudaMemPool_t pool;
         AMG_CK(cudaDeviceGetDefaultMemPool(&pool, device));
@@ -153,6 +154,12 @@ amgcu_status amgcu_ctx_destroy(amgcu_ctx ctx) {
     ctx->c.partials.release();
     ctx->c.tickets.release();
     ctx->c.arnoldi_v0.release();
+    for (auto& w : ctx->c.ssws) {
+        w.counters.release();
+        w.status.release();
+        w.lists.release();
+        w.lens.release();
+    }
     ctx->c.scan_tmp.release();  // every stream-ordered buffer before its stream goes
     cudaStreamSynchronize(ctx->c.s);
     if (ctx->c.pin) cudaFreeHost(ctx->c.pin);
@@ -416,6 +423,32 @@ amgcu_status amgcu_spmv(amgcu_ctx ctx, const amgcu_csr* A, const double* x, doub
         DBuf<double> dx = up_vec(c, x, A->n_cols), dy(static_cast<size_t>(A->n_rows), c.s);
         spmv(c, d, dx.get(), dy.get());
         down_vec(c, y, dy.get(), A->n_rows);
+    });
+}
+
+amgcu_status amgcu_dot(amgcu_ctx ctx, const double* x, const double* y, int64_t n, int32_t take_sqrt, double* out) {
+    return guarded(ctx, [&] {
+        if (n < 0) throw InvalidArgument("dot: negative length");
+        Ctx& c = ctx->c;
+        DBuf<double> dx = up_vec(c, x, n);
+        DBuf<double> dy = take_sqrt ? DBuf<double>() : up_vec(c, y, n);
+        DBuf<double> r(1, c.s);
+        if (take_sqrt)
+            nrm2(c, dx.get(), n, r.get());
+        else
+            dot(c, dx.get(), dy.get(), n, r.get());
+        *out = read_scalar(c, r.get());
+    });
+}
+
+amgcu_status amgcu_dot_device(amgcu_ctx ctx, const double* x_dev, const double* y_dev, int64_t n, int32_t take_sqrt,
+                              double* out_dev) {
+    return guarded(ctx, [&] {
+        if (n < 0) throw InvalidArgument("dot: negative length");
+        if (take_sqrt)
+            nrm2(ctx->c, x_dev, n, out_dev);
+        else
+            dot(ctx->c, x_dev, y_dev, n, out_dev);
     });
 }
 

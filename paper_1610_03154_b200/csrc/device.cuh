@@ -115,6 +115,16 @@ bool sync_trace_on();
 bool prof_other_enabled();
 void prof_other_add(const void* kernel, double ms);
 
+// workspace of the exact-order reductions (seqsum.cu): tickets, tile look-back status,
+// tile and group lists
+struct SeqSumWs {
+    DBuf<unsigned int> counters;
+    DBuf<unsigned char> status;
+    DBuf<unsigned char> lists;
+    DBuf<int32_t> lens;
+    int64_t tiles = 0;
+};
+
 struct Ctx {
     bool profile = false;
     uint32_t prof_mask = 0xffffffffu;  // families timed while profile is on
@@ -125,7 +135,8 @@ struct Ctx {
     cudaStream_t side = nullptr;  // independent side work (the evolution-SOC ledger count)
     cudaStream_t side2 = nullptr;  // candidate Gauss-Seidel, overlapping the aggregation
     int sms = 148;
-    bool seq = false;  // sequential (reference-order) global reductions
+    cudaStream_t main_s = nullptr;  // the context's own stream (c.s outside StreamScopes)
+    bool seq = true;  // global reductions in the reference's order (seqsum.cu); false: trees
     int64_t launches = 0;
     int64_t syncs = 0;  // host synchronisations of the stream
     int blas_family = kProfBlas1;  // family the BLAS-1 launchers record under
@@ -142,6 +153,7 @@ struct Ctx {
     // (spectral.hpp:32-36); prefixes serve every smaller level.
     DBuf<double> arnoldi_v0;
     size_t arnoldi_v0_n = 0;
+    SeqSumWs ssws[2];  // [0] main stream, [1] any other stream
 };
 
 // block-partial scratch and wavefront tickets of the tree reductions (>= count partials)

@@ -38,12 +38,12 @@ void compact_pattern(Ctx& c, const DCsr& N, const double* vals, int32_t bs, DCsr
 void entry_rows(Ctx& c, const DCsr& A, int32_t* rows);
 
 // ---- BLAS-1 with device-resident scalars (blas.cu) -----------------------------------
-// *out = sum_i x_i y_i.  seq mode: reference order (sparse.hpp:309-313);
-// otherwise a deterministic two-stage tree.
+// *out = sum_i x_i y_i.  seq mode (default): the reference's order (sparse.hpp:309-313),
+// bit for bit; otherwise a deterministic two-stage tree.
 void dot(Ctx& c, const double* x, const double* y, int64_t n, double* out);
 // *out = sqrt(dot(x, x))
 void nrm2(Ctx& c, const double* x, int64_t n, double* out);
-// x += st[2] p, r -= st[2] q, *out = ||r|| in one pass (false in parity mode: not launched)
+// x += st[2] p, r -= st[2] q, *out = ||r|| in one pass
 bool pcg_update_nrm(Ctx& c, const double* st, const int32_t* bad, const double* p, const double* q, double* x,
                     double* r, int64_t n, double* out);
 // y += s * x with s = sign * (*alpha)   (axpy, sparse.hpp:317-319)
@@ -56,6 +56,12 @@ void axpy_dot(Ctx& c, const double* alpha, double sign, const double* x, double*
 void scale_const(Ctx& c, double alpha, double* x, int64_t n);
 // grid of the tree reductions for length n (the cooperative Arnoldi reproduces it)
 unsigned dot_grid(Ctx& c, int64_t n);
+// seqsum.cu: the same sums in the reference's exact order, one launch each
+void seqsum_dot(Ctx& c, const double* x, const double* y, int64_t n, double* out, bool take_sqrt);
+void seqsum_axpy_dot(Ctx& c, const double* alpha, double sign, const double* x, double* y, const double* z, int64_t n,
+                     double* out, bool take_sqrt);
+void seqsum_pcg_update_nrm(Ctx& c, const double* st, const int32_t* bad, const double* p, const double* q, double* x,
+                           double* r, int64_t n, double* out);
 
 // ---- strength / aggregation (strength.cu, aggregate.cu) --------------------------------
 void symmetric_strength(Ctx& c, const DCsr& A, double theta, DCsr& S);

@@ -37,3 +37,10 @@ def gpu():
 def gpu_seq():
     import paper_1610_03154_b200.api as api
     return api.Context(0, sequential_reductions=True)
+
+
+@pytest.fixture(scope="session")
+def gpu_tree():
+    """tree reductions: reproducible, not the reference's summation order"""
+    import paper_1610_03154_b200.api as api
+    return api.Context(0, sequential_reductions=False)

@@ -113,20 +113,20 @@ def test_is_symmetric(gpu, port):
     assert api.is_symmetric(U, ctx=gpu) == port.is_symmetric(U)
 
 
-def test_spectral_radius(gpu_seq, gpu, port):
-    for A in (poisson1d(32), aniso2d(12, 0.1), aniso2d(20, 1.0)):
+def test_spectral_radius(gpu_seq, gpu_tree, port):
+    for A in (poisson1d(32), aniso2d(12, 0.1), aniso2d(20, 1.0), aniso2d(300, 0.01)):
         want = port.spectral_radius_estimate(A)
         assert api.spectral_radius_estimate(A, ctx=gpu_seq) == want
-        assert abs(api.spectral_radius_estimate(A, ctx=gpu) - want) <= 1e-12 * want
+        assert abs(api.spectral_radius_estimate(A, ctx=gpu_tree) - want) <= 1e-12 * want
 
 
-def test_spectral_radius_cooperative_matches_steps(gpu, monkeypatch):
+def test_spectral_radius_cooperative_matches_steps(gpu_tree, monkeypatch):
     """The one-launch cooperative Arnoldi reproduces the launch-per-step path bit for bit
     (same reduction trees), at sizes that use one and several virtual blocks per block."""
     for A in (poisson1d(5), aniso2d(30, 0.1), aniso2d(150, 1.0), aniso2d(800, 0.01)):
-        coop = api.spectral_radius_estimate(A, ctx=gpu)
+        coop = api.spectral_radius_estimate(A, ctx=gpu_tree)
         monkeypatch.setenv("AMGCU_ARNOLDI_STEPS", "1")
-        steps = api.spectral_radius_estimate(A, ctx=gpu)
+        steps = api.spectral_radius_estimate(A, ctx=gpu_tree)
         monkeypatch.delenv("AMGCU_ARNOLDI_STEPS")
         assert coop == steps, (A.n_rows, coop, steps)
 

@@ -161,9 +161,9 @@ def test_work_ledger_options(gpu_seq, port):
 
 
 @pytest.mark.parametrize("name,gen,so,vo", CASES, ids=[c[0] for c in CASES])
-def test_setup_parallel_reductions(gpu, port, name, gen, so, vo):
+def test_setup_parallel_reductions(gpu_tree, port, name, gen, so, vo):
     A, B, Bh, b = gen()
-    hg = api.setup(A, B, so, Bh, ctx=gpu)
+    hg = api.setup(A, B, so, Bh, ctx=gpu_tree)
     ho = port.setup(A, B, so, Bh)
     compare(hg, ho, bitwise=False)
     xg, rg = api.solve(hg, b, None, vo)
