@@ -1,22 +1,30 @@
 #!/usr/bin/env python3
 """RN-AMG setup + solve benchmark (BASELINE.json metric) on B200.
 
-Workload (BASELINE.json configs[1], the metric's config): 2D rotated
-anisotropic diffusion, bilinear Q1 on a 1024 x 1024 element grid (1,046,529
-DOFs, 9,406,489 nnz), eps = 1e-3, psi = pi/8, evolution SOC (drop 4.0),
-degree-2 pattern with prefilter theta = 0.1, 6 energy-min CG iterations,
-V(1,1) weighted Jacobi (omega = 4/(3 rho)), PCG to 1e-8 relative residual.
-Synthetic input generated by the config generator (seeded b, seed 1).
+Workload (default --config 5, the largest BASELINE config: 37.8 M nonzeros): 2D plane-
+strain linear elasticity, bilinear Q1 on a 1024 x 1024 element grid, 2 DOFs per node
+(2,099,200 DOFs), E = 1, nu = 0.3, left edge clamped; near-nullspace B = 3 rigid-body
+modes; node-wise block SOC theta = 0.1, 2x2-block aggregation, 4 energy-min CG
+iterations with the 3-column constraint projection, V(1,1) weighted Jacobi, PCG to
+1e-8 relative residual.  Synthetic input from the config generator (b seeded, seed 3).
+--config 1..4 selects the other BASELINE configs.
 
-One step = rn_setup + solve of that problem.  `value` is the device time of a
-step with A, B and b already resident in HBM (CUDA events on the library
-stream, L2 flushed before every step); `e2e` is the same step through the
-public C ABI with pinned host buffers (host->device copies of A, B, b and the
-device->host read of x inside the timed region).
+One step = rn_setup + solve of that problem.  `value` is the device time of a step
+with A, B and b already resident in HBM (CUDA events on the library stream, L2
+flushed before every step); `e2e` is the same step through the public C ABI with
+pinned host buffers (host->device copies of A, B, b and the device->host read of x
+inside the timed region).  Every global sum is the reference's left-to-right chain
+bit for bit (the default context mode), so the hierarchy, the iteration count and the
+residual history are the reference's.
 
 --impl reference times the reference's own CPU implementation of the path
-(oracle/_ref: the reference headers compiled unmodified against the Eigen
-stand-in) on the box's host cores on the same workload.
+(oracle/_ref: the reference headers compiled unmodified against the Eigen stand-in)
+on the box's host, on inputs from oracle/build/libconfiggen.so (libamgcu.so is not
+loaded).  One reference setup+solve at full size takes minutes (its injection scans
+every node per aggregate), so each step is a bounded sample -- the same config on a
+smaller grid -- and `value` scales the sample's seconds by the DOFs ratio (a lower
+bound on the reference's full-size time).  The GPU arm's cpu_baseline samples the
+own-code restatement (oracle/rnamg_port.cpp) the same way.
 
 Multi-GPU (--gpus N under torchrun): replicas only -- every rank solves its
 own copy of the problem, no data-path collective;
@@ -50,10 +58,12 @@ def parse():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--size", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--max-restarts", type=int, default=50)
+    ap.add_argument("--cpu-budget", type=float, default=float(os.environ.get("AMG_CPU_BUDGET_S", "200")),
+                    help="seconds of CPU work the reference arm / cpu_baseline sample may take")
     return ap.parse_args()
 
 
@@ -143,11 +153,11 @@ class ClockSampler:
 
 
 def oracle_run(kind, config, size, max_restarts):
-    """CPU run of one setup + solve (kind 'port' or 'ref'); returns (setup_s, solve_s, iterations, converged)."""
-    import paper_1610_03154_b200.api as api
-    from oracle.pyoracle import Oracle
-    A, B, Bh, b = api.generate_config(config, size)
-    so, vo = api.config_options(config)
+    """CPU run of one setup + solve (kind 'port' or 'ref') on inputs from the oracle-side
+    generator library (no libamgcu.so); returns (setup_s, solve_s, iterations, converged, levels)."""
+    from oracle.pyoracle import Oracle, config_options, generate_config
+    A, B, Bh, b = generate_config(config, size)
+    so, vo = config_options(config)
     o = Oracle(kind)
     t0 = time.perf_counter()
     h = o.setup(A, B, so, Bh)
@@ -163,8 +173,53 @@ def oracle_run(kind, config, size, max_restarts):
     return t1 - t0, t2 - t1, its, bool(rep.converged), h.n_levels()
 
 
+def dofs(config, size):
+    """unknowns of config `config` at grid size `size` (problems.cpp)"""
+    if config == 1:
+        return size * size
+    if config == 2:
+        return (size - 1) * (size - 1)
+    if config == 5:
+        return 2 * size * (size + 1)
+    return size * size
+
+
+SAMPLE_SIZES = {1: (256, 192, 128, 96), 2: (512, 384, 256, 128), 3: (512, 384, 256, 128),
+                4: (512, 384, 256, 128), 5: (512, 384, 256, 128)}
+
+
+def cpu_sample(kind, config, size, runs, budget_s, max_restarts):
+    """Bounded CPU sample of the workload: the same config on a smaller grid, sized so
+    `runs` setup+solves fit in budget_s.  A calibration run at the smallest candidate
+    grid (untimed; it also loads the library) predicts the others with a super-linear
+    model (t ~ n^1.7, the reference's measured C5 growth from 256^2 to 512^2).
+    Returns (sample_size, calibration_s)."""
+    cands = [s for s in SAMPLE_SIZES[config] if s <= size] or [size]
+    base = cands[-1]
+    r = oracle_run(kind, config, base, max_restarts)
+    t_base = r[0] + r[1]
+    for s in cands:
+        est = t_base * (dofs(config, s) / dofs(config, base)) ** 1.7
+        if runs * est <= budget_s or s == base:
+            return s, t_base
+    return base, t_base
+
+
+def scaled_value(t_sample, config, size, sample):
+    """seconds of the full workload from a sample: t x (DOFs ratio) -- linear scaling, a
+    lower bound for the reference (its injection scan grows with n_agg x n)"""
+    return t_sample * dofs(config, size) / dofs(config, sample)
+
+
+def config_dict(config, size, n, nnz):
+    """the workload description both arms print (identical dicts)"""
+    return {"workload": CONFIG_NAMES[config], "config": config, "size": size, "n": n, "nnz": nnz,
+            "l2": "GPU arm: flushed (256 MB write) before every step"}
+
+
 def run_reference(args, ws, rank):
-    """--impl reference: the reference's CPU implementation, rank 0 only."""
+    """--impl reference: the reference's CPU implementation (oracle/_ref: the reference
+    headers compiled unmodified), rank 0 only, inputs from oracle/build/libconfiggen.so."""
     if rank != 0:
         return
     from oracle.pyoracle import available
@@ -176,36 +231,36 @@ def run_reference(args, ws, rank):
     else:
         kind = "ref"
         why = None
-    # the reference is single-threaded; independent steps run as concurrent
-    # processes on the host's cores so the run ends in a few step-times
-    import multiprocessing as mp
-    cores = os.cpu_count() or 1
-    ctx = mp.get_context("spawn")
+    from oracle.pyoracle import generate_config
+    A_full = generate_config(config, size)[0]  # the workload's shape, for the config dict
+    n_full, nnz_full = A_full.n_rows, A_full.nnz()
+    del A_full
     t0 = time.perf_counter()
-    # warm-ups load the library and touch the code paths on a small instance of the same
-    # config; the timed steps are the full workload (one reference setup at full size is
-    # minutes of single-threaded CPU: its injection scans all nodes per aggregate)
-    warm_size = min(size, 64)
-    jobs = [(kind, config, warm_size, args.max_restarts)] * args.warmup + \
-           [(kind, config, size, args.max_restarts)] * max(1, args.steps)
-    with ctx.Pool(max(1, min(len(jobs), cores))) as pool:
-        res = pool.starmap(oracle_run, jobs)
+    runs = args.warmup + max(1, args.steps)
+    sample, t_cal = cpu_sample(kind, config, size, runs, args.cpu_budget, args.max_restarts)
+    for _ in range(args.warmup):
+        oracle_run(kind, config, sample, args.max_restarts)
+    timed = [oracle_run(kind, config, sample, args.max_restarts) for _ in range(max(1, args.steps))]
     wall = time.perf_counter() - t0
-    timed = res[args.warmup:]
     per_step = [r[0] + r[1] for r in timed]
-    v = sum(per_step) / len(per_step)
+    t_s = sum(per_step) / len(per_step)
+    v = scaled_value(t_s, config, size, sample)
     line = {
-        "impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": 0, "steps": args.steps,
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (config generator, seeded)",
-        "config": {"workload": CONFIG_NAMES[config], "config": config, "size": size,
+        "config": config_dict(config, size, n_full, nnz_full),
+        "result": {"sample_size": sample, "sample_s": t_s,
                    "setup_s": sum(r[0] for r in timed) / len(timed), "solve_s": sum(r[1] for r in timed) / len(timed),
                    "iterations": timed[0][2], "converged": timed[0][3], "levels": timed[0][4]},
         "cpu_baseline": {"value": v, "unit": "s", "cores": 1, "kind": "reference" if kind == "ref" else "port",
-                         "sample": f"full workload per timed step (one setup+solve each, single-threaded); "
-                                   f"{len(timed)} timed steps + {args.warmup} warm-ups at {warm_size}^2 run as "
-                                   f"concurrent processes, wall {wall:.1f}s",
-                         "host_cores": cores},
+                         "sample": f"config {config} at {sample}^2 ({dofs(config, sample)} DOFs), one setup+solve "
+                                   f"per step, single thread (the reference is single-threaded); value = sample "
+                                   f"seconds x DOFs ratio {dofs(config, size) / dofs(config, sample):.3f} (linear "
+                                   f"scaling: a lower bound, the reference's injection scan grows as n_agg x n); "
+                                   f"{args.warmup} warm-ups + {len(timed)} timed steps at the sample size, "
+                                   f"calibration {t_cal:.1f}s, wall {wall:.1f}s",
+                         "host_cores": os.cpu_count()},
         "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     if why:
@@ -392,10 +447,9 @@ def run_ours(args, ws, rank, local):
         "metric": METRIC, "value": mean_ms / 1e3, "unit": "s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": mean_ms, "higher_is_better": False, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (config generator, seeded b)",
-        "config": {"workload": CONFIG_NAMES[config], "config": config, "size": size, "n": n, "nnz": nnz,
-                   "iterations": its, "converged": conv, "levels": levels,
-                   "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
-                   "l2": "flushed (256 MB write) before every step"},
+        "config": config_dict(config, size, n, nnz),
+        "result": {"iterations": its, "converged": conv, "levels": levels,
+                   "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU"},
         "e2e": {"value": e2e_mean / 1e3, "unit": "s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": int(round(launches)),
         "roofline": roofline,
@@ -410,12 +464,16 @@ def run_ours(args, ws, rank, local):
     }
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         try:
-            ts, tv, cits, cconv, clev = oracle_run("port", config, size, args.max_restarts)
-            line["cpu_baseline"] = {"value": ts + tv, "unit": "s", "cores": 1, "kind": "port",
-                                    "sample": "full workload, one setup+solve of the CPU restatement "
-                                              "(oracle/rnamg_port.cpp, single thread)",
-                                    "setup_s": ts, "solve_s": tv, "iterations": cits, "converged": cconv}
-            line["config"]["iterations_cpu"] = cits
+            sample, t_cal = cpu_sample("port", config, size, 1, args.cpu_budget / 8, args.max_restarts)
+            ts, tv, cits, cconv, clev = oracle_run("port", config, sample, args.max_restarts)
+            line["cpu_baseline"] = {"value": scaled_value(ts + tv, config, size, sample), "unit": "s", "cores": 1,
+                                    "kind": "port",
+                                    "sample": f"config {config} at {sample}^2 ({dofs(config, sample)} DOFs): one "
+                                              f"setup+solve of the CPU restatement (oracle/rnamg_port.cpp, single "
+                                              f"thread) in {ts + tv:.2f}s, scaled by the DOFs ratio "
+                                              f"{dofs(config, size) / dofs(config, sample):.3f}",
+                                    "sample_setup_s": ts, "sample_solve_s": tv, "sample_iterations": cits,
+                                    "sample_converged": cconv}
         except Exception as e:  # the GPU number stands on its own
             line["cpu_baseline"] = {"value": None, "unit": "s", "cores": 1, "kind": "port", "sample": f"failed: {e}"}
     if rank == 0:

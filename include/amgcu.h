@@ -125,11 +125,15 @@ amgcu_status amgcu_ctx_destroy(amgcu_ctx ctx);
 /* Message of the last failed call on this context (or of the last failed
  * amgcu_ctx_create when ctx is NULL). */
 const char* amgcu_last_error(amgcu_ctx ctx);
-/* 1: every global reduction (dots, norms, Arnoldi) runs in index order on one
- * warp, reproducing the reference's sequential sums bit for bit (parity-debug
- * mode, SURVEY.md §7 hard part 1).  0 (default): deterministic parallel
- * two-stage reductions. */
+/* 1 (default): every global reduction (dots, norms, the Arnoldi Gram-Schmidt, the
+ * energy-min and Krylov scalars) is the reference's left-to-right sum from +0.0,
+ * bit for bit (sparse.hpp:309-313), evaluated in parallel by csrc/seqsum.cu.
+ * 0: deterministic parallel two-stage trees (reproducible, not the reference's bits). */
 amgcu_status amgcu_ctx_set_sequential_reductions(amgcu_ctx ctx, int on);
+/* 1 (default): forward Gauss-Seidel candidate improvement runs on a second stream,
+ * overlapping the level's strength / aggregation / pattern work; 0: in order.  The
+ * result is bitwise the same either way. */
+amgcu_status amgcu_ctx_set_candidate_overlap(amgcu_ctx ctx, int on);
 /* Synchronise the context stream; returns the accumulated device time of the
  * kernels launched since the last reset (CUDA events on the context stream). */
 amgcu_status amgcu_ctx_synchronize(amgcu_ctx ctx);

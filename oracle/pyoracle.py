@@ -12,7 +12,8 @@ import os
 
 import numpy as np
 
-from paper_1610_03154_b200._abi import (CsrC, SolveReportC, f64p, i32p, as_f64, as_i32, ptr_f64, ptr_i32)
+from paper_1610_03154_b200._abi import (CsrC, SetupOptionsC, SolveOptionsC, SolveReportC, f64p, i32p, as_f64, as_i32,
+                                        ptr_f64, ptr_i32)
 from paper_1610_03154_b200.types import (CandidateSet, Level, SetupOptions, SolveOptions, SolveReport, SparseMatrix,
                                          StrengthConfig, raise_for)
 
@@ -23,6 +24,58 @@ LIBS = {
 }
 
 _cache = {}
+GEN_LIB = os.path.join(HERE, "build", "libconfiggen.so")
+
+
+def _gen():
+    if GEN_LIB not in _cache:
+        if not os.path.exists(GEN_LIB):
+            raise FileNotFoundError(f"{GEN_LIB} not built (run __graft_entry__.build())")
+        lib = C.CDLL(GEN_LIB)
+        lib.gen_last_error.restype = C.c_char_p
+        lib.gen_generate_config.argtypes = [C.c_int32, C.c_int32, C.POINTER(CsrC), C.POINTER(C.c_int32),
+                                            C.POINTER(f64p), C.POINTER(C.c_int32), C.POINTER(f64p), C.POINTER(f64p)]
+        lib.gen_config_options.argtypes = [C.c_int32, C.POINTER(SetupOptionsC), C.POINTER(SolveOptionsC)]
+        lib.gen_free.argtypes = [C.c_void_p]
+        _cache[GEN_LIB] = lib
+    return _cache[GEN_LIB]
+
+
+def generate_config(config: int, n: int):
+    """BASELINE config `config` at size n from oracle/build/libconfiggen.so (the product's
+    generators compiled for the CPU alone): (A, B, Bhat or None, b), the same bytes as
+    paper_1610_03154_b200.api.generate_config without loading libamgcu.so."""
+    lib = _gen()
+    A = CsrC()
+    k, hl = C.c_int32(), C.c_int32()
+    B, Bh, b = f64p(), f64p(), f64p()
+    code = lib.gen_generate_config(config, n, C.byref(A), C.byref(k), C.byref(B), C.byref(hl), C.byref(Bh), C.byref(b))
+    if code != 0:
+        raise_for(code, lib.gen_last_error().decode())
+    M = SparseMatrix.from_c(A)
+    for p in (A.row_offsets, A.col_indices, A.values):
+        lib.gen_free(C.cast(p, C.c_void_p))
+    nn = M.n_rows
+
+    def take(p, count):
+        a = np.ctypeslib.as_array(p, shape=(count,)).copy()
+        lib.gen_free(C.cast(p, C.c_void_p))
+        return a
+
+    Bd = take(B, nn * k.value)
+    Bhd = take(Bh, nn * k.value) if hl.value else None
+    bd = take(b, nn)
+    return M, CandidateSet(nn, k.value, Bd), (CandidateSet(nn, k.value, Bhd) if Bhd is not None else None), bd
+
+
+def config_options(config: int):
+    """(SetupOptions, SolveOptions) of BASELINE config `config` (libconfiggen.so)"""
+    so, vo = SetupOptionsC(), SolveOptionsC()
+    lib = _gen()
+    code = lib.gen_config_options(config, C.byref(so), C.byref(vo))
+    if code != 0:
+        raise_for(code, lib.gen_last_error().decode())
+    return SetupOptions.from_c(so), SolveOptions(vo.method, vo.cycle, vo.tol, vo.max_iters)
 
 
 def available(kind: str) -> bool:

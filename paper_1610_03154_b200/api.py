@@ -24,7 +24,8 @@ lib = C.CDLL(_LIB_PATH)
 
 lib.amgcu_last_error.restype = C.c_char_p
 lib.amgcu_last_error.argtypes = [C.c_void_p]
-for _name in ("amgcu_ctx_create", "amgcu_ctx_destroy", "amgcu_ctx_set_sequential_reductions", "amgcu_ctx_synchronize",
+for _name in ("amgcu_ctx_create", "amgcu_ctx_destroy", "amgcu_ctx_set_sequential_reductions",
+              "amgcu_ctx_set_candidate_overlap", "amgcu_ctx_synchronize",
               "amgcu_ctx_launch_count", "amgcu_ctx_sync_count", "amgcu_setup", "amgcu_setup_device", "amgcu_hier_destroy",
               "amgcu_hier_levels", "amgcu_hier_get_matrix", "amgcu_hier_get_candidates", "amgcu_hier_level_symmetric",
               "amgcu_hier_relax_weights", "amgcu_hier_complexity", "amgcu_hier_ledger", "amgcu_solve", "amgcu_solve_device", "amgcu_cycle",
@@ -36,6 +37,7 @@ for _name in ("amgcu_ctx_create", "amgcu_ctx_destroy", "amgcu_ctx_set_sequential
 lib.amgcu_ctx_create.argtypes = [C.c_int, C.POINTER(C.c_void_p)]
 lib.amgcu_ctx_destroy.argtypes = [C.c_void_p]
 lib.amgcu_ctx_set_sequential_reductions.argtypes = [C.c_void_p, C.c_int]
+lib.amgcu_ctx_set_candidate_overlap.argtypes = [C.c_void_p, C.c_int]
 lib.amgcu_ctx_synchronize.argtypes = [C.c_void_p]
 lib.amgcu_ctx_launch_count.argtypes = [C.c_void_p, C.POINTER(C.c_int64)]
 lib.amgcu_ctx_sync_count.argtypes = [C.c_void_p, C.POINTER(C.c_int64)]
@@ -108,6 +110,10 @@ class Context:
 
     def set_sequential_reductions(self, on: bool):
         self._chk(lib.amgcu_ctx_set_sequential_reductions(self.handle, 1 if on else 0))
+
+    def set_candidate_overlap(self, on: bool):
+        """forward-GS candidate improvement on a second stream beside the aggregation (default on)"""
+        self._chk(lib.amgcu_ctx_set_candidate_overlap(self.handle, 1 if on else 0))
 
     def synchronize(self):
         self._chk(lib.amgcu_ctx_synchronize(self.handle))

@@ -103,6 +103,17 @@ def build_oracle(force=False):
         os.replace(out + ".tmp", out)
         with open(stamp, "w") as f:
             f.write(key)
+    # the config generators as a CPU library of their own (the reference arm's inputs)
+    gen = os.path.join(odir, "build", "libconfiggen.so")
+    gsrcs = [os.path.join(odir, "config_gen.cpp"), os.path.join(CSRC, "problems.cpp"),
+             os.path.join(CSRC, "host_common.h"), os.path.join(ROOT, "include", "amgcu.h")]
+    gstamp = gen + ".stamp"
+    gkey = _digest(gsrcs)
+    if force or not os.path.exists(gen) or not os.path.exists(gstamp) or open(gstamp).read() != gkey:
+        _run(["g++"] + CXX_FLAGS + ["-shared", gsrcs[0], gsrcs[1], "-o", gen + ".tmp"])
+        os.replace(gen + ".tmp", gen)
+        with open(gstamp, "w") as f:
+            f.write(gkey)
     ref_root = os.environ.get("AMG_REFERENCE_ROOT", "/root/reference")
     ref_so = os.path.join(odir, "_ref", "libamgref.so")
     if os.path.isdir(os.path.join(ref_root, "proj", "include", "amg")):

@@ -178,6 +178,10 @@ amgcu_status amgcu_ctx_set_sequential_reductions(amgcu_ctx ctx, int on) {
     return guarded(ctx, [&] { ctx->c.seq = on != 0; });
 }
 
+amgcu_status amgcu_ctx_set_candidate_overlap(amgcu_ctx ctx, int on) {
+    return guarded(ctx, [&] { ctx->c.cand_overlap = on != 0; });
+}
+
 amgcu_status amgcu_ctx_synchronize(amgcu_ctx ctx) {
     return guarded(ctx, [&] { sync(ctx->c); });
 }

@@ -137,6 +137,7 @@ struct Ctx {
     int sms = 148;
     cudaStream_t main_s = nullptr;  // the context's own stream (c.s outside StreamScopes)
     bool seq = true;  // global reductions in the reference's order (seqsum.cu); false: trees
+    bool cand_overlap = true;  // candidate Gauss-Seidel on side2, beside the aggregation (setup.cu)
     int64_t launches = 0;
     int64_t syncs = 0;  // host synchronisations of the stream
     int blas_family = kProfBlas1;  // family the BLAS-1 launchers record under

@@ -27,9 +27,15 @@
 //     published when the record was built) by relaxed global loads.
 // Every row sum runs in the reference's order (acc -= a * x, product rounded first, no
 // FMA), so the result is bit-identical to the CPU sweep.  Values are published in
-// per-sweep buffers pre-filled with kPending.  All CTAs are resident (the launcher
-// checks), and every row depends only on rows earlier in (sweep, position) order, so
-// the launch cannot deadlock: the earliest unfinished row always has its values.
+// per-sweep buffers pre-filled with kPending.  A CTA takes its block of 32 segments from
+// a ticket when it starts.  A row of sweep s reads rows earlier in (sweep, position)
+// order: sweep s values of its own or earlier CTAs, and sweep s - 1 values of any CTA.
+// Alone on the device every CTA is resident (the launcher keeps nctas <= SMs), so the
+// earliest unfinished row always progresses.  On the second stream (candidate sweeps
+// beside the aggregation, setup.cu) some CTAs may wait for SMs held by main-stream
+// kernels; those kernels depend on nothing the sweeps hold (the main stream joins the
+// sweeps only through an event, which holds no SM), so they finish, the SMs free up,
+// every CTA becomes resident, and the same argument applies.
 
 constexpr int kLnLanes = 32;  // segments per CTA
 constexpr int kLnRb = 8;      // rows per record block

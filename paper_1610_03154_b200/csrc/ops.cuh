@@ -29,6 +29,8 @@ void filter_matrix(Ctx& c, const DCsr& G, bool theta_set, double theta, int32_t 
 bool is_symmetric(Ctx& c, const DCsr& A, double tol);
 // dinv[i] = 1 / A(i,i); throws RuntimeError(prefix + row) for the lowest zero diagonal
 void inverse_diagonal(Ctx& c, const DCsr& A, double* dinv, const char* prefix);
+// the same without the throw: the first zero-diagonal row, or -1
+int32_t inverse_diagonal_check(Ctx& c, const DCsr& A, double* dinv);
 void diagonal(Ctx& c, const DCsr& A, double* d);
 // max_i |v_i| (exact)
 double max_abs(Ctx& c, const double* v, int64_t n);
@@ -107,6 +109,8 @@ double spectral_radius(Ctx& c, const DCsr& A, int steps, const double* dinv, int
 // The lane-per-segment Gauss-Seidel kernel (gs_lanes.cuh) for forward sweeps: its plan
 // for a matrix (segments, longest row; host synchronisations) and one column's sweeps
 // (no host synchronisation: may run on another stream than the plan's)
+constexpr int kGsMaxColumns = 8;  // candidate columns one Gauss-Seidel launch relaxes
+
 struct LanePlan {
     bool ok = false;
     int32_t nf = 0, longest_row = 0;

@@ -18,7 +18,7 @@ namespace amgcu {
 
 namespace {
 
-constexpr int kMaxK = 8;
+constexpr int kMaxK = kGsMaxColumns;
 
 // Gauss-Seidel sweeps, segment-parallel.
 //

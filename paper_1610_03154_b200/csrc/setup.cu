@@ -128,7 +128,9 @@ void postfilter(Ctx& c, const amgcu_setup_options& o, const DCsr& A, const DCsr&
 // stream: it depends on A and B only, so its sweeps (lane kernel, latency-bound, 32 SMs
 // per 1024 segments) overlap the strength / aggregation / pattern work of the level.
 // start: host synchronisations (zero-diagonal check, lane plan) on the main stream, then
-// the sweeps on side2; join: the main stream waits for them, then normalizes.
+// the sweeps on side2; join: the main stream waits for them, then normalizes.  The sweeps
+// are the same kernels as the in-order path (no reductions), so the result is bitwise the
+// same with the overlap on or off (Ctx::cand_overlap, tests/test_gpu_config_scale.py).
 struct CandidateSweeps {
     bool active = false;
     cudaStream_t main = nullptr;
@@ -146,30 +148,33 @@ struct CandidateSweeps {
 };
 
 bool candidate_sweeps_start(Ctx& c, const DCsr& A, double* B, int32_t k, int sweeps, int scheme, CandidateSweeps& cs) {
-    if (scheme != 1 || sweeps <= 0 || !c.side2 || c.seq || A.nr != A.nc) return false;
-    static const bool off = [] {
-        const char* e = std::getenv("AMGCU_CAND_OVERLAP");
-        return e && e[0] == '0';
-    }();
-    if (off) return false;
+    if (scheme != 1 || sweeps <= 0 || !c.side2 || !c.cand_overlap || A.nr != A.nc || k > kGsMaxColumns) return false;
     const int32_t n = A.nr;
     cs.dinv.alloc(static_cast<size_t>(n), c.s);
-    inverse_diagonal(c, A, cs.dinv.get(), "relax: zero diagonal at row ");
+    // a zero diagonal is reported where the reference meets it (improve_candidates runs
+    // after the stagnation check, hierarchy.hpp:191-208): leave it to the in-order path
+    if (inverse_diagonal_check(c, A, cs.dinv.get()) >= 0) return false;
     cs.plan = lane_plan(c, A, sweeps);
     if (!cs.plan.ok) return false;
+    // the done event exists before anything is queued on side2, and is recorded however
+    // the queueing ends, so the destructor's wait always covers every queued sweep
+    AMG_CK(cudaEventCreateWithFlags(&cs.done, cudaEventDisableTiming));
+    cs.main = c.s;
     cudaEvent_t ready;
     AMG_CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
-    AMG_CK(cudaEventRecord(ready, c.s));
-    AMG_CK(cudaStreamWaitEvent(c.side2, ready, 0));
+    cudaError_t e = cudaEventRecord(ready, c.s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(c.side2, ready, 0);
     cudaEventDestroy(ready);
-    {
+    AMG_CK(e);
+    try {
         StreamScope on_side(c, c.side2);
         for (int32_t j = 0; j < k; ++j)
             gs_lanes_run(c, A, cs.plan, cs.dinv.get(), B + static_cast<size_t>(j) * n, nullptr, sweeps);
+    } catch (...) {
+        cudaEventRecord(cs.done, c.side2);
+        throw;
     }
-    AMG_CK(cudaEventCreateWithFlags(&cs.done, cudaEventDisableTiming));
     AMG_CK(cudaEventRecord(cs.done, c.side2));
-    cs.main = c.s;
     cs.active = true;
     return true;
 }

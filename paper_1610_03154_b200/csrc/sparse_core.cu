@@ -1072,12 +1072,17 @@ bool is_symmetric(Ctx& c, const DCsr& A, double tol) {
 }
 
 void inverse_diagonal(Ctx& c, const DCsr& A, double* dinv, const char* prefix) {
+    const int32_t b = inverse_diagonal_check(c, A, dinv);
+    if (b >= 0) throw RuntimeError(std::string(prefix) + std::to_string(b));
+}
+
+int32_t inverse_diagonal_check(Ctx& c, const DCsr& A, double* dinv) {
     const int32_t n = std::min(A.nr, A.nc);
     DBuf<int32_t> bad(1, c.s);
     fill_i32(c, bad.get(), INT_MAX, 1);
     launch(c, k_diag, blocks_for(n, 256), 256, 0, n, A.rp.get(), A.ci.get(), A.va.get(), dinv, true, bad.get());
     const int32_t b = read_scalar(c, bad.get());
-    if (b != INT_MAX) throw RuntimeError(std::string(prefix) + std::to_string(b));
+    return b == INT_MAX ? -1 : b;
 }
 
 void diagonal(Ctx& c, const DCsr& A, double* d) {

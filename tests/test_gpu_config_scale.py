@@ -1,15 +1,13 @@
-"""Config-scale GPU parity against the CPU restatement (BASELINE.json configs).
+"""Config-scale GPU parity against the CPU restatement (BASELINE.json configs) at the
+BASELINE sizes, in the mode bench.py measures (the default context: every global sum
+is the reference's left-to-right chain, csrc/seqsum.cu).
 
-Parity mode (sequential reductions, the reference's summation order): every
-level's A, P, R and B must be bit-identical and the solve must take the same
-number of iterations with residual histories within 1e-10.
-
-Production mode (deterministic parallel reductions): the integer structure
-(every level's row offsets and column indices, the number of levels) and the
-iteration count must be identical; values agree to 1e-10 on the fine levels.
-The remaining difference is the reference's own sequential-sum rounding in
-its dot products (about sqrt(n) eps per dot), amplified by the energy-min CG
-on the coarse levels; it is reported, not hidden.
+Every level's A, P, R and B must be bit-identical (hence the aggregates, roots, SOC and
+patterns behind them), the symmetry branch of every level the same, and the solve must
+take the same number of iterations with residual histories and x within 1e-10.  The
+coarsest-level solve is the one place the GPU differs by design (an explicit inverse
+instead of the reference's per-cycle COD solve), so the solve-phase numbers are
+compared to 1e-10, not bitwise.
 """
 import numpy as np
 import pytest
@@ -49,19 +47,40 @@ def _bitwise_hierarchy(hg, ho):
         assert hg.symmetric(l) == ho.symmetric(l)
 
 
-@pytest.mark.parametrize("cfg,size,restarts", [(1, 96, 0), (2, 1024, 0), (3, 512, 2), (4, 512, 2), (5, 1024, 0)],
-                         ids=["C1-96", "C2-full", "C3-512", "C4-512", "C5-full"])
-def test_parity_mode_bitwise(gpu_seq, port, cfg, size, restarts):
-    hg, ho, b, vo = _setup_both(cfg, size, gpu_seq, port)
+FULL = [(1, 256, 0), (2, 1024, 0), (3, 2048, 2), (4, 2048, 3), (5, 1024, 0)]
+FULL_IDS = ["C1-256", "C2-1024", "C3-2048", "C4-2048", "C5-1024"]
+
+
+@pytest.mark.parametrize("cfg,size,restarts", FULL + [(1, 96, 0), (3, 512, 2), (4, 512, 2)],
+                         ids=FULL_IDS + ["C1-96", "C3-512", "C4-512"])
+def test_default_mode_bitwise(gpu, port, cfg, size, restarts):
+    hg, ho, b, vo = _setup_both(cfg, size, gpu, port)
     _bitwise_hierarchy(hg, ho)
     xg, rg, xo, ro = _solve_both(hg, ho, b, vo, port, restarts)
     assert rg.iterations == ro.iterations and rg.converged == ro.converged
     assert rel_max_err(rg.residual_history, ro.residual_history) <= 1e-10
+    assert rel_max_err(xg, xo) <= 1e-10
 
 
-def test_production_mode_c2_full(gpu, port):
-    """the bench workload: structure identical at every level, iterations identical"""
-    hg, ho, b, vo = _setup_both(2, 1024, gpu, port)
+@pytest.mark.parametrize("cfg,size", [(2, 1024), (5, 1024)], ids=["C2-1024", "C5-1024"])
+def test_candidate_overlap_bitwise(cfg, size):
+    """forward-GS candidate improvement on the second stream (beside the aggregation) and
+    in order give the same bits: same kernels, only the scheduling differs"""
+    A, B, Bh, b = api.generate_config(cfg, size)
+    so, vo = api.config_options(cfg)
+    hs = []
+    for overlap in (True, False):
+        ctx = api.Context(0)
+        ctx.set_candidate_overlap(overlap)
+        hs.append((ctx, api.setup(A, B, so, Bh, ctx=ctx)))
+    (c1, h1), (c2, h2) = hs
+    _bitwise_hierarchy(h1, h2)
+
+
+def test_tree_mode_structure_c2(gpu_tree, port):
+    """tree reductions (not the reference's summation order): C2's structure and
+    iteration count still match; values agree to 1e-10 on the fine levels"""
+    hg, ho, b, vo = _setup_both(2, 1024, gpu_tree, port)
     assert hg.n_levels() == ho.n_levels()
     for l in range(hg.n_levels()):
         for which in ((0, 1, 2) if l + 1 < hg.n_levels() else (0,)):
@@ -71,4 +90,3 @@ def test_production_mode_c2_full(gpu, port):
                 assert rel_max_err(g.values, o.values) <= 1e-10, (l, which)
     xg, rg, xo, ro = _solve_both(hg, ho, b, vo, port)
     assert rg.iterations == ro.iterations and rg.converged and ro.converged
-    assert rel_max_err(xg, xo) <= 1e-6
