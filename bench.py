@@ -61,6 +61,8 @@ def parse():
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--size", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--family-timing", type=int, default=1,
+                    help="1: CUDA events around the dominant kernel family's launches in the timed region")
     ap.add_argument("--max-restarts", type=int, default=50)
     ap.add_argument("--cpu-budget", type=float, default=float(os.environ.get("AMG_CPU_BUDGET_S", "200")),
                     help="seconds of CPU work the reference arm / cpu_baseline sample may take")
@@ -383,6 +385,8 @@ def run_ours(args, ws, rank, local):
     # "other" (untagged launches) and families without an algorithmic byte model are not kernels to roof
     kernel_fams = [f for f in fams if f[4] > 0 and f[2] != "other"]
     lib.amgcu_ctx_set_profile_mask(ctx.handle, C.c_uint32(1 << kernel_fams[0][1]))
+    if not args.family_timing:
+        lib.amgcu_ctx_set_profiling(ctx.handle, 0)
 
     # timed region: device-resident inputs
     sampler = ClockSampler(local)

@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(kLnThreads, 1)
                const double* __restrict__ va, const double* __restrict__ inv_diag, const double* __restrict__ b,
                int nsw, const int32_t* __restrict__ segs, int32_t nseg, double* __restrict__ X,
                unsigned int* __restrict__ ticket, unsigned long long* __restrict__ stats, unsigned poll_ns,
-               unsigned pf_ns) {
+               unsigned pf_ns, int32_t ncol, size_t xcol_stride) {
     extern __shared__ unsigned long long ln_smem[];
     using Rec = LnRec<T, BLK, SLOTS, RING>;
     Rec& R = *reinterpret_cast<Rec*>(ln_smem);
@@ -127,11 +127,20 @@ __global__ void __launch_bounds__(kLnThreads, 1)
     constexpr int kLnRing = Rec::kLnRing;
     // prefetch: a row's entries (and then their published values) loaded in batches of
     constexpr int kPfChunk = 8;
-    __shared__ unsigned int blk;
+    __shared__ unsigned int blk, colv;
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    if (threadIdx.x == 0) blk = atomicAdd(ticket, 1u);
+    // tickets interleave the columns (independent sweeps of the same matrix): ticket t is
+    // block t / ncol of column t % ncol, so a block's predecessor in its column always
+    // holds a smaller ticket
+    if (threadIdx.x == 0) {
+        const unsigned t = atomicAdd(ticket, 1u);
+        blk = t / static_cast<unsigned>(ncol);
+        colv = t % static_cast<unsigned>(ncol);
+    }
     __syncthreads();
+    X += static_cast<size_t>(colv) * xcol_stride;
+    if (b) b += static_cast<size_t>(colv) * static_cast<size_t>(n);
     const int32_t g0 = static_cast<int32_t>(blk) * kLnLanes;
     for (int e = threadIdx.x; e < (kLnLanes + 2) * kLnRing; e += blockDim.x) {
         R.ring[e / kLnRing][e % kLnRing].v = kPending;

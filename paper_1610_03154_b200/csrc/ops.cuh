@@ -117,8 +117,9 @@ struct LanePlan {
     DBuf<int32_t> segf;
 };
 LanePlan lane_plan(Ctx& c, const DCsr& A, int nsw);
+// forward sweeps of the k columns of x (n x k column-major; b likewise, or null)
 void gs_lanes_run(Ctx& c, const DCsr& A, const LanePlan& pl, const double* inv_diag, double* x, const double* b,
-                  int nsw);
+                  int nsw, int32_t k);
 
 void gauss_seidel(Ctx& c, const DCsr& A, const double* inv_diag, double* x, const double* b, int k, int sweeps,
                   bool symmetric_sweep);

@@ -872,50 +872,63 @@ LanePlan lane_plan(Ctx& c, const DCsr& A, int nsw) {
     return pl;
 }
 
-// Forward sweeps of one column by the lane-per-segment kernel (gs_lanes.cuh).
+// Forward sweeps of k columns (n x k column-major x, b) by the lane-per-segment kernel
+// (gs_lanes.cuh).  The columns are independent sweeps of the same matrix (the reference
+// relaxes each candidate column in turn, interpolation.hpp:91); one launch runs as many
+// columns side by side as keep every CTA resident (32 segments per CTA, one CTA per SM).
 void gs_lanes_run(Ctx& c, const DCsr& A, const LanePlan& pl, const double* inv_diag, double* x, const double* b,
-                  int nsw) {
+                  int nsw, int32_t k) {
     const int32_t n = A.nr;
     const int32_t nf = pl.nf, longest_row = pl.longest_row;
     const int32_t nctas = (nf + kLnLanes - 1) / kLnLanes;
+    const int32_t group = std::max<int32_t>(1, std::min<int32_t>(k, c.sms / std::max<int32_t>(1, nctas)));
     const DBuf<int32_t>& segf = pl.segf;
     const size_t stride = static_cast<size_t>(n);
-    DBuf<double> X(stride * (nsw + 1), c.s);
-    copy_d2d(c, X.get(), x, static_cast<int64_t>(stride));
-    launch(c, k_fill_pending, blocks_for(static_cast<int64_t>(stride) * nsw, 256), 256, 0,
-           static_cast<int64_t>(stride) * nsw, X.get() + stride);
+    const size_t cstride = stride * (nsw + 1);
+    DBuf<double> X(cstride * group, c.s);
     DBuf<unsigned int> ticket(1, c.s);
-    AMG_CK(cudaMemsetAsync(ticket.get(), 0, sizeof(unsigned int), c.s));
     const double bytes = nsw * (12.0 * A.nnz + 4.0 * (n + 1) + 8.0 * n + 16.0 * n);
     // AMGCU_GS_STATS=1: solver iteration / stall counters on stderr
     static const bool want_stats = std::getenv("AMGCU_GS_STATS") != nullptr;
     DBuf<unsigned long long> st;
-    if (want_stats) {
-        st.alloc(32, c.s);
-        AMG_CK(cudaMemsetAsync(st.get(), 0, 32 * sizeof(unsigned long long), c.s));
-        AMG_CK(cudaMemsetAsync(st.get() + 24, 0xff, sizeof(unsigned long long), c.s));
-    }
-    auto runl = [&](auto kern, size_t smem) {
-        AMG_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        launch_prof(c, kProfGaussSeidel, bytes, kern, static_cast<unsigned>(nctas), kLnThreads, smem, n, A.rp.get(),
-                    A.ci.get(), A.va.get(), inv_diag, b, nsw, static_cast<const int32_t*>(segf.get()), nf, X.get(),
-                    ticket.get(), st.get(), gs_env_u("AMGCU_GS_POLL_NS", 128u), gs_env_u("AMGCU_GS_PF_NS", 128u));
-    };
-    if (longest_row <= 9) runl(k_gs_lanes<8, 3, 4, 64>, ln_smem_bytes<8, 3, 4, 64>());
-    else runl(k_gs_lanes<20, 2, 2, 32>, ln_smem_bytes<20, 2, 2, 32>());
-    copy_d2d(c, x, X.get() + stride * nsw, static_cast<int64_t>(stride));
-    if (want_stats) {
-        unsigned long long h[32];
-        copy_d2h(c, h, st.get(), 32);
-        sync(c);
-        std::fprintf(stderr, "[gs lanes] n=%d segs=%d ctas=%d iterations(all ctas)=%llu rows=%llu lane-iters=%llu "
-                     "record-stalls=%llu value-stalls=%llu\n", n, nf, nctas, h[0], h[1], h[2], h[3],
-                     h[2] - h[1] - h[3]);
-        const double it = static_cast<double>(h[0]);
-        std::fprintf(stderr, "[gs lanes] cycles/iteration: rows %.0f sync %.0f publish %.0f total %.0f\n",
-                     h[16] / it, h[17] / it, h[18] / it, h[19] / it);
-        std::fprintf(stderr, "[gs lanes] solver span %.1f us, max iterations per CTA %llu, max cycles per CTA %llu\n",
-                     (h[25] - h[24]) * 1e-3, h[26], h[27]);
+    for (int32_t c0 = 0; c0 < k; c0 += group) {
+        const int32_t g = std::min(group, k - c0);
+        for (int32_t j = 0; j < g; ++j) {
+            copy_d2d(c, X.get() + cstride * j, x + stride * (c0 + j), static_cast<int64_t>(stride));
+            launch(c, k_fill_pending, blocks_for(static_cast<int64_t>(stride) * nsw, 256), 256, 0,
+                   static_cast<int64_t>(stride) * nsw, X.get() + cstride * j + stride);
+        }
+        AMG_CK(cudaMemsetAsync(ticket.get(), 0, sizeof(unsigned int), c.s));
+        if (want_stats) {
+            st.alloc(32, c.s);
+            AMG_CK(cudaMemsetAsync(st.get(), 0, 32 * sizeof(unsigned long long), c.s));
+            AMG_CK(cudaMemsetAsync(st.get() + 24, 0xff, sizeof(unsigned long long), c.s));
+        }
+        const double* bg = b ? b + stride * c0 : nullptr;
+        auto runl = [&](auto kern, size_t smem) {
+            AMG_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+            launch_prof(c, kProfGaussSeidel, bytes * g, kern, static_cast<unsigned>(nctas * g), kLnThreads, smem, n,
+                        A.rp.get(), A.ci.get(), A.va.get(), inv_diag, bg, nsw, static_cast<const int32_t*>(segf.get()),
+                        nf, X.get(), ticket.get(), st.get(), gs_env_u("AMGCU_GS_POLL_NS", 128u),
+                        gs_env_u("AMGCU_GS_PF_NS", 128u), g, cstride);
+        };
+        if (longest_row <= 9) runl(k_gs_lanes<8, 3, 4, 64>, ln_smem_bytes<8, 3, 4, 64>());
+        else runl(k_gs_lanes<20, 2, 2, 32>, ln_smem_bytes<20, 2, 2, 32>());
+        for (int32_t j = 0; j < g; ++j)
+            copy_d2d(c, x + stride * (c0 + j), X.get() + cstride * j + stride * nsw, static_cast<int64_t>(stride));
+        if (want_stats) {
+            unsigned long long h[32];
+            copy_d2h(c, h, st.get(), 32);
+            sync(c);
+            std::fprintf(stderr, "[gs lanes] n=%d segs=%d ctas=%d columns=%d iterations(all ctas)=%llu rows=%llu "
+                         "lane-iters=%llu record-stalls=%llu value-stalls=%llu\n", n, nf, nctas, g, h[0], h[1], h[2],
+                         h[3], h[2] - h[1] - h[3]);
+            const double it = static_cast<double>(h[0]);
+            std::fprintf(stderr, "[gs lanes] cycles/iteration: rows %.0f sync %.0f publish %.0f total %.0f\n",
+                         h[16] / it, h[17] / it, h[18] / it, h[19] / it);
+            std::fprintf(stderr, "[gs lanes] solver span %.1f us, max iterations per CTA %llu, max cycles per CTA %llu\n",
+                         (h[25] - h[24]) * 1e-3, h[26], h[27]);
+        }
     }
 }
 
@@ -929,10 +942,8 @@ void gauss_seidel(Ctx& c, const DCsr& A, const double* inv_diag, double* x, cons
         const LanePlan pl = lane_plan(c, A, nsw);
         if (pl.ok) {
             // the columns are independent sweeps (the reference relaxes each candidate
-            // column in turn, interpolation.hpp:91): one lane-per-segment launch per column
-            for (int col = 0; col < k; ++col)
-                gs_lanes_run(c, A, pl, inv_diag, x + static_cast<size_t>(col) * n,
-                             b ? b + static_cast<size_t>(col) * n : nullptr, nsw);
+            // column in turn, interpolation.hpp:91): side by side in lane-per-segment launches
+            gs_lanes_run(c, A, pl, inv_diag, x, b, nsw, k);
             return;
         }
     }

@@ -168,8 +168,7 @@ bool candidate_sweeps_start(Ctx& c, const DCsr& A, double* B, int32_t k, int swe
     AMG_CK(e);
     try {
         StreamScope on_side(c, c.side2);
-        for (int32_t j = 0; j < k; ++j)
-            gs_lanes_run(c, A, cs.plan, cs.dinv.get(), B + static_cast<size_t>(j) * n, nullptr, sweeps);
+        gs_lanes_run(c, A, cs.plan, cs.dinv.get(), B, nullptr, sweeps, k);
     } catch (...) {
         cudaEventRecord(cs.done, c.side2);
         throw;

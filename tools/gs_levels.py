@@ -13,7 +13,8 @@ ctx = api.Context(0)
 h = api.setup(A, B, so, Bh, ctx=ctx)
 for l in range(h.n_levels() - 1):
     M = h.matrix(l, 0)
-    Bl = CandidateSet(M.n_rows, 1, np.ones(M.n_rows))
+    k = h.candidates(l, 0).k
+    Bl = CandidateSet(M.n_rows, k, np.ones(M.n_rows * k))
     api.improve_candidates(M, Bl, so.candidate_sweeps, 1, 0.0, ctx=ctx)
     ctx.set_profiling(True)
     api.improve_candidates(M, Bl, so.candidate_sweeps, 1, 0.0, ctx=ctx)
@@ -21,4 +22,4 @@ for l in range(h.n_levels() - 1):
     ctx.set_profiling(False)
     rl = np.diff(M.row_offsets)
     bw = int(np.max(np.abs(M.col_indices - np.repeat(np.arange(M.n_rows), rl)))) if M.nnz() else 0
-    print(f"L{l} n {M.n_rows} bs {M.block_size} longest row {int(rl.max())} bandwidth {bw}: {ms:.3f} ms", flush=True)
+    print(f"L{l} k {k} n {M.n_rows} bs {M.block_size} longest row {int(rl.max())} bandwidth {bw}: {ms:.3f} ms", flush=True)
