@@ -19,6 +19,7 @@ namespace amgcu {
 namespace {
 
 constexpr int kMaxK = kGsMaxColumns;
+constexpr size_t kGsCtaSmem = 220 * 1024;  // dynamic shared memory of the single-CTA kernel
 
 // Gauss-Seidel sweeps, segment-parallel.
 //
@@ -650,7 +651,7 @@ template <int K>
 __device__ __forceinline__ void gs_warp_row(int32_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
                                             const double* __restrict__ va, const double* __restrict__ inv_diag,
                                             const double* __restrict__ b, int s, int32_t q, bool bwd,
-                                            double* __restrict__ X, unsigned max_ns) {
+                                            double* __restrict__ X, unsigned max_ns, double* __restrict__ sp) {
     const int lane = threadIdx.x & 31;
     const int32_t i = bwd ? n - 1 - q : q;
     const size_t stride = static_cast<size_t>(n) * K;
@@ -691,15 +692,23 @@ __device__ __forceinline__ void gs_warp_row(int32_t n, const int32_t* __restrict
             }
             prod[c] = use ? a * __longlong_as_double(static_cast<long long>(v)) : 0.0;
         }
-        // ordered subtraction by lane 0 (CSR order; the diagonal is skipped)
-        const unsigned um = __ballot_sync(0xffffffffu, use);
+        // ordered subtraction by lane 0 (CSR order; the diagonal is skipped): the products
+        // are staged in shared memory and lane 0 runs a fixed 32-step chain over them,
+        // unused lanes contributing +0.0 (x - (+0) is x for every x, -0 included).  The
+        // loads have constant addresses and issue ahead of the chain, the K columns'
+        // chains interleave, and no shuffle sits in this (to the compiler possibly
+        // divergent) loop, where it would compile to a WARPSYNC.COLLECTIVE sequence.
 #pragma unroll
-        for (int c = 0; c < K; ++c) {
-            for (unsigned m = um; m; m &= m - 1) {
-                const double pr = __shfl_sync(0xffffffffu, prod[c], __ffs(m) - 1);
-                acc[c] -= pr;
+        for (int c = 0; c < K; ++c) sp[c * 32 + lane] = prod[c];
+        __syncwarp();
+        if (lane == 0) {
+#pragma unroll
+            for (int l = 0; l < 32; ++l) {
+#pragma unroll
+                for (int c = 0; c < K; ++c) acc[c] -= sp[c * 32 + l];
             }
         }
+        __syncwarp();
     }
     if (lane == 0) {
         const double d = inv_diag[i];
@@ -708,6 +717,118 @@ __device__ __forceinline__ void gs_warp_row(int32_t n, const int32_t* __restrict
             cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> out(
                 *reinterpret_cast<unsigned long long*>(&xout[static_cast<size_t>(c) * n + i]));
             out.store(static_cast<unsigned long long>(__double_as_longlong(acc[c] * d)), cuda::memory_order_relaxed);
+        }
+    }
+}
+
+// Small levels (the coarse end of a hierarchy): one CTA holds the whole iterate in
+// shared memory and relaxes it in place, all sweeps in one launch.  Items are (sweep,
+// position) in sweep-major order, item t on warp t % 32; a row's version counter
+// (shared) says how many sweeps it has finished.  Row i in sweep s waits for its own
+// version s, then reads the rows before it in sweep order at version s + 1 (new
+// values) and the rows after it at version s (old values).  In place is exact because the pattern is structurally
+// symmetric (checked by the launcher): a row j after i that i reads is itself a reader
+// of i, so it cannot write its sweep-s value before i has published (and therefore
+// finished reading).  Every item waits only on earlier items, and all warps are
+// resident, so the launch cannot deadlock.  Each row sums in CSR order with the
+// diagonal skipped: the lanes stage a 32-entry chunk's products in shared memory and
+// lane 0 runs a fixed 32-step chain over them, unused lanes contributing +0.0 (an exact
+// identity).
+constexpr int kCtaWarps = 32;
+
+__device__ __forceinline__ int32_t ld_ver(const int32_t* p) {
+    int32_t v;
+    asm volatile("ld.acquire.cta.shared.b32 %0, [%1];" : "=r"(v) : "r"(static_cast<unsigned>(__cvta_generic_to_shared(p)))
+                 : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_ver(int32_t* p, int32_t v) {
+    asm volatile("st.release.cta.shared.b32 [%0], %1;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(p))), "r"(v)
+                 : "memory");
+}
+
+template <int K>
+__global__ void __launch_bounds__(kCtaWarps * 32, 1)
+    k_gs_cta(int32_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci, const double* __restrict__ va,
+             const double* __restrict__ inv_diag, const double* __restrict__ b, int nsweeps,
+             const unsigned char* __restrict__ backward, double* __restrict__ x) {
+    extern __shared__ __align__(16) double cta_smem[];
+    double* xs = cta_smem;                                       // K x n, column-major like x
+    double* sp = xs + static_cast<size_t>(K) * n + static_cast<size_t>(threadIdx.x >> 5) * (K * 32);  // products
+    int32_t* ver = reinterpret_cast<int32_t*>(xs + static_cast<size_t>(K) * n + kCtaWarps * K * 32);
+    for (int32_t t = threadIdx.x; t < K * n; t += blockDim.x) xs[t] = x[t];
+    for (int32_t t = threadIdx.x; t < n; t += blockDim.x) ver[t] = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    volatile double* vx = xs;
+    const int64_t items = static_cast<int64_t>(nsweeps) * n;
+    for (int64_t t = warp; t < items; t += kCtaWarps) {
+        const int s = static_cast<int>(t / n);
+        const int32_t q = static_cast<int32_t>(t - static_cast<int64_t>(s) * n);
+        const bool bwd = backward[s] != 0;
+        const int32_t i = bwd ? n - 1 - q : q;
+        double acc[K];
+#pragma unroll
+        for (int c = 0; c < K; ++c) acc[c] = b ? b[static_cast<size_t>(c) * n + i] : 0.0;
+        const int32_t lo = rp[i], hi = rp[i + 1];
+        // the row's own previous sweep first: nothing else orders (s - 1, i) before (s, i)
+        // when the row's neighbours do not (the last row of a forward half-sweep starts
+        // the backward one, and reads only rows that did not wait for it)
+        while (ld_ver(ver + i) < s) __nanosleep(32);
+        for (int32_t e0 = lo; e0 < hi; e0 += 32) {
+            const int32_t p = e0 + lane;
+            const bool act = p < hi;
+            int32_t j = i;
+            double a = 0.0;
+            if (act) {
+                j = __ldg(ci + p);
+                a = __ldg(va + p);
+            }
+            const bool use = act && j != i;
+            const int32_t need = ((j < i) != bwd) ? s + 1 : s;
+            // warp-uniform wait: the warp stays converged for the staging below
+            while (__any_sync(0xffffffffu, use && ld_ver(ver + j) < need)) __nanosleep(32);
+#pragma unroll
+            for (int c = 0; c < K; ++c) sp[c * 32 + lane] = use ? a * vx[static_cast<size_t>(c) * n + j] : 0.0;
+            __syncwarp();
+            if (lane == 0) {
+#pragma unroll
+                for (int l = 0; l < 32; ++l) {
+#pragma unroll
+                    for (int c = 0; c < K; ++c) acc[c] -= sp[c * 32 + l];
+                }
+            }
+            __syncwarp();
+        }
+        if (lane == 0) {
+            const double d = inv_diag[i];
+#pragma unroll
+            for (int c = 0; c < K; ++c) vx[static_cast<size_t>(c) * n + i] = acc[c] * d;
+            st_ver(ver + i, s + 1);
+        }
+        __syncwarp();
+    }
+    __syncthreads();
+    for (int32_t t = threadIdx.x; t < K * n; t += blockDim.x) x[t] = xs[t];
+}
+
+// flag = 1 if some stored (i, j) has no stored (j, i)
+__global__ void k_pattern_asym(int32_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                               int32_t* __restrict__ flag) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    for (int32_t p = rp[i]; p < rp[i + 1]; ++p) {
+        const int32_t j = ci[p];
+        int32_t lo = rp[j], hi = rp[j + 1];
+        while (lo < hi) {
+            const int32_t mid = (lo + hi) >> 1;
+            if (ci[mid] < i) lo = mid + 1;
+            else hi = mid;
+        }
+        if (lo == rp[j + 1] || ci[lo] != i) {
+            *flag = 1;
+            return;
         }
     }
 }
@@ -724,18 +845,20 @@ __global__ void __launch_bounds__(kWrWarps * 32)
                    int nsweeps, const unsigned char* __restrict__ backward, double* __restrict__ X,
                    unsigned int* __restrict__ ticket, unsigned max_ns) {
     __shared__ unsigned int blk;
+    __shared__ double stage[kWrWarps][K * 32];  // per warp: the chunk's products (gs_warp_row)
     if (threadIdx.x == 0) blk = atomicAdd(ticket, 1u);
     __syncthreads();
+    double* sp = stage[threadIdx.x / 32];
     const int64_t item = static_cast<int64_t>(blk) * kWrWarps + threadIdx.x / 32;
     if (kRowMajor) {
         if (item >= n) return;
         for (int s = 0; s < nsweeps; ++s) gs_warp_row<K>(n, rp, ci, va, inv_diag, b, s, static_cast<int32_t>(item),
-                                                         false, X, max_ns);
+                                                         false, X, max_ns, sp);
     } else {
         if (item >= static_cast<int64_t>(nsweeps) * n) return;
         const int s = static_cast<int>(item / n);
         gs_warp_row<K>(n, rp, ci, va, inv_diag, b, s, static_cast<int32_t>(item - static_cast<int64_t>(s) * n),
-                       backward[s] != 0, X, max_ns);
+                       backward[s] != 0, X, max_ns, sp);
     }
 }
 
@@ -932,12 +1055,53 @@ void gs_lanes_run(Ctx& c, const DCsr& A, const LanePlan& pl, const double* inv_d
     }
 }
 
+// The single-CTA shared-memory kernel (k_gs_cta) for levels whose iterate fits on one SM
+// and whose pattern is structurally symmetric.  Returns false when it does not apply.
+bool gs_cta_run(Ctx& c, const DCsr& A, const double* inv_diag, double* x, const double* b, int k, int nsw,
+                bool symmetric_sweep) {
+    static const bool off = [] {
+        const char* e = std::getenv("AMGCU_GS_CTA");
+        return e && e[0] == '0';
+    }();
+    const int32_t n = A.nr;
+    const size_t smem = sizeof(double) * (static_cast<size_t>(k) * n + kCtaWarps * 32 * k) + sizeof(int32_t) * n;
+    if (off || smem > kGsCtaSmem || std::getenv("AMGCU_GS_TRACE")) return false;
+    {
+        DBuf<int32_t> flag(1, c.s);
+        AMG_CK(cudaMemsetAsync(flag.get(), 0, sizeof(int32_t), c.s));
+        launch(c, k_pattern_asym, blocks_for(n, 256), 256, 0, n, A.rp.get(), A.ci.get(), flag.get());
+        if (read_scalar(c, flag.get())) return false;
+    }
+    std::vector<unsigned char> hb(nsw);
+    for (int s = 0; s < nsw; ++s) hb[s] = symmetric_sweep ? static_cast<unsigned char>(s & 1) : 0;
+    DBuf<unsigned char> bwd(static_cast<size_t>(nsw), c.s);
+    copy_h2d(c, bwd.get(), hb.data(), nsw);
+    const double bytes = nsw * (12.0 * A.nnz + 4.0 * (n + 1) + 8.0 * n + 16.0 * n * k);
+    auto run = [&](auto kern) {
+        AMG_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        launch_prof(c, kProfGaussSeidel, bytes, kern, 1, kCtaWarps * 32, smem, n, A.rp.get(), A.ci.get(), A.va.get(),
+                    inv_diag, b, nsw, static_cast<const unsigned char*>(bwd.get()), x);
+    };
+    switch (k) {
+        case 1: run(k_gs_cta<1>); break;
+        case 2: run(k_gs_cta<2>); break;
+        case 3: run(k_gs_cta<3>); break;
+        case 4: run(k_gs_cta<4>); break;
+        case 5: run(k_gs_cta<5>); break;
+        case 6: run(k_gs_cta<6>); break;
+        case 7: run(k_gs_cta<7>); break;
+        default: run(k_gs_cta<8>); break;
+    }
+    return true;
+}
+
 void gauss_seidel(Ctx& c, const DCsr& A, const double* inv_diag, double* x, const double* b, int k, int sweeps,
                   bool symmetric_sweep) {
     if (k > kMaxK) throw InvalidArgument("relax: at most 8 candidate columns on the GPU path");
     const int32_t n = A.nr;
     const int nsw = symmetric_sweep ? 2 * sweeps : sweeps;
     if (nsw == 0 || n == 0) return;
+    if (gs_cta_run(c, A, inv_diag, x, b, k, nsw, symmetric_sweep)) return;
     if (!symmetric_sweep) {
         const LanePlan pl = lane_plan(c, A, nsw);
         if (pl.ok) {
@@ -997,13 +1161,15 @@ void gauss_seidel(Ctx& c, const DCsr& A, const double* inv_diag, double* x, cons
             AMG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gs_warp_rows<1, true>, kWrWarps * 32, 0));
             const int64_t resident_warps = static_cast<int64_t>(per_sm) * c.sms * kWrWarps;
             row_major = 2 * static_cast<int64_t>(bwidth) + 2 * kWrWarps < resident_warps;
+            // AMGCU_GS_ROWMAJOR=0/1 overrides (comparison runs)
+            if (const char* e = std::getenv("AMGCU_GS_ROWMAJOR")) row_major = e[0] == '1';
         }
         const int64_t items = row_major ? n : static_cast<int64_t>(nsw) * n;
         const unsigned grid = static_cast<unsigned>((items + kWrWarps - 1) / kWrWarps);
         auto runw = [&](auto kern) {
             launch_prof(c, kProfGaussSeidel, bytes, kern, grid, kWrWarps * 32, 0, n, A.rp.get(), A.ci.get(),
                         A.va.get(), inv_diag, b, nsw, static_cast<const unsigned char*>(bwd.get()), X.get(),
-                        ticket.get(), std::min(gs_max_ns(), kWarpRowPollNs));
+                        ticket.get(), gs_env_u("AMGCU_GS_WR_NS", kWarpRowPollNs));
         };
 #define AMGCU_WR(KK) (row_major ? runw(k_gs_warp_rows<KK, true>) : runw(k_gs_warp_rows<KK, false>))
         switch (k) {
