@@ -125,6 +125,13 @@ struct SeqSumWs {
     int64_t tiles = 0;
 };
 
+// AMGCU_PHASE_TRACE=1: events on the main stream at the setup's phase boundaries
+// (per level), printed with their durations when the setup returns (setup.cu)
+struct PhaseTrace {
+    bool on = false;
+    std::vector<std::pair<std::string, cudaEvent_t>> marks;
+};
+
 struct Ctx {
     bool profile = false;
     uint32_t prof_mask = 0xffffffffu;  // families timed while profile is on
@@ -155,6 +162,7 @@ struct Ctx {
     DBuf<double> arnoldi_v0;
     size_t arnoldi_v0_n = 0;
     SeqSumWs ssws[2];  // [0] main stream, [1] any other stream
+    PhaseTrace phases;
 };
 
 // block-partial scratch and wavefront tickets of the tree reductions (>= count partials)

@@ -111,12 +111,14 @@ double spectral_radius(Ctx& c, const DCsr& A, int steps, const double* dinv, int
 // (no host synchronisation: may run on another stream than the plan's)
 constexpr int kGsMaxColumns = 8;  // candidate columns one Gauss-Seidel launch relaxes
 
-struct LanePlan {
+struct LanePlan {  // the forward-sweep plan of a matrix (relax.cu: lane_plan)
+    enum Kind { kNone = 0, kLanes = 1, kSegWarp = 2, kCta = 3 };
     bool ok = false;
+    int kind = kNone;
     int32_t nf = 0, longest_row = 0;
     DBuf<int32_t> segf;
 };
-LanePlan lane_plan(Ctx& c, const DCsr& A, int nsw);
+LanePlan lane_plan(Ctx& c, const DCsr& A, int nsw, int k);
 // forward sweeps of the k columns of x (n x k column-major; b likewise, or null)
 void gs_lanes_run(Ctx& c, const DCsr& A, const LanePlan& pl, const double* inv_diag, double* x, const double* b,
                   int nsw, int32_t k);

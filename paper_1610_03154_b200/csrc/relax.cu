@@ -116,6 +116,7 @@ constexpr int gs_max_poll() {
 // left the ring.  K = 1 only.
 constexpr int kRing = 64;
 constexpr int kShortSegment = 8;
+constexpr int kSegWarpMinLen = 16;  // mean segment length from which the warp-per-segment kernel runs
 constexpr unsigned kWarpRowPollNs = 32;  // poll back-off cap of the warp-per-row kernel  // mean segment length below which the warp-per-row kernel is used
 constexpr int32_t kProductTerm = -1;  // term whose product a * x is precomputed (K = 1)
 constexpr int kSibling = 4;  // entry class: pending value of a sibling segment
@@ -735,6 +736,11 @@ __device__ __forceinline__ void gs_warp_row(int32_t n, const int32_t* __restrict
 // lane 0 runs a fixed 32-step chain over them, unused lanes contributing +0.0 (an exact
 // identity).
 constexpr int kCtaWarps = 32;
+// dynamic shared memory of k_gs_cta: the iterate, the per-warp product stages, versions
+inline size_t gs_cta_smem(int32_t n, int k) {
+    return sizeof(double) * (static_cast<size_t>(k) * n + static_cast<size_t>(kCtaWarps) * 32 * k) +
+           sizeof(int32_t) * static_cast<size_t>(n);
+}
 
 __device__ __forceinline__ int32_t ld_ver(const int32_t* p) {
     int32_t v;
@@ -830,6 +836,155 @@ __global__ void k_pattern_asym(int32_t n, const int32_t* __restrict__ rp, const 
             *flag = 1;
             return;
         }
+    }
+}
+
+// Long segments of long rows (coarse levels of vector problems: C5 level 1 has 342
+// segments of 684 rows of up to 50 entries): a warp per segment relaxes the segment's
+// rows in order, every forward sweep in turn.  A row's lanes take its entries 32 at a
+// time; the products are staged in shared memory and lane 0 subtracts them in CSR
+// order (the diagonal and unused lanes contribute +0.0, an exact identity).  Values of
+// the warp's own segment from this sweep come from a shared ring of its last kSwRing
+// rows (or its own global stores); other segments' values are polled in the per-sweep
+// buffers (pre-filled with kPending).  Items (sweep, row) run in that order within a
+// segment, every wait is on an item earlier in (sweep, position) order, and the
+// launcher keeps every warp resident, so the earliest unfinished item always runs.
+constexpr int kSwWarps = 4;
+constexpr int kSwRing = 64;
+
+template <int K>
+__global__ void __launch_bounds__(kSwWarps * 32)
+    k_gs_seg_warp(int32_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                  const double* __restrict__ va, const double* __restrict__ inv_diag, const double* __restrict__ b,
+                  int nsweeps, const int32_t* __restrict__ segs, int32_t nseg, double* __restrict__ X,
+                  unsigned int* __restrict__ ticket, unsigned max_ns) {
+    __shared__ unsigned int blk;
+    __shared__ double ring[kSwWarps][K][kSwRing];
+    __shared__ double stage[kSwWarps][K][32];
+    if (threadIdx.x == 0) blk = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int w = threadIdx.x >> 5;
+    const int32_t g = static_cast<int32_t>(blk) * kSwWarps + w;
+    if (g >= nseg) return;
+    const int32_t q0 = segs[g], q1 = segs[g + 1];
+    const size_t stride = static_cast<size_t>(n) * K;
+    double (*rg)[kSwRing] = ring[w];
+    double (*sp)[32] = stage[w];
+    // software pipeline over the items u = (sweep, row): the row bounds two items ahead
+    // and the first 32 entries one item ahead are loaded before they are needed
+    const int32_t len = q1 - q0;
+    const int64_t total = static_cast<int64_t>(len) * nsweeps;
+    auto row_of = [&](int64_t u) { return q0 + static_cast<int32_t>(u % len); };
+    int32_t lo1 = __ldg(rp + q0), hi1 = __ldg(rp + q0 + 1);  // item 0
+    int32_t j1 = -1;
+    double a1 = 0.0;
+    if (lo1 + lane < hi1) {
+        j1 = __ldg(ci + lo1 + lane);
+        a1 = __ldg(va + lo1 + lane);
+    }
+    int32_t lo2 = 0, hi2 = 0;  // item 1
+    if (total > 1) {
+        const int32_t r = row_of(1);
+        lo2 = __ldg(rp + r);
+        hi2 = __ldg(rp + r + 1);
+    }
+    for (int64_t u = 0; u < total; ++u) {
+        const int s = static_cast<int>(u / len);
+        const int32_t i = row_of(u);
+        const int32_t lo = lo1, hi = hi1;
+        const int32_t jf = j1;
+        const double af = a1;
+        // advance the pipeline: item u + 1's first chunk, item u + 2's bounds
+        lo1 = lo2;
+        hi1 = hi2;
+        j1 = -1;
+        a1 = 0.0;
+        if (u + 1 < total && lo1 + lane < hi1) {
+            j1 = __ldg(ci + lo1 + lane);
+            a1 = __ldg(va + lo1 + lane);
+        }
+        if (u + 2 < total) {
+            const int32_t r = row_of(u + 2);
+            lo2 = __ldg(rp + r);
+            hi2 = __ldg(rp + r + 1);
+        }
+        const double* xin = X + static_cast<size_t>(s) * stride;
+        double* xout = X + static_cast<size_t>(s + 1) * stride;
+        double acc[K];
+#pragma unroll
+        for (int c = 0; c < K; ++c) acc[c] = b ? b[static_cast<size_t>(c) * n + i] : 0.0;
+        for (int32_t e0 = lo; e0 < hi; e0 += 32) {
+            const int32_t p = e0 + lane;
+            const bool act = p < hi;
+            int32_t j = i;
+            double a = 0.0;
+            if (e0 == lo) {
+                if (act) {
+                    j = jf;
+                    a = af;
+                }
+            } else if (act) {
+                j = __ldg(ci + p);
+                a = __ldg(va + p);
+            }
+            const bool use = act && j != i;
+            // where the value comes from: own ring (this sweep, own segment, recent),
+            // own or settled stores (no poll), or another segment's buffer (poll)
+            const bool newer = j < i;
+            const bool own = j >= q0 && j < q1;
+            const bool from_ring = use && newer && own && i - j <= kSwRing;
+            const bool settled = !newer && (s == 0 || own);
+            const double* src = (newer ? xout : xin) + j;
+            unsigned long long v[K];
+#pragma unroll
+            for (int c = 0; c < K; ++c) {
+                v[c] = 0ull;
+                if (use && !from_ring)
+                    v[c] = settled ? static_cast<unsigned long long>(__double_as_longlong(src[static_cast<size_t>(c) * n]))
+                                   : load_relaxed_bits(src + static_cast<size_t>(c) * n);
+            }
+            unsigned ns = 8;
+            while (true) {
+                bool pend = false;
+#pragma unroll
+                for (int c = 0; c < K; ++c) pend |= use && !from_ring && v[c] == kPending;
+                if (!__any_sync(0xffffffffu, pend)) break;
+                if (pend) {
+                    __nanosleep(ns);
+#pragma unroll
+                    for (int c = 0; c < K; ++c)
+                        if (v[c] == kPending) v[c] = load_relaxed_bits(src + static_cast<size_t>(c) * n);
+                }
+                ns = ns < max_ns ? 2 * ns : max_ns;
+            }
+#pragma unroll
+            for (int c = 0; c < K; ++c) {
+                const double xv = from_ring ? rg[c][j % kSwRing] : __longlong_as_double(static_cast<long long>(v[c]));
+                sp[c][lane] = use ? a * xv : 0.0;
+            }
+            __syncwarp();
+            if (lane == 0) {
+#pragma unroll
+                for (int l = 0; l < 32; ++l) {
+#pragma unroll
+                    for (int c = 0; c < K; ++c) acc[c] -= sp[c][l];
+                }
+            }
+            __syncwarp();
+        }
+        if (lane == 0) {
+            const double d = inv_diag[i];
+#pragma unroll
+            for (int c = 0; c < K; ++c) {
+                const double xn = acc[c] * d;
+                rg[c][i % kSwRing] = xn;
+                cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> out(
+                    *reinterpret_cast<unsigned long long*>(&xout[static_cast<size_t>(c) * n + i]));
+                out.store(static_cast<unsigned long long>(__double_as_longlong(xn)), cuda::memory_order_relaxed);
+            }
+        }
+        __syncwarp();
     }
 }
 
@@ -973,16 +1128,35 @@ __global__ void k_jacobi(int32_t n, const int32_t* __restrict__ rp, const int32_
 
 }  // namespace
 
-// The lane-per-segment kernel's plan for a matrix (forward sweeps): segments with a
-// block-size window (so the stride-m chains of interleaved vector unknowns count) and
-// the longest row.  It applies to rows of at most 21 entries, segments of at least 16
-// rows on average, every CTA of 32 segments resident at once, and 32-bit tags.
-LanePlan lane_plan(Ctx& c, const DCsr& A, int nsw) {
+// The forward-sweep plan of a matrix: which sync-free kernel relaxes its k columns, and
+// its segments.  In order of preference:
+//   kCta      the iterate fits one SM and the pattern is structurally symmetric;
+//   kLanes    lane per segment (gs_lanes.cuh): one column, rows of at most 9 entries
+//             (the 8-term records), 32 segments per resident CTA;
+//   kSegWarp  warp per segment (k_gs_seg_warp): any row length, every warp resident.
+// Segments use a block-size window, so the stride-m chains of interleaved vector
+// unknowns continue a segment; both segment kernels need them 16 rows long on average.
+// Host synchronisations happen here; the run (fwd_gs_run) has none, so it may be
+// queued on another stream than the plan's.
+LanePlan lane_plan(Ctx& c, const DCsr& A, int nsw, int k) {
     LanePlan pl;
-    const char* ln_env = std::getenv("AMGCU_GS_LANES");
-    if ((ln_env && ln_env[0] == '0') || std::getenv("AMGCU_GS_TRACE")) return pl;
     const int32_t n = A.nr;
-    if (n == 0 || n >= (1 << 24) || static_cast<int64_t>(nsw) * n >= (int64_t(1) << 31)) return pl;
+    if (n == 0 || nsw == 0 || k > kMaxK || std::getenv("AMGCU_GS_TRACE")) return pl;
+    if (n >= (1 << 24) || static_cast<int64_t>(nsw) * n * k >= (int64_t(1) << 31)) return pl;
+    {
+        const char* e = std::getenv("AMGCU_GS_CTA");  // "0": off (read per call: tests toggle it)
+        const size_t smem = gs_cta_smem(n, k);
+        if (!(e && e[0] == '0') && smem <= kGsCtaSmem) {
+            DBuf<int32_t> flag(1, c.s);
+            AMG_CK(cudaMemsetAsync(flag.get(), 0, sizeof(int32_t), c.s));
+            launch(c, k_pattern_asym, blocks_for(n, 256), 256, 0, n, A.rp.get(), A.ci.get(), flag.get());
+            if (!read_scalar(c, flag.get())) {
+                pl.kind = LanePlan::kCta;
+                pl.ok = true;
+                return pl;
+            }
+        }
+    }
     DBuf<int32_t> st(2, c.s);
     AMG_CK(cudaMemsetAsync(st.get(), 0, 2 * sizeof(int32_t), c.s));
     launch(c, k_bandwidth, blocks_for(n, 256), 256, 0, n, A.rp.get(), A.ci.get(), st.get());
@@ -990,8 +1164,23 @@ LanePlan lane_plan(Ctx& c, const DCsr& A, int nsw) {
     stage_scalar(c, 1, st.get() + 1);
     sync(c);
     pl.longest_row = staged<int32_t>(c, 1);
-    pl.ok = pl.longest_row <= 21 && (pl.nf + kLnLanes - 1) / kLnLanes <= c.sms &&
-            static_cast<int64_t>(pl.nf) * 16 <= n;
+    if (static_cast<int64_t>(pl.nf) * kSegWarpMinLen > n) return pl;
+    const char* ln_env = std::getenv("AMGCU_GS_LANES");
+    const char* sw_env = std::getenv("AMGCU_GS_SEGWARP");
+    const bool lanes_off = ln_env && ln_env[0] == '0', sw_off = sw_env && sw_env[0] == '0';
+    if (!lanes_off && k == 1 && pl.longest_row <= 9 && (pl.nf + kLnLanes - 1) / kLnLanes <= c.sms) {
+        pl.kind = LanePlan::kLanes;
+        pl.ok = true;
+        return pl;
+    }
+    if (!sw_off && k <= 4) {
+        int per_sm = 0;
+        AMG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gs_seg_warp<4>, kSwWarps * 32, 0));
+        if ((pl.nf + kSwWarps - 1) / kSwWarps <= static_cast<int64_t>(per_sm) * c.sms) {
+            pl.kind = LanePlan::kSegWarp;
+            pl.ok = true;
+        }
+    }
     return pl;
 }
 
@@ -999,8 +1188,8 @@ LanePlan lane_plan(Ctx& c, const DCsr& A, int nsw) {
 // (gs_lanes.cuh).  The columns are independent sweeps of the same matrix (the reference
 // relaxes each candidate column in turn, interpolation.hpp:91); one launch runs as many
 // columns side by side as keep every CTA resident (32 segments per CTA, one CTA per SM).
-void gs_lanes_run(Ctx& c, const DCsr& A, const LanePlan& pl, const double* inv_diag, double* x, const double* b,
-                  int nsw, int32_t k) {
+void gs_lanes_kernel_run(Ctx& c, const DCsr& A, const LanePlan& pl, const double* inv_diag, double* x,
+                         const double* b, int nsw, int32_t k) {
     const int32_t n = A.nr;
     const int32_t nf = pl.nf, longest_row = pl.longest_row;
     const int32_t nctas = (nf + kLnLanes - 1) / kLnLanes;
@@ -1055,23 +1244,12 @@ void gs_lanes_run(Ctx& c, const DCsr& A, const LanePlan& pl, const double* inv_d
     }
 }
 
-// The single-CTA shared-memory kernel (k_gs_cta) for levels whose iterate fits on one SM
-// and whose pattern is structurally symmetric.  Returns false when it does not apply.
-bool gs_cta_run(Ctx& c, const DCsr& A, const double* inv_diag, double* x, const double* b, int k, int nsw,
-                bool symmetric_sweep) {
-    static const bool off = [] {
-        const char* e = std::getenv("AMGCU_GS_CTA");
-        return e && e[0] == '0';
-    }();
+// The single-CTA shared-memory kernel (k_gs_cta): levels whose iterate fits on one SM
+// and whose pattern is structurally symmetric (checked by the caller).
+void gs_cta_kernel_run(Ctx& c, const DCsr& A, const double* inv_diag, double* x, const double* b, int k, int nsw,
+                       bool symmetric_sweep) {
     const int32_t n = A.nr;
-    const size_t smem = sizeof(double) * (static_cast<size_t>(k) * n + kCtaWarps * 32 * k) + sizeof(int32_t) * n;
-    if (off || smem > kGsCtaSmem || std::getenv("AMGCU_GS_TRACE")) return false;
-    {
-        DBuf<int32_t> flag(1, c.s);
-        AMG_CK(cudaMemsetAsync(flag.get(), 0, sizeof(int32_t), c.s));
-        launch(c, k_pattern_asym, blocks_for(n, 256), 256, 0, n, A.rp.get(), A.ci.get(), flag.get());
-        if (read_scalar(c, flag.get())) return false;
-    }
+    const size_t smem = gs_cta_smem(n, k);
     std::vector<unsigned char> hb(nsw);
     for (int s = 0; s < nsw; ++s) hb[s] = symmetric_sweep ? static_cast<unsigned char>(s & 1) : 0;
     DBuf<unsigned char> bwd(static_cast<size_t>(nsw), c.s);
@@ -1092,6 +1270,54 @@ bool gs_cta_run(Ctx& c, const DCsr& A, const double* inv_diag, double* x, const 
         case 7: run(k_gs_cta<7>); break;
         default: run(k_gs_cta<8>); break;
     }
+}
+
+// Warp-per-segment forward sweeps (k_gs_seg_warp) of the k columns.
+void gs_segwarp_kernel_run(Ctx& c, const DCsr& A, const LanePlan& pl, const double* inv_diag, double* x,
+                           const double* b, int nsw, int32_t k) {
+    const int32_t n = A.nr;
+    const size_t stride = static_cast<size_t>(n) * k;
+    DBuf<double> X(stride * (nsw + 1), c.s);
+    copy_d2d(c, X.get(), x, static_cast<int64_t>(stride));
+    launch(c, k_fill_pending, blocks_for(static_cast<int64_t>(stride) * nsw, 256), 256, 0,
+           static_cast<int64_t>(stride) * nsw, X.get() + stride);
+    DBuf<unsigned int> ticket(1, c.s);
+    AMG_CK(cudaMemsetAsync(ticket.get(), 0, sizeof(unsigned int), c.s));
+    const double bytes = nsw * (12.0 * A.nnz + 4.0 * (n + 1) + 8.0 * n + 16.0 * n * k);
+    const unsigned nctas = static_cast<unsigned>((pl.nf + kSwWarps - 1) / kSwWarps);
+    auto runs = [&](auto kern) {
+        launch_prof(c, kProfGaussSeidel, bytes, kern, nctas, kSwWarps * 32, 0, n, A.rp.get(), A.ci.get(), A.va.get(),
+                    inv_diag, b, nsw, static_cast<const int32_t*>(pl.segf.get()), pl.nf, X.get(), ticket.get(),
+                    gs_env_u("AMGCU_GS_SW_NS", 64u));
+    };
+    switch (k) {
+        case 1: runs(k_gs_seg_warp<1>); break;
+        case 2: runs(k_gs_seg_warp<2>); break;
+        case 3: runs(k_gs_seg_warp<3>); break;
+        default: runs(k_gs_seg_warp<4>); break;
+    }
+    copy_d2d(c, x, X.get() + stride * nsw, static_cast<int64_t>(stride));
+}
+
+void gs_lanes_run(Ctx& c, const DCsr& A, const LanePlan& pl, const double* inv_diag, double* x, const double* b,
+                  int nsw, int32_t k) {
+    switch (pl.kind) {
+        case LanePlan::kCta: gs_cta_kernel_run(c, A, inv_diag, x, b, k, nsw, false); return;
+        case LanePlan::kLanes: gs_lanes_kernel_run(c, A, pl, inv_diag, x, b, nsw, k); return;
+        case LanePlan::kSegWarp: gs_segwarp_kernel_run(c, A, pl, inv_diag, x, b, nsw, k); return;
+        default: throw std::logic_error("gauss_seidel: no forward-sweep plan");
+    }
+}
+
+// the symmetric sweeps' use of the single-CTA kernel (the forward plan covers the rest)
+bool gs_cta_sym(Ctx& c, const DCsr& A, const double* inv_diag, double* x, const double* b, int k, int nsw) {
+    const char* e = std::getenv("AMGCU_GS_CTA");
+    if ((e && e[0] == '0') || gs_cta_smem(A.nr, k) > kGsCtaSmem || std::getenv("AMGCU_GS_TRACE")) return false;
+    DBuf<int32_t> flag(1, c.s);
+    AMG_CK(cudaMemsetAsync(flag.get(), 0, sizeof(int32_t), c.s));
+    launch(c, k_pattern_asym, blocks_for(A.nr, 256), 256, 0, A.nr, A.rp.get(), A.ci.get(), flag.get());
+    if (read_scalar(c, flag.get())) return false;
+    gs_cta_kernel_run(c, A, inv_diag, x, b, k, nsw, true);
     return true;
 }
 
@@ -1101,12 +1327,13 @@ void gauss_seidel(Ctx& c, const DCsr& A, const double* inv_diag, double* x, cons
     const int32_t n = A.nr;
     const int nsw = symmetric_sweep ? 2 * sweeps : sweeps;
     if (nsw == 0 || n == 0) return;
-    if (gs_cta_run(c, A, inv_diag, x, b, k, nsw, symmetric_sweep)) return;
-    if (!symmetric_sweep) {
-        const LanePlan pl = lane_plan(c, A, nsw);
+    if (symmetric_sweep) {
+        if (gs_cta_sym(c, A, inv_diag, x, b, k, nsw)) return;
+    } else {
+        const LanePlan pl = lane_plan(c, A, nsw, k);
         if (pl.ok) {
             // the columns are independent sweeps (the reference relaxes each candidate
-            // column in turn, interpolation.hpp:91): side by side in lane-per-segment launches
+            // column in turn, interpolation.hpp:91): side by side in one launch
             gs_lanes_run(c, A, pl, inv_diag, x, b, nsw, k);
             return;
         }

@@ -22,6 +22,32 @@ void normalize_candidates(Ctx& c, double* B, int32_t n, int32_t k);
 
 namespace {
 
+void phase(Ctx& c, const char* name, int level) {
+    if (!c.phases.on) return;
+    cudaEvent_t e;
+    AMG_CK(cudaEventCreate(&e));
+    AMG_CK(cudaEventRecord(e, c.s));
+    c.phases.marks.emplace_back("L" + std::to_string(level) + " " + name, e);
+}
+
+void phase_report(Ctx& c) {
+    if (!c.phases.on || c.phases.marks.empty()) return;
+    AMG_CK(cudaEventSynchronize(c.phases.marks.back().second));
+    std::string line = "[phases]";
+    float total = 0.f;
+    for (size_t q = 1; q < c.phases.marks.size(); ++q) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, c.phases.marks[q - 1].second, c.phases.marks[q].second);
+        total += ms;
+        char buf[96];
+        std::snprintf(buf, sizeof(buf), " %s %.2f", c.phases.marks[q].first.c_str(), ms);
+        line += buf;
+    }
+    std::fprintf(stderr, "%s | total %.2f ms\n", line.c_str(), total);
+    for (auto& m : c.phases.marks) cudaEventDestroy(m.second);
+    c.phases.marks.clear();
+}
+
 __global__ void k_evolution_weights(int32_t n, const double* __restrict__ d, double omega, double* __restrict__ winv,
                                     int32_t* __restrict__ bad) {
     const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -154,7 +180,7 @@ bool candidate_sweeps_start(Ctx& c, const DCsr& A, double* B, int32_t k, int swe
     // a zero diagonal is reported where the reference meets it (improve_candidates runs
     // after the stagnation check, hierarchy.hpp:191-208): leave it to the in-order path
     if (inverse_diagonal_check(c, A, cs.dinv.get()) >= 0) return false;
-    cs.plan = lane_plan(c, A, sweeps);
+    cs.plan = lane_plan(c, A, sweeps, k);
     if (!cs.plan.ok) return false;
     // the done event exists before anything is queued on side2, and is recorded however
     // the queueing ends, so the destructor's wait always covers every queued sweep
@@ -199,9 +225,11 @@ bool coarsen(Ctx& c, DHier& H, int level, const double* Bhat, Coarsened& out) {
     CandidateSweeps cand;
     DCsr S0, Sa, S;
     DAgg agg;
+    phase(c, "begin", level);
     {
         OpsScope scope(c, &cagg);
         strength_of(c, L, o, S0);
+        phase(c, "strength", level);
         // the candidates' sweeps depend on A and B only: start them now, beside the
         // aggregation and pattern work (joined before the injection)
         Bimp.alloc(static_cast<size_t>(A.nr) * k, c.s);
@@ -212,7 +240,9 @@ bool coarsen(Ctx& c, DHier& H, int level, const double* Bhat, Coarsened& out) {
         }
         amalgamate(c, S0, m, Sa);
         normalize_strength(c, Sa, S);
+        phase(c, "amalgamate", level);
         greedy_aggregate(c, S, agg);
+        phase(c, "aggregate", level);
         tally(c, static_cast<double>(S.nnz));  // hierarchy.hpp:197
     }
     if (agg.n_agg >= agg.n_nodes) {
@@ -245,6 +275,7 @@ bool coarsen(Ctx& c, DHier& H, int level, const double* Bhat, Coarsened& out) {
     DBuf<int32_t> droots;
     unamalgamate(c, N, agg, m, Nd0, droots);
     root_node_pattern(c, Nd0, droots.get(), agg.n_agg * m, Nd);
+    phase(c, "pattern", level);
 
     const int32_t n = A.nr;
     {
@@ -254,6 +285,7 @@ bool coarsen(Ctx& c, DHier& H, int level, const double* Bhat, Coarsened& out) {
         else
             improve_candidates(c, A, Bimp.get(), k, o.candidate_sweeps, o.cand_scheme, o.cand_weight, &L);
     }
+    phase(c, "candidates", level);
     DCsr T;
     DBuf<double> Bc;
     inject_tentative(c, agg, Nd, Bimp.get(), k, m, T, Bc);
@@ -269,6 +301,7 @@ bool coarsen(Ctx& c, DHier& H, int level, const double* Bhat, Coarsened& out) {
         out.P = std::move(Pp);
     }
 
+    phase(c, "energy_min", level);
     if (L.symmetric) {
         transpose(c, out.P, out.R);
         out.Bhc.alloc(Bc.size(), c.s);
@@ -295,10 +328,12 @@ bool coarsen(Ctx& c, DHier& H, int level, const double* Bhat, Coarsened& out) {
         transpose(c, Rt, out.R);
         out.Bhc = std::move(Bhc);
     }
+    phase(c, "R", level);
     {
         OpsScope scope(c, &crap);
         galerkin(c, out.R, A, out.P, out.Ac);
     }
+    phase(c, "RAP", level);
     L.ledger[0] = cagg;
     L.ledger[1] = ccand;
     L.ledger[2] = cint;
@@ -482,6 +517,11 @@ std::unique_ptr<DHier> rn_setup(Ctx& c, const DCsr& A, const double* B, int32_t 
     if (k < m) throw InvalidArgument("rn_setup: need at least block_size candidates");
     require_supported_relax(o.pre_scheme, "rn_setup");
     require_supported_relax(o.post_scheme, "rn_setup");
+    static const bool trace_phases = [] {
+        const char* e = std::getenv("AMGCU_PHASE_TRACE");
+        return e && e[0] == '1';
+    }();
+    c.phases.on = trace_phases;
     auto H = std::make_unique<DHier>();
     H->ctx = &c;
     H->o = o;
@@ -519,6 +559,7 @@ std::unique_ptr<DHier> rn_setup(Ctx& c, const DCsr& A, const double* B, int32_t 
         next.B = std::move(step.Bcoarse);
         next.symmetric = is_symmetric(c, next.A, 1e-12);
         H->lv.push_back(std::move(next));
+        phase(c, "next_level", l);
     }
     // finalize_hierarchy (hierarchy.hpp:164-172): relaxation workspaces and the
     // coarsest-level factorisation; its counts open the solve bucket (hierarchy.hpp:171)
@@ -551,7 +592,9 @@ std::unique_ptr<DHier> rn_setup(Ctx& c, const DCsr& A, const double* B, int32_t 
                    static_cast<const double*>(L.inv_diag.get()), L.wd_post.get());
         }
     }
+    phase(c, "finalize", static_cast<int>(H->lv.size()) - 1);
     coarse_factor(c, *H);
+    phase(c, "coarse_factor", static_cast<int>(H->lv.size()) - 1);
     for (DLevel& L : H->lv)
         if (L.evo_count) {
             L.evo_ops = evolution_ops_finish(c, L.A, *L.evo_count);
@@ -566,6 +609,8 @@ std::unique_ptr<DHier> rn_setup(Ctx& c, const DCsr& A, const double* B, int32_t 
         static const bool ht = std::getenv("AMGCU_HOST_TRACE") != nullptr;
         const auto t0 = std::chrono::steady_clock::now();
         prepare_solve(*H);
+        phase(c, "prepare_solve", static_cast<int>(H->lv.size()) - 1);
+        phase_report(c);
         if (ht)
             std::fprintf(stderr, "[host] prepare_solve %.3f ms\n",
                          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());

@@ -256,6 +256,60 @@ def test_improve_candidates(gpu_seq, port):
             assert got.data.tobytes() == want.data.tobytes(), (scheme, w)
 
 
+def wide_stencil(nx, ny, r, rng, interleave=1):
+    """(2r+1)^2-point couplings on an nx x ny grid (rows of up to (2r+1)^2 entries),
+    diagonally dominant, interleave > 1 repeats every node as that many coupled DOFs"""
+    t = []
+    m = interleave
+    for y in range(ny):
+        for x in range(nx):
+            for d in range(m):
+                row = (y * nx + x) * m + d
+                off = 0.0
+                for dy in range(-r, r + 1):
+                    for dx in range(-r, r + 1):
+                        xx, yy = x + dx, y + dy
+                        if 0 <= xx < nx and 0 <= yy < ny:
+                            for e in range(m):
+                                col = (yy * nx + xx) * m + e
+                                if col != row:
+                                    v = -rng.uniform(0.1, 1.0)
+                                    off += -v
+                                    t.append((row, col, v))
+                t.append((row, row, off + 1.0))
+    return from_triplets(nx * ny * m, nx * ny * m, t)
+
+
+@pytest.mark.parametrize("k", [1, 3])
+def test_gauss_seidel_segment_warps(gpu_seq, port, k, monkeypatch):
+    """Warp-per-segment kernel: long segments (grid rows) of rows longer than 32 entries
+    (7x7 couplings, and 5x5 with 2 interleaved DOFs per node), several sweeps, bitwise
+    (the single-CTA kernel, which would take these small cases, is switched off)"""
+    monkeypatch.setenv("AMGCU_GS_CTA", "0")
+    rng = np.random.default_rng(7)
+    for A_ in (wide_stencil(40, 12, 3, rng), wide_stencil(24, 10, 2, rng, interleave=2)):
+        assert max(np.diff(A_.row_offsets)) > 32
+        B = CandidateSet(A_.n_rows, k, rng.uniform(0.5, 1.5, A_.n_rows * k))
+        for sweeps in (1, 4):
+            got = api.improve_candidates(A_, B, sweeps, 1, 0.0, ctx=gpu_seq)
+            want = port.improve_candidates(A_, B, sweeps, 1, 0.0)
+            assert got.data.tobytes() == want.data.tobytes(), (A_.n_rows, k, sweeps)
+
+
+@pytest.mark.parametrize("k", [1, 3])
+def test_gauss_seidel_cta(gpu_seq, port, k):
+    """Single-CTA shared-memory kernel (small levels): forward and symmetric sweeps, wide
+    rows, interleaved DOFs, bitwise"""
+    rng = np.random.default_rng(11)
+    for A_ in (wide_stencil(12, 9, 3, rng), wide_stencil(8, 7, 2, rng, interleave=2), random_spd_sparse(40, 0.2, rng)):
+        B = CandidateSet(A_.n_rows, k, rng.uniform(0.5, 1.5, A_.n_rows * k))
+        for scheme in (1, 2):
+            for sweeps in (1, 4):
+                got = api.improve_candidates(A_, B, sweeps, scheme, 0.0, ctx=gpu_seq)
+                want = port.improve_candidates(A_, B, sweeps, scheme, 0.0)
+                assert got.data.tobytes() == want.data.tobytes(), (A_.n_rows, k, scheme, sweeps)
+
+
 def test_gauss_seidel_long_segments(gpu_seq, port):
     """Segments of many 32-row blocks (the solver / prefetcher / poller hand-offs
     across blocks), forward, symmetric and multi-column sweeps."""

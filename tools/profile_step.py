@@ -22,11 +22,13 @@ ctx = api.Context(0)
 for r in range(a.reps):
     t0 = time.perf_counter()
     h = api.setup(A, B, so, Bh, ctx=ctx)
+    ctx.synchronize()
+    ts = time.perf_counter() - t0
     x, rep = api.solve(h, b, None, vo)
     restarts = 0
     while vo.method == 2 and not rep.converged and not rep.diverged and restarts < a.max_restarts:
         x, rep = api.solve(h, b, x, vo)
         restarts += 1
     print(f"rep {r}: levels {h.n_levels()} its {rep.iterations} conv {rep.converged} "
-          f"wall {time.perf_counter() - t0:.3f}s launches {ctx.launch_count()}", flush=True)
+          f"wall {time.perf_counter() - t0:.3f}s (setup {ts:.3f}s) launches {ctx.launch_count()}", flush=True)
     del h
