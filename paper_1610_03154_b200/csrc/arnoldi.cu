@@ -33,17 +33,6 @@ __global__ void k_spmv_dinv(int32_t nr, const int32_t* __restrict__ rp, const in
     y[i] *= dinv[i];
 }
 
-void ensure_start_vector(Ctx& c, size_t n) {
-    if (c.arnoldi_v0_n >= n) return;
-    std::vector<double> v(n);
-    std::mt19937 gen(20240911u);
-    std::uniform_real_distribution<double> dist(-0.5, 0.5);
-    for (size_t i = 0; i < n; ++i) v[i] = 1.0 + dist(gen);
-    c.arnoldi_v0.alloc(n, c.s);
-    copy_h2d(c, c.arnoldi_v0.get(), v.data(), static_cast<int64_t>(n));
-    sync(c);
-    c.arnoldi_v0_n = n;
-}
 
 // The whole Arnoldi process in one cooperative launch (production mode),
 // bit-identical to the launch-per-step path: every reduction reproduces the
@@ -241,18 +230,33 @@ __global__ void __launch_bounds__(kArnThreads, 3)  // >= 3 blocks per SM: 444 bl
 
 }  // namespace
 
-double spectral_radius(Ctx& c, const DCsr& A, int steps, const double* dinv, int* built_out) {
+ArnoldiJob::~ArnoldiJob() {
+    if (done) {
+        cudaEventSynchronize(done);  // the buffers below are still being written
+        cudaEventDestroy(done);
+    }
+    if (hpin) cudaFreeHost(hpin);
+}
+
+// Queues the whole Arnoldi process on the context's current stream (c.s) and an
+// asynchronous copy of H to pinned memory; no host synchronisation, so it may run on a
+// side stream while the setup goes on (spectral_radius_finish collects it).  The start
+// vector must already cover n (ensure_start_vector on the main stream).
+std::unique_ptr<ArnoldiJob> spectral_radius_start(Ctx& c, const DCsr& A, int steps, const double* dinv) {
     if (A.nr != A.nc) throw InvalidArgument("spectral_radius_estimate: square matrix required");
     const int32_t n = A.nr;
-    if (n == 0) return 0.0;
+    auto job = std::make_unique<ArnoldiJob>();
+    job->n = n;
+    if (n == 0) return job;
     BlasFamilyScope scope(c, kProfArnoldiBlas1);
     const int m = std::min<int>(steps, n);
-    ensure_start_vector(c, static_cast<size_t>(n));
-    DBuf<double> V(static_cast<size_t>(n) * (m + 1), c.s);
-    DBuf<double> Hd(static_cast<size_t>(m + 1) * m + 1, c.s);
+    job->m = m;
+    if (c.arnoldi_v0_n < static_cast<size_t>(n)) throw std::logic_error("spectral_radius_start: start vector too short");
+    job->V.alloc(static_cast<size_t>(n) * (m + 1), c.s);
+    job->Hd.alloc(static_cast<size_t>(m + 1) * m + 1, c.s);
+    DBuf<double>& V = job->V;
+    DBuf<double>& Hd = job->Hd;
     AMG_CK(cudaMemsetAsync(Hd.get(), 0, sizeof(double) * ((m + 1) * m + 1), c.s));
-    int built = 0;
-    std::vector<double> H(static_cast<size_t>(m + 1) * m);
     // AMGCU_ARNOLDI_STEPS=1 forces the launch-per-step path (the cooperative kernel's reference)
     const char* steps_env = std::getenv("AMGCU_ARNOLDI_STEPS");
     if (!c.seq && !(steps_env && steps_env[0] == '1')) {
@@ -293,8 +297,6 @@ double spectral_radius(Ctx& c, const DCsr& A, int steps, const double* dinv, int
             r.bytes += m * (12.0 * A.nnz + 4.0 * (n + 1) + 24.0 * n) + (m * (m + 1) / 2.0) * 32.0 * n;
             r.pending.emplace_back(e0, e1);
         }
-        copy_d2h(c, H.data(), Hd.get(), static_cast<int64_t>(H.size()));
-        sync(c);
     } else {
         double* nrm = Hd.get() + (m + 1) * m;
         copy_d2d(c, V.get(), c.arnoldi_v0.get(), n);
@@ -321,9 +323,25 @@ double spectral_radius(Ctx& c, const DCsr& A, int steps, const double* dinv, int
             // remaining steps (on whatever the division produces) changes nothing that is used
             scale_recip_dev(c, hsub, w, n);
         }
-        copy_d2h(c, H.data(), Hd.get(), static_cast<int64_t>(H.size()));
-        sync(c);
     }
+    const size_t hn = static_cast<size_t>(m + 1) * m;
+    AMG_CK(cudaMallocHost(reinterpret_cast<void**>(&job->hpin), sizeof(double) * hn));
+    copy_d2h(c, job->hpin, Hd.get(), static_cast<int64_t>(hn));
+    AMG_CK(cudaEventCreateWithFlags(&job->done, cudaEventDisableTiming));
+    AMG_CK(cudaEventRecord(job->done, c.s));
+    return job;
+}
+
+double spectral_radius_finish(Ctx& c, ArnoldiJob& job, int* built_out) {
+    if (job.n == 0) {
+        if (built_out) *built_out = 0;
+        return 0.0;
+    }
+    const int m = job.m;
+    AMG_CK(cudaEventSynchronize(job.done));
+    ++c.syncs;
+    std::vector<double> H(job.hpin, job.hpin + static_cast<size_t>(m + 1) * m);
+    int built = 0;
     for (int j = 0; j < m; ++j) {
         built = j + 1;
         if (H[static_cast<size_t>(j + 1) * m + j] < 1e-14) break;
@@ -337,6 +355,25 @@ double spectral_radius(Ctx& c, const DCsr& A, int steps, const double* dinv, int
     double rho = 0.0;
     for (int i = 0; i < built; ++i) rho = std::max(rho, std::abs(std::complex<double>(wr[i], wi[i])));
     return rho;
+}
+
+void ensure_start_vector(Ctx& c, size_t n) {
+    if (c.arnoldi_v0_n >= n) return;
+    std::vector<double> v(n);
+    std::mt19937 gen(20240911u);
+    std::uniform_real_distribution<double> dist(-0.5, 0.5);
+    for (size_t i = 0; i < n; ++i) v[i] = 1.0 + dist(gen);
+    c.arnoldi_v0.alloc(n, c.s);
+    copy_h2d(c, c.arnoldi_v0.get(), v.data(), static_cast<int64_t>(n));
+    sync(c);
+    c.arnoldi_v0_n = n;
+}
+
+double spectral_radius(Ctx& c, const DCsr& A, int steps, const double* dinv, int* built_out) {
+    if (A.nr != A.nc) throw InvalidArgument("spectral_radius_estimate: square matrix required");
+    ensure_start_vector(c, static_cast<size_t>(A.nr));
+    auto job = spectral_radius_start(c, A, steps, dinv);
+    return spectral_radius_finish(c, *job, built_out);
 }
 
 }  // namespace amgcu

@@ -17,6 +17,7 @@ struct DLevel {
     bool symmetric = true;
     double rho = std::nan("");  // rho(D^-1 A), cached
     int rho_built = 0;             // its Arnoldi dimension (the reference's SpMV count per estimate)
+    std::unique_ptr<ArnoldiJob> rho_job;  // rho in flight on the side stream (setup.cu: rho_start_async)
     // WorkLedger raw op counts of coarsening this level (work.hpp buckets 0..3); the
     // evolution-SOC part of bucket 0 is counted on demand (evo_steps > 0)
     double ledger[4] = {0.0, 0.0, 0.0, 0.0};

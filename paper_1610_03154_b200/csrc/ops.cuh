@@ -102,6 +102,23 @@ void aggregate_indicator(Ctx& c, const DAgg& agg, DCsr& Cm);
 // ---- spectral radius (arnoldi.cu) ----------------------------------------------------
 // *built_out (optional) receives the Krylov dimension reached (the reference's SpMV count)
 double spectral_radius(Ctx& c, const DCsr& A, int steps, const double* dinv, int* built_out = nullptr);
+// the same in two halves: start queues the Arnoldi process and the copy of H on c.s (no
+// host synchronisation: it may run on a side stream), finish waits and takes the
+// eigenvalues.  The start vector must cover n first (ensure_start_vector, main stream).
+struct ArnoldiJob {
+    int32_t n = 0;
+    int m = 0;
+    DBuf<double> V, Hd;
+    double* hpin = nullptr;
+    cudaEvent_t done = nullptr;
+    ArnoldiJob() = default;
+    ArnoldiJob(const ArnoldiJob&) = delete;
+    ArnoldiJob& operator=(const ArnoldiJob&) = delete;
+    ~ArnoldiJob();
+};
+void ensure_start_vector(Ctx& c, size_t n);
+std::unique_ptr<ArnoldiJob> spectral_radius_start(Ctx& c, const DCsr& A, int steps, const double* dinv);
+double spectral_radius_finish(Ctx& c, ArnoldiJob& job, int* built_out);
 
 // ---- relaxation (relax.cu) -----------------------------------------------------------
 // sync-free wavefront Gauss-Seidel sweeps (relaxation.hpp:115-127) over k columns

@@ -30,13 +30,16 @@ struct SyncSites {
     cudaEvent_t open_ev = nullptr;
     std::chrono::steady_clock::time_point open_t;  // host time the synchronisation returned
     std::map<std::string, double> host_ms;          // host time from the return to the next launch
+    std::map<std::string, double> host_max, idle_max;  // the largest single gap of a site
     bool on = std::getenv("AMGCU_SYNC_TRACE") != nullptr;
     void resolve() {
         for (auto& p : pending) {
             float ms = 0.f;
             if (cudaEventSynchronize(p.second.second) == cudaSuccess &&
-                cudaEventElapsedTime(&ms, p.second.first, p.second.second) == cudaSuccess)
+                cudaEventElapsedTime(&ms, p.second.first, p.second.second) == cudaSuccess) {
                 idle_ms[p.first] += ms;
+                idle_max[p.first] = std::max<double>(idle_max[p.first], ms);
+            }
             cudaEventDestroy(p.second.first);
             cudaEventDestroy(p.second.second);
         }
@@ -47,8 +50,9 @@ struct SyncSites {
         resolve();
         double tot = 0.0;
         for (auto& kv : n) {
-            std::fprintf(stderr, "sync %6ld  idle %8.3f ms  host %8.3f ms  %s\n", kv.second, idle_ms[kv.first],
-                         host_ms[kv.first], kv.first.c_str());
+            std::fprintf(stderr, "sync %6ld  idle %8.3f ms (max %7.3f)  host %8.3f ms (max %7.3f)  %s\n", kv.second,
+                         idle_ms[kv.first], idle_max[kv.first], host_ms[kv.first], host_max[kv.first],
+                         kv.first.c_str());
             tot += idle_ms[kv.first];
         }
         std::fprintf(stderr, "sync total GPU idle after synchronisations: %.3f ms\n", tot);
@@ -83,8 +87,9 @@ void gap_before_launch(cudaStream_t s) {
     SyncSites& ss = sync_sites();
     std::lock_guard<std::mutex> g(ss.m);
     if (!ss.open_ev) return;
-    ss.host_ms[ss.open_site] +=
-        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - ss.open_t).count();
+    const double gap = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - ss.open_t).count();
+    ss.host_ms[ss.open_site] += gap;
+    ss.host_max[ss.open_site] = std::max(ss.host_max[ss.open_site], gap);
     cudaEvent_t e;
     cudaEventCreate(&e);
     cudaEventRecord(e, s);

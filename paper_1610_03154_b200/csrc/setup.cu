@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <string>
 
+#include <cooperative_groups.h>
 #include <cusolverDn.h>
 
 #include "hier.cuh"
@@ -357,6 +358,143 @@ __global__ void k_identity(int32_t n, double* __restrict__ I) {
     I[t] = (t / n == t % n) ? 1.0 : 0.0;
 }
 
+// Inverse of the coarsest operator by Gauss-Jordan elimination with partial pivoting on
+// [A | I] (n x 2n, row-major, L2-resident for the sizes it serves), one cooperative
+// launch.  Step k: block 0 finds the pivot row p (largest |M(i,k)|, i >= k, lowest i on
+// ties); every thread then swaps rows k and p, scales the new row k by 1 / pivot and
+// saves column k (the elimination factors); finally every row i != k subtracts
+// f_i x row k over the columns that can still change (A's columns after k, and I's).
+// A's columns <= k are never read again.  status[0] = 1 on a zero pivot (singular).
+constexpr int kGjThreads = 256;
+
+__global__ void __launch_bounds__(kGjThreads)
+    k_gauss_jordan(int32_t n, double* __restrict__ M, double* __restrict__ f, double* __restrict__ piv,
+                   int32_t* __restrict__ prow, int32_t* __restrict__ status) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    const int64_t w = 2 * static_cast<int64_t>(n);
+    const int64_t gtid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t gthreads = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    __shared__ double sv[kGjThreads];
+    __shared__ int32_t si[kGjThreads];
+    for (int32_t k = 0; k < n; ++k) {
+        if (blockIdx.x == 0) {
+            double best = -1.0;
+            int32_t bi = n;
+            for (int32_t i = k + threadIdx.x; i < n; i += kGjThreads) {
+                const double v = fabs(M[i * w + k]);
+                if (v > best) {
+                    best = v;
+                    bi = i;
+                }
+            }
+            sv[threadIdx.x] = best;
+            si[threadIdx.x] = bi;
+            __syncthreads();
+            for (int off = kGjThreads / 2; off > 0; off >>= 1) {
+                if (threadIdx.x < off) {
+                    const double o = sv[threadIdx.x + off];
+                    const int32_t oi = si[threadIdx.x + off];
+                    if (o > sv[threadIdx.x] || (o == sv[threadIdx.x] && oi < si[threadIdx.x])) {
+                        sv[threadIdx.x] = o;
+                        si[threadIdx.x] = oi;
+                    }
+                }
+                __syncthreads();
+            }
+            if (threadIdx.x == 0) {
+                const int32_t p = si[0];
+                *prow = p;
+                *piv = M[p * w + k];
+                if (!(sv[0] > 0.0)) *status = 1;
+            }
+        }
+        grid.sync();
+        if (*reinterpret_cast<volatile int32_t*>(status)) return;  // uniform: every block sees it
+        const int32_t p = *reinterpret_cast<volatile int32_t*>(prow);
+        const double inv = 1.0 / *reinterpret_cast<volatile double*>(piv);
+        // swap rows k and p (scaling the new row k), and save column k
+        for (int64_t j = k + gtid; j < w; j += gthreads) {
+            const double ak = M[k * w + j], ap = M[p * w + j];
+            M[k * w + j] = ap * inv;
+            if (p != k) M[p * w + j] = ak;
+        }
+        for (int64_t i = gtid; i < n; i += gthreads) {
+            if (i == k) continue;
+            f[i] = (i == p) ? M[k * w + k] : M[i * w + k];
+        }
+        grid.sync();
+        // eliminate: columns k+1 .. 2n-1 of every row but k
+        const int64_t cols = w - (k + 1);
+        const int64_t total = static_cast<int64_t>(n) * cols;
+        for (int64_t t = gtid; t < total; t += gthreads) {
+            const int64_t i = t / cols;
+            if (i == k) continue;
+            const int64_t j = k + 1 + (t - i * cols);
+            M[i * w + j] -= f[i] * M[k * w + j];
+        }
+        grid.sync();
+    }
+}
+
+__global__ void k_gj_extract(int32_t n, const double* __restrict__ M, double* __restrict__ inv) {
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= static_cast<int64_t>(n) * n) return;
+    const int64_t i = t / n, j = t - i * n;
+    inv[t] = M[i * 2 * static_cast<int64_t>(n) + n + j];
+}
+
+__global__ void k_gj_init(int32_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                          const double* __restrict__ va, double* __restrict__ M) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double* row = M + static_cast<int64_t>(i) * 2 * n;
+    for (int32_t p = rp[i]; p < rp[i + 1]; ++p) row[ci[p]] = va[p];
+    row[n + i] = 1.0;
+}
+
+constexpr int32_t kGjMax = 4096;  // [A | I] of 4096 rows is 268 MB; above, LU through cuSOLVER
+
+// Gauss-Jordan inverse of the CSR operator A (n <= kGjMax) into inv (row-major); false
+// when a zero pivot shows it singular
+bool gauss_jordan_inverse(Ctx& c, const DCsr& A, double* inv) {
+    const int32_t n = A.nr;
+    DBuf<double> M(static_cast<size_t>(n) * 2 * n, c.s), f(static_cast<size_t>(n), c.s), piv(1, c.s);
+    DBuf<int32_t> prow(1, c.s), status(1, c.s);
+    AMG_CK(cudaMemsetAsync(M.get(), 0, sizeof(double) * n * 2 * n, c.s));
+    AMG_CK(cudaMemsetAsync(status.get(), 0, sizeof(int32_t), c.s));
+    launch(c, k_gj_init, blocks_for(n, 128), 128, 0, n, A.rp.get(), A.ci.get(), A.va.get(), M.get());
+    int per_sm = 0;
+    AMG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gauss_jordan, kGjThreads, 0));
+    const int grid = std::max(1, std::min(per_sm, 4) * c.sms);
+    int32_t nn = n;
+    double* pM = M.get();
+    double* pf = f.get();
+    double* ppiv = piv.get();
+    int32_t* pprow = prow.get();
+    int32_t* pst = status.get();
+    void* args[] = {&nn, &pM, &pf, &ppiv, &pprow, &pst};
+    const double bytes = 8.0 * 2.0 * static_cast<double>(n) * n * 2.0 * 0.5 * n;
+    if (c.profile && ((c.prof_mask >> kProfCoarseSolve) & 1u)) {
+        cudaEvent_t e0 = prof_event(c), e1 = prof_event(c);
+        AMG_CK(cudaEventRecord(e0, c.s));
+        AMG_CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_gauss_jordan), dim3(grid), dim3(kGjThreads), args,
+                                           0, c.s));
+        AMG_CK(cudaEventRecord(e1, c.s));
+        c.prof[kProfCoarseSolve].launches += 1;
+        c.prof[kProfCoarseSolve].bytes += bytes;
+        c.prof[kProfCoarseSolve].pending.emplace_back(e0, e1);
+    } else {
+        AMG_CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_gauss_jordan), dim3(grid), dim3(kGjThreads), args,
+                                           0, c.s));
+    }
+    ++c.launches;
+    if (read_scalar(c, status.get())) return false;
+    launch(c, k_gj_extract, blocks_for(static_cast<int64_t>(n) * n, 256), 256, 0, n,
+           static_cast<const double*>(M.get()), inv);
+    return true;
+}
+
 constexpr int32_t kCoarseGpuThreshold = 512;
 
 // inverse of the row-major D (n x n) into inv (row-major).  Reading D as
@@ -395,6 +533,11 @@ void require_supported_relax(int scheme, const char* who) {
 
 double level_rho(Ctx& c, DLevel& L) {
     if (!std::isnan(L.rho)) return L.rho;
+    if (L.rho_job) {
+        L.rho = spectral_radius_finish(c, *L.rho_job, &L.rho_built);
+        L.rho_job.reset();
+        return L.rho;
+    }
     if (L.inv_diag.empty()) {
         L.inv_diag.alloc(static_cast<size_t>(L.A.nr), c.s);
         inverse_diagonal(c, L.A, L.inv_diag.get(), "spectral_radius_estimate: zero diagonal at row ");
@@ -404,6 +547,40 @@ double level_rho(Ctx& c, DLevel& L) {
         L.rho = spectral_radius(c, L.A, 15, L.inv_diag.get(), &L.rho_built);
     }
     return L.rho;
+}
+
+// The smoother weights need rho(D^-1 A) of every level but the coarsest only at
+// finalize_hierarchy; when nothing earlier needs it (no spectral evolution weights, no
+// Jacobi candidates), each level's Arnoldi starts on the side stream as soon as the level
+// exists and overlaps the coarsening of the levels below it (exact-order reductions
+// only: the tree reductions share one scratch between streams).  level_rho collects it.
+bool rho_overlap_applies(Ctx& c, const amgcu_setup_options& o) {
+    static const bool off = [] {
+        const char* e = std::getenv("AMGCU_RHO_OVERLAP");
+        return e && e[0] == '0';
+    }();
+    const bool weights = (o.pre_scheme == 0 && o.pre_weight == 0.0) || (o.post_scheme == 0 && o.post_weight == 0.0);
+    const bool early = (o.strength_measure == 2 && o.weighting == 0) || (o.cand_scheme == 0 && o.cand_weight == 0.0);
+    return !off && c.seq && c.side && weights && !early;
+}
+
+void rho_start_async(Ctx& c, DLevel& L) {
+    if (!std::isnan(L.rho) || L.rho_job || L.A.nr == 0) return;
+    if (L.inv_diag.empty()) {
+        DBuf<double> d(static_cast<size_t>(L.A.nr), c.s);
+        // a zero diagonal is reported where the reference meets it (finalize): not here
+        if (inverse_diagonal_check(c, L.A, d.get()) >= 0) return;
+        L.inv_diag = std::move(d);
+    }
+    cudaEvent_t ready;
+    AMG_CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    cudaError_t e = cudaEventRecord(ready, c.s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(c.side, ready, 0);
+    cudaEventDestroy(ready);
+    AMG_CK(e);
+    OpsScope none(c, nullptr);  // counted per reference call site (rho_tallied)
+    StreamScope on_side(c, c.side);
+    L.rho_job = spectral_radius_start(c, L.A, 15, L.inv_diag.get());
 }
 
 // one reference call of spectral_radius_estimate on the level (spectral.hpp:44: one SpMV per
@@ -481,21 +658,24 @@ void normalize_candidates(Ctx& c, double* B, int32_t n, int32_t k) {
 
 
 // CoarseSolver::factor (hierarchy.hpp:59-68).  The coarsest operator is
-// inverted once; each cycle then applies the inverse with one dense GEMV.
-// Small levels: complete orthogonal decomposition on the host (the reference's
-// algorithm, also valid for singular operators).  Large levels (a stagnated
-// hierarchy can stop at ~10^4 rows): LU with partial pivoting on the GPU
-// (cuSOLVER getrf/getrs), falling back to the COD if the LU is singular.
+// inverted once; each cycle then applies the inverse with one dense GEMV (a single
+// pass over n^2 doubles, where triangular solves would take n dependent steps).
+// Up to 512 rows: complete orthogonal decomposition on the host (the reference's
+// algorithm, also valid for singular operators).  513..4096 rows: Gauss-Jordan with
+// partial pivoting in one cooperative launch (k_gauss_jordan).  Above (a stagnated
+// hierarchy can stop at ~10^4 rows, C1): LU with partial pivoting through cuSOLVER
+// getrf/getrs.  A singular operator falls back to the COD.
 void coarse_factor(Ctx& c, DHier& H) {
     const DLevel& Lc = H.lv.back();
     const int32_t nL = Lc.A.nr;
     H.coarse_n = nL;
     H.coarse_pinv.alloc(static_cast<size_t>(nL) * nL, c.s);
+    if (nL > kCoarseGpuThreshold && nL <= kGjMax && gauss_jordan_inverse(c, Lc.A, H.coarse_pinv.get())) return;
     // dense row-major copy of A_L
     DBuf<double> D(static_cast<size_t>(nL) * nL, c.s);
     AMG_CK(cudaMemsetAsync(D.get(), 0, sizeof(double) * nL * nL, c.s));
     launch(c, k_densify, blocks_for(nL, 128), 128, 0, nL, Lc.A.rp.get(), Lc.A.ci.get(), Lc.A.va.get(), D.get());
-    if (nL > kCoarseGpuThreshold && dense_inverse_gpu(c, D.get(), nL, H.coarse_pinv.get())) return;
+    if (nL > kGjMax && dense_inverse_gpu(c, D.get(), nL, H.coarse_pinv.get())) return;
     std::vector<double> hD(static_cast<size_t>(nL) * nL);
     copy_d2h(c, hD.data(), D.get(), static_cast<int64_t>(hD.size()));
     sync(c);
@@ -505,6 +685,41 @@ void coarse_factor(Ctx& c, DHier& H) {
     cod.pseudo_inverse(pinv.data());
     copy_h2d(c, H.coarse_pinv.get(), pinv.data(), static_cast<int64_t>(pinv.size()));
     sync(c);
+}
+
+// The setup's temporaries come from the stream-ordered pool (release threshold raised at
+// context creation, so freed memory stays mapped).  A request no free block can hold
+// makes the pool map new memory, which can stall the host for hundreds of ms (the
+// SpGEMM expansion buffers of a 2 M-row level are ~1 GB).  Reserving one large block up
+// front, sized from the operator (AMGCU_POOL_RESERVE_MB overrides), lets the later
+// requests be carved out of mapped memory.
+void reserve_pool(Ctx& c, const DCsr& A, int32_t k) {
+    cudaMemPool_t pool;
+    AMG_CK(cudaDeviceGetDefaultMemPool(&pool, c.device));
+    uint64_t reserved = 0;
+    AMG_CK(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved));
+    double want = 48.0 * (12.0 * static_cast<double>(A.nnz) + 8.0 * static_cast<double>(A.nr) * (k + 4));
+    if (const char* e = std::getenv("AMGCU_POOL_RESERVE_MB")) want = std::atof(e) * 1048576.0;
+    size_t free_b = 0, total_b = 0;
+    AMG_CK(cudaMemGetInfo(&free_b, &total_b));
+    want = std::min(want, 0.5 * static_cast<double>(free_b) + static_cast<double>(reserved));
+    if (static_cast<double>(reserved) >= want) return;
+    void* p = nullptr;
+    if (cudaMallocAsync(&p, static_cast<size_t>(want) - reserved, c.s) != cudaSuccess) {
+        cudaGetLastError();
+        return;
+    }
+    AMG_CK(cudaFreeAsync(p, c.s));
+}
+
+void pool_report(Ctx& c) {
+    cudaMemPool_t pool;
+    AMG_CK(cudaDeviceGetDefaultMemPool(&pool, c.device));
+    uint64_t used_high = 0, reserved = 0;
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &used_high);
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
+    std::fprintf(stderr, "[host] pool: used high %.1f MB, reserved %.1f MB\n", used_high / 1048576.0,
+                 reserved / 1048576.0);
 }
 
 std::unique_ptr<DHier> rn_setup(Ctx& c, const DCsr& A, const double* B, int32_t k, const double* left,
@@ -522,6 +737,7 @@ std::unique_ptr<DHier> rn_setup(Ctx& c, const DCsr& A, const double* B, int32_t 
         return e && e[0] == '1';
     }();
     c.phases.on = trace_phases;
+    reserve_pool(c, A, k);
     auto H = std::make_unique<DHier>();
     H->ctx = &c;
     H->o = o;
@@ -535,6 +751,11 @@ std::unique_ptr<DHier> rn_setup(Ctx& c, const DCsr& A, const double* B, int32_t 
         L0.B.alloc(static_cast<size_t>(A.nr) * k, c.s);
         copy_d2d(c, L0.B.get(), B, static_cast<int64_t>(A.nr) * k);
         L0.symmetric = is_symmetric(c, L0.A, 1e-12);
+    }
+    const bool rho_async = rho_overlap_applies(c, o);
+    if (rho_async) {
+        ensure_start_vector(c, static_cast<size_t>(A.nr));
+        if (A.nr > o.max_size && o.max_levels > 1) rho_start_async(c, H->lv.back());
     }
     DBuf<double> Bhat(static_cast<size_t>(A.nr) * k, c.s);
     copy_d2d(c, Bhat.get(), left ? left : B, static_cast<int64_t>(A.nr) * k);
@@ -559,6 +780,8 @@ std::unique_ptr<DHier> rn_setup(Ctx& c, const DCsr& A, const double* B, int32_t 
         next.B = std::move(step.Bcoarse);
         next.symmetric = is_symmetric(c, next.A, 1e-12);
         H->lv.push_back(std::move(next));
+        if (rho_async && H->lv.back().A.nr > o.max_size && static_cast<int>(H->lv.size()) < o.max_levels)
+            rho_start_async(c, H->lv.back());
         phase(c, "next_level", l);
     }
     // finalize_hierarchy (hierarchy.hpp:164-172): relaxation workspaces and the
@@ -611,6 +834,7 @@ std::unique_ptr<DHier> rn_setup(Ctx& c, const DCsr& A, const double* B, int32_t 
         prepare_solve(*H);
         phase(c, "prepare_solve", static_cast<int>(H->lv.size()) - 1);
         phase_report(c);
+        if (ht) pool_report(c);
         if (ht)
             std::fprintf(stderr, "[host] prepare_solve %.3f ms\n",
                          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());

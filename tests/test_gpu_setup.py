@@ -287,3 +287,24 @@ def test_setup_solve_remaining_schemes(gpu_seq, port, relax):
         assert rel_max_err(rg.residual_history, ro.residual_history) <= 1e-10
         assert rel_max_err(xg, xo) <= 1e-10
         assert hg.ledger().tobytes() == ho.ledger().tobytes()
+
+
+@pytest.mark.parametrize("cfg,size,max_size", [(2, 96, 1600), (5, 96, 2200), (1, 64, 1000)], ids=["C2-96", "C5-96", "C1-64"])
+def test_coarse_gauss_jordan(gpu, port, cfg, size, max_size):
+    """coarsest level of 513..4096 rows: inverted by the Gauss-Jordan kernel (the CPU side
+    by the reference's COD): hierarchy bitwise, solve to 1e-10 with the same iterations"""
+    A, B, Bh, b = api.generate_config(cfg, size)
+    so, vo = api.config_options(cfg)
+    so.max_size = max_size
+    hg = api.setup(A, B, so, Bh, ctx=gpu)
+    ho = port.setup(A, B, so, Bh)
+    n_coarse = hg.matrix(hg.n_levels() - 1, 0).n_rows
+    assert 512 < n_coarse <= 4096, n_coarse
+    assert hg.n_levels() == ho.n_levels()
+    for l in range(hg.n_levels()):
+        assert hg.matrix(l, 0) == ho.matrix(l, 0)
+    xg, rg = api.solve(hg, b, None, vo)
+    xo, ro = port.solve(ho, b, None, vo)
+    assert rg.iterations == ro.iterations and rg.converged == ro.converged
+    assert rel_max_err(rg.residual_history, ro.residual_history) <= 1e-10
+    assert rel_max_err(xg, xo) <= 1e-10

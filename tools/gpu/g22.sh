@@ -1,0 +1,1 @@
+AMGCU_SYNC_TRACE=1 AMGCU_PHASE_TRACE=1 timeout 600 python tools/profile_step.py --config 5 --size 1024 --reps 10 > gpurun_out/g22.log 2>&1

@@ -15,10 +15,13 @@ ap.add_argument("--config", type=int, default=2)
 ap.add_argument("--size", type=int, default=1024)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--max-restarts", type=int, default=20)
+ap.add_argument("--no-cand-overlap", action="store_true")
 a = ap.parse_args()
 A, B, Bh, b = api.generate_config(a.config, a.size)
 so, vo = api.config_options(a.config)
 ctx = api.Context(0)
+if a.no_cand_overlap:
+    ctx.set_candidate_overlap(False)
 for r in range(a.reps):
     t0 = time.perf_counter()
     h = api.setup(A, B, so, Bh, ctx=ctx)
