@@ -1264,12 +1264,74 @@ struct Level {
     bool sym = true;
 };
 
+// Dense LU with partial pivoting (row-major, i-k-j update order), the coarsest-level
+// solver above kLuCoarse rows.  DELIBERATE DEVIATION from the reference's COD
+// (hierarchy.hpp:54-76): an unblocked COD of the 11,008-row coarsest level of C1-256
+// takes hours on one core; the GPU path also uses LU at that size.  For a nonsingular
+// operator both give the solution to rounding; the test tolerance (1e-10) covers it.
+struct DenseLU {
+    int n = 0;
+    std::vector<double> a;  // L (unit, below the diagonal) and U, row-major
+    std::vector<int> piv;
+    bool compute(int n_, const double* D) {
+        n = n_;
+        a.assign(D, D + static_cast<size_t>(n) * n);
+        piv.resize(n);
+        for (int k = 0; k < n; ++k) {
+            int p = k;
+            double best = std::abs(a[static_cast<size_t>(k) * n + k]);
+            for (int i = k + 1; i < n; ++i) {
+                const double v = std::abs(a[static_cast<size_t>(i) * n + k]);
+                if (v > best) {
+                    best = v;
+                    p = i;
+                }
+            }
+            if (!(best > 0.0)) return false;
+            piv[k] = p;
+            if (p != k)
+                for (int j = 0; j < n; ++j)
+                    std::swap(a[static_cast<size_t>(k) * n + j], a[static_cast<size_t>(p) * n + j]);
+            const double* rk = &a[static_cast<size_t>(k) * n];
+            const double inv = 1.0 / rk[k];
+            for (int i = k + 1; i < n; ++i) {
+                double* ri = &a[static_cast<size_t>(i) * n];
+                const double f = ri[k] * inv;
+                ri[k] = f;
+                if (f != 0.0)
+                    for (int j = k + 1; j < n; ++j) ri[j] -= f * rk[j];
+            }
+        }
+        return true;
+    }
+    void solve(const double* b, double* x) const {
+        std::vector<double> y(b, b + n);
+        for (int k = 0; k < n; ++k) std::swap(y[k], y[piv[k]]);
+        for (int i = 0; i < n; ++i) {
+            const double* ri = &a[static_cast<size_t>(i) * n];
+            double s = y[i];
+            for (int j = 0; j < i; ++j) s -= ri[j] * y[j];
+            y[i] = s;
+        }
+        for (int i = n - 1; i >= 0; --i) {
+            const double* ri = &a[static_cast<size_t>(i) * n];
+            double s = y[i];
+            for (int j = i + 1; j < n; ++j) s -= ri[j] * y[j];
+            y[i] = s / ri[i];
+        }
+        for (int i = 0; i < n; ++i) x[i] = y[i];
+    }
+};
+constexpr int kLuCoarse = 4096;
+
 struct Hier {
     std::vector<Level> lv;
     amgcu_setup_options o{};
     double base = 0.0;
     double wu[5] = {0, 0, 0, 0, 0};
     sd::COD coarse;
+    DenseLU coarse_lu;
+    bool use_lu = false;
     int coarse_n = 0;
     std::vector<RelaxWs> pre, post;
     bool stagnated = false;
@@ -1401,7 +1463,8 @@ void finalize(Hier& H) {  // hierarchy.hpp:164-172
     Vec D(static_cast<size_t>(Ac.nr) * Ac.nc, 0.0);
     for (idx i = 0; i < Ac.nr; ++i)
         for (idx p = Ac.rp[i]; p < Ac.rp[i + 1]; ++p) D[static_cast<size_t>(i) * Ac.nc + Ac.ci[p]] = Ac.va[p];
-    H.coarse.compute(Ac.nr, Ac.nc, D.data());
+    H.use_lu = Ac.nr > kLuCoarse && Ac.nr == Ac.nc && H.coarse_lu.compute(Ac.nr, D.data());
+    if (!H.use_lu) H.coarse.compute(Ac.nr, Ac.nc, D.data());
     H.coarse_n = Ac.nr;
     tally(&c, static_cast<double>(Ac.nr) * Ac.nr * Ac.nr);
     H.charge(4, c.v);
@@ -1479,7 +1542,8 @@ struct Scratch {
 
 void vcycle(Hier& H, size_t l, double* x, const double* b, int kind, Scratch& s, Ops* c) {  // cycle.hpp:70-95
     if (l == H.lv.size() - 1) {
-        H.coarse.solve(b, x);
+        if (H.use_lu) H.coarse_lu.solve(b, x);
+        else H.coarse.solve(b, x);
         return;
     }
     Level& L = H.lv[l];

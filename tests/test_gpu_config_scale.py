@@ -9,10 +9,13 @@ coarsest-level solve is the one place the GPU differs by design (an explicit inv
 instead of the reference's per-cycle COD solve), so the solve-phase numbers are
 compared to 1e-10, not bitwise.
 """
+import os
+
 import numpy as np
 import pytest
 
 import paper_1610_03154_b200.api as api
+from tests.golden.make_full_dumps import FULL as FULL_DUMPS, OUT as DUMP_DIR, XSTRIDE, hierarchy_hashes, problem_key
 from tests.helpers import rel_max_err, same_structure
 
 pytestmark = pytest.mark.gpu
@@ -47,19 +50,52 @@ def _bitwise_hierarchy(hg, ho):
         assert hg.symmetric(l) == ho.symmetric(l)
 
 
-FULL = [(1, 256, 0), (2, 1024, 0), (3, 2048, 2), (4, 2048, 3), (5, 1024, 0)]
-FULL_IDS = ["C1-256", "C2-1024", "C3-2048", "C4-2048", "C5-1024"]
-
-
-@pytest.mark.parametrize("cfg,size,restarts", FULL + [(1, 96, 0), (3, 512, 2), (4, 512, 2)],
-                         ids=FULL_IDS + ["C1-96", "C3-512", "C4-512"])
+@pytest.mark.parametrize("cfg,size,restarts", [(1, 96, 0), (3, 512, 2), (4, 512, 2)], ids=["C1-96", "C3-512", "C4-512"])
 def test_default_mode_bitwise(gpu, port, cfg, size, restarts):
+    """reduced sizes against the CPU restatement run here"""
     hg, ho, b, vo = _setup_both(cfg, size, gpu, port)
     _bitwise_hierarchy(hg, ho)
     xg, rg, xo, ro = _solve_both(hg, ho, b, vo, port, restarts)
     assert rg.iterations == ro.iterations and rg.converged == ro.converged
     assert rel_max_err(rg.residual_history, ro.residual_history) <= 1e-10
     assert rel_max_err(xg, xo) <= 1e-10
+
+
+@pytest.mark.parametrize("name", list(FULL_DUMPS))
+def test_full_size_against_dump(gpu, name):
+    """BASELINE sizes (C1-256, C2-1024, C3-2048, C4-2048, C5-1024) against the committed
+    dumps of the CPU restatement (tests/golden/make_full_dumps.py): every array of every
+    level's A, P, R, B, Bc bit-identical (SHA-256), symmetry flags and level count equal,
+    the same iteration count, residual history and (converged solves) x within 1e-10"""
+    cfg, size, restarts = FULL_DUMPS[name]
+    d = np.load(os.path.join(DUMP_DIR, f"{name.lower()}_port.npz"))
+    A, B, Bh, b = api.generate_config(cfg, size)
+    so, vo = api.config_options(cfg)
+    assert str(d["problem"]) == problem_key(A, B, Bh, b, so, vo), "generator or options changed: regenerate the dump"
+    hg = api.setup(A, B, so, Bh, ctx=gpu)
+    assert [hg.n_levels(), int(hg.stagnated)] == list(d["levels"])
+    got = hierarchy_hashes(hg)
+    want = dict(zip(d["keys"].tolist(), d["values"].tolist()))
+    assert sorted(got) == sorted(want)
+    bad = [k for k in want if got[k] != want[k]]
+    assert not bad, bad[:8]
+    x, rg = api.solve(hg, b, None, vo)
+    hist = list(rg.residual_history)
+    its = rg.iterations
+    for _ in range(restarts):
+        if rg.converged or rg.diverged:
+            break
+        x, rg = api.solve(hg, b, x, vo)
+        hist += list(rg.residual_history)
+        its += rg.iterations
+    assert [its, int(rg.converged)] == list(d["its"][:2])
+    assert rel_max_err(np.array(hist), d["hist"]) <= 1e-10
+    if rg.converged:
+        assert rel_max_err(x[::XSTRIDE], d["x_sample"]) <= 1e-10
+    # C3's FGMRES(30) stagnates (DESIGN.md §7) in both implementations: the iterate then
+    # drifts along directions the residual hardly sees (the coarsest solves differ by
+    # rounding: inverse on the GPU, COD on the CPU), so only the residual history --
+    # equal to 1e-10 above -- is comparable, not x
 
 
 @pytest.mark.parametrize("cfg,size", [(2, 1024), (5, 1024)], ids=["C2-1024", "C5-1024"])
