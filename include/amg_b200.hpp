@@ -10,10 +10,15 @@
 // compiles unchanged.  Everything runs on the GPU behind include/amgcu.h;
 // status codes come back as the reference's exception types.
 //
-// Differences by design: Hierarchy owns device-resident levels; its `levels`
-// member is a host mirror filled on demand by Hierarchy::download().
+// Hierarchy owns the device-resident levels; like the reference's, its `levels`,
+// `ledger`, `options` and `stagnated` members are filled by setup (levels: a host
+// mirror downloaded once at the end of setup) and `ledger` is charged by every solve
+// and cycle.  Callers of the reference's API (proj/tools/amg_main.cpp:249-282,
+// proj/tests/acceptance.cpp, complexity.hpp) therefore compile and behave unchanged;
+// tests/cpp/run_single.cpp exercises that surface.
 #pragma once
 
+#include <algorithm>
 #include <array>
 #include <cmath>
 #include <cstdint>
@@ -43,6 +48,21 @@ struct SparseMatrix {  // sparse.hpp:25-62
         : n_rows(rows), n_cols(cols), row_offsets(static_cast<std::size_t>(rows) + 1, 0) {}
     index_t nnz() const { return static_cast<index_t>(col_indices.size()); }
     index_t row_nnz(index_t i) const { return row_offsets[i + 1] - row_offsets[i]; }
+    std::span<const index_t> row_cols(index_t i) const {  // sparse.hpp:40-48
+        return {col_indices.data() + row_offsets[i], static_cast<std::size_t>(row_nnz(i))};
+    }
+    std::span<const double> row_vals(index_t i) const {
+        return {values.data() + row_offsets[i], static_cast<std::size_t>(row_nnz(i))};
+    }
+    std::span<double> row_vals(index_t i) {
+        return {values.data() + row_offsets[i], static_cast<std::size_t>(row_nnz(i))};
+    }
+    double coeff(index_t i, index_t j) const {  // sparse.hpp:50-56: value at (i, j), 0 if not stored
+        auto cols = row_cols(i);
+        auto it = std::lower_bound(cols.begin(), cols.end(), j);
+        if (it == cols.end() || *it != j) return 0.0;
+        return values[row_offsets[i] + static_cast<index_t>(it - cols.begin())];
+    }
     bool operator==(const SparseMatrix& o) const {
         return n_rows == o.n_rows && n_cols == o.n_cols && row_offsets == o.row_offsets &&
                col_indices == o.col_indices && values == o.values;
@@ -59,6 +79,12 @@ struct CandidateSet {  // dense.hpp:15-32
     }
     double& at(index_t i, index_t j) { return data[static_cast<std::size_t>(j) * n + i]; }
     double at(index_t i, index_t j) const { return data[static_cast<std::size_t>(j) * n + i]; }
+    std::span<double> col(index_t j) {  // dense.hpp:28-31
+        return {data.data() + static_cast<std::size_t>(j) * n, static_cast<std::size_t>(n)};
+    }
+    std::span<const double> col(index_t j) const {
+        return {data.data() + static_cast<std::size_t>(j) * n, static_cast<std::size_t>(n)};
+    }
 };
 
 inline CandidateSet constant_candidates(index_t n) {
@@ -217,13 +243,33 @@ inline amgcu_setup_options flatten(const SetupOptions& o) {
 
 }  // namespace b200
 
+// Raw multiply counter (work.hpp:11-22): a multiply-add counts as one operation.
+struct OpCounter {
+    double ops = 0.0;
+    void add(double n) { ops += n; }
+    void reset() { ops = 0.0; }
+};
+
+inline void count(OpCounter* c, double n) {
+    if (c) c->add(n);
+}
+
 // Cumulative cost ledger in work units (work.hpp:27-67): raw op counts / nnz(A_0).
 enum class WorkBucket : int { aggregation = 0, candidates = 1, interp = 2, rap = 3, solve_other = 4 };
 
 struct WorkLedger {
     double base_nnz = 0.0;
     std::array<double, 5> wu{};
+    void register_base(double nnz) {
+        if (nnz <= 0.0) throw std::invalid_argument("WorkLedger: base nnz must be positive");
+        base_nnz = nnz;
+    }
     bool active() const { return base_nnz > 0.0; }
+    void charge(WorkBucket b, double raw_ops) {
+        if (!active()) throw std::logic_error("WorkLedger: base nnz not registered");
+        wu[static_cast<int>(b)] += raw_ops / base_nnz;
+    }
+    void charge(WorkBucket b, const OpCounter& c) { charge(b, c.ops); }
     double operator[](WorkBucket b) const { return wu[static_cast<int>(b)]; }
     double setup_total() const { return wu[0] + wu[1] + wu[2] + wu[3]; }
     double total() const {
@@ -233,34 +279,27 @@ struct WorkLedger {
     }
 };
 
-// Device-resident hierarchy (hierarchy.hpp:80-91).
+// Device-resident hierarchy (hierarchy.hpp:80-91) with the reference's members.
 struct Hierarchy {
     std::shared_ptr<amgcu_hier_s> handle;
+    std::vector<Level> levels;  // host mirror of every level (downloaded by setup)
     SetupOptions options;
-    std::vector<Level> levels;  // host mirror, filled by download()
+    WorkLedger ledger;          // charged by setup, every solve and every cycle
     bool stagnated = false;
 
-    int n_levels() const {
-        int32_t n = 0, s = 0;
-        b200::check(amgcu_hier_levels(handle.get(), &n, &s), b200::default_ctx());
-        return n;
+    int n_levels() const { return static_cast<int>(levels.size()); }
+    const SparseMatrix& finest() const { return levels.front().A; }
+    const SparseMatrix& coarsest() const { return levels.back().A; }
+
+    // the library's ledger (buckets as the reference charges them; the evolution-SOC
+    // part is counted on the first call) into `ledger`
+    void refresh_ledger() {
+        b200::check(amgcu_hier_ledger(handle.get(), ledger.wu.data()), b200::default_ctx());
     }
-    // the hierarchy's WorkLedger (the reference's Hierarchy::ledger, charged by setup and
-    // every solve); the evolution-SOC part is counted on the first call
-    WorkLedger ledger() const {
-        WorkLedger w;
-        b200::check(amgcu_hier_ledger(handle.get(), w.wu.data()), b200::default_ctx());
-        int32_t n = 0, s = 0;
-        b200::check(amgcu_hier_levels(handle.get(), &n, &s), b200::default_ctx());
-        amgcu_csr a0{};
-        b200::check(amgcu_hier_get_matrix(handle.get(), 0, 0, &a0), b200::default_ctx());
-        w.base_nnz = static_cast<double>(a0.nnz);
-        amgcu_csr_free(&a0);
-        return w;
-    }
-    // copy every level's A, P, R, B, Bc to the host mirror (untimed diagnostics)
+    // copy every level's A, P, R, B, Bc and symmetry flag to the host mirror
     void download() {
-        const int L = n_levels();
+        int32_t L = 0, st = 0;
+        b200::check(amgcu_hier_levels(handle.get(), &L, &st), b200::default_ctx());
         levels.assign(L, Level{});
         for (int l = 0; l < L; ++l) {
             for (int which = 0; which < (l + 1 < L ? 3 : 1); ++which) {
@@ -284,6 +323,47 @@ struct Hierarchy {
     }
 };
 
+// Core sparse kernels of the path (sparse.hpp:141-228) on the GPU through the C ABI,
+// with the reference's signatures and op counts.
+inline void spmv(const SparseMatrix& A, std::span<const double> x, std::span<double> y, OpCounter* c = nullptr) {
+    if (static_cast<index_t>(x.size()) != A.n_cols || static_cast<index_t>(y.size()) != A.n_rows)
+        throw std::invalid_argument("spmv: dimension mismatch");
+    amgcu_csr a = b200::view(A);
+    b200::check(amgcu_spmv(b200::default_ctx(), &a, x.data(), y.data()), b200::default_ctx());
+    count(c, static_cast<double>(A.nnz()));
+}
+
+inline std::vector<double> spmv(const SparseMatrix& A, std::span<const double> x, OpCounter* c = nullptr) {
+    std::vector<double> y(static_cast<std::size_t>(A.n_rows));
+    spmv(A, x, y, c);
+    return y;
+}
+
+inline SparseMatrix transpose(const SparseMatrix& A) {
+    amgcu_csr a = b200::view(A), out{};
+    b200::check(amgcu_transpose(b200::default_ctx(), &a, &out), b200::default_ctx());
+    return b200::take(out);
+}
+
+inline SparseMatrix matmul(const SparseMatrix& A, const SparseMatrix& B, OpCounter* c = nullptr) {
+    amgcu_csr a = b200::view(A), bm = b200::view(B), out{};
+    b200::check(amgcu_matmul(b200::default_ctx(), &a, &bm, &out), b200::default_ctx());
+    double ops = 0.0;  // sparse.hpp:195: sum over A's entries of nnz(row k of B)
+    for (index_t p = 0; p < A.nnz(); ++p) ops += static_cast<double>(B.row_nnz(A.col_indices[p]));
+    count(c, ops);
+    return b200::take(out);
+}
+
+inline SparseMatrix galerkin_product(const SparseMatrix& R, const SparseMatrix& A, const SparseMatrix& P,
+                                     OpCounter* c = nullptr) {
+    if (R.n_cols != A.n_rows || A.n_cols != P.n_rows)
+        throw std::invalid_argument("galerkin_product: dimension mismatch");
+    SparseMatrix AP = matmul(A, P, c);
+    SparseMatrix C = matmul(R, AP, c);
+    C.block_size = P.block_size;
+    return C;
+}
+
 inline Hierarchy rn_setup(const SparseMatrix& A, const CandidateSet& B, const SetupOptions& opts,
                           const CandidateSet* left_candidates = nullptr) {
     if (B.n != A.n_rows) throw std::invalid_argument("rn_setup: candidate size mismatch");
@@ -302,6 +382,9 @@ inline Hierarchy rn_setup(const SparseMatrix& A, const CandidateSet& B, const Se
     int32_t n = 0, s = 0;
     b200::check(amgcu_hier_levels(h, &n, &s), ctx);
     out.stagnated = s != 0;
+    out.ledger.register_base(static_cast<double>(A.nnz()));
+    out.refresh_ledger();
+    out.download();
     return out;
 }
 
@@ -333,32 +416,64 @@ inline SolveReport solve(Hierarchy& h, std::span<const double> b, std::vector<do
     rep.chi_cc = r.chi_cc;
     rep.work_units_solve = r.work_units_solve;
     rep.work_units_setup = r.work_units_setup;
+    h.refresh_ledger();
     return rep;
 }
 
-inline void cycle(Hierarchy& h, std::span<double> x, std::span<const double> b, CycleKind kind = CycleKind::V) {
+namespace b200 {
+// the cycle cost model of cycle.hpp:66-69 (what cycle_apply counts): per non-coarsest
+// level, pre + post sweeps at |A| each (gsne 2 |A|), one residual |A|, |R| and |P|;
+// a W cycle visits every level below the second coarsest twice
+inline double cycle_ops(const Hierarchy& h, int level, CycleKind kind) {
+    if (level == h.n_levels() - 1) return 0.0;
+    const Level& lev = h.levels[level];
+    auto sweep = [](RelaxScheme s, double nnz) { return s == RelaxScheme::gsne ? 2.0 * nnz : nnz; };
+    const double a = static_cast<double>(lev.A.nnz());
+    double ops = h.options.pre_relax.sweeps * sweep(h.options.pre_relax.scheme, a) + a +
+                 static_cast<double>(lev.R.nnz()) + static_cast<double>(lev.P.nnz()) +
+                 h.options.post_relax.sweeps * sweep(h.options.post_relax.scheme, a);
+    ops += cycle_ops(h, level + 1, kind);
+    if (kind == CycleKind::W && level + 1 < h.n_levels() - 1) ops += cycle_ops(h, level + 1, kind);
+    return ops;
+}
+}  // namespace b200
+
+// cycle.hpp:100-107: one cycle on A x = b in place, work counted into c
+inline void cycle(Hierarchy& h, std::span<double> x, std::span<const double> b, CycleKind kind = CycleKind::V,
+                  OpCounter* c = nullptr) {
+    if (static_cast<index_t>(x.size()) != h.finest().n_rows || static_cast<index_t>(b.size()) != h.finest().n_rows)
+        throw std::invalid_argument("cycle: size mismatch");
     b200::check(amgcu_cycle(h.handle.get(), x.data(), b.data(), static_cast<int32_t>(kind)), b200::default_ctx());
+    count(c, b200::cycle_ops(h, 0, kind));
 }
 
-// Complexity measures and the setup report (complexity.hpp:15-88).  The report functions
-// read the host mirror, downloading it first if needed.  setup_report_json returns the
-// reference's setup_report() document as text (the reference builds it with nlohmann::json).
-inline double operator_complexity(Hierarchy& h) {
-    double oc = 0.0, cc = 0.0;
-    b200::check(amgcu_hier_complexity(h.handle.get(), &oc, &cc), b200::default_ctx());
-    return oc;
+// Complexity measures and the setup report (complexity.hpp:15-88), computed from the
+// host mirror `levels` exactly as the reference does (a Hierarchy assembled by hand,
+// as in proj/tests/test_complexity.cpp, works too).
+inline double operator_complexity(const Hierarchy& h) {
+    const double base = static_cast<double>(h.finest().nnz());
+    double sum = 0.0;
+    for (const Level& l : h.levels) sum += static_cast<double>(l.A.nnz());
+    return sum / base;
 }
 
-inline double cycle_complexity(Hierarchy& h) {
-    double oc = 0.0, cc = 0.0;
-    b200::check(amgcu_hier_complexity(h.handle.get(), &oc, &cc), b200::default_ctx());
-    return cc;
+inline double cycle_complexity(const Hierarchy& h, int pre_sweeps = -1, int post_sweeps = -1) {
+    if (pre_sweeps < 0) pre_sweeps = h.options.pre_relax.sweeps;
+    if (post_sweeps < 0) post_sweeps = h.options.post_relax.sweeps;
+    const double base = static_cast<double>(h.finest().nnz());
+    double sum = 0.0;
+    for (int l = 0; l + 1 < h.n_levels(); ++l) {
+        const Level& lev = h.levels[l];
+        sum += static_cast<double>(pre_sweeps + post_sweeps + 1) * lev.A.nnz();
+        sum += static_cast<double>(lev.P.nnz()) + static_cast<double>(lev.R.nnz());
+    }
+    return sum / base;
 }
 
-inline std::string setup_report_json(Hierarchy& h) {
-    if (h.levels.empty()) h.download();
-    const WorkLedger w = h.ledger();
-    const int L = static_cast<int>(h.levels.size());
+// setup_report's document as JSON text (the reference builds it with nlohmann::json)
+inline std::string setup_report_json(const Hierarchy& h) {
+    const WorkLedger& w = h.ledger;
+    const int L = h.n_levels();
     std::string j = "{\"levels\": [";
     char buf[512];
     for (int l = 0; l < L; ++l) {
@@ -382,10 +497,24 @@ inline std::string setup_report_json(Hierarchy& h) {
     return j + buf;
 }
 
-inline std::string setup_report_csv(Hierarchy& h) {
-    if (h.levels.empty()) h.download();
+#if __has_include(<json.hpp>)
+}  // namespace amg
+#include <json.hpp>
+namespace amg {
+// complexity.hpp:39-71: with nlohmann::json on the include path (as the reference's
+// callers have it), setup_report returns the same json document
+inline nlohmann::json setup_report(const Hierarchy& h) { return nlohmann::json::parse(setup_report_json(h)); }
+#else
+struct SetupReport {  // without nlohmann::json: the document as text, .dump() like the json
+    std::string text;
+    std::string dump(int = -1) const { return text; }
+};
+inline SetupReport setup_report(const Hierarchy& h) { return {setup_report_json(h)}; }
+#endif
+
+inline std::string setup_report_csv(const Hierarchy& h) {
     std::string os = "level,rows,nnz,nnz_per_row,nnz_P,nnz_R\n";
-    const int L = static_cast<int>(h.levels.size());
+    const int L = h.n_levels();
     char buf[256];
     for (int l = 0; l < L; ++l) {
         const Level& lev = h.levels[l];
@@ -401,7 +530,7 @@ inline std::string setup_report_csv(Hierarchy& h) {
         os += "\n";
     }
     std::snprintf(buf, sizeof(buf), "operator_complexity,%g,,,,\ncycle_complexity,%g,,,,\nsetup_work_units,%g,,,,\n",
-                  operator_complexity(h), cycle_complexity(h), h.ledger().setup_total());
+                  operator_complexity(h), cycle_complexity(h), h.ledger.setup_total());
     return os + buf;
 }
 
