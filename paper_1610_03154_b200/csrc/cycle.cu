@@ -16,6 +16,7 @@
 #include <cooperative_groups.h>
 
 #include <chrono>
+#include <cstring>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -126,6 +127,7 @@ SellView view(const DSell& s) {
 // lane 0 sums them in CSR order -- the reference's sequential sum, with the
 // loads of a long row in flight together instead of one thread walking it.
 constexpr int kWarpRowsPerBlock = 8;
+constexpr int32_t kWarpRowMaxRows = 65536;  // from this many rows, thread per row even for long rows
 constexpr int kWarpCap = 256;  // products staged per pass
 
 template <typename Gather>
@@ -464,11 +466,17 @@ void build_sell_finish(Ctx& c, const DCsr& A, DSell& S, int slot) {
     launch(c, k_sell_fill, blocks_for(static_cast<int64_t>(S.nslices) * kSlice, 256), 256, 0, A.nr, A.rp.get(),
            A.ci.get(), A.va.get(), static_cast<const int64_t*>(S.slice_ptr.get()), S.ci.get(), S.va.get(),
            S.slice_len.get());
-    // long rows on average: the warp-per-row kernels over the CSR
+    // long rows on average and too few rows to fill the GPU thread per row: the
+    // warp-per-row kernels over the CSR (with enough rows, thread per row over the SELL
+    // slices keeps 16 loads in flight per thread and no lane waits on a serial sum)
     S.crp = A.rp.get();
     S.cci = A.ci.get();
     S.cva = A.va.get();
-    S.warp_rows = A.nr > 0 && A.nnz >= kWarpRowThreshold * static_cast<int64_t>(A.nr);
+    static const int64_t max_rows = [] {
+        const char* e = std::getenv("AMGCU_WARP_ROW_MAX");
+        return e ? std::atoll(e) : static_cast<int64_t>(kWarpRowMaxRows);
+    }();
+    S.warp_rows = A.nr > 0 && A.nnz >= kWarpRowThreshold * static_cast<int64_t>(A.nr) && A.nr < max_rows;
 }
 
 unsigned rows_grid(int32_t n) { return blocks_for(n, 128); }
@@ -860,6 +868,99 @@ SolveResult solve(DHier& h, const double* b, double* x, const amgcu_solve_option
                 break;
             }
         }
+        return finish();
+    }
+
+    static const bool pcg_spec = [] {
+        const char* e = std::getenv("AMGCU_PCG_SPEC");
+        return !(e && e[0] == '0');
+    }();
+    if (o.method == 1 && pcg_spec && c.side && c.seq) {  // PCG (cycle.hpp:174-209), pipelined
+        // The residual norm only decides whether to stop; nothing else waits for it.  So
+        // after the update it is summed on the side stream while the main stream goes on
+        // with the next iteration's work up to (not including) its update: the cycle
+        // M r, (r, z), beta, p = z + beta p, q = A p, (p, q), alpha.  The host then reads
+        // the norm; if the reference stops there, x and r are final (the queued work only
+        // touched z, p, q and the scalars) and its work units are not counted.  Every
+        // value is computed by the same kernels in the same order as the plain loop.
+        if (!L0.symmetric) throw InvalidArgument("solve: pcg requires a symmetric operator");
+        DBuf<double> z(static_cast<size_t>(n), c.s), p(static_cast<size_t>(n), c.s), q(static_cast<size_t>(n), c.s);
+        double* hs = nullptr;  // pinned: {rn, bad}
+        AMG_CK(cudaMallocHost(reinterpret_cast<void**>(&hs), 2 * sizeof(double)));
+        struct PinGuard {
+            double* p;
+            ~PinGuard() { cudaFreeHost(p); }
+        } pin_guard{hs};
+        cudaEvent_t upd, nrm;
+        AMG_CK(cudaEventCreateWithFlags(&upd, cudaEventDisableTiming));
+        AMG_CK(cudaEventCreateWithFlags(&nrm, cudaEventDisableTiming));
+        struct EvGuard {
+            cudaEvent_t a, b;
+            cudaStream_t side;
+            ~EvGuard() {
+                cudaStreamSynchronize(side);  // the side stream's norm reads r and writes hs
+                cudaEventDestroy(a);
+                cudaEventDestroy(b);
+            }
+        } ev_guard{upd, nrm, c.side};
+        auto head = [&] {  // q = A p, (p, q), alpha
+            d.spmv_fam(L0.sA, kProfKrylovSpmv, 12.0 * L0.A.nnz + 4.0 * (n + 1) + 16.0 * n,
+                       static_cast<const double*>(p.get()), q.get());
+            d.ops += static_cast<double>(L0.A.nnz);
+            dot(c, p.get(), q.get(), n, S + 1);
+            launch(c, k_pcg_alpha, 1, 1, 0, S, bad.get());
+        };
+        d.precond(r.get(), z.get(), o.cycle);
+        copy_d2d(c, p.get(), z.get(), n);
+        dot(c, r.get(), z.get(), n, S + 0);  // rz
+        head();
+        for (int it = 1; it <= o.max_iters; ++it) {
+            launch_prof(c, kProfBlas1, 48.0 * n, k_pcg_update, stream_grid(c, n), 256, 0, static_cast<int64_t>(n),
+                        static_cast<const double*>(S), static_cast<const int32_t*>(bad.get()),
+                        static_cast<const double*>(p.get()), static_cast<const double*>(q.get()), x, r.get());
+            // this iteration's breakdown flag, before the next alpha overwrites it
+            AMG_CK(cudaMemcpyAsync(hs + 1, bad.get(), sizeof(int32_t), cudaMemcpyDeviceToHost, c.s));
+            AMG_CK(cudaEventRecord(upd, c.s));
+            {
+                StreamScope on_side(c, c.side);
+                AMG_CK(cudaStreamWaitEvent(c.side, upd, 0));
+                nrm2(c, r.get(), n, S + 5);
+                copy_d2h(c, hs, S + 5, 1);
+                AMG_CK(cudaEventRecord(nrm, c.side));
+            }
+            const double ops_before = d.ops;
+            if (it < o.max_iters) {
+                d.precond(r.get(), z.get(), o.cycle);
+                dot(c, r.get(), z.get(), n, S + 3);
+                launch(c, k_pcg_beta, 1, 1, 0, S);
+                launch_prof(c, kProfBlas1, 24.0 * n, k_pcg_dir, stream_grid(c, n), 256, 0, static_cast<int64_t>(n),
+                            static_cast<const double*>(S), static_cast<const double*>(z.get()), p.get());
+                head();
+            }
+            AMG_CK(cudaEventSynchronize(nrm));
+            ++c.syncs;
+            int32_t hbad = 0;
+            std::memcpy(&hbad, hs + 1, sizeof(int32_t));
+            if (hbad) {
+                rep.diverged = true;
+                d.ops = ops_before;
+                break;
+            }
+            const double rn = hs[0];
+            rep.history.push_back(rn);
+            rep.iterations = it;
+            if (rn <= target) {
+                rep.converged = true;
+                d.ops = ops_before;
+                break;
+            }
+            if (rn > blowup || !std::isfinite(rn)) {
+                rep.diverged = true;
+                d.ops = ops_before;
+                break;
+            }
+        }
+        sync(c);
         return finish();
     }
 
