@@ -20,6 +20,7 @@ namespace {
 
 constexpr int kMaxK = kGsMaxColumns;
 constexpr size_t kGsCtaSmem = 220 * 1024;  // dynamic shared memory of the single-CTA kernel
+constexpr int32_t kGsCtaMaxRows = 1024;     // below: the single-CTA kernel first (C5: 1.6-1.9 ms vs 2.3-2.8)
 
 // Gauss-Seidel sweeps, segment-parallel.
 //
@@ -116,7 +117,7 @@ constexpr int gs_max_poll() {
 // left the ring.  K = 1 only.
 constexpr int kRing = 64;
 constexpr int kShortSegment = 8;
-constexpr int kSegWarpMinLen = 16;  // mean segment length from which the warp-per-segment kernel runs
+constexpr int kSegWarpMinLen = 16;  // mean segment length from which the lane-per-segment kernel runs
 constexpr unsigned kWarpRowPollNs = 32;  // poll back-off cap of the warp-per-row kernel  // mean segment length below which the warp-per-row kernel is used
 constexpr int32_t kProductTerm = -1;  // term whose product a * x is precomputed (K = 1)
 constexpr int kSibling = 4;  // entry class: pending value of a sibling segment
@@ -757,7 +758,7 @@ template <int K>
 __global__ void __launch_bounds__(kCtaWarps * 32, 1)
     k_gs_cta(int32_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci, const double* __restrict__ va,
              const double* __restrict__ inv_diag, const double* __restrict__ b, int nsweeps,
-             const unsigned char* __restrict__ backward, double* __restrict__ x) {
+             const unsigned char* __restrict__ backward, double* __restrict__ x, unsigned spin_ns) {
     extern __shared__ __align__(16) double cta_smem[];
     double* xs = cta_smem;                                       // K x n, column-major like x
     double* sp = xs + static_cast<size_t>(K) * n + static_cast<size_t>(threadIdx.x >> 5) * (K * 32);  // products
@@ -781,7 +782,8 @@ __global__ void __launch_bounds__(kCtaWarps * 32, 1)
         // the row's own previous sweep first: nothing else orders (s - 1, i) before (s, i)
         // when the row's neighbours do not (the last row of a forward half-sweep starts
         // the backward one, and reads only rows that did not wait for it)
-        while (ld_ver(ver + i) < s) __nanosleep(32);
+        while (ld_ver(ver + i) < s)
+            if (spin_ns) __nanosleep(spin_ns);
         for (int32_t e0 = lo; e0 < hi; e0 += 32) {
             const int32_t p = e0 + lane;
             const bool act = p < hi;
@@ -794,7 +796,8 @@ __global__ void __launch_bounds__(kCtaWarps * 32, 1)
             const bool use = act && j != i;
             const int32_t need = ((j < i) != bwd) ? s + 1 : s;
             // warp-uniform wait: the warp stays converged for the staging below
-            while (__any_sync(0xffffffffu, use && ld_ver(ver + j) < need)) __nanosleep(32);
+            while (__any_sync(0xffffffffu, use && ld_ver(ver + j) < need))
+                if (spin_ns) __nanosleep(spin_ns);
 #pragma unroll
             for (int c = 0; c < K; ++c) sp[c * 32 + lane] = use ? a * vx[static_cast<size_t>(c) * n + j] : 0.0;
             __syncwarp();
@@ -1130,33 +1133,34 @@ __global__ void k_jacobi(int32_t n, const int32_t* __restrict__ rp, const int32_
 
 // The forward-sweep plan of a matrix: which sync-free kernel relaxes its k columns, and
 // its segments.  In order of preference:
-//   kCta      the iterate fits one SM and the pattern is structurally symmetric;
+//   kCta      fewer than 1024 rows, the iterate fits one SM and the pattern is
+//             structurally symmetric: values handed over in shared memory;
 //   kLanes    lane per segment (gs_lanes.cuh): one column, rows of at most 9 entries
-//             (the 8-term records), 32 segments per resident CTA;
-//   kSegWarp  warp per segment (k_gs_seg_warp): any row length, every warp resident.
+//             (the 8-term records), segments of 16 rows on average, 32 per resident CTA;
+//   kSegWarp  warp per segment (k_gs_seg_warp): any row or segment length, every warp
+//             resident (C5: level 1 194 -> 12 ms, level 3 9.5 -> 3.2 ms);
+//   kCta      as above for larger levels that still fit.
 // Segments use a block-size window, so the stride-m chains of interleaved vector
-// unknowns continue a segment; both segment kernels need them 16 rows long on average.
-// Host synchronisations happen here; the run (fwd_gs_run) has none, so it may be
-// queued on another stream than the plan's.
+// unknowns continue a segment.  Host synchronisations happen here; the run
+// (gs_lanes_run) has none, so it may be queued on another stream than the plan's.
 LanePlan lane_plan(Ctx& c, const DCsr& A, int nsw, int k) {
     LanePlan pl;
     const int32_t n = A.nr;
     if (n == 0 || nsw == 0 || k > kMaxK || std::getenv("AMGCU_GS_TRACE")) return pl;
     if (n >= (1 << 24) || static_cast<int64_t>(nsw) * n * k >= (int64_t(1) << 31)) return pl;
-    {
-        const char* e = std::getenv("AMGCU_GS_CTA");  // "0": off (read per call: tests toggle it)
-        const size_t smem = gs_cta_smem(n, k);
-        if (!(e && e[0] == '0') && smem <= kGsCtaSmem) {
-            DBuf<int32_t> flag(1, c.s);
-            AMG_CK(cudaMemsetAsync(flag.get(), 0, sizeof(int32_t), c.s));
-            launch(c, k_pattern_asym, blocks_for(n, 256), 256, 0, n, A.rp.get(), A.ci.get(), flag.get());
-            if (!read_scalar(c, flag.get())) {
-                pl.kind = LanePlan::kCta;
-                pl.ok = true;
-                return pl;
-            }
-        }
-    }
+    const char* cta_env = std::getenv("AMGCU_GS_CTA");  // "0": off (read per call: tests toggle it)
+    const bool cta_fits = !(cta_env && cta_env[0] == '0') && gs_cta_smem(n, k) <= kGsCtaSmem;
+    auto try_cta = [&] {
+        DBuf<int32_t> flag(1, c.s);
+        AMG_CK(cudaMemsetAsync(flag.get(), 0, sizeof(int32_t), c.s));
+        launch(c, k_pattern_asym, blocks_for(n, 256), 256, 0, n, A.rp.get(), A.ci.get(), flag.get());
+        if (read_scalar(c, flag.get())) return false;
+        pl.kind = LanePlan::kCta;
+        pl.ok = true;
+        return true;
+    };
+    // the smallest levels: one SM holds everything and hands values over in shared memory
+    if (cta_fits && n < kGsCtaMaxRows && try_cta()) return pl;
     DBuf<int32_t> st(2, c.s);
     AMG_CK(cudaMemsetAsync(st.get(), 0, 2 * sizeof(int32_t), c.s));
     launch(c, k_bandwidth, blocks_for(n, 256), 256, 0, n, A.rp.get(), A.ci.get(), st.get());
@@ -1164,23 +1168,27 @@ LanePlan lane_plan(Ctx& c, const DCsr& A, int nsw, int k) {
     stage_scalar(c, 1, st.get() + 1);
     sync(c);
     pl.longest_row = staged<int32_t>(c, 1);
-    if (static_cast<int64_t>(pl.nf) * kSegWarpMinLen > n) return pl;
     const char* ln_env = std::getenv("AMGCU_GS_LANES");
     const char* sw_env = std::getenv("AMGCU_GS_SEGWARP");
     const bool lanes_off = ln_env && ln_env[0] == '0', sw_off = sw_env && sw_env[0] == '0';
-    if (!lanes_off && k == 1 && pl.longest_row <= 9 && (pl.nf + kLnLanes - 1) / kLnLanes <= c.sms) {
+    if (!lanes_off && k == 1 && pl.longest_row <= 9 && (pl.nf + kLnLanes - 1) / kLnLanes <= c.sms &&
+        static_cast<int64_t>(pl.nf) * kSegWarpMinLen <= n) {
         pl.kind = LanePlan::kLanes;
         pl.ok = true;
         return pl;
     }
+    // warp per segment: any segment length (short segments only mean more warps), as
+    // long as every warp can be resident at once
     if (!sw_off && k <= 4) {
         int per_sm = 0;
         AMG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gs_seg_warp<4>, kSwWarps * 32, 0));
         if ((pl.nf + kSwWarps - 1) / kSwWarps <= static_cast<int64_t>(per_sm) * c.sms) {
             pl.kind = LanePlan::kSegWarp;
             pl.ok = true;
+            return pl;
         }
     }
+    if (cta_fits && n >= kGsCtaMaxRows) try_cta();
     return pl;
 }
 
@@ -1258,7 +1266,7 @@ void gs_cta_kernel_run(Ctx& c, const DCsr& A, const double* inv_diag, double* x,
     auto run = [&](auto kern) {
         AMG_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         launch_prof(c, kProfGaussSeidel, bytes, kern, 1, kCtaWarps * 32, smem, n, A.rp.get(), A.ci.get(), A.va.get(),
-                    inv_diag, b, nsw, static_cast<const unsigned char*>(bwd.get()), x);
+                    inv_diag, b, nsw, static_cast<const unsigned char*>(bwd.get()), x, gs_env_u("AMGCU_GS_CTA_NS", 32u));
     };
     switch (k) {
         case 1: run(k_gs_cta<1>); break;
