@@ -101,6 +101,7 @@ __global__ void k_gather_transpose(int64_t nnz, const int32_t* __restrict__ pos,
 // one block over a global scratch region.
 // ---------------------------------------------------------------------------------
 constexpr int kSmallCap = 512;
+constexpr int kSortCap = 64;  // rows up to this many products: the sort kernel
 
 __global__ void k_product_count(int32_t nr, const int32_t* __restrict__ arp, const int32_t* __restrict__ aci,
                                 const int32_t* __restrict__ brp, int64_t* __restrict__ np) {
@@ -118,7 +119,7 @@ __global__ void k_collect_big(int32_t nr, const int64_t* __restrict__ np, int32_
                               int32_t* __restrict__ count) {
     const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= nr) return;
-    if (np[i] > kSmallCap) list[atomicAdd(count, 1)] = i;
+    if (np[i] > kSortCap) list[atomicAdd(count, 1)] = i;
 }
 
 __device__ __forceinline__ unsigned next_pow2(unsigned v) {
@@ -152,7 +153,6 @@ __device__ __forceinline__ void expand_row(int32_t i, const int32_t* __restrict_
 }
 
 constexpr int kGemmWarps = 8;
-constexpr int kSortCap = 64;  // rows up to this many products: the sort kernel
 
 // Warp-cooperative expansion: lanes take A entries (32 at a time), a warp scan
 // of their B-row lengths gives each product's sequence number, and each lane
@@ -889,6 +889,193 @@ void transpose(Ctx& c, const DCsr& A, DCsr& T) {
 }
 
 namespace {
+// ---------------------------------------------------------------------------------
+// SpGEMM rows of more than kSortCap products whose output columns fall in a window of
+// at most kBmWords * 32 (the Galerkin products and patterns of aggregation hierarchies:
+// a coarse row's columns are its aggregate's neighbours).  Warp per row, no hashing,
+// no sorting:
+//   1. window [cmin, cmax] from the first / last column of each B row the row touches;
+//   2. symbolic: one bit per output column in a shared bitmap (atomicOr);
+//   3. rank of a column = popcount of the bits before it (per-word prefix + popc), so
+//      the distinct columns are numbered in ascending order without a sort;
+//   4. numeric in the reference's order (sparse.hpp:190-201): A entries in CSR order,
+//      each B row's entries by the lanes (distinct columns, so no two lanes share an
+//      accumulator), acc[rank] += a * b starting from 0.0, a warp barrier between A
+//      entries; bit-identical to the reference's row accumulator;
+//   5. the non-zero sums written in column order (exact zeros dropped).
+// Rows whose window or distinct count is too large are listed for the hash kernels.
+// ---------------------------------------------------------------------------------
+constexpr int kBmWords = 256;  // window of 8192 columns
+constexpr int kBmAcc = 1024;   // distinct output columns held per row
+constexpr int kBmWarps = 4;
+struct BmShared {
+    uint32_t bits[kBmWords];
+    int32_t pre[kBmWords];
+    double acc[kBmAcc];
+    int32_t at[kWarp], ab0[kWarp], ab1[kWarp];  // a chunk of A entries: column, B row range
+    double aa[kWarp];
+};
+
+__global__ void __launch_bounds__(kBmWarps * kWarp)
+    k_spgemm_bitmap(int32_t nlist, const int32_t* __restrict__ list, const int32_t* __restrict__ arp,
+                    const int32_t* __restrict__ aci, const double* __restrict__ ava, const int32_t* __restrict__ brp,
+                    const int32_t* __restrict__ bci, const double* __restrict__ bva, const int64_t* __restrict__ poff,
+                    int32_t* __restrict__ tcol, double* __restrict__ tval, int32_t* __restrict__ cnt,
+                    int32_t* __restrict__ fb, int32_t* __restrict__ fbn) {
+    extern __shared__ unsigned long long bm_smem[];
+    const int w = threadIdx.x / kWarp;
+    const int lane = threadIdx.x & (kWarp - 1);
+    const int32_t slot = blockIdx.x * kBmWarps + w;
+    if (slot >= nlist) return;
+    BmShared& sh = reinterpret_cast<BmShared*>(bm_smem)[w];
+    const int32_t i = list[slot];
+    const int32_t alo = arp[i], ahi = arp[i + 1];
+    // 1. window
+    int32_t cmin = INT_MAX, cmax = -1;
+    for (int32_t p = alo + lane; p < ahi; p += kWarp) {
+        const int32_t t = __ldg(aci + p);
+        const int32_t b0 = __ldg(brp + t), b1 = __ldg(brp + t + 1);
+        if (b1 > b0) {
+            cmin = min(cmin, __ldg(bci + b0));
+            cmax = max(cmax, __ldg(bci + b1 - 1));
+        }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        cmin = min(cmin, __shfl_xor_sync(0xffffffffu, cmin, off));
+        cmax = max(cmax, __shfl_xor_sync(0xffffffffu, cmax, off));
+    }
+    if (cmax < 0) {
+        if (lane == 0) cnt[i] = 0;
+        return;
+    }
+    const int32_t width = cmax - cmin + 1;
+    if (width > kBmWords * kWarp) {
+        if (lane == 0) fb[atomicAdd(fbn, 1)] = i;
+        return;
+    }
+    const int nw = (width + kWarp - 1) / kWarp;
+    for (int e = lane; e < kBmWords; e += kWarp) sh.bits[e] = 0u;
+    __syncwarp();
+    // 2. symbolic
+    for (int32_t p0 = alo; p0 < ahi; p0 += kWarp) {
+        const int32_t p = p0 + lane;
+        if (p < ahi) {
+            const int32_t t = __ldg(aci + p);
+            sh.ab0[lane] = __ldg(brp + t);
+            sh.ab1[lane] = __ldg(brp + t + 1);
+        }
+        __syncwarp();
+        const int m = min(kWarp, ahi - p0);
+        for (int u = 0; u < m; ++u) {
+            const int32_t q1 = sh.ab1[u];
+            for (int32_t q = sh.ab0[u] + lane; q < q1; q += kWarp) {
+                const int32_t cc = __ldg(bci + q) - cmin;
+                atomicOr(&sh.bits[cc >> 5], 1u << (cc & 31));
+            }
+        }
+        __syncwarp();
+    }
+    // 3. ranks: lane l owns words [8l, 8l + 8)
+    constexpr int kWpl = kBmWords / kWarp;
+    int mine = 0;
+#pragma unroll
+    for (int u = 0; u < kWpl; ++u) mine += __popc(sh.bits[lane * kWpl + u]);
+    int incl = mine;
+#pragma unroll
+    for (int off = 1; off < kWarp; off <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += y;
+    }
+    const int D = __shfl_sync(0xffffffffu, incl, kWarp - 1);
+    if (D > kBmAcc) {
+        if (lane == 0) fb[atomicAdd(fbn, 1)] = i;
+        return;
+    }
+    {
+        int r = incl - mine;
+#pragma unroll
+        for (int u = 0; u < kWpl; ++u) {
+            sh.pre[lane * kWpl + u] = r;
+            r += __popc(sh.bits[lane * kWpl + u]);
+        }
+    }
+    for (int e = lane; e < D; e += kWarp) sh.acc[e] = 0.0;
+    __syncwarp();
+    // 4. numeric, A entries in CSR order
+    for (int32_t p0 = alo; p0 < ahi; p0 += kWarp) {
+        const int32_t p = p0 + lane;
+        if (p < ahi) {
+            const int32_t t = __ldg(aci + p);
+            sh.aa[lane] = __ldg(ava + p);
+            sh.ab0[lane] = __ldg(brp + t);
+            sh.ab1[lane] = __ldg(brp + t + 1);
+        }
+        __syncwarp();
+        const int m = min(kWarp, ahi - p0);
+        for (int u = 0; u < m; ++u) {
+            const double a = sh.aa[u];
+            const int32_t q1 = sh.ab1[u];
+            for (int32_t q = sh.ab0[u] + lane; q < q1; q += kWarp) {
+                const int32_t cc = __ldg(bci + q) - cmin;
+                const int wd = cc >> 5;
+                const int r = sh.pre[wd] + __popc(sh.bits[wd] & ((1u << (cc & 31)) - 1u));
+                sh.acc[r] += a * __ldg(bva + q);
+            }
+            __syncwarp();
+        }
+    }
+    // 5. non-zero sums in column order
+    (void)nw;
+    int nz = 0;
+#pragma unroll
+    for (int u = 0; u < kWpl; ++u) {
+        const int wd = lane * kWpl + u;
+        uint32_t b = sh.bits[wd];
+        int r = sh.pre[wd];
+        while (b) {
+            nz += sh.acc[r] != 0.0 ? 1 : 0;
+            ++r;
+            b &= b - 1;
+        }
+    }
+    int zin = nz;
+#pragma unroll
+    for (int off = 1; off < kWarp; off <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, zin, off);
+        if (lane >= off) zin += y;
+    }
+    const int64_t base = poff[i];
+    int o = zin - nz;
+#pragma unroll
+    for (int u = 0; u < kWpl; ++u) {
+        const int wd = lane * kWpl + u;
+        uint32_t b = sh.bits[wd];
+        int r = sh.pre[wd];
+        while (b) {
+            const int bit = __ffs(b) - 1;
+            const double v = sh.acc[r];
+            if (v != 0.0) {
+                tcol[base + o] = cmin + wd * kWarp + bit;
+                tval[base + o] = v;
+                ++o;
+            }
+            ++r;
+            b &= b - 1;
+        }
+    }
+    if (lane == kWarp - 1) cnt[i] = zin;
+}
+
+size_t bitmap_smem() {
+    static const size_t bytes = [] {
+        const size_t b = sizeof(BmShared) * kBmWarps;
+        AMG_CK(cudaFuncSetAttribute(k_spgemm_bitmap, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(b)));
+        return b;
+    }();
+    return bytes;
+}
+
 size_t hash_smem() {
     static const size_t bytes = [] {
         const size_t b = sizeof(HashShared) * kHashWarps;
@@ -917,12 +1104,28 @@ size_t mid_smem() {
 }
 }  // namespace
 
+// the rows' staged (column, value) lists (at poff, cnt entries each) into canonical CSR
+void compact_rows(Ctx& c, int32_t nr, int32_t nc, const DBuf<int64_t>& poff, const DBuf<int32_t>& tcol,
+                  const DBuf<double>& tval, DBuf<int32_t>& cnt, DCsr& C) {
+    C.nr = nr;
+    C.nc = nc;
+    C.bs = 1;
+    C.rp.alloc(static_cast<size_t>(nr) + 1, c.s);
+    const int64_t nnz = exclusive_scan_i32(c, cnt.get(), C.rp.get(), nr);
+    C.nnz = nnz;
+    C.ci.alloc(static_cast<size_t>(nnz), c.s);
+    C.va.alloc(static_cast<size_t>(nnz), c.s);
+    launch(c, k_copy_rows, blocks_for(static_cast<int64_t>(nr) * kWarp, 256), 256, 0, nr,
+           static_cast<const int64_t*>(poff.get()), static_cast<const int32_t*>(tcol.get()),
+           static_cast<const double*>(tval.get()), static_cast<const int32_t*>(C.rp.get()), C.ci.get(), C.va.get());
+}
+
 void spgemm(Ctx& c, const DCsr& A, const DCsr& B, DCsr& C, double* ops) {
     if (A.nc != B.nr) throw InvalidArgument("matmul: dimension mismatch");
     const int32_t nr = A.nr;
     DBuf<int64_t> np(static_cast<size_t>(nr) + 1, c.s), poff(static_cast<size_t>(nr) + 1, c.s);
     launch(c, k_product_count, blocks_for(nr, 256), 256, 0, nr, A.rp.get(), A.ci.get(), B.rp.get(), np.get());
-    // rows above the shared-memory capacity are listed now, so the product total and
+    // rows above the sort kernel's capacity are listed now, so the product total and
     // their count come back with one synchronisation
     DBuf<int32_t> big_list(static_cast<size_t>(nr), c.s), big_count(1, c.s);
     AMG_CK(cudaMemsetAsync(big_count.get(), 0, sizeof(int32_t), c.s));
@@ -933,33 +1136,48 @@ void spgemm(Ctx& c, const DCsr& A, const DCsr& B, DCsr& C, double* ops) {
     stage_scalar(c, 1, static_cast<const int32_t*>(big_count.get()));
     sync(c);
     const int64_t total = nr > 0 ? staged<int64_t>(c, 0) : 0;
-    const int32_t nbig = staged<int32_t>(c, 1);
+    const int32_t nlong = staged<int32_t>(c, 1);
     if (ops) *ops = static_cast<double>(total);
     tally(c, static_cast<double>(total));  // matmul's op count (sparse.hpp:195)
     DBuf<int32_t> tcol(static_cast<size_t>(total), c.s), cnt(static_cast<size_t>(nr) + 1, c.s);
     DBuf<double> tval(static_cast<size_t>(total), c.s);
-    launch_prof(c, kProfSpgemm,
-                12.0 * A.nnz + 4.0 * (A.nr + 1) + 12.0 * B.nnz + 4.0 * (B.nr + 1) + 12.0 * static_cast<double>(total) +
-                    4.0 * nr,
-                k_spgemm_hash<kSmallCap, kHashWarps, kSortCap>, blocks_for(nr, kHashWarps), kHashWarps * kWarp,
-                hash_smem(), nr, A.rp.get(), A.ci.get(), A.va.get(), B.rp.get(), B.ci.get(), B.va.get(),
-                static_cast<const int64_t*>(poff.get()), tcol.get(), tval.get(), cnt.get(),
-                static_cast<const int32_t*>(nullptr));
-    launch_prof(c, kProfSpgemm, 0.0, k_spgemm_small, blocks_for(nr, kGemmWarps), kGemmWarps * kWarp, 0, nr, A.rp.get(),
-                A.ci.get(), A.va.get(), B.rp.get(), B.ci.get(), B.va.get(), static_cast<const int64_t*>(poff.get()),
-                tcol.get(), tval.get(), cnt.get());
-    // rows above the warp kernels' capacity: up to kMidCap products one warp per block
-    // over the list, the rest block per row
-    static const bool mid_on = std::getenv("AMGCU_SPGEMM_NO_MID") == nullptr;
-    const int64_t mid_cap = mid_on ? kMidCap : kSmallCap;
-    if (nbig > 0 && mid_on)
-        launch_prof(c, kProfSpgemm, 0.0, k_spgemm_hash<kMidCap, 1, kSmallCap>, static_cast<unsigned>(nbig), kWarp,
-                    mid_smem(), nbig, A.rp.get(), A.ci.get(), A.va.get(), B.rp.get(), B.ci.get(), B.va.get(),
-                    static_cast<const int64_t*>(poff.get()), tcol.get(), tval.get(), cnt.get(),
-                    static_cast<const int32_t*>(big_list.get()));
-    if (nbig > 0) {
-        std::vector<int32_t> hl(nbig);
-        copy_d2h(c, hl.data(), big_list.get(), nbig);
+    const double io_bytes = 12.0 * A.nnz + 4.0 * (A.nr + 1) + 12.0 * B.nnz + 4.0 * (B.nr + 1);
+    launch_prof(c, kProfSpgemm, io_bytes + 12.0 * static_cast<double>(total) + 4.0 * nr, k_spgemm_small,
+                blocks_for(nr, kGemmWarps), kGemmWarps * kWarp, 0, nr, A.rp.get(), A.ci.get(), A.va.get(), B.rp.get(),
+                B.ci.get(), B.va.get(), static_cast<const int64_t*>(poff.get()), tcol.get(), tval.get(), cnt.get());
+    if (nlong == 0) {
+        compact_rows(c, nr, B.nc, poff, tcol, tval, cnt, C);
+        return;
+    }
+    // rows of more than kSortCap products: the bitmap kernel; rows it cannot hold (window
+    // or distinct count too large) are listed for the hash kernels
+    DBuf<int32_t> fb(static_cast<size_t>(nlong), c.s), fbn(1, c.s);
+    AMG_CK(cudaMemsetAsync(fbn.get(), 0, sizeof(int32_t), c.s));
+    static const bool bm_on = std::getenv("AMGCU_SPGEMM_NO_BITMAP") == nullptr;
+    if (bm_on) {
+        launch_prof(c, kProfSpgemm, 0.0, k_spgemm_bitmap, blocks_for(nlong, kBmWarps), kBmWarps * kWarp,
+                    bitmap_smem(), nlong, static_cast<const int32_t*>(big_list.get()), A.rp.get(), A.ci.get(),
+                    A.va.get(), B.rp.get(), B.ci.get(), B.va.get(), static_cast<const int64_t*>(poff.get()),
+                    tcol.get(), tval.get(), cnt.get(), fb.get(), fbn.get());
+        stage_scalar(c, 0, static_cast<const int32_t*>(fbn.get()));
+        sync(c);
+    }
+    const int32_t nfb = bm_on ? staged<int32_t>(c, 0) : nlong;
+    const int32_t* fl = bm_on ? fb.get() : big_list.get();
+    if (nfb > 0) {
+        launch_prof(c, kProfSpgemm, 0.0, k_spgemm_hash<kSmallCap, kHashWarps, kSortCap>, blocks_for(nfb, kHashWarps),
+                    kHashWarps * kWarp, hash_smem(), nfb, A.rp.get(), A.ci.get(), A.va.get(), B.rp.get(), B.ci.get(),
+                    B.va.get(), static_cast<const int64_t*>(poff.get()), tcol.get(), tval.get(), cnt.get(), fl);
+        // rows above the warp kernels' capacity: up to kMidCap products one warp per block
+        // over the list, the rest block per row
+        static const bool mid_on = std::getenv("AMGCU_SPGEMM_NO_MID") == nullptr;
+        const int64_t mid_cap = mid_on ? kMidCap : kSmallCap;
+        if (mid_on)
+            launch_prof(c, kProfSpgemm, 0.0, k_spgemm_hash<kMidCap, 1, kSmallCap>, static_cast<unsigned>(nfb), kWarp,
+                        mid_smem(), nfb, A.rp.get(), A.ci.get(), A.va.get(), B.rp.get(), B.ci.get(), B.va.get(),
+                        static_cast<const int64_t*>(poff.get()), tcol.get(), tval.get(), cnt.get(), fl);
+        std::vector<int32_t> hl(nfb);
+        copy_d2h(c, hl.data(), fl, nfb);
         std::vector<int64_t> hpoff(static_cast<size_t>(nr) + 1);
         copy_d2h(c, hpoff.data(), poff.get(), nr + 1);
         sync(c);
@@ -1009,17 +1227,7 @@ void spgemm(Ctx& c, const DCsr& A, const DCsr& B, DCsr& C, double* ops) {
             sync(c);
         }
     }
-    C.nr = nr;
-    C.nc = B.nc;
-    C.bs = 1;
-    C.rp.alloc(static_cast<size_t>(nr) + 1, c.s);
-    const int64_t nnz = exclusive_scan_i32(c, cnt.get(), C.rp.get(), nr);
-    C.nnz = nnz;
-    C.ci.alloc(static_cast<size_t>(nnz), c.s);
-    C.va.alloc(static_cast<size_t>(nnz), c.s);
-    launch(c, k_copy_rows, blocks_for(static_cast<int64_t>(nr) * kWarp, 256), 256, 0, nr,
-           static_cast<const int64_t*>(poff.get()), static_cast<const int32_t*>(tcol.get()),
-           static_cast<const double*>(tval.get()), static_cast<const int32_t*>(C.rp.get()), C.ci.get(), C.va.get());
+    compact_rows(c, nr, B.nc, poff, tcol, tval, cnt, C);
 }
 
 void galerkin(Ctx& c, const DCsr& R, const DCsr& A, const DCsr& P, DCsr& C, double* ops) {
