@@ -1,0 +1,2 @@
+timeout 300 python tools/gs_levels.py 5 1024 > gpurun_out/g32_gs_c5.log 2>&1
+timeout 600 python -m pytest tests/test_gpu_kernels.py -q -x -p no:cacheprovider -k "gauss or candidates or segment or cta" > gpurun_out/g32_pytest.log 2>&1; echo "exit $?" >> gpurun_out/g32_pytest.log
