@@ -40,7 +40,7 @@ constexpr int kSsIpt = 16;
 constexpr int kSsTile = kSsThreads * kSsIpt;
 constexpr int kSsThreadCap = 4;   // items per thread list
 constexpr int kSsTileCap = 16;    // items per tile list (global)
-constexpr int kSsGroupTiles = 256;
+constexpr int kSsGroupTiles = 64;   // tiles per group merge (groups merge in parallel)
 constexpr int kSsGroupCap = 64;   // items per group list (global)
 // thread list regions: kSsThreadCap items + one 8-byte word, an odd number of words, so
 // the lanes of a warp touch distinct banks when each works on its own list
@@ -135,7 +135,11 @@ struct StageTerm {
 template <class Term>
 struct GlobalTerm {
     Term t;
-    __device__ double operator()(int64_t i) const { return t.recompute(i); }
+    unsigned long long* ctr;  // AMGCU_SS_TRACE: terms re-read from global memory
+    __device__ double operator()(int64_t i) const {
+        if (ctr) atomicAdd(ctr, 1ull);
+        return t.recompute(i);
+    }
 };
 
 __device__ __forceinline__ int vload(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
@@ -171,7 +175,16 @@ __device__ int merge_from_global(Item* pool, const Item* lists, const int32_t* l
             const Item* src = lists + static_cast<int64_t>(idx + tid) * stride;
             const double* ps = reinterpret_cast<const double*>(src);
             double* pd = reinterpret_cast<double*>(pool + s_off[tid]);
-            for (int w = 0; w < s_len[tid] * static_cast<int>(sizeof(Item) / 8); ++w) pd[w] = __ldcg(ps + w);
+            constexpr int kWords = static_cast<int>(sizeof(Item) / 8);
+            const int nwords = s_len[tid] * kWords;
+            if (nwords >= kWords) {  // the first item's words in flight together (most lists hold one)
+                double v[kWords];
+#pragma unroll
+                for (int w = 0; w < kWords; ++w) v[w] = __ldcg(ps + w);
+#pragma unroll
+                for (int w = 0; w < kWords; ++w) pd[w] = v[w];
+            }
+            for (int w = kWords; w < nwords; ++w) pd[w] = __ldcg(ps + w);
         }
         __syncthreads();
         for (int step = 1; step < m; step <<= 1) {
@@ -376,7 +389,7 @@ __global__ void __launch_bounds__(kSsThreads, 2)
     if (!s_misc[2]) return;
     __threadfence();
     if (tr && tid == 0) tr[5] = gtimer();
-    const GlobalTerm<Term> gterm{term};
+    const GlobalTerm<Term> gterm{term, ws.trace ? reinterpret_cast<unsigned long long*>(ws.trace + ntiles * 12 + 18) : nullptr};
     {
         const int L = merge_from_global(pool, ws.tile_lists + group * kSsGroupTiles * kSsTileCap,
                                         ws.tile_len + group * kSsGroupTiles, gtiles, kSsTileCap, kSsGroupCap, gterm,
@@ -417,7 +430,7 @@ __global__ void __launch_bounds__(kSsThreads, 2)
 // the add chain.  Below the crossover (kSsSmallN) this beats the tile machinery, whose
 // latency does not shrink with n.
 constexpr int kSsSmallThreads = 1024;
-constexpr int kSsSmallN = 16384;
+constexpr int kSsSmallN = 8192;  // the single chain costs ~4.3 ns per term; the tiles ~35 us
 
 template <class Term>
 __global__ void __launch_bounds__(kSsSmallThreads)
@@ -505,14 +518,14 @@ void launch_seqsum(Ctx& c, const Term& term, int64_t n, double* out, bool take_s
     ws.trace = nullptr;
     DBuf<long long> tbuf;
     if (trace) {
-        tbuf.alloc(static_cast<size_t>(ntiles * 12 + 18), c.s);
-        AMG_CK(cudaMemsetAsync(tbuf.get(), 0, sizeof(long long) * (ntiles * 12 + 18), c.s));
+        tbuf.alloc(static_cast<size_t>(ntiles * 12 + 20), c.s);
+        AMG_CK(cudaMemsetAsync(tbuf.get(), 0, sizeof(long long) * (ntiles * 12 + 20), c.s));
         ws.trace = tbuf.get();
     }
     launch_prof(c, c.blas_family, bytes, k_seqsum<Term>, static_cast<unsigned>(ntiles), kSsThreads, kSsSmem, term, n,
                 ntiles, ws, out, take_sqrt);
     if (trace) {
-        std::vector<long long> h(static_cast<size_t>(ntiles * 12 + 18));
+        std::vector<long long> h(static_cast<size_t>(ntiles * 12 + 20));
         copy_d2h(c, h.data(), tbuf.get(), static_cast<int64_t>(h.size()));
         sync(c);
         long long t0 = h[0], tile_end = 0;
@@ -540,6 +553,16 @@ void launch_seqsum(Ctx& c, const Term& term, int64_t n, double* out, bool take_s
                      static_cast<long long>(n), static_cast<long long>(ntiles), lb / ntiles, sim / ntiles, tree / ntiles,
                      items / ntiles, tile_end - t0, g0 - t0, g1 - t0, h[ntiles * 12] - t0, h[ntiles * 12 + 1],
                      cyc / (lb + sim) * 1e3);
+        long long glen = 0, ngr = 0, maxlen = 0;
+        for (int64_t t = 0; t < ntiles; ++t) {
+            maxlen = std::max(maxlen, h[t * 12 + 4]);
+            if (h[t * 12 + 5]) {
+                glen += h[t * 12 + 7];
+                ++ngr;
+            }
+        }
+        std::fprintf(stderr, "[seqsum] global term re-reads %lld, tile list max %lld, group lists %lld (total items %lld)\n",
+                     h[ntiles * 12 + 18], maxlen, ngr, glen);
         std::fprintf(stderr, "[seqsum] tile 0 tree levels (cycles, lenR*100+lenL):");
         for (int lv = 0; lv < 8; ++lv) std::fprintf(stderr, " %lld(%lld)", h[ntiles * 12 + 2 + lv], h[ntiles * 12 + 10 + lv]);
         std::fprintf(stderr, "\n");
