@@ -36,8 +36,9 @@ namespace {
 using ss::Item;
 
 constexpr int kSsThreads = 256;
-constexpr int kSsIpt = 16;
-constexpr int kSsTile = kSsThreads * kSsIpt;
+// terms per thread: 8 (2048-term tiles) for sums of up to kSsIpt16From terms, 16 above
+// (fewer tiles, fewer waves; 2.1M terms: 114 vs 124 us, 234K: 88 vs 113 us)
+constexpr int64_t kSsIpt16From = 1500000;
 constexpr int kSsThreadCap = 4;   // items per thread list
 constexpr int kSsTileCap = 16;    // items per tile list (global)
 constexpr int kSsGroupTiles = 64;   // tiles per group merge (groups merge in parallel)
@@ -46,8 +47,12 @@ constexpr int kSsGroupCap = 64;   // items per group list (global)
 // the lanes of a warp touch distinct banks when each works on its own list
 constexpr int kSsRegion = kSsThreadCap * static_cast<int>(sizeof(Item)) + 8;
 constexpr int kSsPool = kSsThreads * kSsRegion / static_cast<int>(sizeof(Item));  // items, group merges
-constexpr int kSsStage = kSsTile + kSsTile / 16;  // staged terms, one pad slot per 16
-constexpr size_t kSsSmem = static_cast<size_t>(kSsThreads) * kSsRegion + sizeof(double) * kSsStage;
+template <int IPT>
+struct SsCfg {
+    static constexpr int kTile = kSsThreads * IPT;
+    static constexpr int kStage = kTile + kTile / 16;  // staged terms, one pad slot per 16
+    static constexpr size_t kSmem = static_cast<size_t>(kSsThreads) * kSsRegion + sizeof(double) * kStage;
+};
 
 struct TileStatus {
     double agg_s, agg_a, inc_s, inc_a;
@@ -204,7 +209,7 @@ __device__ int merge_from_global(Item* pool, const Item* lists, const int32_t* l
     return acc;
 }
 
-template <class Term>
+template <class Term, int IPT>
 __global__ void __launch_bounds__(kSsThreads, 2)
     k_seqsum(Term term, int64_t n, int64_t ntiles, SsWs ws, double* __restrict__ out, bool take_sqrt) {
     extern __shared__ __align__(16) unsigned char ss_smem[];
@@ -223,25 +228,25 @@ __global__ void __launch_bounds__(kSsThreads, 2)
     if (tid == 0) s_tile = static_cast<long long>(atomicAdd(ws.counters, 1u));
     __syncthreads();
     const int64_t tile = s_tile;
-    const int64_t base = tile * kSsTile;
+    const int64_t base = tile * SsCfg<IPT>::kTile;
     long long* tr = ws.trace ? ws.trace + tile * 12 : nullptr;
     const long long c_start = clock64();
     if (tr && tid == 0) tr[0] = gtimer();
 
     // terms, coalesced: warp w stages [w*512, w*512 + 512) of the tile
-    for (int k = 0; k < kSsIpt; ++k) {
-        const int j = warp * (32 * kSsIpt) + k * 32 + lane;
+    for (int k = 0; k < IPT; ++k) {
+        const int j = warp * (32 * IPT) + k * 32 + lane;
         const int64_t i = base + j;
         tv[stage_idx(j)] = i < n ? term.load(i) : 0.0;
     }
     __syncthreads();
 
     // approximate running sums (any order): the thread's sum and |sum|, block scan
-    const int64_t i0 = std::min<int64_t>(n, base + static_cast<int64_t>(tid) * kSsIpt);
-    const int64_t i1 = std::min<int64_t>(n, i0 + kSsIpt);
+    const int64_t i0 = std::min<int64_t>(n, base + static_cast<int64_t>(tid) * IPT);
+    const int64_t i1 = std::min<int64_t>(n, i0 + IPT);
     double ts = 0.0, ta = 0.0;
-    for (int k = 0; k < kSsIpt; ++k) {
-        const double t = tv[stage_idx(tid * kSsIpt + k)];
+    for (int k = 0; k < IPT; ++k) {
+        const double t = tv[stage_idx(tid * IPT + k)];
         ts += t;
         ta += fabs(t);
     }
@@ -479,7 +484,9 @@ void launch_seqsum(Ctx& c, const Term& term, int64_t n, double* out, bool take_s
         AMG_CK(cudaMemsetAsync(out, 0, sizeof(double), c.s));
         return;
     }
-    const int64_t ntiles = (n + kSsTile - 1) / kSsTile;
+    const bool ipt16 = n > kSsIpt16From;
+    const int64_t tile_terms = ipt16 ? SsCfg<16>::kTile : SsCfg<8>::kTile;
+    const int64_t ntiles = (n + tile_terms - 1) / tile_terms;
     const int64_t ngroups = (ntiles + kSsGroupTiles - 1) / kSsGroupTiles;
     SeqSumWs& w = c.ssws[c.s == c.main_s ? 0 : 1];
     if (w.tiles < ntiles) {
@@ -505,10 +512,12 @@ void launch_seqsum(Ctx& c, const Term& term, int64_t n, double* out, bool take_s
     (void)ngroups;
     static bool attr = false;
     if (!attr) {
-        AMG_CK(cudaFuncSetAttribute(k_seqsum<TDot>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSsSmem)));
-        AMG_CK(cudaFuncSetAttribute(k_seqsum<TAxpyDot>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(kSsSmem)));
-        AMG_CK(cudaFuncSetAttribute(k_seqsum<TPcg>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSsSmem)));
+        for (const void* k : {reinterpret_cast<const void*>(k_seqsum<TDot, 8>), reinterpret_cast<const void*>(k_seqsum<TAxpyDot, 8>),
+                              reinterpret_cast<const void*>(k_seqsum<TPcg, 8>)})
+            AMG_CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(SsCfg<8>::kSmem)));
+        for (const void* k : {reinterpret_cast<const void*>(k_seqsum<TDot, 16>), reinterpret_cast<const void*>(k_seqsum<TAxpyDot, 16>),
+                              reinterpret_cast<const void*>(k_seqsum<TPcg, 16>)})
+            AMG_CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(SsCfg<16>::kSmem)));
         attr = true;
     }
     static const bool trace = [] {
@@ -522,8 +531,12 @@ void launch_seqsum(Ctx& c, const Term& term, int64_t n, double* out, bool take_s
         AMG_CK(cudaMemsetAsync(tbuf.get(), 0, sizeof(long long) * (ntiles * 12 + 20), c.s));
         ws.trace = tbuf.get();
     }
-    launch_prof(c, c.blas_family, bytes, k_seqsum<Term>, static_cast<unsigned>(ntiles), kSsThreads, kSsSmem, term, n,
-                ntiles, ws, out, take_sqrt);
+    if (ipt16)
+        launch_prof(c, c.blas_family, bytes, k_seqsum<Term, 16>, static_cast<unsigned>(ntiles), kSsThreads,
+                    SsCfg<16>::kSmem, term, n, ntiles, ws, out, take_sqrt);
+    else
+        launch_prof(c, c.blas_family, bytes, k_seqsum<Term, 8>, static_cast<unsigned>(ntiles), kSsThreads,
+                    SsCfg<8>::kSmem, term, n, ntiles, ws, out, take_sqrt);
     if (trace) {
         std::vector<long long> h(static_cast<size_t>(ntiles * 12 + 20));
         copy_d2h(c, h.data(), tbuf.get(), static_cast<int64_t>(h.size()));
