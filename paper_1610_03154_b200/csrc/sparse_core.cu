@@ -906,8 +906,8 @@ namespace {
 // Rows whose window or distinct count is too large are listed for the hash kernels.
 // ---------------------------------------------------------------------------------
 constexpr int kBmWords = 256;  // window of 8192 columns
-constexpr int kBmAcc = 1024;   // distinct output columns held per row
-constexpr int kBmWarps = 4;
+constexpr int kBmAcc = 256;    // distinct output columns held per row (more: the hash kernels)
+constexpr int kBmWarps = 8;
 struct BmShared {
     uint32_t bits[kBmWords];
     int32_t pre[kBmWords];

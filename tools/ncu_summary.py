@@ -17,7 +17,9 @@ CAPTURES = ("gs", "gs_seg", "lfmis", "evolution", "spgemm_hash", "spgemm_sort", 
             "jacobi", "prolong", "sell_spmv", "vcycle_fused", "count")
 SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1.0, "nsecond": 1.0, "us": 1e3,
          "usecond": 1e3, "ms": 1e6, "msecond": 1e6}
-for rep in [f"gpurun_out/{tag}_{c}.ncu-rep" for c in CAPTURES if glob.glob(f"gpurun_out/{tag}_{c}.ncu-rep")]:
+reps = [f"gpurun_out/{tag}_{c}.ncu-rep" for c in CAPTURES if glob.glob(f"gpurun_out/{tag}_{c}.ncu-rep")]
+reps += sorted(r for r in glob.glob(f"gpurun_out/{tag}_*.ncu-rep") if r not in reps)
+for rep in reps:
     det = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True, text=True).stdout
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics",
                           "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum"],
