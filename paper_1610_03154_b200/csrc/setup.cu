@@ -359,79 +359,75 @@ __global__ void k_identity(int32_t n, double* __restrict__ I) {
 }
 
 // Inverse of the coarsest operator by Gauss-Jordan elimination with partial pivoting on
-// [A | I] (n x 2n, row-major, L2-resident for the sizes it serves), one cooperative
-// launch.  Step k: block 0 finds the pivot row p (largest |M(i,k)|, i >= k, lowest i on
-// ties); every thread then swaps rows k and p, scales the new row k by 1 / pivot and
-// saves column k (the elimination factors); finally every row i != k subtracts
-// f_i x row k over the columns that can still change (A's columns after k, and I's).
-// A's columns <= k are never read again.  status[0] = 1 on a zero pivot (singular).
+// [A | I] (n x 2n, stored column-major, L2-resident for the sizes it serves), one
+// cooperative launch with ONE grid barrier per step.  Step k reads the pivot (row p,
+// value) chosen at the end of step k - 1 and never writes column k, so every warp can
+// process its own columns j > k from the unswapped matrix: the new row k is M(p, j) /
+// pivot, row p receives the old row k eliminated, every other row i subtracts
+// M(i, k) x (new row k); the elimination factors are column k, read in place.  The warp
+// that owns column k + 1 then picks the next pivot (largest |M(i, k+1)|, i > k, lowest
+// i on ties).  The arithmetic per element is that of a swap, scale, eliminate sequence.
+// status[0] = 1 on a zero pivot (singular).
 constexpr int kGjThreads = 256;
 
 __global__ void __launch_bounds__(kGjThreads)
-    k_gauss_jordan(int32_t n, double* __restrict__ M, double* __restrict__ f, double* __restrict__ piv,
-                   int32_t* __restrict__ prow, int32_t* __restrict__ status) {
+    k_gauss_jordan(int32_t n, double* __restrict__ M, double* __restrict__ pivv, int32_t* __restrict__ pivr,
+                   int32_t* __restrict__ status) {
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
+    const int lane = threadIdx.x & 31;
+    const int64_t gwarp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
     const int64_t w = 2 * static_cast<int64_t>(n);
-    const int64_t gtid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int64_t gthreads = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    __shared__ double sv[kGjThreads];
-    __shared__ int32_t si[kGjThreads];
+    auto col = [&](int64_t j) { return M + j * n; };
+    // the first pivot: warp 0 scans column 0
+    auto pick = [&](const double* cj, int32_t from, int slot) {
+        double best = -1.0;
+        int32_t bi = n;
+        for (int32_t i = from + lane; i < n; i += 32) {
+            const double v = fabs(cj[i]);
+            if (v > best) {
+                best = v;
+                bi = i;
+            }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const double ob = __shfl_xor_sync(0xffffffffu, best, off);
+            const int32_t oi = __shfl_xor_sync(0xffffffffu, bi, off);
+            if (ob > best || (ob == best && oi < bi)) {
+                best = ob;
+                bi = oi;
+            }
+        }
+        if (lane == 0) {
+            pivr[slot] = bi;
+            pivv[slot] = bi < n ? cj[bi] : 0.0;
+            if (!(best > 0.0)) *status = 1;
+        }
+    };
+    if (gwarp == 0) pick(col(0), 0, 0);
+    grid.sync();
     for (int32_t k = 0; k < n; ++k) {
-        if (blockIdx.x == 0) {
-            double best = -1.0;
-            int32_t bi = n;
-            for (int32_t i = k + threadIdx.x; i < n; i += kGjThreads) {
-                const double v = fabs(M[i * w + k]);
-                if (v > best) {
-                    best = v;
-                    bi = i;
-                }
-            }
-            sv[threadIdx.x] = best;
-            si[threadIdx.x] = bi;
-            __syncthreads();
-            for (int off = kGjThreads / 2; off > 0; off >>= 1) {
-                if (threadIdx.x < off) {
-                    const double o = sv[threadIdx.x + off];
-                    const int32_t oi = si[threadIdx.x + off];
-                    if (o > sv[threadIdx.x] || (o == sv[threadIdx.x] && oi < si[threadIdx.x])) {
-                        sv[threadIdx.x] = o;
-                        si[threadIdx.x] = oi;
-                    }
-                }
-                __syncthreads();
-            }
-            if (threadIdx.x == 0) {
-                const int32_t p = si[0];
-                *prow = p;
-                *piv = M[p * w + k];
-                if (!(sv[0] > 0.0)) *status = 1;
-            }
-        }
-        grid.sync();
         if (*reinterpret_cast<volatile int32_t*>(status)) return;  // uniform: every block sees it
-        const int32_t p = *reinterpret_cast<volatile int32_t*>(prow);
-        const double inv = 1.0 / *reinterpret_cast<volatile double*>(piv);
-        // swap rows k and p (scaling the new row k), and save column k
-        for (int64_t j = k + gtid; j < w; j += gthreads) {
-            const double ak = M[k * w + j], ap = M[p * w + j];
-            M[k * w + j] = ap * inv;
-            if (p != k) M[p * w + j] = ak;
-        }
-        for (int64_t i = gtid; i < n; i += gthreads) {
-            if (i == k) continue;
-            f[i] = (i == p) ? M[k * w + k] : M[i * w + k];
-        }
-        grid.sync();
-        // eliminate: columns k+1 .. 2n-1 of every row but k
-        const int64_t cols = w - (k + 1);
-        const int64_t total = static_cast<int64_t>(n) * cols;
-        for (int64_t t = gtid; t < total; t += gthreads) {
-            const int64_t i = t / cols;
-            if (i == k) continue;
-            const int64_t j = k + 1 + (t - i * cols);
-            M[i * w + j] -= f[i] * M[k * w + j];
+        const int slot = k & 1;
+        const int32_t p = *reinterpret_cast<volatile int32_t*>(pivr + slot);
+        const double inv = 1.0 / *reinterpret_cast<volatile double*>(pivv + slot);
+        const double* ck = col(k);
+        const double fp = ck[k];  // the old row k's factor (it moves to row p)
+        for (int64_t j = k + 1 + gwarp; j < w; j += nwarps) {
+            double* cj = col(j);
+            const double a = cj[k], newk = cj[p] * inv;
+            __syncwarp();  // every lane has read rows k and p before any lane writes them
+            for (int32_t i = lane; i < n; i += 32) {
+                double v;
+                if (i == k) v = newk;
+                else if (i == p) v = a - fp * newk;
+                else v = cj[i] - ck[i] * newk;
+                cj[i] = v;
+            }
+            __syncwarp();
+            if (j == k + 1 && k + 1 < n) pick(cj, k + 1, slot ^ 1);
         }
         grid.sync();
     }
@@ -441,16 +437,15 @@ __global__ void k_gj_extract(int32_t n, const double* __restrict__ M, double* __
     const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (t >= static_cast<int64_t>(n) * n) return;
     const int64_t i = t / n, j = t - i * n;
-    inv[t] = M[i * 2 * static_cast<int64_t>(n) + n + j];
+    inv[t] = M[(n + j) * static_cast<int64_t>(n) + i];  // row-major inverse from the column-major [A | I]
 }
 
 __global__ void k_gj_init(int32_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
                           const double* __restrict__ va, double* __restrict__ M) {
     const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    double* row = M + static_cast<int64_t>(i) * 2 * n;
-    for (int32_t p = rp[i]; p < rp[i + 1]; ++p) row[ci[p]] = va[p];
-    row[n + i] = 1.0;
+    for (int32_t p = rp[i]; p < rp[i + 1]; ++p) M[static_cast<int64_t>(ci[p]) * n + i] = va[p];
+    M[static_cast<int64_t>(n + i) * n + i] = 1.0;
 }
 
 constexpr int32_t kGjMax = 4096;  // [A | I] of 4096 rows is 268 MB; above, LU through cuSOLVER
@@ -459,36 +454,39 @@ constexpr int32_t kGjMax = 4096;  // [A | I] of 4096 rows is 268 MB; above, LU t
 // when a zero pivot shows it singular
 bool gauss_jordan_inverse(Ctx& c, const DCsr& A, double* inv) {
     const int32_t n = A.nr;
-    DBuf<double> M(static_cast<size_t>(n) * 2 * n, c.s), f(static_cast<size_t>(n), c.s), piv(1, c.s);
-    DBuf<int32_t> prow(1, c.s), status(1, c.s);
+    DBuf<double> M(static_cast<size_t>(n) * 2 * n, c.s), pivv(2, c.s);
+    DBuf<int32_t> pivr(2, c.s), status(1, c.s);
     AMG_CK(cudaMemsetAsync(M.get(), 0, sizeof(double) * n * 2 * n, c.s));
     AMG_CK(cudaMemsetAsync(status.get(), 0, sizeof(int32_t), c.s));
     launch(c, k_gj_init, blocks_for(n, 128), 128, 0, n, A.rp.get(), A.ci.get(), A.va.get(), M.get());
     int per_sm = 0;
     AMG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gauss_jordan, kGjThreads, 0));
-    const int grid = std::max(1, std::min(per_sm, 4) * c.sms);
+    // enough warps for the 2n columns of a step, at most the co-resident grid
+    const int want = static_cast<int>((2 * static_cast<int64_t>(n) * 32 + kGjThreads - 1) / kGjThreads);
+    const int grid = std::max(1, std::min(std::min(per_sm, 4) * c.sms, want));
     int32_t nn = n;
     double* pM = M.get();
-    double* pf = f.get();
-    double* ppiv = piv.get();
-    int32_t* pprow = prow.get();
+    double* ppv = pivv.get();
+    int32_t* ppr = pivr.get();
     int32_t* pst = status.get();
-    void* args[] = {&nn, &pM, &pf, &ppiv, &pprow, &pst};
+    void* args[] = {&nn, &pM, &ppv, &ppr, &pst};
     const double bytes = 8.0 * 2.0 * static_cast<double>(n) * n * 2.0 * 0.5 * n;
-    if (c.profile && ((c.prof_mask >> kProfCoarseSolve) & 1u)) {
-        cudaEvent_t e0 = prof_event(c), e1 = prof_event(c);
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    const bool prof = c.profile && ((c.prof_mask >> kProfCoarseSolve) & 1u);
+    if (prof) {
+        e0 = prof_event(c);
+        e1 = prof_event(c);
         AMG_CK(cudaEventRecord(e0, c.s));
-        AMG_CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_gauss_jordan), dim3(grid), dim3(kGjThreads), args,
-                                           0, c.s));
+    }
+    AMG_CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_gauss_jordan), dim3(grid), dim3(kGjThreads), args, 0,
+                                       c.s));
+    ++c.launches;
+    if (prof) {
         AMG_CK(cudaEventRecord(e1, c.s));
         c.prof[kProfCoarseSolve].launches += 1;
         c.prof[kProfCoarseSolve].bytes += bytes;
         c.prof[kProfCoarseSolve].pending.emplace_back(e0, e1);
-    } else {
-        AMG_CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_gauss_jordan), dim3(grid), dim3(kGjThreads), args,
-                                           0, c.s));
     }
-    ++c.launches;
     if (read_scalar(c, status.get())) return false;
     launch(c, k_gj_extract, blocks_for(static_cast<int64_t>(n) * n, 256), 256, 0, n,
            static_cast<const double*>(M.get()), inv);

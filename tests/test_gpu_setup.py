@@ -16,7 +16,7 @@ import paper_1610_03154_b200.api as api
 from paper_1610_03154_b200.types import (EvolutionWeighting, FilterRule, KrylovKind, RelaxConfig, RelaxScheme,
                                          SetupOptions,
                                          SolveMethod, SolveOptions, StrengthConfig, StrengthMeasure,
-                                         constant_candidates)
+                                         constant_candidates, from_triplets)
 from tests.helpers import aniso2d, poisson1d, rel_max_err, same_structure
 
 pytestmark = pytest.mark.gpu
@@ -307,4 +307,28 @@ def test_coarse_gauss_jordan(gpu, port, cfg, size, max_size):
     xo, ro = port.solve(ho, b, None, vo)
     assert rg.iterations == ro.iterations and rg.converged == ro.converged
     assert rel_max_err(rg.residual_history, ro.residual_history) <= 1e-10
+    assert rel_max_err(xg, xo) <= 1e-10
+
+
+def test_coarse_gauss_jordan_pivoting(gpu, port):
+    """a coarsest operator whose partial pivoting must swap rows (non-symmetric, small
+    diagonal): the Gauss-Jordan inverse against the CPU solve, 1e-10"""
+    rng = np.random.default_rng(5)
+    n = 700
+    t = []
+    for i in range(n):
+        for j in range(max(0, i - 3), min(n, i + 4)):
+            v = rng.uniform(-1.0, 1.0)
+            if i == j:
+                v *= 1e-3
+            t.append((i, j, v))
+    A = from_triplets(n, n, t)
+    so = SetupOptions(max_size=1000)  # one level: the coarsest is A itself
+    hg = api.setup(A, constant_candidates(n), so, ctx=gpu)
+    ho = port.setup(A, constant_candidates(n), so)
+    assert hg.n_levels() == 1
+    b = rng.uniform(-1.0, 1.0, n)
+    vo = SolveOptions(max_iters=1)
+    xg, rg = api.solve(hg, b, None, vo)
+    xo, ro = port.solve(ho, b, None, vo)
     assert rel_max_err(xg, xo) <= 1e-10
