@@ -77,11 +77,12 @@ def dist_env():
 
 
 # kernel family -> kernel symbol captured by tools/ncu_capture.sh
-PROFILE_TAG = "r02"  # profiles/<tag>_traffic.json, written by tools/ncu_summary.py
-FAMILY_KERNEL = {"gauss_seidel_wavefront": "k_gs_lanes<8, 3, 4, 64>", "aggregate_lfmis": "k_lfmis_lists",
-                 "evolution_soc": "k_evolution2", "spgemm": "k_spgemm_hash", "arnoldi_blas1": "k_arnoldi_coop",
+PROFILE_TAG = "r03"  # profiles/<tag>_traffic.json, written by tools/ncu_summary.py
+FAMILY_KERNEL = {"gauss_seidel_wavefront": "k_gs_seg_warp<3>", "aggregate_lfmis": "k_lfmis_lists",
+                 "spgemm": "k_spgemm_bitmap", "arnoldi_blas1": "k_seqsum<TAxpyDot, 16>", "blas1": "k_seqsum<TDot, 16>",
                  "emin_masked_product": "k_masked_rows", "vcycle_relax0_residual": "k_relax0_residual",
-                 "vcycle_post_relax": "k_jacobi_sweep", "vcycle_prolong": "k_prolong", "krylov_spmv": "k_sell_spmv"}
+                 "vcycle_post_relax": "k_jacobi_sweep", "vcycle_prolong": "k_prolong", "krylov_spmv": "k_sell_spmv",
+                 "vcycle_coarse_fused": "k_vcycle_fused", "coarse_solve": "k_gauss_jordan"}
 
 
 def ncu_traffic(family):

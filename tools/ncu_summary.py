@@ -5,6 +5,7 @@ import csv
 import glob
 import io
 import json
+import re
 import subprocess
 import sys
 
@@ -28,7 +29,10 @@ for rep in reps:
     for r in csv.reader(io.StringIO(det)):
         if len(r) < 15 or r[0] == "ID":
             continue
-        d = launches.setdefault(r[0], {"kernel": r[4].split("(")[0].split("::")[-1], "report": rep})
+        # ncu's --kernel-name-base function leaves "unnamed>::" (anonymous namespace) prefixes
+        base = r[4][:r[4].index("(")] if "(" in r[4] else r[4]
+        name = base.replace("void ", "").replace("amgcu::<unnamed>::", "").replace("unnamed>::", "")
+        d = launches.setdefault(r[0], {"kernel": name, "report": rep})
         if r[12] in want:
             key = want[r[12]]
             if key == "mem" and "mem" in d:
