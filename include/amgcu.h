@@ -134,6 +134,17 @@ amgcu_status amgcu_ctx_set_sequential_reductions(amgcu_ctx ctx, int on);
  * overlapping the level's strength / aggregation / pattern work; 0: in order.  The
  * result is bitwise the same either way. */
 amgcu_status amgcu_ctx_set_candidate_overlap(amgcu_ctx ctx, int on);
+/* Energy-minimisation masked product (interpolation.hpp:186-210): levels of at least
+ * min_rows rows (default 0: all) use the band-staged kernel -- per-CTA pieces of X and
+ * the per-entry match records brought into shared memory by TMA bulk copies; levels
+ * its plan refuses (pattern rows above 24 slots, referenced rows that do not fit the
+ * shared-memory budget) use the register-merge kernel.  min_rows < 0: never.  The
+ * result is bitwise the same either way. */
+amgcu_status amgcu_ctx_set_masked_band(amgcu_ctx ctx, int32_t min_rows);
+/* Levels whose plan was accepted / refused so far, and the last refusal's reason bits
+ * (1 referenced rows beyond the window, 2 too many runs, 4 stage beyond 16-bit offsets,
+ * 8 a pattern row above 24 slots, 64 shared-memory budget). */
+amgcu_status amgcu_ctx_masked_band_stats(amgcu_ctx ctx, int64_t* accepted, int64_t* refused, int32_t* last_fail);
 /* Synchronise the context stream; returns the accumulated device time of the
  * kernels launched since the last reset (CUDA events on the context stream). */
 amgcu_status amgcu_ctx_synchronize(amgcu_ctx ctx);

@@ -25,7 +25,7 @@ lib = C.CDLL(_LIB_PATH)
 lib.amgcu_last_error.restype = C.c_char_p
 lib.amgcu_last_error.argtypes = [C.c_void_p]
 for _name in ("amgcu_ctx_create", "amgcu_ctx_destroy", "amgcu_ctx_set_sequential_reductions",
-              "amgcu_ctx_set_candidate_overlap", "amgcu_ctx_synchronize",
+              "amgcu_ctx_set_candidate_overlap", "amgcu_ctx_set_masked_band", "amgcu_ctx_masked_band_stats", "amgcu_ctx_synchronize",
               "amgcu_ctx_launch_count", "amgcu_ctx_sync_count", "amgcu_setup", "amgcu_setup_device", "amgcu_hier_destroy",
               "amgcu_hier_levels", "amgcu_hier_get_matrix", "amgcu_hier_get_candidates", "amgcu_hier_level_symmetric",
               "amgcu_hier_relax_weights", "amgcu_hier_complexity", "amgcu_hier_ledger", "amgcu_solve", "amgcu_solve_device", "amgcu_cycle",
@@ -38,6 +38,8 @@ lib.amgcu_ctx_create.argtypes = [C.c_int, C.POINTER(C.c_void_p)]
 lib.amgcu_ctx_destroy.argtypes = [C.c_void_p]
 lib.amgcu_ctx_set_sequential_reductions.argtypes = [C.c_void_p, C.c_int]
 lib.amgcu_ctx_set_candidate_overlap.argtypes = [C.c_void_p, C.c_int]
+lib.amgcu_ctx_set_masked_band.argtypes = [C.c_void_p, C.c_int32]
+lib.amgcu_ctx_masked_band_stats.argtypes = [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int32)]
 lib.amgcu_ctx_synchronize.argtypes = [C.c_void_p]
 lib.amgcu_ctx_launch_count.argtypes = [C.c_void_p, C.POINTER(C.c_int64)]
 lib.amgcu_ctx_sync_count.argtypes = [C.c_void_p, C.POINTER(C.c_int64)]
@@ -114,6 +116,16 @@ class Context:
     def set_candidate_overlap(self, on: bool):
         """forward-GS candidate improvement on a second stream beside the aggregation (default on)"""
         self._chk(lib.amgcu_ctx_set_candidate_overlap(self.handle, 1 if on else 0))
+
+    def set_masked_band(self, min_rows: int):
+        """levels of at least min_rows rows run the band-staged (TMA) masked product; < 0: never"""
+        self._chk(lib.amgcu_ctx_set_masked_band(self.handle, int(min_rows)))
+
+    def masked_band_stats(self):
+        """(plans accepted, plans refused, reason bits of the last refusal)"""
+        a, r, f = C.c_int64(0), C.c_int64(0), C.c_int32(0)
+        self._chk(lib.amgcu_ctx_masked_band_stats(self.handle, C.byref(a), C.byref(r), C.byref(f)))
+        return a.value, r.value, f.value
 
     def synchronize(self):
         self._chk(lib.amgcu_ctx_synchronize(self.handle))

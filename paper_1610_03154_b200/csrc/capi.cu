@@ -182,6 +182,18 @@ amgcu_status amgcu_ctx_set_candidate_overlap(amgcu_ctx ctx, int on) {
     return guarded(ctx, [&] { ctx->c.cand_overlap = on != 0; });
 }
 
+amgcu_status amgcu_ctx_set_masked_band(amgcu_ctx ctx, int32_t min_rows) {
+    return guarded(ctx, [&] { ctx->c.band_min_rows = min_rows; });
+}
+
+amgcu_status amgcu_ctx_masked_band_stats(amgcu_ctx ctx, int64_t* accepted, int64_t* refused, int32_t* last_fail) {
+    return guarded(ctx, [&] {
+        *accepted = ctx->c.band_accepted;
+        *refused = ctx->c.band_refused;
+        *last_fail = ctx->c.band_last_fail;
+    });
+}
+
 amgcu_status amgcu_ctx_synchronize(amgcu_ctx ctx) {
     return guarded(ctx, [&] { sync(ctx->c); });
 }

@@ -145,6 +145,11 @@ struct Ctx {
     cudaStream_t main_s = nullptr;  // the context's own stream (c.s outside StreamScopes)
     bool seq = true;  // global reductions in the reference's order (seqsum.cu); false: trees
     bool cand_overlap = true;  // candidate Gauss-Seidel on side2, beside the aggregation (setup.cu)
+    // energy-min masked product: band-staged kernel (masked_band.cuh) on levels of at least
+    // this many rows; -1: never
+    int32_t band_min_rows = 0;
+    int64_t band_accepted = 0, band_refused = 0;  // plans built / refused (failure bits or shared-memory budget)
+    int32_t band_last_fail = 0;                   // failure bits of the last refused plan (64: budget)
     int64_t launches = 0;
     int64_t syncs = 0;  // host synchronisations of the stream
     int blas_family = kProfBlas1;  // family the BLAS-1 launchers record under

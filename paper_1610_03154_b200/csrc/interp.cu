@@ -6,6 +6,8 @@
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "interp.cuh"
@@ -653,6 +655,109 @@ __global__ void k_project(int32_t n, const int32_t* __restrict__ nrp, const int3
     }
 }
 
+#include "masked_band.cuh"
+
+// AMGCU_MASKED_BAND=0 keeps the register-merge kernel on every level (A/B runs)
+bool masked_band_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("AMGCU_MASKED_BAND");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+// blocks of k_cg_columns: the window of columns in flight (AMGCU_CGCOL_BLOCKS_PER_SM, default 2)
+unsigned cg_column_blocks(const Ctx& c) {
+    static const int per_sm = [] {
+        const char* e = std::getenv("AMGCU_CGCOL_BLOCKS_PER_SM");
+        const int v = e ? std::atoi(e) : 2;
+        return v > 0 ? v : 2;
+    }();
+    return static_cast<unsigned>(c.sms * per_sm);
+}
+
+using BandKernel = void (*)(int32_t, int32_t, int32_t, int32_t, int32_t, const int32_t*, const mband::Rec*, const int32_t*,
+                            const int32_t*, const double*, int32_t, const double*, int32_t, const double*,
+                            const unsigned char*, double*, double*, const mband::Run*, const int32_t*, const int32_t*);
+BandKernel band_kernel(int32_t k, bool masks) {
+    switch (k) {
+        case 1: return masks ? mband::k_masked_band<1, true> : mband::k_masked_band<1, false>;
+        case 2: return masks ? mband::k_masked_band<2, true> : mband::k_masked_band<2, false>;
+        case 3: return masks ? mband::k_masked_band<3, true> : mband::k_masked_band<3, false>;
+        default: return masks ? mband::k_masked_band<0, true> : mband::k_masked_band<0, false>;
+    }
+}
+
+// The plan of the band-staged masked product for (A, N): runs per CTA, records per A entry.
+// Rows per CTA: from the average row lengths, halved while the runs of some CTA do not fit
+// the run table or the shared-memory budget (one host synchronisation per attempt).
+mband::Plan masked_band_plan(Ctx& c, const DCsr& A, const DCsr& N, int32_t k) {
+    mband::Plan pl;
+    const int32_t n = N.nr;
+    if (!masked_band_enabled() || c.band_min_rows < 0 || n < c.band_min_rows || A.nnz == 0 || N.nnz == 0) return pl;
+    const double da = static_cast<double>(A.nnz) / n, ln = static_cast<double>(N.nnz) / n;
+    const double per_row = 16.0 * da + 8.0 * ln * 4.5 + 16.0;
+    int32_t R = 128;
+    while (R > 4 && R * per_row > 44.0 * 1024.0) R >>= 1;
+    const bool trace = std::getenv("AMGCU_BAND_TRACE") != nullptr;
+    DBuf<int32_t> info(8, c.s);
+    int32_t h[8];
+    auto refuse = [&](int why) {
+        ++c.band_refused;
+        c.band_last_fail = why;
+        return mband::Plan{};
+    };
+    for (;; R >>= 1) {
+        pl.R = R;
+        pl.nctas = static_cast<int32_t>(blocks_for(n, R));
+        pl.runs.alloc(static_cast<size_t>(pl.nctas) * mband::kMaxRuns, c.s);
+        pl.nruns.alloc(static_cast<size_t>(pl.nctas), c.s);
+        AMG_CK(cudaMemsetAsync(info.get(), 0, sizeof(int32_t) * 8, c.s));
+        launch_prof(c, kProfEminCg, 0.0, mband::k_runs, static_cast<unsigned>(pl.nctas), mband::kThreads, 0, n, R,
+                    A.rp.get(), A.ci.get(), N.rp.get(), pl.runs.get(), pl.nruns.get(), info.get());
+        copy_d2h(c, h, info.get(), 8);
+        sync(c);
+        pl.cap_a = h[1];
+        pl.cap_x = h[2];
+        pl.cap_s = h[3];
+        pl.smem = mband::smem_bytes(R, pl.cap_a, pl.cap_x, pl.cap_s, k);
+        if (trace)
+            std::fprintf(stderr, "[band] n %d nnzA %lld nnzN %lld k %d R %d fail %d cap_a %d cap_x %d cap_s %d longest %d smem %zu\n",
+                         n, static_cast<long long>(A.nnz), static_cast<long long>(N.nnz), k, R, h[0], h[1], h[2], h[3], h[4],
+                         pl.smem);
+        if (h[4] > mband::kMaskSlots) return refuse(8);
+        if (h[0] == 0 && pl.smem <= mband::kSmemBudget) break;
+        if (R <= 4) return refuse(h[0] ? h[0] : 64);
+    }
+    pl.masks = h[4] > mband::kNibSlots;
+    pl.recs.alloc(static_cast<size_t>(A.nnz) + 1, c.s);
+    pl.matches.alloc(1, c.s);
+    AMG_CK(cudaMemsetAsync(pl.matches.get(), 0, sizeof(unsigned long long), c.s));
+    AMG_CK(cudaMemsetAsync(info.get(), 0, sizeof(int32_t) * 8, c.s));
+    if (pl.masks)
+        launch_prof(c, kProfEminCg, 0.0, mband::k_records<true>, static_cast<unsigned>(pl.nctas), mband::kThreads, 0, n, R,
+                    A.rp.get(), A.ci.get(), A.va.get(), N.rp.get(), N.ci.get(), static_cast<const mband::Run*>(pl.runs.get()),
+                    static_cast<const int32_t*>(pl.nruns.get()), pl.recs.get(), info.get(), pl.matches.get());
+    else
+        launch_prof(c, kProfEminCg, 0.0, mband::k_records<false>, static_cast<unsigned>(pl.nctas), mband::kThreads, 0, n, R,
+                    A.rp.get(), A.ci.get(), A.va.get(), N.rp.get(), N.ci.get(), static_cast<const mband::Run*>(pl.runs.get()),
+                    static_cast<const int32_t*>(pl.nruns.get()), pl.recs.get(), info.get(), pl.matches.get());
+    // a record that found no run (cannot happen: the runs cover every referenced row) is
+    // reported with the hierarchy's other deferred checks: the flag is read with the CG's own
+    // final synchronisation through pl.info
+    pl.info = std::move(info);
+    static bool attr_set[8] = {false, false, false, false, false, false, false, false};
+    const int slot = (k >= 1 && k <= 3 ? k : 0) * 2 + (pl.masks ? 1 : 0);
+    if (!attr_set[slot]) {
+        AMG_CK(cudaFuncSetAttribute(band_kernel(k, pl.masks), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(mband::kSmemBudget)));
+        attr_set[slot] = true;
+    }
+    pl.ok = true;
+    ++c.band_accepted;
+    return pl;
+}
+
 __global__ void k_negate(int64_t n, const double* __restrict__ x, double* __restrict__ y) {
     const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (p < n) y[p] = -x[p];
@@ -709,28 +814,50 @@ __global__ void k_cg_ctl_denom(double* __restrict__ st, int32_t* __restrict__ f,
 
 // per column j, entries in increasing row order (CSC positions): e, g, h and the
 // safe step (column_safe_step, interpolation.hpp:247-260), min-reduced into alpha_bits
-__global__ void k_cg_columns(int32_t nc, const int32_t* __restrict__ colptr, const int32_t* __restrict__ pos,
-                             const double* __restrict__ P, const double* __restrict__ APm, const double* __restrict__ D,
-                             const double* __restrict__ ADm, unsigned long long* __restrict__ alpha_bits,
-                             const int32_t* __restrict__ f) {
+// Thread per column; a block walks the column blocks grid-stride, so the columns in
+// flight at any time are one contiguous window (grid * 128 columns): their entries lie
+// in a band of rows whose slots stay in L2 while the neighbouring columns -- which
+// share the 32-byte sectors -- read them.  With every column in flight at once the
+// four arrays streamed through L2 in sector-sized gathers (C5 level 0: 4.1 GB of DRAM
+// traffic for 0.54 GB of data).  The loads of 8 entries are issued before their sums.
+__global__ void __launch_bounds__(128)
+    k_cg_columns(int32_t nc, const int32_t* __restrict__ colptr, const int32_t* __restrict__ pos,
+                 const double* __restrict__ P, const double* __restrict__ APm, const double* __restrict__ D,
+                 const double* __restrict__ ADm, unsigned long long* __restrict__ alpha_bits,
+                 const int32_t* __restrict__ f) {
     if (f[0]) return;
-    const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= nc) return;
-    double e = 0.0, g = 0.0, h = 0.0;
-    for (int32_t q = colptr[j]; q < colptr[j + 1]; ++q) {
-        const int32_t p = pos[q];
-        e += P[p] * APm[p];
-        g += D[p] * APm[p];
-        h += D[p] * ADm[p];
+    constexpr int U = 8;
+    for (int32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < nc; j += gridDim.x * blockDim.x) {
+        double e = 0.0, g = 0.0, h = 0.0;
+        const int32_t qe = colptr[j + 1];
+        for (int32_t q = colptr[j]; q < qe; q += U) {
+            double vp[U], va[U], vd[U], vm[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const bool in = q + u < qe;
+                const int32_t p = in ? __ldg(&pos[q + u]) : 0;
+                vp[u] = in ? __ldg(&P[p]) : 0.0;
+                va[u] = in ? __ldg(&APm[p]) : 0.0;
+                vd[u] = in ? __ldg(&D[p]) : 0.0;
+                vm[u] = in ? __ldg(&ADm[p]) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (q + u < qe) {
+                    e += vp[u] * va[u];
+                    g += vd[u] * va[u];
+                    h += vd[u] * vm[u];
+                }
+        }
+        if (h <= 0.0) continue;
+        const double norm_j = sqrt(sd::dmax(e, 0.0));
+        const double tol = 2.5e-13 * sd::dmax(norm_j, 1.0e-30);
+        const double budget = tol * (2.0 * norm_j + tol);
+        const double disc = g * g + h * budget;
+        const double beta = (-g + sqrt(sd::dmax(disc, 0.0))) / h;
+        if (beta >= 0.0)  // all finite steps are >= 0; NaN never wins (std::min semantics)
+            atomicMin(alpha_bits, static_cast<unsigned long long>(__double_as_longlong(beta)));
     }
-    if (h <= 0.0) return;
-    const double norm_j = sqrt(sd::dmax(e, 0.0));
-    const double tol = 2.5e-13 * sd::dmax(norm_j, 1.0e-30);
-    const double budget = tol * (2.0 * norm_j + tol);
-    const double disc = g * g + h * budget;
-    const double beta = (-g + sqrt(sd::dmax(disc, 0.0))) / h;
-    if (beta >= 0.0)  // all finite steps are >= 0; NaN never wins (std::min semantics)
-        atomicMin(alpha_bits, static_cast<unsigned long long>(__double_as_longlong(beta)));
 }
 
 __global__ void k_cg_ctl_alpha(double* __restrict__ st, int32_t* __restrict__ f,
@@ -1115,7 +1242,9 @@ void energy_minimize(Ctx& c, const DCsr& A, const DCsr& T, const double* B, cons
         tally(c, kk * kk * rc.len + kk * kk * kk * rc.rows);
         proj_ops = 2.0 * kk * rc.len + kk * kk * rc.rows;
     }
-    DBuf<double> P(static_cast<size_t>(nz), c.s);
+    // vectors the band kernel stages by 16-byte pieces are padded to an even length
+    const size_t nzs = (static_cast<size_t>(nz) + 1) & ~static_cast<size_t>(1);
+    DBuf<double> P(nzs, c.s);
     {
         DBuf<int32_t> err(1, c.s);
         AMG_CK(cudaMemsetAsync(err.get(), 0, sizeof(int32_t), c.s));
@@ -1130,6 +1259,20 @@ void energy_minimize(Ctx& c, const DCsr& A, const DCsr& T, const double* B, cons
     };
     const unsigned mp_block = 128;
     const unsigned ew = blocks_for(nz, 256);
+    // Y = (M X)|_N, Yp its projection (either may be null); M's plan when the level takes the band kernel
+    auto masked = [&](const DCsr& M, const mband::Plan& pl, int family, double bytes, const double* x, double* y,
+                      double* yp, const int32_t* stop) {
+        if (pl.ok)
+            launch_prof(c, family, bytes, band_kernel(k, pl.masks), static_cast<unsigned>(pl.nctas), mband::kThreads, pl.smem,
+                        n, pl.R, pl.cap_a, pl.cap_x, pl.cap_s, M.rp.get(), static_cast<const mband::Rec*>(pl.recs.get()),
+                        N.rp.get(), N.ci.get(), x, k, Bc, nc, static_cast<const double*>(gp.get()),
+                        static_cast<const unsigned char*>(is_root.get()), y, yp,
+                        static_cast<const mband::Run*>(pl.runs.get()), static_cast<const int32_t*>(pl.nruns.get()), stop);
+        else
+            launch_prof(c, family, bytes, k_masked_rows, mp_grid, mp_block, 0, n, M.rp.get(), M.ci.get(), M.va.get(),
+                        N.rp.get(), N.ci.get(), x, k, Bc, nc, static_cast<const double*>(gp.get()),
+                        static_cast<const unsigned char*>(is_root.get()), y, yp, stop);
+    };
 
     if (krylov == 0) {
         DBuf<double> dinv(static_cast<size_t>(n), c.s);
@@ -1139,12 +1282,10 @@ void energy_minimize(Ctx& c, const DCsr& A, const DCsr& T, const double* B, cons
         DBuf<int32_t> colptr, pos;
         transpose_positions(c, N, colptr, pos, nullptr);
         DBuf<double> APm(static_cast<size_t>(nz), c.s), R(static_cast<size_t>(nz), c.s), Z(static_cast<size_t>(nz), c.s),
-            D(static_cast<size_t>(nz), c.s), ADm(static_cast<size_t>(nz), c.s), ADp(static_cast<size_t>(nz), c.s);
+            D(nzs, c.s), ADm(static_cast<size_t>(nz), c.s), ADp(static_cast<size_t>(nz), c.s);
         AMG_CK(cudaMemsetAsync(D.get(), 0, sizeof(double) * nz, c.s));
-        launch(c, k_masked_rows, mp_grid, mp_block, 0, n, A.rp.get(), A.ci.get(), A.va.get(), N.rp.get(),
-               N.ci.get(), static_cast<const double*>(P.get()), k, Bc, nc, static_cast<const double*>(gp.get()),
-               static_cast<const unsigned char*>(is_root.get()), APm.get(), static_cast<double*>(nullptr),
-               static_cast<const int32_t*>(nullptr));
+        const mband::Plan plan = masked_band_plan(c, A, N, k);
+        masked(A, plan, kProfOther, 0.0, P.get(), APm.get(), nullptr, nullptr);
         launch(c, k_negate, ew, 256, 0, nz, static_cast<const double*>(APm.get()), R.get());
         launch_prof(c, kProfEminCg, 0.0, k_project, blocks_for(n, 128), 128, 0, n, N.rp.get(), N.ci.get(), k, Bc, nc,
                static_cast<const double*>(gp.get()), static_cast<const unsigned char*>(is_root.get()), R.get());
@@ -1165,14 +1306,10 @@ void energy_minimize(Ctx& c, const DCsr& A, const DCsr& T, const double* B, cons
             launch_prof(c, kProfEminCg, 0.0, k_cg_ctl_newsum, 1, 1, 0, S, F);
             launch_prof(c, kProfEminCg, 0.0, k_cg_dir, ew, 256, 0, nz, static_cast<const double*>(Z.get()), D.get(),
                    static_cast<const double*>(S), static_cast<const int32_t*>(F));
-            launch_prof(c, kProfMaskedProduct, mp_bytes(A, 2), k_masked_rows, mp_grid, mp_block, 0, n, A.rp.get(),
-                   A.ci.get(), A.va.get(), N.rp.get(),
-                   N.ci.get(), static_cast<const double*>(D.get()), k, Bc, nc, static_cast<const double*>(gp.get()),
-                   static_cast<const unsigned char*>(is_root.get()), ADm.get(), ADp.get(),
-                   static_cast<const int32_t*>(F));
+            masked(A, plan, kProfMaskedProduct, mp_bytes(A, 2), D.get(), ADm.get(), ADp.get(), F);
             dot(c, D.get(), ADm.get(), nz, S + 7);
             launch_prof(c, kProfEminCg, 0.0, k_cg_ctl_denom, 1, 1, 0, S, F, abits.get());
-            launch_prof(c, kProfEminCg, 0.0, k_cg_columns, blocks_for(nc, 128), 128, 0, nc, static_cast<const int32_t*>(colptr.get()),
+            launch_prof(c, kProfEminCg, 0.0, k_cg_columns, std::min(blocks_for(nc, 128), cg_column_blocks(c)), 128, 0, nc, static_cast<const int32_t*>(colptr.get()),
                    static_cast<const int32_t*>(pos.get()), static_cast<const double*>(P.get()),
                    static_cast<const double*>(APm.get()), static_cast<const double*>(D.get()),
                    static_cast<const double*>(ADm.get()), abits.get(), static_cast<const int32_t*>(F));
@@ -1182,14 +1319,21 @@ void energy_minimize(Ctx& c, const DCsr& A, const DCsr& T, const double* B, cons
                    static_cast<const double*>(S), static_cast<const int32_t*>(F), s);
         }
         int32_t fh[8];
+        int32_t band_bad = 0;
+        unsigned long long band_matches = 0;
         copy_d2h(c, fh, F, 8);
+        if (plan.ok) {
+            copy_d2h(c, &band_bad, plan.info.get(), 1);
+            copy_d2h(c, &band_matches, plan.matches.get(), 1);
+        }
         sync(c);
+        if (band_bad) throw std::logic_error("energy_minimize: band plan left an entry without its run");
         st.iterations = fh[2];
         st.breakdown = fh[3] != 0;
         if (counting) {
             // the reference's counts (interpolation.hpp:319,333,355): the initial masked product
             // and projection, every completed iteration, and the part of the stopping one
-            const double M = masked_count(c, A, N), z = static_cast<double>(nz);
+            const double M = plan.ok ? static_cast<double>(band_matches) : masked_count(c, A, N), z = static_cast<double>(nz);
             const double full = z + (M + proj_ops + 3.0 * z) + 3.0 * z;
             double ops = M + proj_ops + fh[2] * full;
             if (fh[4] == 1) ops += z;
@@ -1205,41 +1349,42 @@ void energy_minimize(Ctx& c, const DCsr& A, const DCsr& T, const double* B, cons
     transpose(c, A, At);
     spgemm(c, At, A, AtA);
     DBuf<double> R0(static_cast<size_t>(nz), c.s);
-    launch(c, k_masked_rows, mp_grid, mp_block, 0, n, AtA.rp.get(), AtA.ci.get(), AtA.va.get(), N.rp.get(),
-           N.ci.get(), static_cast<const double*>(P.get()), k, Bc, nc, static_cast<const double*>(gp.get()),
-           static_cast<const unsigned char*>(is_root.get()), R0.get(), static_cast<double*>(nullptr),
-           static_cast<const int32_t*>(nullptr));
+    const mband::Plan plan = masked_band_plan(c, AtA, N, k);
+    masked(AtA, plan, kProfOther, 0.0, P.get(), R0.get(), nullptr, nullptr);
     launch(c, k_negate, ew, 256, 0, nz, static_cast<const double*>(R0.get()), R0.get());
     launch_prof(c, kProfEminCg, 0.0, k_project, blocks_for(n, 128), 128, 0, n, N.rp.get(), N.ci.get(), k, Bc, nc,
            static_cast<const double*>(gp.get()), static_cast<const unsigned char*>(is_root.get()), R0.get());
     DBuf<double> scal(2, c.s);
     nrm2(c, R0.get(), nz, scal.get());
+    int32_t band_bad = 0;
+    unsigned long long band_matches = 0;
+    if (plan.ok) {
+        copy_d2h(c, &band_bad, plan.info.get(), 1);
+        copy_d2h(c, &band_matches, plan.matches.get(), 1);
+    }
     const double beta = read_scalar(c, scal.get());
-    const double Mg = counting ? masked_count(c, AtA, N) : 0.0;
+    if (band_bad) throw std::logic_error("energy_minimize: band plan left an entry without its run");
+    const double Mg = !counting ? 0.0 : plan.ok ? static_cast<double>(band_matches) : masked_count(c, AtA, N);
     tally(c, Mg + proj_ops + static_cast<double>(nz));  // interpolation.hpp:374
     if (beta < 1e-300) {
         compact_pattern(c, N, P.get(), T.bs, Pout);
         return;
     }
     const int m = iters;
-    DBuf<double> V(static_cast<size_t>(nz) * (m + 1), c.s);
+    DBuf<double> V(nzs * (m + 1), c.s);  // Krylov vectors at an even stride
     DBuf<double> Hd(static_cast<size_t>(m + 1) * m, c.s);
     AMG_CK(cudaMemsetAsync(Hd.get(), 0, sizeof(double) * (m + 1) * m, c.s));
     copy_d2d(c, V.get(), R0.get(), nz);
     scale_const(c, 1.0 / beta, V.get(), nz);
     int built = 0;
     for (int s = 0; s < m; ++s) {
-        double* W = V.get() + static_cast<size_t>(s + 1) * nz;
-        launch_prof(c, kProfMaskedProduct, mp_bytes(AtA, 1), k_masked_rows, mp_grid, mp_block, 0, n, AtA.rp.get(),
-               AtA.ci.get(), AtA.va.get(), N.rp.get(),
-               N.ci.get(), static_cast<const double*>(V.get() + static_cast<size_t>(s) * nz), k, Bc, nc,
-               static_cast<const double*>(gp.get()), static_cast<const unsigned char*>(is_root.get()),
-               static_cast<double*>(nullptr), W, static_cast<const int32_t*>(nullptr));
+        double* W = V.get() + static_cast<size_t>(s + 1) * nzs;
+        masked(AtA, plan, kProfMaskedProduct, mp_bytes(AtA, 1), V.get() + static_cast<size_t>(s) * nzs, nullptr, W, nullptr);
         double* hn_d = Hd.get() + (s + 1) * m + s;
         dot(c, W, V.get(), nz, Hd.get() + s);
         for (int t = 0; t <= s; ++t)
-            axpy_dot(c, Hd.get() + t * m + s, -1.0, V.get() + static_cast<size_t>(t) * nz, W,
-                     t < s ? V.get() + static_cast<size_t>(t + 1) * nz : nullptr, nz,
+            axpy_dot(c, Hd.get() + t * m + s, -1.0, V.get() + static_cast<size_t>(t) * nzs, W,
+                     t < s ? V.get() + static_cast<size_t>(t + 1) * nzs : nullptr, nz,
                      t < s ? Hd.get() + (t + 1) * m + s : hn_d, t == s);
         const double hn = read_scalar(c, hn_d);
         built = s + 1;
@@ -1277,7 +1422,7 @@ void energy_minimize(Ctx& c, const DCsr& A, const DCsr& T, const double* B, cons
     // V holds built+1 vectors only up to the last normalised one (V[s+1] is filled
     // in place while building); the reference combines V[0..built-1]
     for (int t = 0; t < built; ++t)
-        launch_prof(c, kProfEminCg, 0.0, k_axpy_host, ew, 256, 0, nz, y[t], static_cast<const double*>(V.get() + static_cast<size_t>(t) * nz),
+        launch_prof(c, kProfEminCg, 0.0, k_axpy_host, ew, 256, 0, nz, y[t], static_cast<const double*>(V.get() + static_cast<size_t>(t) * nzs),
                U.get());
     DCsr Tc, Uc, AT, AU;
     compact_pattern(c, N, P.get(), T.bs, Tc);

@@ -113,6 +113,27 @@ def test_candidate_overlap_bitwise(cfg, size):
     _bitwise_hierarchy(h1, h2)
 
 
+@pytest.mark.parametrize("cfg,size", [(1, 96), (2, 200), (3, 160), (4, 160), (5, 96), (5, 1024)],
+                         ids=["C1-96", "C2-200", "C3-160", "C4-160", "C5-96", "C5-1024"])
+def test_masked_band_bitwise(cfg, size):
+    """energy-min masked product: the band-staged kernel (TMA bulk copies of the X pieces
+    and match records into shared memory, csrc/masked_band.cuh) on every level it accepts
+    against the register-merge kernel on every level -- same per-slot order of additions
+    (interpolation.hpp:196-206), so the hierarchies are bit-identical"""
+    A, B, Bh, b = api.generate_config(cfg, size)
+    so, vo = api.config_options(cfg)
+    hs = []
+    for min_rows in (1, -1):
+        ctx = api.Context(0)
+        ctx.set_masked_band(min_rows)
+        hs.append((ctx, api.setup(A, B, so, Bh, ctx=ctx)))
+    (c1, h1), (c2, h2) = hs
+    acc, ref, why = c1.masked_band_stats()
+    assert acc > 0, (acc, ref, why)
+    assert c2.masked_band_stats()[0] == 0
+    _bitwise_hierarchy(h1, h2)
+
+
 def test_tree_mode_structure_c2(gpu_tree, port):
     """tree reductions (not the reference's summation order): C2's structure and
     iteration count still match; values agree to 1e-10 on the fine levels"""
