@@ -216,7 +216,11 @@ struct FusedLevel {
 };
 
 constexpr int kFusedThreads = 256;
-constexpr int32_t kFusedMaxRows = 65536;  // the fused cycle starts at the first level this small
+constexpr int32_t kFusedMaxRows = 65536;  // the fused cycle starts at the first level this small ...
+// ... whose operator also has at most this many entries: the cooperative grid runs one row per
+// warp at a time (2,368 warps), so a level with more work than that is latency-bound inside it
+// (C5 level 2, 39K rows x 69 entries: 42 us per relaxation pass against ~10 us standalone)
+constexpr int64_t kFusedMaxNnz = 1500000;
 constexpr int kFusedWarps = kFusedThreads / 32;
 
 struct FusedCtx {
@@ -529,7 +533,9 @@ struct Driver {
         static const int32_t max_rows = std::getenv("AMGCU_FUSED_MAX_ROWS")
                                             ? std::atoi(std::getenv("AMGCU_FUSED_MAX_ROWS"))
                                             : kFusedMaxRows;
-        if (!fused_enabled() || l == 0 || l + 1 >= L || h.lv[l].A.nr > max_rows) return false;
+        static const int64_t max_nnz = std::getenv("AMGCU_FUSED_MAX_NNZ") ? std::atoll(std::getenv("AMGCU_FUSED_MAX_NNZ"))
+                                                                            : kFusedMaxNnz;
+        if (!fused_enabled() || l == 0 || l + 1 >= L || h.lv[l].A.nr > max_rows || h.lv[l].A.nnz > max_nnz) return false;
         if (h.o.pre_scheme != 0 || h.o.post_scheme != 0 || h.o.pre_sweeps != 1 || h.o.post_sweeps != 1) return false;
         const int nlev = static_cast<int>(L - l);
         // the caller passes level l's own b / x (apply from level l - 1), so the

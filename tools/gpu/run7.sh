@@ -1,0 +1,5 @@
+python -m pytest tests/test_gpu_config_scale.py tests/test_gpu_setup.py tests/test_gpu_golden.py -q -x -k "masked_band or ledger or golden or full_size" > gpurun_out/t7.log 2>&1
+tail -3 gpurun_out/t7.log
+for c in "5 1024" "2 1024" "4 2048"; do set -- $c
+python tools/family_times.py --config $1 --size $2 --tag c$1 2>&1 | grep "^\[" | tr ' ' '\n' | grep -E "emin_|total" | tr '\n' ' '; echo
+done
