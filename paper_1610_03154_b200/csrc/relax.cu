@@ -874,113 +874,176 @@ __global__ void __launch_bounds__(kSwWarps * 32)
     const size_t stride = static_cast<size_t>(n) * K;
     double (*rg)[kSwRing] = ring[w];
     double (*sp)[32] = stage[w];
-    // software pipeline over the items u = (sweep, row): the row bounds two items ahead
-    // and the first 32 entries one item ahead are loaded before they are needed
+    // software pipeline over the items u = (sweep, row), so that no global-memory latency
+    // sits between the end of one row and the start of the next: the row bounds three
+    // items ahead, the first 32 entries two items ahead, and -- issued while lane 0 adds
+    // the current row's products -- the next item's inverse diagonal and the values its
+    // first 32 entries read outside the ring (a value still pending then is polled when
+    // the item runs; a published value is final, the per-sweep buffers are written once)
     const int32_t len = q1 - q0;
     const int64_t total = static_cast<int64_t>(len) * nsweeps;
-    auto row_of = [&](int64_t u) { return q0 + static_cast<int32_t>(u % len); };
-    int32_t lo1 = __ldg(rp + q0), hi1 = __ldg(rp + q0 + 1);  // item 0
-    int32_t j1 = -1;
-    double a1 = 0.0;
-    if (lo1 + lane < hi1) {
-        j1 = __ldg(ci + lo1 + lane);
-        a1 = __ldg(va + lo1 + lane);
-    }
-    int32_t lo2 = 0, hi2 = 0;  // item 1
-    if (total > 1) {
-        const int32_t r = row_of(1);
-        lo2 = __ldg(rp + r);
-        hi2 = __ldg(rp + r + 1);
-    }
+    // (sweep, position) of item u, kept incrementally (no 64-bit divisions in the loop)
+    int s_cur = 0;
+    int32_t pos_cur = 0;
+    auto ahead = [&](int k, int& s_, int32_t& pos_) {  // item u + k, k <= 3
+        s_ = s_cur;
+        pos_ = pos_cur + k;
+        while (pos_ >= len) {
+            pos_ -= len;
+            ++s_;
+        }
+    };
+    auto row_ahead = [&](int k) {
+        int s_;
+        int32_t pos_;
+        ahead(k, s_, pos_);
+        return q0 + pos_;
+    };
+    struct Src {
+        bool use, ring, settled;
+        const double* p;
+    };
+    auto classify = [&](int32_t i, int s, int32_t j, bool act) {
+        Src r;
+        r.use = act && j != i;
+        const bool newer = j < i;
+        const bool own = j >= q0 && j < q1;
+        // where the value comes from: own ring (this sweep, own segment, recent),
+        // own or settled stores (no poll), or another segment's buffer (poll)
+        r.ring = r.use && newer && own && i - j <= kSwRing;
+        r.settled = !newer && (s == 0 || own);
+        r.p = X + static_cast<size_t>(newer ? s + 1 : s) * stride + j;
+        return r;
+    };
+    auto fetch = [&](const Src& r, unsigned long long (&v)[K]) {
+#pragma unroll
+        for (int c = 0; c < K; ++c) {
+            v[c] = 0ull;
+            if (r.use && !r.ring)
+                v[c] = r.settled ? static_cast<unsigned long long>(__double_as_longlong(r.p[static_cast<size_t>(c) * n]))
+                                 : load_relaxed_bits(r.p + static_cast<size_t>(c) * n);
+        }
+    };
+    auto first_chunk = [&](int32_t lo_, int32_t hi_, int32_t& j_, double& a_) {
+        j_ = -1;
+        a_ = 0.0;
+        if (lo_ + lane < hi_) {
+            j_ = __ldg(ci + lo_ + lane);
+            a_ = __ldg(va + lo_ + lane);
+        }
+    };
+    auto bounds = [&](int64_t u, int k, int32_t& lo_, int32_t& hi_) {  // item u + k
+        lo_ = hi_ = 0;
+        if (u + k < total) {
+            const int32_t r = row_ahead(k);
+            lo_ = __ldg(rp + r);
+            hi_ = __ldg(rp + r + 1);
+        }
+    };
+    int32_t lo1, hi1, lo2, hi2, lo3, hi3;  // items u, u + 1, u + 2 at the top of iteration u
+    bounds(0, 0, lo1, hi1);
+    bounds(0, 1, lo2, hi2);
+    bounds(0, 2, lo3, hi3);
+    int32_t j1, j2;
+    double a1, a2;
+    first_chunk(lo1, hi1, j1, a1);
+    first_chunk(lo2, hi2, j2, a2);
+    unsigned long long v1[K];  // item u's prefetched values
+    double d1 = inv_diag[q0];
+    fetch(classify(q0, 0, j1 < 0 ? q0 : j1, j1 >= 0), v1);
     for (int64_t u = 0; u < total; ++u) {
-        const int s = static_cast<int>(u / len);
-        const int32_t i = row_of(u);
+        const int s = s_cur;
+        const int32_t i = q0 + pos_cur;
         const int32_t lo = lo1, hi = hi1;
         const int32_t jf = j1;
-        const double af = a1;
-        // advance the pipeline: item u + 1's first chunk, item u + 2's bounds
+        const double af = a1, dcur = d1;
+        unsigned long long vf[K];
+#pragma unroll
+        for (int c = 0; c < K; ++c) vf[c] = v1[c];
+        // advance the pipeline: item u + 2's first chunk, item u + 3's bounds
         lo1 = lo2;
         hi1 = hi2;
-        j1 = -1;
-        a1 = 0.0;
-        if (u + 1 < total && lo1 + lane < hi1) {
-            j1 = __ldg(ci + lo1 + lane);
-            a1 = __ldg(va + lo1 + lane);
-        }
-        if (u + 2 < total) {
-            const int32_t r = row_of(u + 2);
-            lo2 = __ldg(rp + r);
-            hi2 = __ldg(rp + r + 1);
-        }
-        const double* xin = X + static_cast<size_t>(s) * stride;
+        j1 = j2;
+        a1 = a2;
+        lo2 = lo3;
+        hi2 = hi3;
+        first_chunk(lo2, hi2, j2, a2);
+        bounds(u, 3, lo3, hi3);
         double* xout = X + static_cast<size_t>(s + 1) * stride;
         double acc[K];
 #pragma unroll
         for (int c = 0; c < K; ++c) acc[c] = b ? b[static_cast<size_t>(c) * n + i] : 0.0;
-        for (int32_t e0 = lo; e0 < hi; e0 += 32) {
+        for (int32_t e0 = lo; e0 < hi || e0 == lo; e0 += 32) {
             const int32_t p = e0 + lane;
             const bool act = p < hi;
             int32_t j = i;
             double a = 0.0;
+            unsigned long long v[K];
+            Src sr;
             if (e0 == lo) {
                 if (act) {
                     j = jf;
                     a = af;
                 }
-            } else if (act) {
-                j = __ldg(ci + p);
-                a = __ldg(va + p);
-            }
-            const bool use = act && j != i;
-            // where the value comes from: own ring (this sweep, own segment, recent),
-            // own or settled stores (no poll), or another segment's buffer (poll)
-            const bool newer = j < i;
-            const bool own = j >= q0 && j < q1;
-            const bool from_ring = use && newer && own && i - j <= kSwRing;
-            const bool settled = !newer && (s == 0 || own);
-            const double* src = (newer ? xout : xin) + j;
-            unsigned long long v[K];
+                sr = classify(i, s, j, act);
 #pragma unroll
-            for (int c = 0; c < K; ++c) {
-                v[c] = 0ull;
-                if (use && !from_ring)
-                    v[c] = settled ? static_cast<unsigned long long>(__double_as_longlong(src[static_cast<size_t>(c) * n]))
-                                   : load_relaxed_bits(src + static_cast<size_t>(c) * n);
+                for (int c = 0; c < K; ++c) v[c] = vf[c];
+            } else {
+                if (act) {
+                    j = __ldg(ci + p);
+                    a = __ldg(va + p);
+                }
+                sr = classify(i, s, j, act);
+                fetch(sr, v);
             }
             unsigned ns = 8;
             while (true) {
                 bool pend = false;
 #pragma unroll
-                for (int c = 0; c < K; ++c) pend |= use && !from_ring && v[c] == kPending;
+                for (int c = 0; c < K; ++c) pend |= sr.use && !sr.ring && v[c] == kPending;
                 if (!__any_sync(0xffffffffu, pend)) break;
                 if (pend) {
                     __nanosleep(ns);
 #pragma unroll
                     for (int c = 0; c < K; ++c)
-                        if (v[c] == kPending) v[c] = load_relaxed_bits(src + static_cast<size_t>(c) * n);
+                        if (v[c] == kPending) v[c] = load_relaxed_bits(sr.p + static_cast<size_t>(c) * n);
                 }
                 ns = ns < max_ns ? 2 * ns : max_ns;
             }
 #pragma unroll
             for (int c = 0; c < K; ++c) {
-                const double xv = from_ring ? rg[c][j % kSwRing] : __longlong_as_double(static_cast<long long>(v[c]));
-                sp[c][lane] = use ? a * xv : 0.0;
+                const double xv = sr.ring ? rg[c][j % kSwRing] : __longlong_as_double(static_cast<long long>(v[c]));
+                sp[c][lane] = sr.use ? a * xv : 0.0;
             }
             __syncwarp();
+            const bool last = e0 + 32 >= hi;
+            if (last && u + 1 < total) {
+                // the next item's inverse diagonal and out-of-ring values, in flight
+                // while lane 0 adds this row's products
+                int s1;
+                int32_t pos1;
+                ahead(1, s1, pos1);
+                const int32_t i1 = q0 + pos1;
+                d1 = inv_diag[i1];
+                fetch(classify(i1, s1, j1 < 0 ? i1 : j1, j1 >= 0), v1);
+            }
             if (lane == 0) {
+                // the chunk's entries in CSR order (lanes beyond them hold +0.0, an exact identity)
+                const int cnt = min(32, hi - e0);
 #pragma unroll
                 for (int l = 0; l < 32; ++l) {
+                    if (l < cnt) {
 #pragma unroll
-                    for (int c = 0; c < K; ++c) acc[c] -= sp[c][l];
+                        for (int c = 0; c < K; ++c) acc[c] -= sp[c][l];
+                    }
                 }
             }
             __syncwarp();
         }
         if (lane == 0) {
-            const double d = inv_diag[i];
 #pragma unroll
             for (int c = 0; c < K; ++c) {
-                const double xn = acc[c] * d;
+                const double xn = acc[c] * dcur;
                 rg[c][i % kSwRing] = xn;
                 cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> out(
                     *reinterpret_cast<unsigned long long*>(&xout[static_cast<size_t>(c) * n + i]));
@@ -988,6 +1051,10 @@ __global__ void __launch_bounds__(kSwWarps * 32)
             }
         }
         __syncwarp();
+        if (++pos_cur == len) {
+            pos_cur = 0;
+            ++s_cur;
+        }
     }
 }
 
