@@ -77,12 +77,12 @@ def dist_env():
 
 
 # kernel family -> kernel symbol captured by tools/ncu_capture.sh
-PROFILE_TAG = "r03"  # profiles/<tag>_traffic.json, written by tools/ncu_summary.py
+PROFILE_TAG = "r04"  # profiles/<tag>_traffic.json, written by tools/ncu_summary.py
 FAMILY_KERNEL = {"gauss_seidel_wavefront": "k_gs_seg_warp<3>", "aggregate_lfmis": "k_lfmis_lists",
                  "spgemm": "k_spgemm_bitmap", "arnoldi_blas1": "k_seqsum<TAxpyDot, 16>", "blas1": "k_seqsum<TDot, 16>",
-                 "emin_masked_product": "k_masked_rows", "vcycle_relax0_residual": "k_relax0_residual",
+                 "emin_masked_product": "k_masked_band<3, 0>", "vcycle_relax0_residual": "k_relax0_residual",
                  "vcycle_post_relax": "k_jacobi_sweep", "vcycle_prolong": "k_prolong", "krylov_spmv": "k_sell_spmv",
-                 "vcycle_coarse_fused": "k_vcycle_fused", "coarse_solve": "k_gauss_jordan"}
+                 "vcycle_coarse_fused": "k_vcycle_fused", "coarse_solve": "k_gauss_jordan", "emin_cg": "k_cg_columns"}
 
 
 def ncu_traffic(family):
@@ -97,7 +97,7 @@ def ncu_traffic(family):
     if not launches:
         return None, "no ncu capture"
     top = max(launches, key=lambda d: d["dram_bytes"])
-    return top["dram_bytes"], f"ncu --set full, {kern} grid {top['grid']} (profiles/{PROFILE_TAG}_ncu_summary.md)"
+    return top["dram_bytes"], f"ncu --set full, {kern} grid {top['grid']} (profiles/{PROFILE_TAG}_ncu_summary_table.md)"
 
 
 def load_peaks():
