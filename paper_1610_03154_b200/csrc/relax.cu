@@ -845,8 +845,11 @@ __global__ void k_pattern_asym(int32_t n, const int32_t* __restrict__ rp, const 
 // Long segments of long rows (coarse levels of vector problems: C5 level 1 has 342
 // segments of 684 rows of up to 50 entries): a warp per segment relaxes the segment's
 // rows in order, every forward sweep in turn.  A row's lanes take its entries 32 at a
-// time; the products are staged in shared memory and lane 0 subtracts them in CSR
-// order (the diagonal and unused lanes contribute +0.0, an exact identity).  Values of
+// time; the products are staged in shared memory and lane c subtracts column c's in CSR
+// order (the K chains side by side in one instruction stream; the diagonal's slot
+// contributes +0.0, an exact identity).  A lone warp issues a dependent instruction every
+// ~4 cycles, so a row step costs ~300 instructions x 4 cycles (0.6-0.9 us, measured on an
+// isolated chain by tools/gs_chain_rate.py) however far ahead its loads are issued.  Values of
 // the warp's own segment from this sweep come from a shared ring of its last kSwRing
 // rows (or its own global stores); other segments' values are polled in the per-sweep
 // buffers (pre-filled with kPending).  Items (sweep, row) run in that order within a
@@ -863,7 +866,7 @@ __global__ void __launch_bounds__(kSwWarps * 32)
                   unsigned int* __restrict__ ticket, unsigned max_ns) {
     __shared__ unsigned int blk;
     __shared__ double ring[kSwWarps][K][kSwRing];
-    __shared__ double stage[kSwWarps][K][32];
+    __shared__ double stage[kSwWarps][K][33];  // padded: lanes 0..K-1 walk their columns' products side by side
     if (threadIdx.x == 0) blk = atomicAdd(ticket, 1u);
     __syncthreads();
     const int lane = threadIdx.x & 31;
@@ -873,11 +876,11 @@ __global__ void __launch_bounds__(kSwWarps * 32)
     const int32_t q0 = segs[g], q1 = segs[g + 1];
     const size_t stride = static_cast<size_t>(n) * K;
     double (*rg)[kSwRing] = ring[w];
-    double (*sp)[32] = stage[w];
+    double (*sp)[33] = stage[w];
     // software pipeline over the items u = (sweep, row), so that no global-memory latency
     // sits between the end of one row and the start of the next: the row bounds three
-    // items ahead, the first 32 entries two items ahead, and -- issued while lane 0 adds
-    // the current row's products -- the next item's inverse diagonal and the values its
+    // items ahead, the first 32 entries two items ahead, and -- issued while the current
+    // row's products are summed -- the next item's inverse diagonal and the values its
     // first 32 entries read outside the ring (a value still pending then is polled when
     // the item runs; a published value is final, the per-sweep buffers are written once)
     const int32_t len = q1 - q0;
@@ -970,9 +973,9 @@ __global__ void __launch_bounds__(kSwWarps * 32)
         first_chunk(lo2, hi2, j2, a2);
         bounds(u, 3, lo3, hi3);
         double* xout = X + static_cast<size_t>(s + 1) * stride;
-        double acc[K];
-#pragma unroll
-        for (int c = 0; c < K; ++c) acc[c] = b ? b[static_cast<size_t>(c) * n + i] : 0.0;
+        // lane c (< K) carries column c's sum: the K ordered chains run side by side in
+        // one instruction stream instead of one after the other in lane 0
+        double acc = (b && lane < K) ? b[static_cast<size_t>(lane) * n + i] : 0.0;
         for (int32_t e0 = lo; e0 < hi || e0 == lo; e0 += 32) {
             const int32_t p = e0 + lane;
             const bool act = p < hi;
@@ -1027,28 +1030,21 @@ __global__ void __launch_bounds__(kSwWarps * 32)
                 d1 = inv_diag[i1];
                 fetch(classify(i1, s1, j1 < 0 ? i1 : j1, j1 >= 0), v1);
             }
-            if (lane == 0) {
-                // the chunk's entries in CSR order (lanes beyond them hold +0.0, an exact identity)
+            if (lane < K) {
+                // the chunk's entries in CSR order (the diagonal's slot holds +0.0, an exact identity)
                 const int cnt = min(32, hi - e0);
-#pragma unroll
-                for (int l = 0; l < 32; ++l) {
-                    if (l < cnt) {
-#pragma unroll
-                        for (int c = 0; c < K; ++c) acc[c] -= sp[c][l];
-                    }
-                }
+                const double* col = sp[lane];
+#pragma unroll 6
+                for (int l = 0; l < cnt; ++l) acc -= col[l];
             }
             __syncwarp();
         }
-        if (lane == 0) {
-#pragma unroll
-            for (int c = 0; c < K; ++c) {
-                const double xn = acc[c] * dcur;
-                rg[c][i % kSwRing] = xn;
-                cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> out(
-                    *reinterpret_cast<unsigned long long*>(&xout[static_cast<size_t>(c) * n + i]));
-                out.store(static_cast<unsigned long long>(__double_as_longlong(xn)), cuda::memory_order_relaxed);
-            }
+        if (lane < K) {
+            const double xn = acc * dcur;
+            rg[lane][i % kSwRing] = xn;
+            cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> out(
+                *reinterpret_cast<unsigned long long*>(&xout[static_cast<size_t>(lane) * n + i]));
+            out.store(static_cast<unsigned long long>(__double_as_longlong(xn)), cuda::memory_order_relaxed);
         }
         __syncwarp();
         if (++pos_cur == len) {
