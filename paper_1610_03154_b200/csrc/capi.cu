@@ -162,6 +162,7 @@ amgcu_status amgcu_ctx_destroy(amgcu_ctx ctx) {
     }
     ctx->c.scan_tmp.release();  // every stream-ordered buffer before its stream goes
     cudaStreamSynchronize(ctx->c.s);
+    ctx->c.cusolver.reset();  // bound to the context stream
     if (ctx->c.pin) cudaFreeHost(ctx->c.pin);
     cudaStreamSynchronize(ctx->c.side);
     cudaStreamSynchronize(ctx->c.side2);

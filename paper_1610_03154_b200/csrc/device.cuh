@@ -6,6 +6,7 @@
 
 #include <cstdint>
 #include <cstring>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -166,6 +167,9 @@ struct Ctx {
     // (spectral.hpp:32-36); prefixes serve every smaller level.
     DBuf<double> arnoldi_v0;
     size_t arnoldi_v0_n = 0;
+    // cuSOLVER handle of the dense LU above the Gauss-Jordan kernel's range (setup.cu), created
+    // on first use and kept: creating one costs tens of milliseconds
+    std::shared_ptr<void> cusolver;
     SeqSumWs ssws[2];  // [0] main stream, [1] any other stream
     PhaseTrace phases;
 };

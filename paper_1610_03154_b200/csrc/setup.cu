@@ -499,12 +499,12 @@ constexpr int32_t kCoarseGpuThreshold = 512;
 // column-major gives D^T; solving D^T X = I column-major yields X = D^-T,
 // i.e. D^-1 in row-major.  Returns false when the LU is singular.
 bool dense_inverse_gpu(Ctx& c, double* D, int32_t n, double* inv) {
-    cusolverDnHandle_t hs;
-    if (cusolverDnCreate(&hs) != CUSOLVER_STATUS_SUCCESS) throw CudaFailure("cusolverDnCreate failed");
-    struct Guard {
-        cusolverDnHandle_t h;
-        ~Guard() { cusolverDnDestroy(h); }
-    } guard{hs};
+    if (!c.cusolver) {
+        cusolverDnHandle_t h0;
+        if (cusolverDnCreate(&h0) != CUSOLVER_STATUS_SUCCESS) throw CudaFailure("cusolverDnCreate failed");
+        c.cusolver = std::shared_ptr<void>(h0, [](void* h) { cusolverDnDestroy(static_cast<cusolverDnHandle_t>(h)); });
+    }
+    cusolverDnHandle_t hs = static_cast<cusolverDnHandle_t>(c.cusolver.get());
     cusolverDnSetStream(hs, c.s);
     int lwork = 0;
     if (cusolverDnDgetrf_bufferSize(hs, n, n, D, n, &lwork) != CUSOLVER_STATUS_SUCCESS)
