@@ -785,13 +785,21 @@ __device__ __forceinline__ double coeff_at(const int32_t* rp, const int32_t* ci,
     return (lo < rp[i + 1] && ci[lo] == j) ? va[lo] : 0.0;
 }
 
+// bound = tol * max|A| with the maximum read from device memory (k_max_abs's bits): the
+// host never needs it, so is_symmetric takes one synchronisation, not two.  A sub-warp of
+// LPR lanes per row (1 for short rows; long coarse rows spread their entries -- each a
+// binary search in another row -- over 8 or 32 lanes).
+template <int LPR>
 __global__ void k_asym(int32_t nr, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
-                       const double* __restrict__ va, double bound, int32_t* __restrict__ bad) {
-    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+                       const double* __restrict__ va, double tol, const unsigned long long* __restrict__ max_bits,
+                       int32_t* __restrict__ bad) {
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int32_t i = static_cast<int32_t>(t / LPR);
     if (i >= nr) return;
-    for (int32_t p = rp[i]; p < rp[i + 1]; ++p) {
-        const double t = coeff_at(rp, ci, va, ci[p], i);
-        if (fabs(va[p] - t) > bound) {
+    const double bound = tol * __longlong_as_double(static_cast<long long>(*max_bits));
+    for (int32_t p = rp[i] + static_cast<int32_t>(t % LPR); p < rp[i + 1]; p += LPR) {
+        const double at = coeff_at(rp, ci, va, ci[p], i);
+        if (fabs(va[p] - at) > bound) {
             atomicExch(bad, 1);
             return;
         }
@@ -1271,11 +1279,23 @@ double max_abs(Ctx& c, const double* v, int64_t n) {
 
 bool is_symmetric(Ctx& c, const DCsr& A, double tol) {
     if (A.nr != A.nc) return false;
-    const double scale = max_abs(c, A.va.get(), A.nnz);
+    DBuf<unsigned long long> mx(1, c.s);
+    AMG_CK(cudaMemsetAsync(mx.get(), 0, sizeof(unsigned long long), c.s));
+    const unsigned g = std::min<unsigned>(blocks_for(A.nnz, 256), 4u * c.sms);
+    launch(c, k_max_abs, std::max(g, 1u), 256, 0, A.nnz, A.va.get(), mx.get());
     DBuf<int32_t> bad(1, c.s);
     AMG_CK(cudaMemsetAsync(bad.get(), 0, sizeof(int32_t), c.s));
-    launch(c, k_asym, blocks_for(A.nr, 256), 256, 0, A.nr, A.rp.get(), A.ci.get(), A.va.get(), tol * scale,
-           bad.get());
+    const double avg = A.nr ? static_cast<double>(A.nnz) / A.nr : 0.0;
+    const unsigned long long* mb = mx.get();
+    if (avg > 48.0)
+        launch(c, k_asym<32>, blocks_for(static_cast<int64_t>(A.nr) * 32, 256), 256, 0, A.nr, A.rp.get(), A.ci.get(),
+               A.va.get(), tol, mb, bad.get());
+    else if (avg > 12.0)
+        launch(c, k_asym<8>, blocks_for(static_cast<int64_t>(A.nr) * 8, 256), 256, 0, A.nr, A.rp.get(), A.ci.get(),
+               A.va.get(), tol, mb, bad.get());
+    else
+        launch(c, k_asym<1>, blocks_for(A.nr, 256), 256, 0, A.nr, A.rp.get(), A.ci.get(), A.va.get(), tol, mb,
+               bad.get());
     return read_scalar(c, bad.get()) == 0;
 }
 
