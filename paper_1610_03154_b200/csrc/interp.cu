@@ -679,13 +679,19 @@ unsigned cg_column_blocks(const Ctx& c) {
 using BandKernel = void (*)(int32_t, int32_t, int32_t, int32_t, int32_t, const int32_t*, const mband::Rec*, const int32_t*,
                             const int32_t*, const double*, int32_t, const double*, int32_t, const double*,
                             const unsigned char*, double*, double*, const mband::Run*, const int32_t*, const int32_t*);
-BandKernel band_kernel(int32_t k, bool masks) {
+template <int MODE>
+BandKernel band_kernel_k(int32_t k) {
     switch (k) {
-        case 1: return masks ? mband::k_masked_band<1, true> : mband::k_masked_band<1, false>;
-        case 2: return masks ? mband::k_masked_band<2, true> : mband::k_masked_band<2, false>;
-        case 3: return masks ? mband::k_masked_band<3, true> : mband::k_masked_band<3, false>;
-        default: return masks ? mband::k_masked_band<0, true> : mband::k_masked_band<0, false>;
+        case 1: return mband::k_masked_band<1, MODE>;
+        case 2: return mband::k_masked_band<2, MODE>;
+        case 3: return mband::k_masked_band<3, MODE>;
+        default: return mband::k_masked_band<0, MODE>;
     }
+}
+BandKernel band_kernel(int32_t k, int mode) {
+    return mode == mband::kNibbles ? band_kernel_k<mband::kNibbles>(k)
+           : mode == mband::kMasks ? band_kernel_k<mband::kMasks>(k)
+                                   : band_kernel_k<mband::kDirect>(k);
 }
 
 // The plan of the band-staged masked product for (A, N): runs per CTA, records per A entry.
@@ -713,14 +719,14 @@ mband::Plan masked_band_plan(Ctx& c, const DCsr& A, const DCsr& N, int32_t k) {
         c.band_last_fail = why;
         return mband::Plan{};
     };
-    for (;; R >>= 1) {
+    auto run_k_runs = [&](int direct) {
         pl.R = R;
         pl.nctas = static_cast<int32_t>(blocks_for(n, R));
         pl.runs.alloc(static_cast<size_t>(pl.nctas) * mband::kMaxRuns, c.s);
         pl.nruns.alloc(static_cast<size_t>(pl.nctas), c.s);
         AMG_CK(cudaMemsetAsync(info.get(), 0, sizeof(int32_t) * 8, c.s));
         launch_prof(c, kProfEminCg, 0.0, mband::k_runs, static_cast<unsigned>(pl.nctas), mband::kThreads, 0, n, R,
-                    A.rp.get(), A.ci.get(), N.rp.get(), pl.runs.get(), pl.nruns.get(), info.get());
+                    A.rp.get(), A.ci.get(), N.rp.get(), pl.runs.get(), pl.nruns.get(), info.get(), direct);
         copy_d2h(c, h, info.get(), 8);
         sync(c);
         pl.cap_a = h[1];
@@ -728,34 +734,48 @@ mband::Plan masked_band_plan(Ctx& c, const DCsr& A, const DCsr& N, int32_t k) {
         pl.cap_s = h[3];
         pl.smem = mband::smem_bytes(R, pl.cap_a, pl.cap_x, pl.cap_s, k);
         if (trace)
-            std::fprintf(stderr, "[band] n %d nnzA %lld nnzN %lld k %d R %d fail %d cap_a %d cap_x %d cap_s %d longest %d smem %zu\n",
-                         n, static_cast<long long>(A.nnz), static_cast<long long>(N.nnz), k, R, h[0], h[1], h[2], h[3], h[4],
-                         pl.smem);
+            std::fprintf(stderr, "[band] n %d nnzA %lld nnzN %lld k %d R %d direct %d fail %d cap_a %d cap_x %d cap_s %d longest %d smem %zu\n",
+                         n, static_cast<long long>(A.nnz), static_cast<long long>(N.nnz), k, R, direct, h[0], h[1], h[2],
+                         h[3], h[4], pl.smem);
+    };
+    bool direct = false;
+    for (;; R >>= 1) {
+        run_k_runs(0);
         if (h[4] > mband::kMaskSlots) return refuse(8);
         if (h[0] == 0 && pl.smem <= mband::kSmemBudget) break;
-        if (R <= 4) return refuse(h[0] ? h[0] : 64);
+        if (R <= 4) {
+            // scattered references: no staging, x gathered from global memory (L2)
+            if (h[4] > mband::kDirectSlots || N.nnz >= (int64_t(1) << 31)) return refuse(h[0] ? h[0] : 64);
+            const double per_row_direct = 16.0 * da + 8.0 * ln * 2.0 + 16.0;
+            R = 128;
+            while (R > 4 && R * per_row_direct > 44.0 * 1024.0) R >>= 1;
+            run_k_runs(1);
+            if (pl.smem > mband::kSmemBudget) return refuse(64);
+            direct = true;
+            break;
+        }
     }
-    pl.masks = h[4] > mband::kNibSlots;
+    pl.mode = direct ? mband::kDirect : h[4] > mband::kNibSlots ? mband::kMasks : mband::kNibbles;
     pl.recs.alloc(static_cast<size_t>(A.nnz) + 1, c.s);
     pl.matches.alloc(1, c.s);
     AMG_CK(cudaMemsetAsync(pl.matches.get(), 0, sizeof(unsigned long long), c.s));
     AMG_CK(cudaMemsetAsync(info.get(), 0, sizeof(int32_t) * 8, c.s));
-    if (pl.masks)
-        launch_prof(c, kProfEminCg, 0.0, mband::k_records<true>, static_cast<unsigned>(pl.nctas), mband::kThreads, 0, n, R,
-                    A.rp.get(), A.ci.get(), A.va.get(), N.rp.get(), N.ci.get(), static_cast<const mband::Run*>(pl.runs.get()),
+    auto records = [&](auto kern) {
+        launch_prof(c, kProfEminCg, 0.0, kern, static_cast<unsigned>(pl.nctas), mband::kThreads, 0, n, R, A.rp.get(),
+                    A.ci.get(), A.va.get(), N.rp.get(), N.ci.get(), static_cast<const mband::Run*>(pl.runs.get()),
                     static_cast<const int32_t*>(pl.nruns.get()), pl.recs.get(), info.get(), pl.matches.get());
-    else
-        launch_prof(c, kProfEminCg, 0.0, mband::k_records<false>, static_cast<unsigned>(pl.nctas), mband::kThreads, 0, n, R,
-                    A.rp.get(), A.ci.get(), A.va.get(), N.rp.get(), N.ci.get(), static_cast<const mband::Run*>(pl.runs.get()),
-                    static_cast<const int32_t*>(pl.nruns.get()), pl.recs.get(), info.get(), pl.matches.get());
+    };
+    if (pl.mode == mband::kDirect) records(mband::k_records<mband::kDirect>);
+    else if (pl.mode == mband::kMasks) records(mband::k_records<mband::kMasks>);
+    else records(mband::k_records<mband::kNibbles>);
     // a record that found no run (cannot happen: the runs cover every referenced row) is
     // reported with the hierarchy's other deferred checks: the flag is read with the CG's own
     // final synchronisation through pl.info
     pl.info = std::move(info);
-    static bool attr_set[8] = {false, false, false, false, false, false, false, false};
-    const int slot = (k >= 1 && k <= 3 ? k : 0) * 2 + (pl.masks ? 1 : 0);
+    static bool attr_set[12] = {};
+    const int slot = (k >= 1 && k <= 3 ? k : 0) * 3 + pl.mode;
     if (!attr_set[slot]) {
-        AMG_CK(cudaFuncSetAttribute(band_kernel(k, pl.masks), cudaFuncAttributeMaxDynamicSharedMemorySize,
+        AMG_CK(cudaFuncSetAttribute(band_kernel(k, pl.mode), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(mband::kSmemBudget)));
         attr_set[slot] = true;
     }
@@ -1269,7 +1289,7 @@ void energy_minimize(Ctx& c, const DCsr& A, const DCsr& T, const double* B, cons
     auto masked = [&](const DCsr& M, const mband::Plan& pl, int family, double bytes, const double* x, double* y,
                       double* yp, const int32_t* stop) {
         if (pl.ok)
-            launch_prof(c, family, bytes, band_kernel(k, pl.masks), static_cast<unsigned>(pl.nctas), mband::kThreads, pl.smem,
+            launch_prof(c, family, bytes, band_kernel(k, pl.mode), static_cast<unsigned>(pl.nctas), mband::kThreads, pl.smem,
                         n, pl.R, pl.cap_a, pl.cap_x, pl.cap_s, M.rp.get(), static_cast<const mband::Rec*>(pl.recs.get()),
                         N.rp.get(), N.ci.get(), x, k, Bc, nc, static_cast<const double*>(gp.get()),
                         static_cast<const unsigned char*>(is_root.get()), y, yp,

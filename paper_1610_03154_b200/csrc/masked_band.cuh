@@ -23,9 +23,12 @@
 //     are written coalesced.  The projection takes its row sums in slot order by one
 //     thread per row from the shared values (interpolation.hpp:163-176).
 //
-// Levels whose pattern rows exceed 24 slots, or whose referenced rows do not fit the run
-// table and the shared-memory budget even at 4 rows per CTA, keep the register-merge
-// kernel (k_masked_rows).
+// Levels whose referenced rows do not fit the run table and the shared-memory budget even
+// at 4 rows per CTA (scattered coarse operators such as C4's A^T A on levels 2-3) use the
+// DIRECT mode when their pattern rows have at most 16 slots: no staging of X, the record
+// word holds the global offset of X_t's slice (32 bits) and two 16-bit masks, and the
+// slot threads gather x from global memory (such a level's X is a few MB: L2-resident).
+// Anything else keeps the register-merge kernel (k_masked_rows).
 #pragma once
 
 namespace mband {
@@ -33,6 +36,8 @@ namespace mband {
 constexpr int kNibSlots = 12;      // 4-bit indices: slots of N_i a record word holds
 constexpr int kNibNt = 15;         //                 entries of N_t an index can address
 constexpr int kMaskSlots = 24;     // mask pairs: longest pattern row
+constexpr int kDirectSlots = 16;   // direct mode: longest pattern row
+enum Mode : int { kNibbles = 0, kMasks = 1, kDirect = 2 };
 constexpr int kMaxRuns = 64;       // runs of X a CTA stages
 constexpr int kGran = 4;           // rows per bit of the referenced-rows bitmap
 constexpr int kBitWords = 2048;    // 32-bit words of that bitmap (window of 262,144 rows)
@@ -58,7 +63,7 @@ struct Plan {
     bool ok = false;
     int32_t R = 0, nctas = 0;
     int32_t cap_a = 0, cap_x = 0, cap_s = 0;  // records, staged doubles, slots per CTA (maxima)
-    bool masks = false;                        // record words hold mask pairs (pattern rows above 12 slots)
+    int mode = kNibbles;                       // record format (Mode)
     size_t smem = 0;
     DBuf<Rec> recs;
     DBuf<Run> runs;
@@ -72,7 +77,7 @@ struct Plan {
 __global__ void __launch_bounds__(kThreads)
     k_runs(int32_t n, int32_t R, const int32_t* __restrict__ arp, const int32_t* __restrict__ aci,
            const int32_t* __restrict__ nrp, Run* __restrict__ runs, int32_t* __restrict__ nruns,
-           int32_t* __restrict__ info) {
+           int32_t* __restrict__ info, int direct) {
     __shared__ unsigned int bits[kBitWords];
     __shared__ int32_t s_min, s_max;
     const int32_t r0 = blockIdx.x * R, r1 = min(n, r0 + R);
@@ -105,9 +110,10 @@ __global__ void __launch_bounds__(kThreads)
         for (int off = 16; off > 0; off >>= 1) longest = max(longest, __shfl_xor_sync(0xffffffffu, longest, off));
         if ((threadIdx.x & 31) == 0 && longest > 0) atomicMax(&info[4], longest);
     }
-    if (s_max < 0) {
+    if (s_max < 0 || direct) {  // direct mode stages no X: only the capacities
         if (threadIdx.x == 0) {
             nruns[blockIdx.x] = 0;
+            atomicMax(&info[1], a1 - a0);
             atomicMax(&info[3], nslots);
         }
         return;
@@ -190,7 +196,7 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 // ---- plan, step 2: the record of every A entry --------------------------------------------
-template <bool MASKS>
+template <int MODE>
 __global__ void __launch_bounds__(kThreads)
     k_records(int32_t n, int32_t R, const int32_t* __restrict__ arp, const int32_t* __restrict__ aci,
               const double* __restrict__ ava, const int32_t* __restrict__ nrp, const int32_t* __restrict__ nci,
@@ -217,10 +223,11 @@ __global__ void __launch_bounds__(kThreads)
         const int32_t t = aci[e];
         Rec rec;
         rec.a = ava[e];
-        unsigned long long w = MASKS ? 0ull : ~0ull;  // no slot of N_i is in N_t
+        unsigned long long w = MODE == kNibbles ? ~0ull : 0ull;  // no slot of N_i is in N_t
         const int32_t ilo = nrp[i], L = nrp[i + 1] - ilo;
         const int32_t q0 = nrp[t], Lt = nrp[t + 1] - q0;
-        if (L > (MASKS ? kMaskSlots : kNibSlots) || Lt > (MASKS ? kMaskSlots : kNibNt)) {
+        if (L > (MODE == kNibbles ? kNibSlots : MODE == kMasks ? kMaskSlots : kDirectSlots) ||
+            Lt > (MODE == kNibbles ? kNibNt : MODE == kMasks ? kMaskSlots : kDirectSlots)) {
             atomicOr(&info[0], 8);
         } else if (L > 0 && Lt > 0) {
             // the run holding row t: the last one starting at or before it
@@ -230,10 +237,11 @@ __global__ void __launch_bounds__(kThreads)
                 if (s_runs[mid].ta <= t) jl = mid;
                 else jh = mid;
             }
-            if (nr == 0 || !(s_runs[jl].ta <= t && t < s_runs[jl].tb)) {
+            if (MODE != kDirect && (nr == 0 || !(s_runs[jl].ta <= t && t < s_runs[jl].tb))) {
                 atomicOr(&info[0], 16);
             } else {
-                const unsigned int off = static_cast<unsigned int>(s_runs[jl].soff + (q0 - s_runs[jl].xs));
+                const unsigned int off = MODE == kDirect ? static_cast<unsigned int>(q0)
+                                                         : static_cast<unsigned int>(s_runs[jl].soff + (q0 - s_runs[jl].xs));
                 unsigned long long mi = 0ull, mt = 0ull;
                 int32_t q = 0;
                 for (int32_t s = 0; s < L; ++s) {
@@ -241,7 +249,7 @@ __global__ void __launch_bounds__(kThreads)
                     while (q < Lt && nci[q0 + q] < col) ++q;
                     if (q < Lt && nci[q0 + q] == col) {
                         ++found;
-                        if (MASKS) {
+                        if (MODE != kNibbles) {
                             mi |= 1ull << s;
                             mt |= 1ull << q;
                         } else {
@@ -250,8 +258,9 @@ __global__ void __launch_bounds__(kThreads)
                         }
                     }
                 }
-                if (MASKS) w = (mi << 16) | (mt << 40);
-                w = (w & ~0xffffull) | off;
+                if (MODE == kMasks) w = (mi << 16) | (mt << 40);
+                if (MODE == kDirect) w = (mi << 32) | (mt << 48) | off;
+                else w = (w & ~0xffffull) | off;
             }
         }
         rec.w = w;
@@ -319,8 +328,9 @@ __host__ __device__ inline size_t smem_bytes(int32_t R, int32_t cap_a, int32_t c
 }
 
 // KT: the candidate count when it is 1..3 (projection sums in registers), 0 = any k <= 8
-// MASKS: the record words hold mask pairs (pattern rows of 13..24 slots) instead of 4-bit indices
-template <int KT, bool MASKS>
+// MODE: the record format -- 4-bit indices, mask pairs (pattern rows of 13..24 slots), or
+// direct (global offset + 16-bit mask pairs, x gathered from global memory)
+template <int KT, int MODE>
 __global__ void __launch_bounds__(kThreads)
     k_masked_band(int32_t n, int32_t R, int32_t cap_a, int32_t cap_x, int32_t cap_s,
                   const int32_t* __restrict__ arp, const Rec* __restrict__ recs, const int32_t* __restrict__ nrp,
@@ -385,7 +395,7 @@ __global__ void __launch_bounds__(kThreads)
         const Rec* e = s_rec + (s_arp[r] - a0);
         const Rec* const ee = s_rec + (s_arp[r + 1] - a0);
         double acc = 0.0;
-        if (MASKS) {
+        if (MODE == kMasks) {
             const unsigned int below = (1u << slot) - 1u;
             for (; e < ee; ++e) {
                 const double a = e->a;
@@ -394,6 +404,17 @@ __global__ void __launch_bounds__(kThreads)
                 if ((mi >> slot) & 1u) {
                     const unsigned int u = nth_set_bit24(static_cast<unsigned int>(w >> 40), __popc(mi & below));
                     acc += a * s_x[(static_cast<unsigned int>(w) & 0xffffu) + u];
+                }
+            }
+        } else if (MODE == kDirect) {
+            const unsigned int below = (1u << slot) - 1u;
+            for (; e < ee; ++e) {
+                const double a = e->a;
+                const unsigned long long w = e->w;
+                const unsigned int mi = static_cast<unsigned int>(w >> 32) & 0xffffu;
+                if ((mi >> slot) & 1u) {
+                    const unsigned int u = nth_set_bit24(static_cast<unsigned int>(w >> 48), __popc(mi & below));
+                    acc += a * __ldg(x + (static_cast<unsigned int>(w) + u));
                 }
             }
         } else {
