@@ -279,13 +279,12 @@ def run_ours(args, ws, rank, local):
     from paper_1610_03154_b200._abi import CsrC, SolveReportC, f64p
     lib = api.lib
 
-    dist = None
-    if ws > 1:
-        import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+    # replicas only: the barrier and the max-over-ranks come from the
+    # package's replicas helpers, the same code the world-size-2 gloo test exercises
+    import paper_1610_03154_b200.replicas as replicas
     device = torch.device("cuda", local)
     torch.cuda.set_device(device)
+    dist = replicas.init("nccl")
     config = args.config
     size = args.size or DEFAULT_SIZE[config]
     A, B, Bh, b = api.generate_config(config, size)
@@ -391,8 +390,7 @@ def run_ours(args, ws, rank, local):
 
     # timed region: device-resident inputs
     sampler = ClockSampler(local)
-    if dist:
-        dist.barrier()
+    replicas.barrier(dist)
     torch.cuda.synchronize()
     sampler.start()
     launches0 = ctx.launch_count()
@@ -403,8 +401,7 @@ def run_ours(args, ws, rank, local):
         step_ms.append(ms)
     launches = (ctx.launch_count() - launches0) / max(1, args.steps)
     torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
+    replicas.barrier(dist)
     clocks = sampler.stop()
     fam_stats = {}
     for f in range(fam_count):
@@ -414,11 +411,7 @@ def run_ours(args, ws, rank, local):
             fam_stats[lib.amgcu_profile_family_name(f).decode()] = {
                 "launches": l_.value, "ms": ms_.value, "algorithmic_bytes": by_.value}
     lib.amgcu_ctx_set_profiling(ctx.handle, 0)
-    mean_ms = sum(step_ms) / len(step_ms)
-    if dist:
-        t = torch.tensor([mean_ms], dtype=torch.float64, device=device)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        mean_ms = float(t.item())
+    mean_ms = replicas.max_over_ranks(sum(step_ms) / len(step_ms), dist, device)
 
     # e2e: the public C ABI with pinned host buffers
     e2e_ms = []
@@ -426,11 +419,7 @@ def run_ours(args, ws, rank, local):
         flush_l2()
         ms, _, _ = step_e2e()
         e2e_ms.append(ms)
-    e2e_mean = sum(e2e_ms) / len(e2e_ms)
-    if dist:
-        t = torch.tensor([e2e_mean], dtype=torch.float64, device=device)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_mean = float(t.item())
+    e2e_mean = replicas.max_over_ranks(sum(e2e_ms) / len(e2e_ms), dist, device)
     h2d = 4 * (n + 1) + 12 * nnz + 8 * n * k * (2 if Bh is not None else 1) + 8 * n + 8 * n
     d2h = 8 * n
 

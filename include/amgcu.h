@@ -136,10 +136,11 @@ amgcu_status amgcu_ctx_set_sequential_reductions(amgcu_ctx ctx, int on);
 amgcu_status amgcu_ctx_set_candidate_overlap(amgcu_ctx ctx, int on);
 /* Energy-minimisation masked product (interpolation.hpp:186-210): levels of at least
  * min_rows rows (default 0: all) use the band-staged kernel -- per-CTA pieces of X and
- * the per-entry match records brought into shared memory by TMA bulk copies; levels
- * its plan refuses (pattern rows above 24 slots, referenced rows that do not fit the
- * shared-memory budget) use the register-merge kernel.  min_rows < 0: never.  The
- * result is bitwise the same either way. */
+ * the per-entry match records brought into shared memory by TMA bulk copies (levels
+ * whose referenced rows are too scattered to stage gather X from L2 instead); levels
+ * its plan refuses (pattern rows above 24 slots, above 16 when scattered) use the
+ * register-merge kernel.  min_rows < 0: never.  The result is bitwise the same either
+ * way. */
 amgcu_status amgcu_ctx_set_masked_band(amgcu_ctx ctx, int32_t min_rows);
 /* Levels whose plan was accepted / refused so far, and the last refusal's reason bits
  * (1 referenced rows beyond the window, 2 too many runs, 4 stage beyond 16-bit offsets,

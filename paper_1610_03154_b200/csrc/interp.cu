@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cstring>
 
+#include "bitrank.h"
 #include "interp.cuh"
 #include "small_dense.h"
 #include "stl_sort.cuh"

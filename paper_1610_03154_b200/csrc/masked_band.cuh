@@ -31,6 +31,7 @@
 // Anything else keeps the register-merge kernel (k_masked_rows).
 #pragma once
 
+// (bitrank.h is included by interp.cu at file scope: this header sits inside its namespaces)
 namespace mband {
 
 constexpr int kNibSlots = 12;      // 4-bit indices: slots of N_i a record word holds
@@ -270,37 +271,7 @@ __global__ void __launch_bounds__(kThreads)
     if ((threadIdx.x & 31) == 0 && found) atomicAdd(matches, found);
 }
 
-// position of the j-th (0-based) set bit of the 24-bit mask m (j below its popcount)
-__device__ __forceinline__ unsigned int nth_set_bit24(unsigned int m, int j) {
-    unsigned int pos = 0;
-    int c = __popc(m & 0xfffu);
-    if (j >= c) {
-        j -= c;
-        m >>= 12;
-        pos = 12;
-    }
-    c = __popc(m & 0x3fu);
-    if (j >= c) {
-        j -= c;
-        m >>= 6;
-        pos += 6;
-    }
-    c = __popc(m & 0x7u);
-    if (j >= c) {
-        j -= c;
-        m >>= 3;
-        pos += 3;
-    }
-    c = static_cast<int>(m & 1u);
-    if (j >= c) {
-        j -= c;
-        m >>= 1;
-        pos += 1;
-    }
-    c = static_cast<int>(m & 1u);
-    if (j >= c) pos += 1;
-    return pos;
-}
+using ::amgcu::bitrank::nth_set_bit24;  // bitrank.h: position of the j-th set bit of a 24-bit mask
 
 // ---- the iteration kernel -----------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
