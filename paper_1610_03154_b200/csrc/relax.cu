@@ -858,15 +858,18 @@ __global__ void k_pattern_asym(int32_t n, const int32_t* __restrict__ rp, const 
 constexpr int kSwWarps = 4;
 constexpr int kSwRing = 64;
 
-template <int K>
+// E: entries per lane and chunk (a chunk is 32 E entries; rows of up to 64 entries -- the
+// coarse levels of vector problems -- take E = 2 so that the whole row is one pipelined chunk)
+template <int K, int E>
 __global__ void __launch_bounds__(kSwWarps * 32)
     k_gs_seg_warp(int32_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
                   const double* __restrict__ va, const double* __restrict__ inv_diag, const double* __restrict__ b,
                   int nsweeps, const int32_t* __restrict__ segs, int32_t nseg, double* __restrict__ X,
                   unsigned int* __restrict__ ticket, unsigned max_ns) {
+    constexpr int W = 32 * E;
     __shared__ unsigned int blk;
     __shared__ double ring[kSwWarps][K][kSwRing];
-    __shared__ double stage[kSwWarps][K][33];  // padded: lanes 0..K-1 walk their columns' products side by side
+    __shared__ double stage[kSwWarps][K][W + 1];  // padded: lanes 0..K-1 walk their columns' products side by side
     if (threadIdx.x == 0) blk = atomicAdd(ticket, 1u);
     __syncthreads();
     const int lane = threadIdx.x & 31;
@@ -876,12 +879,12 @@ __global__ void __launch_bounds__(kSwWarps * 32)
     const int32_t q0 = segs[g], q1 = segs[g + 1];
     const size_t stride = static_cast<size_t>(n) * K;
     double (*rg)[kSwRing] = ring[w];
-    double (*sp)[33] = stage[w];
+    double (*sp)[W + 1] = stage[w];
     // software pipeline over the items u = (sweep, row), so that no global-memory latency
     // sits between the end of one row and the start of the next: the row bounds three
-    // items ahead, the first 32 entries two items ahead, and -- issued while the current
-    // row's products are summed -- the next item's inverse diagonal and the values its
-    // first 32 entries read outside the ring (a value still pending then is polled when
+    // items ahead, the first chunk's entries two items ahead, and -- issued while the
+    // current row's products are summed -- the next item's inverse diagonal and the values
+    // its first chunk reads outside the ring (a value still pending then is polled when
     // the item runs; a published value is final, the per-sweep buffers are written once)
     const int32_t len = q1 - q0;
     const int64_t total = static_cast<int64_t>(len) * nsweeps;
@@ -927,12 +930,16 @@ __global__ void __launch_bounds__(kSwWarps * 32)
                                  : load_relaxed_bits(r.p + static_cast<size_t>(c) * n);
         }
     };
-    auto first_chunk = [&](int32_t lo_, int32_t hi_, int32_t& j_, double& a_) {
-        j_ = -1;
-        a_ = 0.0;
-        if (lo_ + lane < hi_) {
-            j_ = __ldg(ci + lo_ + lane);
-            a_ = __ldg(va + lo_ + lane);
+    auto first_chunk = [&](int32_t lo_, int32_t hi_, int32_t (&j_)[E], double (&a_)[E]) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            j_[e] = -1;
+            a_[e] = 0.0;
+            const int32_t p = lo_ + e * 32 + lane;
+            if (p < hi_) {
+                j_[e] = __ldg(ci + p);
+                a_[e] = __ldg(va + p);
+            }
         }
     };
     auto bounds = [&](int64_t u, int k, int32_t& lo_, int32_t& hi_) {  // item u + k
@@ -947,27 +954,37 @@ __global__ void __launch_bounds__(kSwWarps * 32)
     bounds(0, 0, lo1, hi1);
     bounds(0, 1, lo2, hi2);
     bounds(0, 2, lo3, hi3);
-    int32_t j1, j2;
-    double a1, a2;
+    int32_t j1[E], j2[E];
+    double a1[E], a2[E];
     first_chunk(lo1, hi1, j1, a1);
     first_chunk(lo2, hi2, j2, a2);
-    unsigned long long v1[K];  // item u's prefetched values
+    unsigned long long v1[E][K];  // item u's prefetched values
     double d1 = inv_diag[q0];
-    fetch(classify(q0, 0, j1 < 0 ? q0 : j1, j1 >= 0), v1);
+#pragma unroll
+    for (int e = 0; e < E; ++e) fetch(classify(q0, 0, j1[e] < 0 ? q0 : j1[e], j1[e] >= 0), v1[e]);
     for (int64_t u = 0; u < total; ++u) {
         const int s = s_cur;
         const int32_t i = q0 + pos_cur;
         const int32_t lo = lo1, hi = hi1;
-        const int32_t jf = j1;
-        const double af = a1, dcur = d1;
-        unsigned long long vf[K];
+        int32_t jf[E];
+        double af[E];
+        unsigned long long vf[E][K];
+        const double dcur = d1;
 #pragma unroll
-        for (int c = 0; c < K; ++c) vf[c] = v1[c];
+        for (int e = 0; e < E; ++e) {
+            jf[e] = j1[e];
+            af[e] = a1[e];
+#pragma unroll
+            for (int c = 0; c < K; ++c) vf[e][c] = v1[e][c];
+        }
         // advance the pipeline: item u + 2's first chunk, item u + 3's bounds
         lo1 = lo2;
         hi1 = hi2;
-        j1 = j2;
-        a1 = a2;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            j1[e] = j2[e];
+            a1[e] = a2[e];
+        }
         lo2 = lo3;
         hi2 = hi3;
         first_chunk(lo2, hi2, j2, a2);
@@ -976,63 +993,76 @@ __global__ void __launch_bounds__(kSwWarps * 32)
         // lane c (< K) carries column c's sum: the K ordered chains run side by side in
         // one instruction stream instead of one after the other in lane 0
         double acc = (b && lane < K) ? b[static_cast<size_t>(lane) * n + i] : 0.0;
-        for (int32_t e0 = lo; e0 < hi || e0 == lo; e0 += 32) {
-            const int32_t p = e0 + lane;
-            const bool act = p < hi;
-            int32_t j = i;
-            double a = 0.0;
-            unsigned long long v[K];
-            Src sr;
-            if (e0 == lo) {
-                if (act) {
-                    j = jf;
-                    a = af;
-                }
-                sr = classify(i, s, j, act);
+        for (int32_t e0 = lo; e0 < hi || e0 == lo; e0 += W) {
+            int32_t j[E];
+            double a[E];
+            unsigned long long v[E][K];
+            Src sr[E];
 #pragma unroll
-                for (int c = 0; c < K; ++c) v[c] = vf[c];
-            } else {
-                if (act) {
-                    j = __ldg(ci + p);
-                    a = __ldg(va + p);
+            for (int e = 0; e < E; ++e) {
+                const int32_t p = e0 + e * 32 + lane;
+                const bool act = p < hi;
+                j[e] = i;
+                a[e] = 0.0;
+                if (e0 == lo) {
+                    if (act) {
+                        j[e] = jf[e];
+                        a[e] = af[e];
+                    }
+                    sr[e] = classify(i, s, j[e], act);
+#pragma unroll
+                    for (int c = 0; c < K; ++c) v[e][c] = vf[e][c];
+                } else {
+                    if (act) {
+                        j[e] = __ldg(ci + p);
+                        a[e] = __ldg(va + p);
+                    }
+                    sr[e] = classify(i, s, j[e], act);
+                    fetch(sr[e], v[e]);
                 }
-                sr = classify(i, s, j, act);
-                fetch(sr, v);
             }
             unsigned ns = 8;
             while (true) {
                 bool pend = false;
 #pragma unroll
-                for (int c = 0; c < K; ++c) pend |= sr.use && !sr.ring && v[c] == kPending;
+                for (int e = 0; e < E; ++e)
+#pragma unroll
+                    for (int c = 0; c < K; ++c) pend |= sr[e].use && !sr[e].ring && v[e][c] == kPending;
                 if (!__any_sync(0xffffffffu, pend)) break;
                 if (pend) {
                     __nanosleep(ns);
 #pragma unroll
-                    for (int c = 0; c < K; ++c)
-                        if (v[c] == kPending) v[c] = load_relaxed_bits(sr.p + static_cast<size_t>(c) * n);
+                    for (int e = 0; e < E; ++e)
+#pragma unroll
+                        for (int c = 0; c < K; ++c)
+                            if (sr[e].use && !sr[e].ring && v[e][c] == kPending)
+                                v[e][c] = load_relaxed_bits(sr[e].p + static_cast<size_t>(c) * n);
                 }
                 ns = ns < max_ns ? 2 * ns : max_ns;
             }
 #pragma unroll
-            for (int c = 0; c < K; ++c) {
-                const double xv = sr.ring ? rg[c][j % kSwRing] : __longlong_as_double(static_cast<long long>(v[c]));
-                sp[c][lane] = sr.use ? a * xv : 0.0;
-            }
+            for (int e = 0; e < E; ++e)
+#pragma unroll
+                for (int c = 0; c < K; ++c) {
+                    const double xv = sr[e].ring ? rg[c][j[e] % kSwRing] : __longlong_as_double(static_cast<long long>(v[e][c]));
+                    sp[c][e * 32 + lane] = sr[e].use ? a[e] * xv : 0.0;
+                }
             __syncwarp();
-            const bool last = e0 + 32 >= hi;
+            const bool last = e0 + W >= hi;
             if (last && u + 1 < total) {
                 // the next item's inverse diagonal and out-of-ring values, in flight
-                // while lane 0 adds this row's products
+                // while this row's products are summed
                 int s1;
                 int32_t pos1;
                 ahead(1, s1, pos1);
                 const int32_t i1 = q0 + pos1;
                 d1 = inv_diag[i1];
-                fetch(classify(i1, s1, j1 < 0 ? i1 : j1, j1 >= 0), v1);
+#pragma unroll
+                for (int e = 0; e < E; ++e) fetch(classify(i1, s1, j1[e] < 0 ? i1 : j1[e], j1[e] >= 0), v1[e]);
             }
             if (lane < K) {
                 // the chunk's entries in CSR order (the diagonal's slot holds +0.0, an exact identity)
-                const int cnt = min(32, hi - e0);
+                const int cnt = min(W, hi - e0);
                 const double* col = sp[lane];
 #pragma unroll 6
                 for (int l = 0; l < cnt; ++l) acc -= col[l];
@@ -1206,6 +1236,13 @@ __global__ void k_jacobi(int32_t n, const int32_t* __restrict__ rp, const int32_
 // Segments use a block-size window, so the stride-m chains of interleaved vector
 // unknowns continue a segment.  Host synchronisations happen here; the run
 // (gs_lanes_run) has none, so it may be queued on another stream than the plan's.
+// rows beyond 32 entries run the warp-per-segment kernel with two entries per lane, so that
+// rows of up to 64 are one pipelined chunk (AMGCU_GS_SW_WIDE=0: always one entry per lane)
+static bool seg_warp_wide(int32_t longest_row) {
+    const char* e = std::getenv("AMGCU_GS_SW_WIDE");
+    return longest_row > 32 && !(e && e[0] == '0');
+}
+
 LanePlan lane_plan(Ctx& c, const DCsr& A, int nsw, int k) {
     LanePlan pl;
     const int32_t n = A.nr;
@@ -1243,8 +1280,17 @@ LanePlan lane_plan(Ctx& c, const DCsr& A, int nsw, int k) {
     // warp per segment: any segment length (short segments only mean more warps), as
     // long as every warp can be resident at once
     if (!sw_off && k <= 4) {
-        int per_sm = 0;
-        AMG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gs_seg_warp<4>, kSwWarps * 32, 0));
+        int per_sm = 0;  // of the variant that will run (gs_segwarp_kernel_run)
+        const bool wide = seg_warp_wide(pl.longest_row);
+        auto occ = [&](auto kern) {
+            AMG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSwWarps * 32, 0));
+        };
+        switch (k) {
+            case 1: wide ? occ(k_gs_seg_warp<1, 2>) : occ(k_gs_seg_warp<1, 1>); break;
+            case 2: wide ? occ(k_gs_seg_warp<2, 2>) : occ(k_gs_seg_warp<2, 1>); break;
+            case 3: wide ? occ(k_gs_seg_warp<3, 2>) : occ(k_gs_seg_warp<3, 1>); break;
+            default: wide ? occ(k_gs_seg_warp<4, 2>) : occ(k_gs_seg_warp<4, 1>); break;
+        }
         if ((pl.nf + kSwWarps - 1) / kSwWarps <= static_cast<int64_t>(per_sm) * c.sms) {
             pl.kind = LanePlan::kSegWarp;
             pl.ok = true;
@@ -1361,11 +1407,13 @@ void gs_segwarp_kernel_run(Ctx& c, const DCsr& A, const LanePlan& pl, const doub
                     inv_diag, b, nsw, static_cast<const int32_t*>(pl.segf.get()), pl.nf, X.get(), ticket.get(),
                     gs_env_u("AMGCU_GS_SW_NS", 64u));
     };
+    // rows beyond 32 entries: two entries per lane, so that rows of up to 64 are one pipelined chunk
+    const bool wide = seg_warp_wide(pl.longest_row);
     switch (k) {
-        case 1: runs(k_gs_seg_warp<1>); break;
-        case 2: runs(k_gs_seg_warp<2>); break;
-        case 3: runs(k_gs_seg_warp<3>); break;
-        default: runs(k_gs_seg_warp<4>); break;
+        case 1: wide ? runs(k_gs_seg_warp<1, 2>) : runs(k_gs_seg_warp<1, 1>); break;
+        case 2: wide ? runs(k_gs_seg_warp<2, 2>) : runs(k_gs_seg_warp<2, 1>); break;
+        case 3: wide ? runs(k_gs_seg_warp<3, 2>) : runs(k_gs_seg_warp<3, 1>); break;
+        default: wide ? runs(k_gs_seg_warp<4, 2>) : runs(k_gs_seg_warp<4, 1>); break;
     }
     copy_d2d(c, x, X.get() + stride * nsw, static_cast<int64_t>(stride));
 }
