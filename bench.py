@@ -78,7 +78,7 @@ def dist_env():
 
 # kernel family -> kernel symbol captured by tools/ncu_capture.sh
 PROFILE_TAG = "r04"  # profiles/<tag>_traffic.json, written by tools/ncu_summary.py
-FAMILY_KERNEL = {"gauss_seidel_wavefront": "k_gs_seg_warp<3>", "aggregate_lfmis": "k_lfmis_lists",
+FAMILY_KERNEL = {"gauss_seidel_wavefront": "k_gs_seg_warp<3, 1>", "aggregate_lfmis": "k_lfmis_lists",
                  "spgemm": "k_spgemm_bitmap", "arnoldi_blas1": "k_seqsum<TAxpyDot, 16>", "blas1": "k_seqsum<TDot, 16>",
                  "emin_masked_product": "k_masked_band<3, 0>", "vcycle_relax0_residual": "k_relax0_residual",
                  "vcycle_post_relax": "k_jacobi_sweep", "vcycle_prolong": "k_prolong", "krylov_spmv": "k_sell_spmv",
