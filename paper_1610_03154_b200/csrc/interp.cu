@@ -724,7 +724,7 @@ mband::Plan masked_band_plan(Ctx& c, const DCsr& A, const DCsr& N, int32_t k) {
         pl.R = R;
         pl.nctas = static_cast<int32_t>(blocks_for(n, R));
         pl.runs.alloc(static_cast<size_t>(pl.nctas) * mband::kMaxRuns, c.s);
-        pl.nruns.alloc(static_cast<size_t>(pl.nctas), c.s);
+        pl.nruns.alloc(static_cast<size_t>(pl.nctas) * 2, c.s);
         AMG_CK(cudaMemsetAsync(info.get(), 0, sizeof(int32_t) * 8, c.s));
         launch_prof(c, kProfEminCg, 0.0, mband::k_runs, static_cast<unsigned>(pl.nctas), mband::kThreads, 0, n, R,
                     A.rp.get(), A.ci.get(), N.rp.get(), pl.runs.get(), pl.nruns.get(), info.get(), direct);

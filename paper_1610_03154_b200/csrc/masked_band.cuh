@@ -68,7 +68,7 @@ struct Plan {
     size_t smem = 0;
     DBuf<Rec> recs;
     DBuf<Run> runs;
-    DBuf<int32_t> nruns;
+    DBuf<int32_t> nruns;  // per CTA: {runs, bytes of X they stage}
     DBuf<int32_t> info;  // k_records' failure bits (checked after the iterations)
     DBuf<unsigned long long> matches;  // sum_i sum_{t in A row i} |N_i cap N_t| (interpolation.hpp:200-206)
 };
@@ -113,7 +113,8 @@ __global__ void __launch_bounds__(kThreads)
     }
     if (s_max < 0 || direct) {  // direct mode stages no X: only the capacities
         if (threadIdx.x == 0) {
-            nruns[blockIdx.x] = 0;
+            nruns[2 * blockIdx.x] = 0;
+            nruns[2 * blockIdx.x + 1] = 0;
             atomicMax(&info[1], a1 - a0);
             atomicMax(&info[3], nslots);
         }
@@ -124,7 +125,8 @@ __global__ void __launch_bounds__(kThreads)
     if (nb > kBitWords * 32) {
         if (threadIdx.x == 0) {
             atomicOr(&info[0], 1);
-            nruns[blockIdx.x] = 0;
+            nruns[2 * blockIdx.x] = 0;
+            nruns[2 * blockIdx.x + 1] = 0;
         }
         return;
     }
@@ -190,7 +192,8 @@ __global__ void __launch_bounds__(kThreads)
         count = 0;
     }
     if (soff > 65535 - kMaskSlots) atomicOr(&info[0], 4);
-    nruns[blockIdx.x] = count;
+    nruns[2 * blockIdx.x] = count;
+    nruns[2 * blockIdx.x + 1] = count ? soff * 8 : 0;
     atomicMax(&info[1], a1 - a0);
     atomicMax(&info[2], soff);
     atomicMax(&info[3], nslots);
@@ -206,7 +209,7 @@ __global__ void __launch_bounds__(kThreads)
     __shared__ Run s_runs[kMaxRuns];
     __shared__ int32_t s_arp[129];
     const int32_t r0 = blockIdx.x * R, r1 = min(n, r0 + R);
-    const int32_t nr = nruns[blockIdx.x];
+    const int32_t nr = nruns[2 * blockIdx.x];
     for (int32_t j = threadIdx.x; j < nr; j += kThreads) s_runs[j] = runs[static_cast<size_t>(blockIdx.x) * kMaxRuns + j];
     for (int32_t j = threadIdx.x; j <= r1 - r0; j += kThreads) s_arp[j] = arp[r0 + j];
     __syncthreads();
@@ -324,18 +327,30 @@ __global__ void __launch_bounds__(kThreads)
 
     const int32_t r0 = blockIdx.x * R, r1 = min(n, r0 + R), nrows = r1 - r0;
     const uint32_t bar_a = smem_addr(bar);
-    const int32_t a0 = arp[r0], a1 = arp[r1];
-    // records are 16 bytes each: the CTA's piece is aligned as it is
-    if (threadIdx.x == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_a) : "memory");
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        const int32_t nr = nruns[blockIdx.x];
+    const int32_t a0 = arp[r0];
+    // warp 0 issues the bulk copies with one round of global loads before them: every lane
+    // reads the run it will copy (entries beyond the run count are never used) while lane 0
+    // reads the CTA's header (run count, staged bytes) and its record range; lane 0 arms the
+    // barrier and copies the records (16 bytes each: aligned as they are), then each lane
+    // copies its run
+    if (threadIdx.x < 32) {
         const Run* rr = runs + static_cast<size_t>(blockIdx.x) * kMaxRuns;
-        uint32_t total = static_cast<uint32_t>(a1 - a0) * 16u;
-        for (int32_t j = 0; j < nr; ++j) total += static_cast<uint32_t>(rr[j].len) * 8u;
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar_a), "r"(total) : "memory");
-        if (a1 > a0) bulk_g2s(s_rec, recs + a0, static_cast<uint32_t>(a1 - a0) * 16u, bar_a);
-        for (int32_t j = 0; j < nr; ++j) bulk_g2s(s_x + rr[j].soff, x + rr[j].xs, static_cast<uint32_t>(rr[j].len) * 8u, bar_a);
+        const int4 h0 = *reinterpret_cast<const int4*>(rr + threadIdx.x);  // xs, len, soff, ta
+        const int32_t nr = nruns[2 * blockIdx.x];
+        if (threadIdx.x == 0) {
+            const uint32_t rec_bytes = static_cast<uint32_t>(arp[r1] - a0) * 16u;
+            const uint32_t total = rec_bytes + static_cast<uint32_t>(nruns[2 * blockIdx.x + 1]);
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_a) : "memory");
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar_a), "r"(total) : "memory");
+            if (rec_bytes) bulk_g2s(s_rec, recs + a0, rec_bytes, bar_a);
+        }
+        __syncwarp();
+        if (static_cast<int32_t>(threadIdx.x) < nr) bulk_g2s(s_x + h0.z, x + h0.x, static_cast<uint32_t>(h0.y) * 8u, bar_a);
+        for (int32_t j = threadIdx.x + 32; j < nr; j += 32) {
+            const int4 h = *reinterpret_cast<const int4*>(rr + j);
+            bulk_g2s(s_x + h.z, x + h.x, static_cast<uint32_t>(h.y) * 8u, bar_a);
+        }
     }
     for (int32_t j = threadIdx.x; j <= nrows; j += kThreads) {
         s_arp[j] = arp[r0 + j];
