@@ -61,6 +61,19 @@ def test_default_mode_bitwise(gpu, port, cfg, size, restarts):
     assert rel_max_err(xg, xo) <= 1e-10
 
 
+@pytest.mark.parametrize("cfg,size,restarts", [(2, 333, 0), (5, 150, 0), (4, 300, 2), (3, 257, 2), (1, 77, 0)],
+                         ids=["C2-333", "C5-150", "C4-300", "C3-257", "C1-77"])
+def test_default_mode_bitwise_ragged_sizes(gpu, port, cfg, size, restarts):
+    """sizes that leave ragged last CTAs / tiles in every blocked kernel (rows per CTA of the
+    band masked product, 32-row SELL slices, 4096-term sum tiles, segment blocks) and that
+    take the band kernel's three record formats on different levels"""
+    hg, ho, b, vo = _setup_both(cfg, size, gpu, port)
+    _bitwise_hierarchy(hg, ho)
+    xg, rg, xo, ro = _solve_both(hg, ho, b, vo, port, restarts)
+    assert rg.iterations == ro.iterations and rg.converged == ro.converged
+    assert rel_max_err(rg.residual_history, ro.residual_history) <= 1e-10
+
+
 @pytest.mark.parametrize("name", list(FULL_DUMPS))
 def test_full_size_against_dump(gpu, name):
     """BASELINE sizes (C1-256, C2-1024, C3-2048, C4-2048, C5-1024) against the committed
