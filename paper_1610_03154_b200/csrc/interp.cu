@@ -667,12 +667,14 @@ bool masked_band_enabled() {
     return on;
 }
 
-// blocks of k_cg_columns: the window of columns in flight (AMGCU_CGCOL_BLOCKS_PER_SM, default 2)
+// blocks of k_cg_columns: the window of columns in flight (AMGCU_CGCOL_BLOCKS_PER_SM, default 4:
+// 32 columns per block of 128 threads; C5 level 0: 345 us and 0.76 GB at 4, 360 us at 3, 385 us
+// and 1.25 GB at 8)
 unsigned cg_column_blocks(const Ctx& c) {
     static const int per_sm = [] {
         const char* e = std::getenv("AMGCU_CGCOL_BLOCKS_PER_SM");
-        const int v = e ? std::atoi(e) : 2;
-        return v > 0 ? v : 2;
+        const int v = e ? std::atoi(e) : 4;
+        return v > 0 ? v : 4;
     }();
     return static_cast<unsigned>(c.sms * per_sm);
 }
@@ -841,42 +843,70 @@ __global__ void k_cg_ctl_denom(double* __restrict__ st, int32_t* __restrict__ f,
 
 // per column j, entries in increasing row order (CSC positions): e, g, h and the
 // safe step (column_safe_step, interpolation.hpp:247-260), min-reduced into alpha_bits
-// Thread per column; a block walks the column blocks grid-stride, so the columns in
-// flight at any time are one contiguous window (grid * 128 columns): their entries lie
-// in a band of rows whose slots stay in L2 while the neighbouring columns -- which
-// share the 32-byte sectors -- read them.  With every column in flight at once the
-// four arrays streamed through L2 in sector-sized gathers (C5 level 0: 4.1 GB of DRAM
-// traffic for 0.54 GB of data).  The loads of 8 entries are issued before their sums.
+// kCgLpc lanes per column; a block walks the column blocks grid-stride, so the columns in
+// flight at any time are one contiguous window (grid * 128 / kCgLpc columns): their entries
+// lie in a band of rows whose slots stay in L2 while the neighbouring columns -- which
+// share the 32-byte sectors -- read them.  With every column in flight at once the four
+// arrays streamed through L2 in sector-sized gathers (C5 level 0: 4.1 GB of DRAM traffic
+// for 0.54 GB of data).  The window is a trade between traffic and threads in flight
+// (DESIGN.md §3); four lanes per column put four times the loads in flight for the same
+// window: lane t loads the entries q = t (mod 4) and forms their products, and the three
+// sums take the products in row order from the lanes by shuffles (every lane of a column
+// carries the same sums).
+constexpr int kCgLpc = 4;
 __global__ void __launch_bounds__(128)
     k_cg_columns(int32_t nc, const int32_t* __restrict__ colptr, const int32_t* __restrict__ pos,
                  const double* __restrict__ P, const double* __restrict__ APm, const double* __restrict__ D,
                  const double* __restrict__ ADm, unsigned long long* __restrict__ alpha_bits,
                  const int32_t* __restrict__ f) {
     if (f[0]) return;
-    constexpr int U = 8;
-    for (int32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < nc; j += gridDim.x * blockDim.x) {
-        double e = 0.0, g = 0.0, h = 0.0;
-        const int32_t qe = colptr[j + 1];
-        for (int32_t q = colptr[j]; q < qe; q += U) {
-            double vp[U], va[U], vd[U], vm[U];
+    const int sub = threadIdx.x % kCgLpc;
+    const int lane = threadIdx.x & 31;
+    const int lead = lane - sub;  // first lane of this column's group
+    const int32_t per_block = blockDim.x / kCgLpc;
+    // every lane of a warp runs the same number of rounds (the shuffles are warp-wide)
+    const int32_t j0 = blockIdx.x * per_block + static_cast<int32_t>(threadIdx.x) / kCgLpc;
+    const int32_t stride = static_cast<int32_t>(gridDim.x) * per_block;
+    const int32_t jw = blockIdx.x * per_block + (static_cast<int32_t>(threadIdx.x) & ~31) / kCgLpc;  // the warp's first column
+    for (int32_t jb = jw, j = j0; jb < nc; jb += stride, j += stride) {
+        const bool on = j < nc;
+        const int32_t qb = on ? colptr[j] : 0, qe = on ? colptr[j + 1] : 0;
+        // rounds of kCgLpc entries; the warp runs as many as its longest column needs
+        int32_t rounds = (qe - qb + kCgLpc - 1) / kCgLpc;
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const bool in = q + u < qe;
-                const int32_t p = in ? __ldg(&pos[q + u]) : 0;
-                vp[u] = in ? __ldg(&P[p]) : 0.0;
-                va[u] = in ? __ldg(&APm[p]) : 0.0;
-                vd[u] = in ? __ldg(&D[p]) : 0.0;
-                vm[u] = in ? __ldg(&ADm[p]) : 0.0;
+        for (int off = 16; off > 0; off >>= 1) rounds = max(rounds, __shfl_xor_sync(0xffffffffu, rounds, off));
+        double e = 0.0, g = 0.0, h = 0.0;
+        for (int32_t r = 0; r < rounds; r += 2) {
+            // two rounds' loads in flight before their sums
+            double pe[2], pg[2], ph[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int32_t q = qb + (r + u) * kCgLpc + sub;
+                pe[u] = pg[u] = ph[u] = 0.0;
+                if (q < qe) {
+                    const int32_t p = __ldg(&pos[q]);
+                    const double vp = __ldg(&P[p]), va = __ldg(&APm[p]), vd = __ldg(&D[p]), vm = __ldg(&ADm[p]);
+                    pe[u] = vp * va;
+                    pg[u] = vd * va;
+                    ph[u] = vd * vm;
+                }
             }
 #pragma unroll
-            for (int u = 0; u < U; ++u)
-                if (q + u < qe) {
-                    e += vp[u] * va[u];
-                    g += vd[u] * va[u];
-                    h += vd[u] * vm[u];
+            for (int u = 0; u < 2; ++u) {
+#pragma unroll
+                for (int t = 0; t < kCgLpc; ++t) {
+                    const double xe = __shfl_sync(0xffffffffu, pe[u], lead + t);
+                    const double xg = __shfl_sync(0xffffffffu, pg[u], lead + t);
+                    const double xh = __shfl_sync(0xffffffffu, ph[u], lead + t);
+                    if (qb + (r + u) * kCgLpc + t < qe) {  // entries past the column's end add nothing
+                        e += xe;
+                        g += xg;
+                        h += xh;
+                    }
                 }
+            }
         }
-        if (h <= 0.0) continue;
+        if (!on || sub != 0 || h <= 0.0) continue;
         const double norm_j = sqrt(sd::dmax(e, 0.0));
         const double tol = 2.5e-13 * sd::dmax(norm_j, 1.0e-30);
         const double budget = tol * (2.0 * norm_j + tol);
@@ -1336,7 +1366,7 @@ void energy_minimize(Ctx& c, const DCsr& A, const DCsr& T, const double* B, cons
             masked(A, plan, kProfMaskedProduct, mp_bytes(A, 2), D.get(), ADm.get(), ADp.get(), F);
             dot(c, D.get(), ADm.get(), nz, S + 7);
             launch_prof(c, kProfEminCg, 0.0, k_cg_ctl_denom, 1, 1, 0, S, F, abits.get());
-            launch_prof(c, kProfEminCg, 0.0, k_cg_columns, std::min(blocks_for(nc, 128), cg_column_blocks(c)), 128, 0, nc, static_cast<const int32_t*>(colptr.get()),
+            launch_prof(c, kProfEminCg, 0.0, k_cg_columns, std::min(blocks_for(static_cast<int64_t>(nc) * kCgLpc, 128), cg_column_blocks(c)), 128, 0, nc, static_cast<const int32_t*>(colptr.get()),
                    static_cast<const int32_t*>(pos.get()), static_cast<const double*>(P.get()),
                    static_cast<const double*>(APm.get()), static_cast<const double*>(D.get()),
                    static_cast<const double*>(ADm.get()), abits.get(), static_cast<const int32_t*>(F));

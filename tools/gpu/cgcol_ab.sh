@@ -1,4 +1,4 @@
-for b in 1 2 3 4 6; do
+for b in 2 3 4 6 8; do
 AMGCU_CGCOL_BLOCKS_PER_SM=$b timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum --clock-control none --csv --log-file gpurun_out/cg_$b.csv -k regex:k_cg_columns -c 4 python tools/profile_step.py --config 5 --size 1024 --reps 1 > /dev/null 2>&1
 python - <<PY
 import csv
