@@ -510,11 +510,18 @@ SS_HD double apply(const Item* r, int nr, double s, const TermAt& term, int64_t*
                 continue;
             }
         }
-        if (it.kind != kRaw) {
-            if (fallback_elems) *fallback_elems += it.i1 - it.i0;
-            for (int64_t i = it.i0; i < it.i1; ++i) s = s + term(i);
-        } else {
-            for (int64_t i = it.i0; i < it.i1; ++i) s = s + raw_term(it, i, term);
+        // element by element, the terms read eight ahead of the chain: here they come from
+        // global memory, and one dependent load per add made long fallbacks latency-bound
+        // (C3's restarted FGMRES: ~40,000 such terms took 20 ms per sum)
+        if (it.kind != kRaw && fallback_elems) *fallback_elems += it.i1 - it.i0;
+        for (int64_t i = it.i0; i < it.i1; i += 8) {
+            double tb[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                tb[u] = i + u < it.i1 ? (it.kind != kRaw ? term(i + u) : raw_term(it, i + u, term)) : 0.0;
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (i + u < it.i1) s = s + tb[u];
         }
     }
     return s;
